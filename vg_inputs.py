@@ -1,0 +1,215 @@
+"""Seeded synthetic inputs for the Vogue environment step (arxiv 2207.03945).
+
+This module is the ONLY code shared by the oracle (``oracle/``) and the CUDA path's
+tests/bench.  It holds parameters and random-number generation, and none of the
+method's arithmetic (no integrate, no binning, no sensing, no reward).
+
+Parameter defaults are SPEC.md's because the paper fixes only ratios and
+dimensions.  Every float is stored as the value of an
+fp32 number (SURVEY.md §8c reading A12): the CUDA path consumes the fp32 value and the
+oracle promotes that same value exactly to fp64.
+
+Workloads C1..C5 are BASELINE.json's ``configs``.
+"""
+from __future__ import annotations
+
+import dataclasses
+import math
+
+import numpy as np
+
+FLOCK = "flock"
+TAG = "tag"
+
+
+def f32(x: float) -> float:
+    """Round a Python float to the nearest fp32 value (returned as a Python float)."""
+    return float(np.float32(x))
+
+
+@dataclasses.dataclass(frozen=True)
+class EnvParams:
+    """World + environment parameters (field names match ``vg_config`` in include/vg.h)."""
+
+    env: str                    # "flock" | "tag"
+    n_agents: int               # N, agents per replica
+    n_replicas: int = 1         # R
+    width: float = 100.0        # L (square torus; reading A9)
+    d_v: float = 10.0           # view range and reward radius = L/10
+    d_r: float = 0.25           # body radius; contact at 2 d_r
+    fov: float = f32(250.0 * math.pi / 180.0)   # "approximately 250 degrees"
+    v: int = 128                # sectors per channel: flock 128, tag 64
+    grid: int = 0               # G cells per axis; 0 = auto (reading A16)
+    s_min: float = f32(0.05)
+    s_max: float = 0.5
+    a_max: float = f32(0.1)
+    theta_max: float = f32(0.2)
+    c_collide: float = 1.0
+    c_near: float = 0.5
+    d_peak: float = 5.25        # (2 d_r + d_v)/2
+    n_chasers: int = 0          # tag: agents [N - n_chasers, N) are chasers (reading A14)
+    r_touch: float = 1.0
+    w_prox: float = f32(0.1)
+    s_max_chaser: float = 0.375  # 0.75 s_max
+
+    @property
+    def channels(self) -> int:
+        return 1 if self.env == FLOCK else 2
+
+    @property
+    def obs_dim(self) -> int:
+        # flock: 128 view + speed = 129; tag: 2 x 64 = 128
+        return self.channels * self.v + (1 if self.env == FLOCK else 0)
+
+    @property
+    def occ_words(self) -> int:
+        return (self.channels * self.v + 31) // 32
+
+    @property
+    def total_agents(self) -> int:
+        return self.n_agents * self.n_replicas
+
+    def replace(self, **kw) -> "EnvParams":
+        return dataclasses.replace(self, **kw)
+
+
+def flock_params(n_agents: int, n_replicas: int = 1, width: float = 100.0,
+                 d_v: float | None = None, **kw) -> EnvParams:
+    """Flock defaults.  d_v defaults to width/10."""
+    width = f32(width)
+    d_v = f32(width / 10.0) if d_v is None else f32(d_v)
+    d_r = f32(kw.pop("d_r", 0.25))
+    d_peak = kw.pop("d_peak", None)
+    d_peak = f32((2.0 * d_r + d_v) / 2.0) if d_peak is None else f32(d_peak)
+    return EnvParams(env=FLOCK, n_agents=n_agents, n_replicas=n_replicas, width=width,
+                     d_v=d_v, d_r=d_r, d_peak=d_peak, v=kw.pop("v", 128), **kw)
+
+
+def tag_params(n_agents: int, n_replicas: int = 1, width: float = 100.0,
+               d_v: float | None = None, n_chasers: int | None = None, **kw) -> EnvParams:
+    """Tag defaults.  1/10 of agents are chasers (reading A14)."""
+    width = f32(width)
+    d_v = f32(width / 10.0) if d_v is None else f32(d_v)
+    d_r = f32(kw.pop("d_r", 0.25))
+    d_peak = kw.pop("d_peak", None)
+    d_peak = f32((2.0 * d_r + d_v) / 2.0) if d_peak is None else f32(d_peak)
+    if n_chasers is None:
+        n_chasers = n_agents // 10
+    return EnvParams(env=TAG, n_agents=n_agents, n_replicas=n_replicas, width=width,
+                     d_v=d_v, d_r=d_r, d_peak=d_peak, v=kw.pop("v", 64),
+                     n_chasers=n_chasers, **kw)
+
+
+# --------------------------------------------------------------------------------------
+# Workloads: BASELINE.json configs[0..4] (SURVEY.md §8d "Concrete synthetic inputs").
+# C5 keeps the paper's density (0.5 agents per unit area, as C2) with d_v = 10:
+# L = RN32(100 * sqrt(200)) so that N / L^2 = 0.5 at N = 10^6.
+# --------------------------------------------------------------------------------------
+C5_WIDTH = f32(100.0 * math.sqrt(200.0))
+
+
+def workload(name: str) -> EnvParams:
+    name = name.lower()
+    if name == "c1":
+        return flock_params(100)
+    if name == "c2":
+        return flock_params(5000)
+    if name == "c3":
+        return tag_params(10000, n_chasers=1000)
+    if name == "c4":
+        return flock_params(5000, n_replicas=1024)
+    if name == "c5":
+        # G = 136 (c = 10.399 >= d_v (1 + 2^-12)) rather than the auto 141, so that the
+        # x-slabs of 1/2/4/8 GPUs are whole, equal column ranges.
+        return flock_params(1_000_000, width=C5_WIDTH, d_v=10.0, grid=136)
+    raise KeyError(name)
+
+
+WORKLOAD_DESCRIPTIONS = {
+    "c1": "flock 1x100, L=100, 100 steps, seeded random actions",
+    "c2": "flock 1x5000, L=100 (paper Fig. 1 scale)",
+    "c3": "tag 1x10000 (9000 runners + 1000 chasers), L=100",
+    "c4": "flock 1024 replicas x 5000, L=100",
+    "c5": "flock single 1,000,000-agent world, L=1414.2136, d_v=10 (paper density)",
+}
+
+
+# --------------------------------------------------------------------------------------
+# Seeded generators (SURVEY.md §8c readings A20, A21)
+# --------------------------------------------------------------------------------------
+TWO_PI_F32 = np.float32(2.0 * math.pi)   # RN32(2 pi): exclusive upper bound of a stored heading
+
+
+def _uniform_f32_below(rng: np.random.Generator, n: int, hi: float) -> np.ndarray:
+    """U[0, hi) drawn in fp64 and rounded to fp32, kept strictly below fp32(hi)."""
+    x = (rng.random(n) * hi).astype(np.float32)
+    x[x >= np.float32(hi)] = np.float32(0.0)
+    return x
+
+
+def init_state(p: EnvParams, seed: int = 0, replicas: range | None = None) -> np.ndarray:
+    """Initial state, fp32 [R, N, 4] = (x, y, theta, s) (reading A20).
+
+    Replica r draws from PCG64(seed + r): positions U[0, L)^2, heading U[0, 2 pi),
+    flock speed (s_min + s_max)/2; tag's fourth column is reserved and set to 0
+    (type comes from the index: the last n_chasers agents are chasers).
+    """
+    reps = range(p.n_replicas) if replicas is None else replicas
+    out = np.empty((len(reps), p.n_agents, 4), dtype=np.float32)
+    for k, r in enumerate(reps):
+        rng = np.random.Generator(np.random.PCG64(seed + r))
+        out[k, :, 0] = _uniform_f32_below(rng, p.n_agents, p.width)
+        out[k, :, 1] = _uniform_f32_below(rng, p.n_agents, p.width)
+        th = (rng.random(p.n_agents) * (2.0 * math.pi)).astype(np.float32)
+        th[th >= TWO_PI_F32] = np.float32(0.0)
+        out[k, :, 2] = th
+        if p.env == FLOCK:
+            out[k, :, 3] = np.float32(0.5 * (p.s_min + p.s_max))
+        else:
+            out[k, :, 3] = np.float32(0.0)
+    return out
+
+
+def clustered_state(p: EnvParams, seed: int = 0, n_clusters: int = 16,
+                    sigma: float | None = None) -> np.ndarray:
+    """Stress variant: Gaussian clusters with sigma = 2 d_v, wrapped."""
+    sigma = 2.0 * p.d_v if sigma is None else sigma
+    out = init_state(p, seed)
+    for r in range(p.n_replicas):
+        rng = np.random.Generator(np.random.PCG64(seed + 7919 * (r + 1)))
+        centres = rng.random((n_clusters, 2)) * p.width
+        which = rng.integers(0, n_clusters, p.n_agents)
+        xy = centres[which] + rng.normal(0.0, sigma, (p.n_agents, 2))
+        xy = np.mod(xy, p.width).astype(np.float32)
+        xy[xy >= np.float32(p.width)] = np.float32(0.0)
+        out[r, :, :2] = xy
+    return out
+
+
+def action_box(p: EnvParams) -> tuple[np.ndarray, np.ndarray]:
+    """Per-agent action bounds [N, 2] (lo, hi)."""
+    lo = np.empty((p.n_agents, 2), dtype=np.float64)
+    hi = np.empty((p.n_agents, 2), dtype=np.float64)
+    if p.env == FLOCK:
+        lo[:, 0], hi[:, 0] = -p.a_max, p.a_max          # accelerate
+        lo[:, 1], hi[:, 1] = -p.theta_max, p.theta_max  # rotate
+    else:
+        lo[:, 0], hi[:, 0] = -p.theta_max, p.theta_max  # rotate
+        lo[:, 1] = 0.0                                   # move along heading
+        hi[:, 1] = p.s_max
+        hi[p.n_agents - p.n_chasers:, 1] = p.s_max_chaser
+    return lo, hi
+
+
+def actions(p: EnvParams, seed: int = 0, step: int = 0,
+            replicas: range | None = None) -> np.ndarray:
+    """Seeded uniform actions in the action box, fp32 [R, N, 2] (reading A21)."""
+    reps = range(p.n_replicas) if replicas is None else replicas
+    lo, hi = action_box(p)
+    out = np.empty((len(reps), p.n_agents, 2), dtype=np.float32)
+    for k, r in enumerate(reps):
+        ss = np.random.SeedSequence([seed ^ 0x9E3779B9, step, r])
+        rng = np.random.Generator(np.random.PCG64(ss))
+        u = rng.random((p.n_agents, 2))
+        out[k] = (lo + u * (hi - lo)).astype(np.float32)
+    return out
