@@ -1,0 +1,350 @@
+#!/usr/bin/env python
+"""bench.py — throughput of the Vogue environment step (arxiv 2207.03945) on B200.
+
+Metric (BASELINE.json): agent-steps/s of vg_step = integrate + bin + sense + reward
+(obs + reward + integrate), on synthetic worlds shaped like the paper's (vg_inputs).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config c5] [--impl ours|reference]
+
+N > 1: launched by torchrun, one process per GPU.  Replica workloads (c1-c4) shard the
+replicas over ranks with no collective ("replicas only"); c5 (one 1M-agent world) runs an
+independent world per rank until slab mode exists.  Rank 0 prints one JSON
+line.  Timing: W untimed warm-up steps; K timed steps, each bracketed by CUDA events on
+the launching stream with a 256 MiB L2 flush between steps (outside the events);
+barrier + synchronize around the timed region; max over ranks.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import vg_inputs as vi  # noqa: E402
+
+METRIC = "agent-steps/sec (obs+reward+integrate)"
+UNIT = "agent-steps/s"
+PAPER_CONTEXT = ("paper Fig. 1 (P:45): 5,000 agents, 500 training steps in ~16 min on a "
+                 "laptop GTX 1650 (whole PPO training, not env-only)")
+ALG_OPS_PER_PAIR = 45          # fp32 ops of the definition per in-radius pair
+SENSE_BYTES_FIXED = 16 + 4 + 4 + 4 + 4   # query record, perm, reward, n_neigh, n_collide
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--config", default="c5", choices=["c1", "c2", "c3", "c4", "c5"])
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--cpu-seconds", type=float, default=15.0,
+                    help="bounded oracle sample for cpu_baseline (seconds of CPU work)")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    return ap.parse_args()
+
+
+def rank_info():
+    return (int(os.environ.get("RANK", 0)), int(os.environ.get("LOCAL_RANK", 0)),
+            int(os.environ.get("WORLD_SIZE", 1)))
+
+
+def local_params(name: str, world_size: int, rank: int):
+    """Per-rank workload: replicas sharded over ranks (no communication)."""
+    p = vi.workload(name)
+    if p.n_replicas > 1:
+        if p.n_replicas % world_size:
+            raise SystemExit(f"{name}: {p.n_replicas} replicas not divisible by {world_size}")
+        return p.replace(n_replicas=p.n_replicas // world_size), "strong"
+    return p, ("weak" if world_size > 1 else "strong")
+
+
+def action_pool(p, torch, device, count=8, seed=0):
+    """Seeded uniform actions in the action box, generated on the device (inputs resident)."""
+    g = torch.Generator(device=device)
+    g.manual_seed(seed)
+    lo, hi = vi.action_box(p)
+    lo = torch.as_tensor(lo, dtype=torch.float32, device=device)
+    hi = torch.as_tensor(hi, dtype=torch.float32, device=device)
+    out = []
+    for _ in range(count):
+        u = torch.rand((p.n_replicas, p.n_agents, 2), generator=g, device=device)
+        out.append((lo + u * (hi - lo)).contiguous())
+    return out
+
+
+class ClockSampler:
+    """NVML SM clock + clock-event reasons sampled every 10 ms in a thread."""
+
+    REASONS = {0x8: "hw_slowdown", 0x40: "hw_thermal_slowdown", 0x20: "sw_thermal_slowdown",
+               0x4: "sw_power_cap", 0x80: "hw_power_brake_slowdown", 0x2: "applications_clocks_setting"}
+
+    def __init__(self, index: int):
+        self.samples, self.reasons, self.max_mhz = [], set(), None
+        self._stop = threading.Event()
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+        except Exception as e:  # pragma: no cover - no NVML
+            self.nv, self.err = None, str(e)
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                self.samples.append(self.nv.nvmlDeviceGetClockInfo(self.h, self.nv.NVML_CLOCK_SM))
+                fn = getattr(self.nv, "nvmlDeviceGetCurrentClocksEventReasons", None) or \
+                    self.nv.nvmlDeviceGetCurrentClocksThrottleReasons
+                r = fn(self.h)
+                for bit, name in self.REASONS.items():
+                    if r & bit:
+                        self.reasons.add(name)
+            except Exception:
+                pass
+            time.sleep(0.01)
+
+    def __enter__(self):
+        if self.nv:
+            self.t = threading.Thread(target=self._run, daemon=True)
+            self.t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        if self.nv:
+            self.t.join()
+
+    def summary(self):
+        if not self.nv:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "note": "NVML unavailable"}
+        return {"sm_mhz": statistics.median(self.samples) if self.samples else None,
+                "sm_max_mhz": self.max_mhz, "reasons": sorted(self.reasons),
+                "samples": len(self.samples)}
+
+
+def measured_peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            return json.load(f), "measured"
+    except Exception:
+        return {"hbm_gbs": 6650.0, "sm_max_mhz": 1965.0}, "fallback (B200_PROFILING.md)"
+
+
+# ------------------------------------------------------------------------- oracle legs
+def oracle_rate(p, seconds: float, seed: int = 0, workers: int | None = None):
+    """Oracle agent-steps/s on a bounded sample: integrate all agents of one replica (fp64),
+    then sense a sample of query rows against all N (rows are independent), extrapolated
+    linearly to the replica.  Returns (rate, sample description, cores used)."""
+    import oracle
+    workers = workers or max(1, len(os.sched_getaffinity(0)))
+    q = p.replace(n_replicas=1)
+    st = vi.init_state(q, seed=seed)
+    act = vi.actions(q, seed=seed, step=0)
+    t0 = time.perf_counter()
+    new = oracle.integrate(q, st, act)
+    t_int = time.perf_counter() - t0
+    rng = np.random.default_rng(seed)
+    probe = rng.choice(q.n_agents, min(q.n_agents, 64 * workers), replace=False)
+    t0 = time.perf_counter()
+    oracle.sense(q, new, rows=probe, workers=workers)
+    per_row = (time.perf_counter() - t0) / len(probe)
+    n_rows = int(min(q.n_agents, max(len(probe), (seconds - t_int) / max(per_row, 1e-9))))
+    rows = rng.choice(q.n_agents, n_rows, replace=False)
+    t0 = time.perf_counter()
+    oracle.sense(q, new, rows=rows, workers=workers)
+    t_sense = time.perf_counter() - t0
+    per_agent = t_int / q.n_agents + t_sense / n_rows
+    sample = (f"one replica of N={q.n_agents}: fp64 integrate of all N ({t_int:.2f} s) + "
+              f"O(N^2) sense of {n_rows} sampled query rows against all N ({t_sense:.2f} s, "
+              f"{workers} processes), linearly extrapolated (rows independent)")
+    return 1.0 / per_agent, sample, workers
+
+
+def run_reference(args):
+    rank, _, world = rank_info()
+    if rank != 0:
+        return 0
+    p = vi.workload(args.config)
+    per_step = max(1.0, min(10.0, 150.0 / max(1, args.steps + args.warmup)))
+    rates = []
+    for k in range(args.warmup + args.steps):
+        rate, sample, cores = oracle_rate(p, per_step, seed=k)
+        if k >= args.warmup:
+            rates.append(rate)
+    value = statistics.median(rates)
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": 0,
+        "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": 1e3 * p.total_agents / value, "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": args.config, "desc": vi.WORKLOAD_DESCRIPTIONS[args.config],
+                   "R": p.n_replicas, "N": p.n_agents},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "oracle",
+                         "sample": f"per step: {sample}"},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# ---------------------------------------------------------------------------- our leg
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+    import paper_2207_03945_b200 as vg
+
+    rank, local, world = rank_info()
+    if world > 1:
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    device = torch.device("cuda", local)
+    torch.cuda.set_device(device)
+    p, scaling = local_params(args.config, world, rank)
+    w = vg.World(p, device=device)
+    out = w.alloc_outputs()
+    state = torch.from_numpy(vi.init_state(p, seed=1000 * rank)).to(device)
+    acts = action_pool(p, torch, device, seed=rank)
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=device)
+
+    for k in range(args.warmup):
+        w.step(state, acts[k % len(acts)], out)
+    torch.cuda.synchronize()
+    w.sync_errors()
+
+    K = args.steps
+    ev0 = [torch.cuda.Event(enable_timing=True) for _ in range(K)]
+    ev1 = [torch.cuda.Event(enable_timing=True) for _ in range(K)]
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    nn_sum = torch.zeros((), dtype=torch.float64, device=device)
+    with ClockSampler(local) as clk:
+        w.profile_begin(K)
+        for k in range(K):
+            flush.fill_(k & 0xFF)                 # evict L2 between steps (not timed)
+            ev0[k].record()
+            w.step(state, acts[k % len(acts)], out)
+            ev1[k].record()
+            nn_sum += out.n_neigh.sum(dtype=torch.float64)   # pairs evaluated (not timed)
+        torch.cuda.synchronize()
+        phases, nrec = w.profile_end()
+    if world > 1:
+        dist.barrier()
+    step_ms = [a.elapsed_time(b) for a, b in zip(ev0, ev1)]
+    total_ms = float(sum(step_ms))
+    w.sync_errors()
+    t = torch.tensor([total_ms], dtype=torch.float64, device=device)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    max_ms = float(t.item())
+    agents_local = p.total_agents
+    agents_all = agents_local * world
+    value = agents_all * K / (max_ms / 1e3)
+
+    # ---- end to end through the public API with host buffers (vg_step_host)
+    e2e = None
+    if not args.no_e2e:
+        acts_h = [a.cpu().pin_memory() for a in acts[:2]]
+        rew_h = torch.empty((p.n_replicas, p.n_agents), dtype=torch.float32).pin_memory()
+        stream = torch.cuda.current_stream(device)
+        for k in range(2):
+            w.step_host(state, acts_h[k % 2], out, rew_h)
+        stream.synchronize()
+        if world > 1:
+            dist.barrier()
+        t0 = time.perf_counter()
+        for k in range(K):
+            w.step_host(state, acts_h[k % 2], out, rew_h)
+            stream.synchronize()               # the step's reward is readable on the host
+        e2e_s = time.perf_counter() - t0
+        te = torch.tensor([e2e_s], dtype=torch.float64, device=device)
+        if world > 1:
+            dist.all_reduce(te, op=dist.ReduceOp.MAX)
+        e2e = {"value": agents_all * K / float(te.item()), "unit": UNIT,
+               "h2d_bytes_per_step": int(acts_h[0].numel() * 4),
+               "d2h_bytes_per_step": int(rew_h.numel() * 4),
+               "note": "vg_step_host: actions H2D from pinned host, reward D2H, stream sync per step, wall clock"}
+
+    if rank == 0:
+        peaks, peak_src = measured_peaks()
+        hbm = float(peaks.get("hbm_gbs", 6441.6))
+        sm_mhz = float(peaks.get("sm_max_mhz", 1965.0))
+        alu_peak = 148 * 128 * sm_mhz * 1e6 / 1e12      # fp32 lane-ops/s, TFLOP/s-equivalent
+        pairs_per_step = float(nn_sum.item()) / K
+        sense_s = phases["sense"] / 1e3 / nrec
+        achieved = ALG_OPS_PER_PAIR * pairs_per_step / sense_s / 1e12
+        n = agents_local
+        obs_b = 4 * w.obs_dim + 4 * w.occ_words + SENSE_BYTES_FIXED
+        stage_bytes = {"integrate_bin": 48 * n, "scan_cells": 8 * w.n_cells,
+                       "scatter": 44 * n, "cell_sort": 40 * n, "sense": obs_b * n}
+        stages = {}
+        for k2, ms in phases.items():
+            avg = ms / nrec
+            gbs = stage_bytes[k2] / (avg / 1e3) / 1e9 if avg > 0 else None
+            stages[k2] = {"ms": round(avg, 5), "alg_bytes": stage_bytes[k2],
+                          "GBps": round(gbs, 1) if gbs else None,
+                          "hbm_frac": round(gbs / hbm, 4) if gbs else None,
+                          "share": round(ms / sum(phases.values()), 4)}
+        traffic = None
+        tpath = os.path.join(ROOT, "profiles", "sense_traffic.json")
+        if os.path.exists(tpath):
+            try:
+                tj = json.load(open(tpath))
+                if tj.get("config") == args.config:
+                    traffic = tj.get("bytes_per_launch")
+            except Exception:
+                pass
+        cpu = None
+        if world == 1 and not args.no_cpu_baseline:
+            rate, sample, cores = oracle_rate(p, args.cpu_seconds)
+            cpu = {"value": rate, "unit": UNIT, "cores": cores, "kind": "oracle",
+                   "sample": sample}
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": K,
+            "warmup": args.warmup, "ms_per_step": max_ms / K, "higher_is_better": True,
+            "scaling": scaling, "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+            "config": {"workload": args.config, "desc": vi.WORKLOAD_DESCRIPTIONS[args.config],
+                       "R_per_gpu": p.n_replicas, "N": p.n_agents, "G": w.grid,
+                       "parallelism": ("replicas" if world > 1 else "single"),
+                       "l2": "256 MiB buffer written between timed steps (outside events)"},
+            "roofline": {"kernel": "k_sense (sector vision + reward)", "bound": "alu",
+                         "achieved": achieved, "peak": alu_peak, "unit": "TFLOP/s",
+                         "frac": achieved / alu_peak, "traffic": traffic,
+                         "basis": f"{ALG_OPS_PER_PAIR} fp32 ops x {pairs_per_step:.4g} "
+                                  f"in-radius pairs per launch / mean k_sense time; peak = "
+                                  f"148 SM x 128 lanes x {sm_mhz:.0f} MHz (1 op/lane/clk)"},
+            "stages": stages,
+            "hbm_peak_gbs": hbm, "peak_source": peak_src,
+            "e2e": e2e,
+            "gpu_launches": 5 * K,
+            "clocks": clk.summary(),
+            "cpu_baseline": cpu,
+            "context": PAPER_CONTEXT,
+        }
+        print(json.dumps(line), flush=True)
+    w.close()
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        return run_reference(args)
+    return run_ours(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

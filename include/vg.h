@@ -1,0 +1,193 @@
+/*
+ * vg.h — C ABI of libvg: the batched environment step of the Vogue MARL environments
+ * (arxiv 2207.03945, "High Performance Simulation for Scalable Multi-Agent Reinforcement
+ * Learning"), flock (§4.1) and tag (§4.2), on B200 (sm_100a).
+ *
+ * Citations: P:n = PAPER.md line n; S:n = SPEC.md line n; An = reading of a gap in the
+ * paper, listed in DESIGN.md §3.
+ *
+ * The paper's model: agents embedded in space interact with the agents in their
+ * spatial proximity; the model advances in discrete time-steps and every interaction of a
+ * step reads the same snapshot ("individual interactions update agents simultaneously").
+ * One environment update: "the agents are accelerated and rotated (according to
+ * actions sampled from the current policy), after which their local view model and rewards
+ * are updated for all pairs of agents in spatial proximity".
+ *
+ * Data layout (all device memory unless stated; all row-major, contiguous, 4-byte aligned;
+ * state/sorted 16-byte aligned):
+ *   state    float [R][N][4]  (x, y, theta, s): position on the L x L torus in [0, L),
+ *            heading theta in [0, RN32(2 pi)) radians (CCW from +x), flock speed s.
+ *            Tag: 4th column is reserved — ignored on input, preserved by integrate; an
+ *            agent's type comes from its index: agents [N - n_chasers, N) are chasers (A14).
+ *   actions  float [R][N][2]  flock (accelerate, rotate); tag (rotate, move)
+ *            (P:194).  Finite out-of-box values are clamped to the box, NaN is an
+ *            error.
+ *   R = n_replicas independent worlds of N = n_agents agents each (replicas never
+ *   interact).
+ *
+ * Ownership: the caller owns state, actions and every output buffer.  The world owns its
+ * scratch (allocated once in vg_world_create).  No call after create allocates, blocks
+ * the host, or copies device->host (except vg_sync_errors and vg_step_host, which say so),
+ * so vg_bin/vg_sense/vg_reward/vg_integrate/vg_step are CUDA-graph capturable.
+ * Concurrency: one stream at a time per world; a world is not thread-safe.
+ *
+ * Errors: every entry point returns vg_status.  Configuration errors are found
+ * synchronously (VG_EINVAL, vg_last_error() names the field).  Device-side state errors
+ * (a position outside [0, L), a non-finite or out-of-range heading, a non-finite
+ * speed, a NaN action) are recorded in a device error word as the smallest offending
+ * global agent index r*N + i; they surface as VG_ESTATE from vg_sync_errors() and from the
+ * next call that finds the word set (a non-blocking read of mapped host memory).
+ */
+#ifndef VG_H
+#define VG_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define VG_ABI_VERSION 1
+
+typedef enum {
+  VG_OK = 0,
+  VG_EINVAL = 1,     /* invalid argument or configuration (message names the field)     */
+  VG_ESTATE = 2,     /* device-side invalid state/action (index in vg_sync_errors)       */
+  VG_ECUDA = 3,      /* CUDA runtime error (message has the CUDA error string)           */
+  VG_ENCCL = 4,      /* NCCL error (slab mode)                                           */
+  VG_EOVERFLOW = 5,  /* fixed-capacity halo buffer overflow (slab mode)                  */
+  VG_ENOMEM = 6      /* device allocation failed in vg_world_create                      */
+} vg_status;
+
+typedef enum { VG_ENV_FLOCK = 0, VG_ENV_TAG = 1 } vg_env;
+typedef enum { VG_VISION_SECTOR = 0 /* hot path (A1) */, VG_VISION_RAY = 1 /* not built */ } vg_vision;
+typedef enum { VG_SHARD_REPLICA = 0, VG_SHARD_SLAB = 1 } vg_shard;
+
+/* World configuration.  All floats are authoritative fp32 values (A12).  Defaults in
+ * brackets are SPEC.md's; the paper fixes only d_v = L/10,
+ * fov ~ 250 deg, v = 128 / 2 x 64 and obs_dim 129 / 128. */
+typedef struct {
+  int32_t env;          /* vg_env                                                          */
+  int32_t vision;       /* vg_vision: must be VG_VISION_SECTOR                             */
+  int32_t shard;        /* vg_shard: VG_SHARD_REPLICA (slab mode: not in this build)       */
+  int32_t n_agents;     /* N > 0, agents per replica                               */
+  int32_t n_replicas;   /* R > 0; R*N < 2^31                                               */
+  float width;          /* L, square torus side (A9)                           [100]       */
+  float d_v;            /* view range = reward radius, 0 < d_v < L/2   [L/10]      */
+  float d_r;            /* body radius; contact at d <= 2 d_r, 2 d_r < d_v [0.25]  */
+  float fov;            /* field of view, radians, 0 < fov <= 2 pi     [250 deg]   */
+  int32_t v;            /* sectors per channel, 1..128 (flock) / 1..64 (tag)   [128 / 64]  */
+  int32_t grid;         /* G cells per axis, 0 = auto: largest G with L/G >= d_v(1+2^-12)
+                           (A16); must satisfy that bound and G >= 3                      */
+  float s_min, s_max;   /* flock speed bounds, 0 <= s_min < s_max      [0.05, 0.5] */
+  float a_max;          /* flock acceleration bound > 0                        [0.1]       */
+  float theta_max;      /* rotation bound, 0 < theta_max <= pi                 [0.2]       */
+  float c_collide;      /* collision penalty > 0 (Fig. 4, A5)                  [1.0]       */
+  float c_near;         /* peak closeness bonus > 0 (A5)                       [0.5]       */
+  float d_peak;         /* bonus peak, 2 d_r < d_peak < d_v                    [(2d_r+d_v)/2] */
+  int32_t n_chasers;    /* tag: 0 <= n_chasers <= N; agents [N - n_chasers, N) are chasers */
+  float r_touch;        /* tag touch reward magnitude                          [1.0]       */
+  float w_prox;         /* tag runner proximity weight                         [0.1]       */
+  float s_max_chaser;   /* tag chaser move bound (runners use s_max)           [0.375]     */
+  int32_t rank, world_size, halo_capacity; /* slab mode (reserved)                        */
+  const void* nccl_unique_id;              /* slab mode (reserved)                        */
+} vg_config;
+
+/* Caller-owned device output buffers; a NULL pointer means "do not write".  Rows are in
+ * agent order r*N + i (not sorted order). */
+typedef struct {
+  float* obs;           /* [R][N][obs_dim]; obs_dim = 129 flock (128 view + s/s_max, P:171,
+                           A24), 128 tag (runner channel 64 | chaser channel 64).
+                           View entry = min over visible neighbours in that sector of
+                           d/d_v, 1.0 if none (A1-A3)                       */
+  float* reward;        /* [R][N] Eq. 1 / Fig. 4 (flock); P:194 rules (tag)               */
+  uint32_t* n_neigh;    /* [R][N] #{j != i : d_ij < d_v} (all directions, A4)             */
+  uint32_t* n_collide;  /* [R][N] #{j : d_ij <= 2 d_r}; tag: same-type contacts only      */
+  uint32_t* n_touch;    /* [R][N] tag only: opposite-type contacts (d <= 2 d_r)           */
+  uint32_t* sector_occ; /* [R][N][occ_words] bit (c*v + k) set iff sector k of channel c
+                           holds a visible neighbour; occ_words = ceil(channels*v/32)     */
+  uint32_t* agent_id;   /* slab mode (reserved)                                           */
+} vg_outputs;
+
+typedef struct {
+  int32_t grid;         /* G                                                               */
+  float cell_size;      /* L / G                                                           */
+  int32_t n_cells;      /* R * G * G                                                       */
+  int32_t obs_dim;      /* 129 flock / 128 tag (for v = 128 / 64)                          */
+  int32_t channels;     /* 1 flock / 2 tag                                                 */
+  int32_t occ_words;    /* ceil(channels * v / 32)                                         */
+  int64_t total_agents; /* R * N                                                           */
+  int64_t scratch_bytes;/* device bytes owned by the world                                 */
+} vg_world_info;
+
+typedef struct vg_world vg_world;
+
+/* Validate cfg and allocate all scratch on the current CUDA device.
+ * Errors: VG_EINVAL (message names the field), VG_ENOMEM, VG_ECUDA.  *out = NULL on error. */
+vg_status vg_world_create(const vg_config* cfg, vg_world** out);
+void vg_world_destroy(vg_world* w);
+vg_status vg_world_query(const vg_world* w, vg_world_info* info);
+
+/* Spatial binning of `state` (A16): cell_id = cy*G + cx with
+ * cx = min(G-1, floor(RN32(x * RN32(G/L)))), a stable counting sort by cell per replica
+ * (within a cell, ascending agent id).  Results are owned by the world and read by
+ * vg_sense / vg_reward; vg_get_bins exposes them.  Validates the state (error word). */
+vg_status vg_bin(vg_world* w, const float* state, void* stream);
+
+/* Sector vision + fused reward for the state last binned (P:158, P:164, P:171-178,
+ * P:184): writes every non-NULL buffer of *outs.  All agents read the same
+ * snapshot.  Requires a prior vg_bin (or vg_step) on the same stream. */
+vg_status vg_sense(vg_world* w, const vg_outputs* outs, void* stream);
+
+/* Reward and neighbour/contact counts only (no bearings, no observation), for the state
+ * last binned.  Writes reward, n_neigh, n_collide, n_touch of *outs (others ignored). */
+vg_status vg_reward(vg_world* w, const vg_outputs* outs, void* stream);
+
+/* Integrate actions into state in place (A7, A8, A10): rotate, then
+ * (flock) accelerate, then move along the new heading, wrapping on the torus. */
+vg_status vg_integrate(vg_world* w, float* state, const float* actions, void* stream);
+
+/* One environment update: integrate, bin, sense + reward — all on device. */
+vg_status vg_step(vg_world* w, float* state, const float* actions, const vg_outputs* outs,
+                  void* stream);
+
+/* vg_step with HOST buffers for the per-step inputs/results: copies actions_host
+ * ([R][N][2], pinned host memory recommended) into a world-owned device buffer, steps,
+ * and copies the reward into reward_host ([R][N], may be NULL) — all asynchronously on
+ * `stream`; the caller synchronizes the stream before reading reward_host. */
+vg_status vg_step_host(vg_world* w, float* state, const float* actions_host,
+                       const vg_outputs* outs, float* reward_host, void* stream);
+
+/* Borrowed device pointers to the last binning (valid until the next vg_bin/vg_step):
+ * cell_id [R][N] (replica-local cy*G+cx), cell_start [R*G*G + 1] (offsets into the flat
+ * [R*N] sorted arrays), perm [R][N] (local agent id of each sorted slot), sorted
+ * [R][N][4] (state records in sorted order; tag: 4th column = type 0/1).  Any argument
+ * may be NULL. */
+vg_status vg_get_bins(const vg_world* w, const uint32_t** cell_id, const uint32_t** cell_start,
+                      const uint32_t** perm, const float** sorted);
+
+/* Synchronize `stream`, read and clear the device error word.  *bad_agent = -1 if clean,
+ * else the smallest offending global agent index (and VG_ESTATE is returned). */
+vg_status vg_sync_errors(vg_world* w, void* stream, int64_t* bad_agent);
+
+/* Phase timing for measurement.  After vg_profile_begin(w, max_steps), each of the next
+ * max_steps vg_step calls records CUDA events on its stream between its phases
+ * (VG_N_PHASES: integrate+cell-id+histogram, cell scan, scatter, cell sort, sense+reward).
+ * vg_profile_end synchronizes `stream` and writes per-phase total milliseconds over the
+ * recorded steps into phase_ms[VG_N_PHASES] and the step count into *n_steps.  Not for
+ * use inside CUDA-graph capture.  Errors: VG_EINVAL, VG_ECUDA. */
+#define VG_N_PHASES 5
+vg_status vg_profile_begin(vg_world* w, int32_t max_steps);
+vg_status vg_profile_end(vg_world* w, void* stream, double* phase_ms, int32_t* n_steps);
+
+/* Thread-local message of the last error on this thread ("" if none). */
+const char* vg_last_error(void);
+
+/* ABI version (VG_ABI_VERSION). */
+int32_t vg_abi_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* VG_H */

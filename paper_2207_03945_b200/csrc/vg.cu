@@ -1,0 +1,457 @@
+// vg.cu — libvg: C ABI (include/vg.h) over the sm_100a kernels in vg_kernels.cuh.
+//
+// Host side: configuration validation (SURVEY.md §8b conventions), derived fp32 constants,
+// scratch ownership, launch sequencing.  No allocation, host synchronization or D2H copy
+// happens after vg_world_create except in vg_sync_errors / vg_step_host (documented).
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <climits>
+#include <new>
+#include <vector>
+
+#include "vg.h"
+#include "vg_kernels.cuh"
+
+namespace {
+
+thread_local char g_err[512] = "";
+
+vg_status fail(vg_status st, const char* fmt, ...) {
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(g_err, sizeof(g_err), fmt, ap);
+  va_end(ap);
+  return st;
+}
+
+#define VG_CUDA(call)                                                                  \
+  do {                                                                                 \
+    cudaError_t e_ = (call);                                                           \
+    if (e_ != cudaSuccess)                                                             \
+      return fail(VG_ECUDA, "%s: %s (%s:%d)", #call, cudaGetErrorString(e_), __FILE__, \
+                  __LINE__);                                                           \
+  } while (0)
+
+}  // namespace
+
+struct vg_world {
+  vg_config cfg;
+  vg::Params P;
+  int device = -1;
+  int n_cells = 0;
+  bool binned = false;
+  size_t scratch_bytes = 0;
+  uint32_t* count = nullptr;       // [n_cells]     per-cell histogram (zero between uses)
+  uint32_t* cell_start = nullptr;  // [n_cells + 1]
+  uint32_t* cell_id = nullptr;     // [R*N]
+  uint32_t* slot = nullptr;        // [R*N]         arrival slot within the cell
+  uint32_t* tmp_id = nullptr;      // [R*N]         arrival-order agent ids
+  uint32_t* perm = nullptr;        // [R*N]         stable order
+  float4* tmp_rec = nullptr;       // [R*N]
+  float4* sorted = nullptr;        // [R*N]
+  float2* act_dev = nullptr;       // [R*N]         staging for vg_step_host
+  unsigned long long* err_dev = nullptr;  // smallest bad agent index (device word)
+  uint32_t* err_flag = nullptr;    // mapped pinned host flag (set by kernels)
+  // phase timing (vg_profile_begin/end): VG_N_PHASES + 1 events per recorded step
+  std::vector<cudaEvent_t> prof_ev;
+  int prof_max = 0, prof_n = 0;
+};
+
+namespace {
+
+// A16: cells per axis G = largest integer with L/G >= d_v (1 + 2^-12), in double.
+int auto_grid(double L, double dv) {
+  const double need = dv * (1.0 + std::ldexp(1.0, -12));
+  int g = (int)std::floor(L / need);
+  while (g > 0 && L / g < need) --g;
+  return g;
+}
+
+vg_status validate(const vg_config& c, int* grid_out) {
+  const double PI = 3.14159265358979323846;
+  if (c.env != VG_ENV_FLOCK && c.env != VG_ENV_TAG) return fail(VG_EINVAL, "env: must be 0 (flock) or 1 (tag)");
+  if (c.vision != VG_VISION_SECTOR) return fail(VG_EINVAL, "vision: only VG_VISION_SECTOR is built (reading A1)");
+  if (c.shard != VG_SHARD_REPLICA) return fail(VG_EINVAL, "shard: only VG_SHARD_REPLICA is built");
+  if (c.n_agents <= 0) return fail(VG_EINVAL, "n_agents: must be > 0 (S:241)");
+  if (c.n_replicas <= 0) return fail(VG_EINVAL, "n_replicas: must be > 0");
+  if ((long long)c.n_agents * c.n_replicas >= (1LL << 31)) return fail(VG_EINVAL, "n_agents*n_replicas: must be < 2^31");
+  if (!(c.width > 0.f) || !std::isfinite(c.width)) return fail(VG_EINVAL, "width: must be finite and > 0");
+  if (!(c.d_v > 0.f) || !(2.0 * c.d_v < c.width)) return fail(VG_EINVAL, "d_v: must satisfy 0 < d_v < width/2 (A9)");
+  if (!(c.d_r > 0.f) || !(2.0 * c.d_r < c.d_v)) return fail(VG_EINVAL, "d_r: must satisfy 0 < 2 d_r < d_v (S:214)");
+  if (!(c.fov > 0.f) || !(c.fov <= (float)(2.0 * PI))) return fail(VG_EINVAL, "fov: must satisfy 0 < fov <= 2 pi (S:149)");
+  const int ch = (c.env == VG_ENV_FLOCK) ? 1 : 2;
+  if (c.v < 1 || ch * c.v > vg::kMaxViewSlots) return fail(VG_EINVAL, "v: must satisfy 1 <= channels*v <= 128");
+  if (!(c.theta_max > 0.f) || !(c.theta_max <= (float)PI)) return fail(VG_EINVAL, "theta_max: must satisfy 0 < theta_max <= pi (S:214)");
+  if (!(c.s_max > 0.f) || !std::isfinite(c.s_max)) return fail(VG_EINVAL, "s_max: must be finite and > 0");
+  if (!(c.s_max < 0.5f * c.width)) return fail(VG_EINVAL, "s_max: must be < width/2");
+  if (c.env == VG_ENV_FLOCK) {
+    if (!(c.s_min >= 0.f) || !(c.s_min < c.s_max)) return fail(VG_EINVAL, "s_min: must satisfy 0 <= s_min < s_max (S:214)");
+    if (!(c.a_max > 0.f) || !std::isfinite(c.a_max)) return fail(VG_EINVAL, "a_max: must be finite and > 0 (S:214)");
+  } else {
+    if (c.n_chasers < 0 || c.n_chasers > c.n_agents) return fail(VG_EINVAL, "n_chasers: must satisfy 0 <= n_chasers <= n_agents");
+    if (!(c.s_max_chaser > 0.f) || !(c.s_max_chaser < 0.5f * c.width)) return fail(VG_EINVAL, "s_max_chaser: must satisfy 0 < s_max_chaser < width/2");
+    if (!(c.r_touch >= 0.f) || !std::isfinite(c.r_touch) || c.r_touch > 1e6f) return fail(VG_EINVAL, "r_touch: must be in [0, 1e6]");
+    if (!(c.w_prox >= 0.f) || !std::isfinite(c.w_prox)) return fail(VG_EINVAL, "w_prox: must be finite and >= 0");
+  }
+  if (!(c.c_collide > 0.f) || !std::isfinite(c.c_collide) || c.c_collide > 1e6f) return fail(VG_EINVAL, "c_collide: must be in (0, 1e6]");
+  if (!(c.c_near > 0.f) || !std::isfinite(c.c_near) || c.c_near > 1e6f) return fail(VG_EINVAL, "c_near: must be in (0, 1e6]");
+  if (!(c.d_peak > 2.f * c.d_r) || !(c.d_peak < c.d_v)) return fail(VG_EINVAL, "d_peak: must satisfy 2 d_r < d_peak < d_v (A5)");
+  int g = c.grid;
+  const double need = (double)c.d_v * (1.0 + std::ldexp(1.0, -12));
+  if (g == 0) g = auto_grid(c.width, c.d_v);
+  if (g < 3) return fail(VG_EINVAL, "grid: G = %d, need G >= 3 (3x3 stencil must not alias)", g);
+  if ((double)c.width / g < need) return fail(VG_EINVAL, "grid: cell size L/G = %g must be >= d_v (1 + 2^-12) = %g (A16)", (double)c.width / g, need);
+  if ((long long)g * g * c.n_replicas >= (1LL << 31)) return fail(VG_EINVAL, "grid: n_replicas * G^2 must be < 2^31");
+  *grid_out = g;
+  return VG_OK;
+}
+
+vg::Params derive(const vg_config& c, int g) {
+  vg::Params P{};
+  P.env = c.env;
+  P.N = c.n_agents;
+  P.R = c.n_replicas;
+  P.G = g;
+  P.G2 = g * g;
+  P.v = c.v;
+  P.channels = (c.env == VG_ENV_FLOCK) ? 1 : 2;
+  P.view_slots = P.channels * c.v;
+  P.obs_dim = P.view_slots + ((c.env == VG_ENV_FLOCK) ? 1 : 0);
+  P.occ_words = (P.view_slots + 31) / 32;
+  P.first_chaser = (c.env == VG_ENV_TAG) ? c.n_agents - c.n_chasers : c.n_agents;
+  P.total = (long long)c.n_agents * c.n_replicas;
+  // fp32 constants (A12): each is one correctly rounded fp32 operation on fp32 inputs.
+  volatile float L = c.width;
+  P.L = L;
+  P.half_L = L * 0.5f;
+  P.gs = (float)g / L;                              // RN32(G/L)  (A16)
+  P.two_pi = (float)(2.0 * 3.14159265358979323846);  // RN32(2 pi)
+  P.s_min = c.s_min;
+  P.s_max = c.s_max;
+  P.a_max = c.a_max;
+  P.theta_max = c.theta_max;
+  P.s_max_chaser = c.s_max_chaser;
+  P.d_v = c.d_v;
+  volatile float dv = c.d_v;
+  P.dv2 = dv * dv;
+  P.inv_dv = 1.0f / dv;
+  P.two_dr = 2.0f * c.d_r;
+  volatile float tdr = P.two_dr;
+  P.contact2 = tdr * tdr;
+  P.half_fov = 0.5f * c.fov;
+  P.inv_fov = 1.0f / c.fov;
+  P.fv = (float)c.v;
+  P.c_collide = c.c_collide;
+  P.d_peak = c.d_peak;
+  P.k_rise = c.c_near / (c.d_peak - P.two_dr);
+  P.k_fall = c.c_near / (c.d_v - c.d_peak);
+  P.w_prox = c.w_prox;
+  P.touch_fix = (long long)std::llrint((double)c.r_touch * 4294967296.0);
+  return P;
+}
+
+inline cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s); }
+
+// Record phase boundary `k` of the current profiled step (no-op when not profiling).
+inline void prof_mark(vg_world* w, int k, cudaStream_t s) {
+  if (w->prof_n < w->prof_max) cudaEventRecord(w->prof_ev[(size_t)w->prof_n * (VG_N_PHASES + 1) + k], s);
+}
+
+vg_status check_pending(const vg_world* w) {
+  if (*reinterpret_cast<volatile uint32_t*>(w->err_flag))
+    return fail(VG_ESTATE, "device-side state error pending; call vg_sync_errors for the agent index");
+  return VG_OK;
+}
+
+vg_status launch_check(const char* what) {
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return fail(VG_ECUDA, "%s launch: %s", what, cudaGetErrorString(e));
+  return VG_OK;
+}
+
+template <int ENV, bool INTEGRATE, bool BIN>
+vg_status launch_k1(vg_world* w, float4* io, const float4* in, const float2* act, cudaStream_t s) {
+  const long long n = w->P.total;
+  const unsigned blocks = (unsigned)((n + 255) / 256);
+  vg::k_integrate_bin<ENV, INTEGRATE, BIN><<<blocks, 256, 0, s>>>(
+      w->P, io, in, act, w->cell_id, w->slot, w->count, w->err_dev, w->err_flag);
+  return launch_check("k_integrate_bin");
+}
+
+template <int ENV>
+vg_status bin_rest(vg_world* w, const float4* state, cudaStream_t s, bool prof = false) {
+  const long long n = w->P.total;
+  vg::k_scan_cells<<<1, 1024, 0, s>>>(w->count, w->cell_start, w->n_cells);
+  if (vg_status st = launch_check("k_scan_cells")) return st;
+  if (prof) prof_mark(w, 2, s);
+  vg::k_scatter<ENV><<<(unsigned)((n + 255) / 256), 256, 0, s>>>(
+      w->P, state, w->cell_id, w->slot, w->cell_start, w->tmp_rec, w->tmp_id);
+  if (vg_status st = launch_check("k_scatter")) return st;
+  if (prof) prof_mark(w, 3, s);
+  const long long threads = (long long)w->n_cells * 32;
+  vg::k_cell_sort<<<(unsigned)((threads + 255) / 256), 256, 0, s>>>(
+      w->n_cells, w->cell_start, w->tmp_rec, w->tmp_id, w->sorted, w->perm);
+  if (vg_status st = launch_check("k_cell_sort")) return st;
+  if (prof) prof_mark(w, 4, s);
+  w->binned = true;
+  return VG_OK;
+}
+
+vg::Outs to_outs(const vg_outputs* o) {
+  vg::Outs r{};
+  if (o) {
+    r.obs = o->obs;
+    r.reward = o->reward;
+    r.n_neigh = o->n_neigh;
+    r.n_collide = o->n_collide;
+    r.n_touch = o->n_touch;
+    r.occ = o->sector_occ;
+  }
+  return r;
+}
+
+template <bool VISION>
+vg_status launch_sense(vg_world* w, const vg_outputs* outs, cudaStream_t s) {
+  const vg::Outs O = to_outs(outs);
+  if (w->P.env == vg::kFlock)
+    vg::k_sense<vg::kFlock, VISION><<<w->n_cells, vg::kSenseWarps * 32, 0, s>>>(
+        w->P, w->cell_start, w->sorted, w->perm, O);
+  else
+    vg::k_sense<vg::kTag, VISION><<<w->n_cells, vg::kSenseWarps * 32, 0, s>>>(
+        w->P, w->cell_start, w->sorted, w->perm, O);
+  return launch_check("k_sense");
+}
+
+template <typename T>
+vg_status dalloc(vg_world* w, T** p, size_t n) {
+  const size_t bytes = n * sizeof(T);
+  cudaError_t e = cudaMalloc(reinterpret_cast<void**>(p), bytes > 0 ? bytes : 16);
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    return fail(VG_ENOMEM, "cudaMalloc(%zu bytes): %s", bytes, cudaGetErrorString(e));
+  }
+  w->scratch_bytes += bytes;
+  return VG_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int32_t vg_abi_version(void) { return VG_ABI_VERSION; }
+
+const char* vg_last_error(void) { return g_err; }
+
+vg_status vg_world_create(const vg_config* cfg, vg_world** out) {
+  g_err[0] = 0;
+  if (!out) return fail(VG_EINVAL, "out: NULL");
+  *out = nullptr;
+  if (!cfg) return fail(VG_EINVAL, "cfg: NULL");
+  int g = 0;
+  if (vg_status st = validate(*cfg, &g)) return st;
+  vg_world* w = new (std::nothrow) vg_world();
+  if (!w) return fail(VG_ENOMEM, "host allocation failed");
+  w->cfg = *cfg;
+  w->P = derive(*cfg, g);
+  w->n_cells = g * g * cfg->n_replicas;
+  cudaGetDevice(&w->device);
+  const size_t n = (size_t)w->P.total;
+  vg_status st = VG_OK;
+  if (!st) st = dalloc(w, &w->count, w->n_cells);
+  if (!st) st = dalloc(w, &w->cell_start, w->n_cells + 1);
+  if (!st) st = dalloc(w, &w->cell_id, n);
+  if (!st) st = dalloc(w, &w->slot, n);
+  if (!st) st = dalloc(w, &w->tmp_id, n);
+  if (!st) st = dalloc(w, &w->perm, n);
+  if (!st) st = dalloc(w, &w->tmp_rec, n);
+  if (!st) st = dalloc(w, &w->sorted, n);
+  if (!st) st = dalloc(w, &w->act_dev, n);
+  if (!st) st = dalloc(w, &w->err_dev, 1);
+  if (!st) {
+    cudaError_t e = cudaHostAlloc(reinterpret_cast<void**>(&w->err_flag), sizeof(uint32_t),
+                                  cudaHostAllocMapped);
+    if (e != cudaSuccess) st = fail(VG_ECUDA, "cudaHostAlloc(flag): %s", cudaGetErrorString(e));
+  }
+  if (!st) {
+    *w->err_flag = 0;
+    const unsigned long long none = ~0ull;
+    cudaError_t e = cudaMemset(w->count, 0, sizeof(uint32_t) * w->n_cells);
+    if (e == cudaSuccess) e = cudaMemcpy(w->err_dev, &none, sizeof(none), cudaMemcpyHostToDevice);
+    if (e != cudaSuccess) st = fail(VG_ECUDA, "world init: %s", cudaGetErrorString(e));
+  }
+  if (st) {
+    vg_world_destroy(w);
+    return st;
+  }
+  *out = w;
+  return VG_OK;
+}
+
+void vg_world_destroy(vg_world* w) {
+  if (!w) return;
+  for (cudaEvent_t e : w->prof_ev) cudaEventDestroy(e);
+  cudaFree(w->count);
+  cudaFree(w->cell_start);
+  cudaFree(w->cell_id);
+  cudaFree(w->slot);
+  cudaFree(w->tmp_id);
+  cudaFree(w->perm);
+  cudaFree(w->tmp_rec);
+  cudaFree(w->sorted);
+  cudaFree(w->act_dev);
+  cudaFree(w->err_dev);
+  if (w->err_flag) cudaFreeHost(w->err_flag);
+  delete w;
+}
+
+vg_status vg_world_query(const vg_world* w, vg_world_info* info) {
+  if (!w || !info) return fail(VG_EINVAL, "world/info: NULL");
+  info->grid = w->P.G;
+  info->cell_size = w->cfg.width / (float)w->P.G;
+  info->n_cells = w->n_cells;
+  info->obs_dim = w->P.obs_dim;
+  info->channels = w->P.channels;
+  info->occ_words = w->P.occ_words;
+  info->total_agents = w->P.total;
+  info->scratch_bytes = (int64_t)w->scratch_bytes;
+  return VG_OK;
+}
+
+vg_status vg_bin(vg_world* w, const float* state, void* stream) {
+  if (!w || !state) return fail(VG_EINVAL, "world/state: NULL");
+  if (vg_status st = check_pending(w)) return st;
+  cudaStream_t s = as_stream(stream);
+  const float4* in = reinterpret_cast<const float4*>(state);
+  if (w->P.env == vg::kFlock) {
+    if (vg_status st = launch_k1<vg::kFlock, false, true>(w, nullptr, in, nullptr, s)) return st;
+    return bin_rest<vg::kFlock>(w, in, s);
+  }
+  if (vg_status st = launch_k1<vg::kTag, false, true>(w, nullptr, in, nullptr, s)) return st;
+  return bin_rest<vg::kTag>(w, in, s);
+}
+
+vg_status vg_sense(vg_world* w, const vg_outputs* outs, void* stream) {
+  if (!w || !outs) return fail(VG_EINVAL, "world/outs: NULL");
+  if (!w->binned) return fail(VG_EINVAL, "vg_sense: no binned state (call vg_bin or vg_step first)");
+  if (vg_status st = check_pending(w)) return st;
+  return launch_sense<true>(w, outs, as_stream(stream));
+}
+
+vg_status vg_reward(vg_world* w, const vg_outputs* outs, void* stream) {
+  if (!w || !outs) return fail(VG_EINVAL, "world/outs: NULL");
+  if (!w->binned) return fail(VG_EINVAL, "vg_reward: no binned state (call vg_bin or vg_step first)");
+  if (vg_status st = check_pending(w)) return st;
+  vg_outputs o = *outs;
+  o.obs = nullptr;
+  o.sector_occ = nullptr;
+  return launch_sense<false>(w, &o, as_stream(stream));
+}
+
+vg_status vg_integrate(vg_world* w, float* state, const float* actions, void* stream) {
+  if (!w || !state || !actions) return fail(VG_EINVAL, "world/state/actions: NULL");
+  if (vg_status st = check_pending(w)) return st;
+  cudaStream_t s = as_stream(stream);
+  float4* io = reinterpret_cast<float4*>(state);
+  const float2* a = reinterpret_cast<const float2*>(actions);
+  w->binned = false;   // the binned snapshot no longer matches state
+  if (w->P.env == vg::kFlock) return launch_k1<vg::kFlock, true, false>(w, io, nullptr, a, s);
+  return launch_k1<vg::kTag, true, false>(w, io, nullptr, a, s);
+}
+
+vg_status vg_step(vg_world* w, float* state, const float* actions, const vg_outputs* outs,
+                  void* stream) {
+  if (!w || !state || !actions || !outs) return fail(VG_EINVAL, "world/state/actions/outs: NULL");
+  if (vg_status st = check_pending(w)) return st;
+  cudaStream_t s = as_stream(stream);
+  float4* io = reinterpret_cast<float4*>(state);
+  const float2* a = reinterpret_cast<const float2*>(actions);
+  prof_mark(w, 0, s);
+  if (w->P.env == vg::kFlock) {
+    if (vg_status st = launch_k1<vg::kFlock, true, true>(w, io, nullptr, a, s)) return st;
+    prof_mark(w, 1, s);
+    if (vg_status st = bin_rest<vg::kFlock>(w, io, s, true)) return st;
+  } else {
+    if (vg_status st = launch_k1<vg::kTag, true, true>(w, io, nullptr, a, s)) return st;
+    prof_mark(w, 1, s);
+    if (vg_status st = bin_rest<vg::kTag>(w, io, s, true)) return st;
+  }
+  vg_status st = launch_sense<true>(w, outs, s);
+  prof_mark(w, 5, s);
+  if (w->prof_n < w->prof_max) ++w->prof_n;
+  return st;
+}
+
+vg_status vg_step_host(vg_world* w, float* state, const float* actions_host,
+                       const vg_outputs* outs, float* reward_host, void* stream) {
+  if (!w || !state || !actions_host || !outs) return fail(VG_EINVAL, "world/state/actions_host/outs: NULL");
+  if (reward_host && !outs->reward) return fail(VG_EINVAL, "reward_host: needs outs->reward");
+  cudaStream_t s = as_stream(stream);
+  VG_CUDA(cudaMemcpyAsync(w->act_dev, actions_host, sizeof(float2) * (size_t)w->P.total,
+                          cudaMemcpyHostToDevice, s));
+  if (vg_status st = vg_step(w, state, reinterpret_cast<const float*>(w->act_dev), outs, stream)) return st;
+  if (reward_host)
+    VG_CUDA(cudaMemcpyAsync(reward_host, outs->reward, sizeof(float) * (size_t)w->P.total,
+                            cudaMemcpyDeviceToHost, s));
+  return VG_OK;
+}
+
+vg_status vg_get_bins(const vg_world* w, const uint32_t** cell_id, const uint32_t** cell_start,
+                      const uint32_t** perm, const float** sorted) {
+  if (!w) return fail(VG_EINVAL, "world: NULL");
+  if (!w->binned) return fail(VG_EINVAL, "vg_get_bins: no binned state");
+  if (cell_id) *cell_id = w->cell_id;
+  if (cell_start) *cell_start = w->cell_start;
+  if (perm) *perm = w->perm;
+  if (sorted) *sorted = reinterpret_cast<const float*>(w->sorted);
+  return VG_OK;
+}
+
+vg_status vg_profile_begin(vg_world* w, int32_t max_steps) {
+  if (!w || max_steps < 0 || max_steps > (1 << 20)) return fail(VG_EINVAL, "world/max_steps");
+  const size_t need = (size_t)max_steps * (VG_N_PHASES + 1);
+  while (w->prof_ev.size() < need) {
+    cudaEvent_t e;
+    VG_CUDA(cudaEventCreate(&e));
+    w->prof_ev.push_back(e);
+  }
+  w->prof_max = max_steps;
+  w->prof_n = 0;
+  return VG_OK;
+}
+
+vg_status vg_profile_end(vg_world* w, void* stream, double* phase_ms, int32_t* n_steps) {
+  if (!w || !phase_ms) return fail(VG_EINVAL, "world/phase_ms: NULL");
+  VG_CUDA(cudaStreamSynchronize(as_stream(stream)));
+  for (int k = 0; k < VG_N_PHASES; ++k) phase_ms[k] = 0.0;
+  for (int i = 0; i < w->prof_n; ++i) {
+    for (int k = 0; k < VG_N_PHASES; ++k) {
+      float ms = 0.f;
+      VG_CUDA(cudaEventElapsedTime(&ms, w->prof_ev[(size_t)i * (VG_N_PHASES + 1) + k],
+                                   w->prof_ev[(size_t)i * (VG_N_PHASES + 1) + k + 1]));
+      phase_ms[k] += ms;
+    }
+  }
+  if (n_steps) *n_steps = w->prof_n;
+  w->prof_max = 0;
+  w->prof_n = 0;
+  return VG_OK;
+}
+
+vg_status vg_sync_errors(vg_world* w, void* stream, int64_t* bad_agent) {
+  if (!w) return fail(VG_EINVAL, "world: NULL");
+  VG_CUDA(cudaStreamSynchronize(as_stream(stream)));
+  unsigned long long v = 0;
+  VG_CUDA(cudaMemcpy(&v, w->err_dev, sizeof(v), cudaMemcpyDeviceToHost));
+  if (bad_agent) *bad_agent = (v == ~0ull) ? -1 : (int64_t)v;
+  if (v != ~0ull) {
+    const unsigned long long none = ~0ull;
+    VG_CUDA(cudaMemcpy(w->err_dev, &none, sizeof(none), cudaMemcpyHostToDevice));
+    *w->err_flag = 0;
+    return fail(VG_ESTATE, "invalid state or action at global agent index %llu", v);
+  }
+  return VG_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,394 @@
+// vg_kernels.cuh — sm_100a device kernels of the Vogue environment step.
+//
+// Citations: P:n = PAPER.md line n, S:n = SPEC.md line n, An = reading in DESIGN.md §3.
+// Pipeline of one step:
+//   K1 k_integrate_bin  integrate + cell id + per-cell histogram slot   (HBM-bound)
+//   K2 k_scan_cells     exclusive scan of the R*G*G cell counts          (latency)
+//   K3 k_scatter        place each agent at cell_start[cell] + slot      (HBM-bound)
+//   K3b k_cell_sort     order each cell by ascending agent id (stable)   (HBM-bound)
+//   K4 k_sense          3x3-stencil neighbour pass: sector vision + reward (FP32/issue-bound)
+// No library kernels: every step of the path runs here.
+#pragma once
+
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace vg {
+
+constexpr int kFlock = 0;
+constexpr int kTag = 1;
+constexpr uint32_t kOneBits = 0x3f800000u;          // 1.0f: "nothing in this sector" (A2)
+constexpr float kBelowOne = 0.99999994f;            // largest float < 1: an occupied sector
+constexpr float kFix = 4294967296.0f;               // 2^32: fixed-point reward unit (A16b)
+constexpr float kFixInv = 2.3283064365386963e-10f;  // 2^-32
+constexpr int kMaxViewSlots = 128;                  // channels * v <= 128
+constexpr unsigned kFull = 0xffffffffu;
+
+// Device copy of the configuration + derived fp32 constants (computed once on the host,
+// DESIGN.md §4.0).  Passed by value to every kernel.
+struct Params {
+  int env, N, R, G, G2, v, channels, view_slots, obs_dim, occ_words, first_chaser;
+  long long total;             // R * N
+  float L, half_L, gs;         // gs = RN32(G / L)   (A16)
+  float two_pi;                // RN32(2 pi): heading range [0, two_pi)   (A10)
+  float s_min, s_max, a_max, theta_max, s_max_chaser;
+  float d_v, dv2, inv_dv, contact2, two_dr;
+  float half_fov, inv_fov, fv;  // fov/2, 1/fov, float(v)
+  float c_collide, d_peak, k_rise, k_fall, w_prox;
+  long long touch_fix;         // r_touch * 2^32
+};
+
+struct Outs {
+  float* obs;
+  float* reward;
+  uint32_t* n_neigh;
+  uint32_t* n_collide;
+  uint32_t* n_touch;
+  uint32_t* occ;
+};
+
+// Record the smallest offending global agent index (S:59 error convention) and raise the
+// host-visible flag (mapped pinned memory, plain store).
+__device__ __forceinline__ void report_bad(unsigned long long* err, volatile uint32_t* flag,
+                                           unsigned long long gi) {
+  atomicMin(err, gi);
+  *flag = 1u;
+}
+
+// Torus wrap of x + dx for x in [0, L), |dx| < L/2 (A10): the subtraction x - L is exact
+// (Sterbenz), so a result that wraps to near 0 keeps full relative precision.
+__device__ __forceinline__ float wrap_pos(float x, float dx, float L) {
+  float t = __fadd_rn(x, dx);
+  if (t >= L) {
+    t = __fadd_rn(__fsub_rn(x, L), dx);
+    if (t < 0.f) t = 0.f;                 // exact sum was just below L: the point is L^- == 0
+  } else if (t < 0.f) {
+    t = __fadd_rn(t, L);
+    if (t >= L) t = 0.f;                  // rounded up to L: the point is 0^-
+  }
+  return t;
+}
+
+// Heading wrap into [0, two_pi) (A10; "heading normalized to [0, 2 pi)").
+__device__ __forceinline__ float wrap_heading(float th, float two_pi) {
+  if (th < 0.f) {
+    th = __fadd_rn(th, two_pi);
+    if (th >= two_pi) th = 0.f;
+  } else if (th >= two_pi) {
+    th = __fsub_rn(th, two_pi);           // exact (Sterbenz)
+  }
+  return th;
+}
+
+// ---------------------------------------------------------------------------------- K1
+// One thread per agent.  INTEGRATE: apply the action: rotate, then
+// (flock) accelerate with clamp(s + a, s_min, s_max) (A7), then move along the new heading
+// (A8), wrapping on the torus.  BIN: cell id cx = min(G-1, floor(RN32(x * gs))) (A16) and
+// an atomic per-(replica, cell) histogram whose return value is the agent's arrival slot.
+template <int ENV, bool INTEGRATE, bool BIN>
+__global__ void __launch_bounds__(256) k_integrate_bin(
+    Params P, float4* __restrict__ state_io, const float4* __restrict__ state_in,
+    const float2* __restrict__ actions, uint32_t* __restrict__ cell_id,
+    uint32_t* __restrict__ slot, uint32_t* __restrict__ count,
+    unsigned long long* __restrict__ err, volatile uint32_t* flag) {
+  const long long gi = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (gi >= P.total) return;
+  const int r = (int)(gi / P.N);
+  const int i = (int)(gi - (long long)r * P.N);
+  float4 s = INTEGRATE ? state_io[gi] : state_in[gi];
+
+  // State invariants: position in [0, L), heading in [0, 2 pi), finite speed.
+  bool bad = !(s.x >= 0.f && s.x < P.L && s.y >= 0.f && s.y < P.L && s.z >= 0.f &&
+               s.z < P.two_pi);
+  if (ENV == kFlock) bad |= !isfinite(s.w);
+
+  if (INTEGRATE) {
+    const float2 a = actions[gi];
+    bad |= isnan(a.x) || isnan(a.y);
+    float turn, dist;
+    if (ENV == kFlock) {
+      const float acc = fminf(fmaxf(a.x, -P.a_max), P.a_max);      // S:257 clamp
+      turn = fminf(fmaxf(a.y, -P.theta_max), P.theta_max);
+      const float sp = fminf(fmaxf(__fadd_rn(s.w, acc), P.s_min), P.s_max);  // A7
+      s.w = sp;
+      dist = sp;
+    } else {
+      turn = fminf(fmaxf(a.x, -P.theta_max), P.theta_max);
+      const float smax = (i >= P.first_chaser) ? P.s_max_chaser : P.s_max;
+      dist = fminf(fmaxf(a.y, 0.f), smax);
+    }
+    s.z = wrap_heading(__fadd_rn(s.z, turn), P.two_pi);
+    float sn, cs;
+    sincosf(s.z, &sn, &cs);
+    s.x = wrap_pos(s.x, __fmul_rn(dist, cs), P.L);
+    s.y = wrap_pos(s.y, __fmul_rn(dist, sn), P.L);
+    state_io[gi] = s;
+  }
+  if (bad) report_bad(err, flag, (unsigned long long)gi);
+
+  if (BIN) {
+    int cx = __float2int_rz(__fmul_rn(s.x, P.gs));
+    int cy = __float2int_rz(__fmul_rn(s.y, P.gs));
+    cx = min(max(cx, 0), P.G - 1);        // clamps also keep a bad state memory-safe
+    cy = min(max(cy, 0), P.G - 1);
+    const uint32_t c = (uint32_t)(cy * P.G + cx);
+    cell_id[gi] = c;
+    slot[gi] = atomicAdd(&count[(size_t)r * P.G2 + c], 1u);
+  }
+}
+
+// ---------------------------------------------------------------------------------- K2
+// Exclusive scan of n counts into start[0..n] (start[n] = total) and re-zero the counts
+// for the next binning.  One CTA of 1024 threads, each owning a contiguous chunk.
+__global__ void __launch_bounds__(1024) k_scan_cells(uint32_t* __restrict__ count,
+                                                      uint32_t* __restrict__ start, int n) {
+  __shared__ uint32_t warp_sums[32];
+  __shared__ uint32_t total_s;
+  const int t = threadIdx.x, lane = t & 31, w = t >> 5;
+  const int per = (n + blockDim.x - 1) / blockDim.x;
+  const int b = min(n, t * per), e = min(n, b + per);
+  uint32_t sum = 0;
+  for (int k = b; k < e; ++k) sum += count[k];
+  uint32_t inc = sum;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint32_t y = __shfl_up_sync(kFull, inc, o);
+    if (lane >= o) inc += y;
+  }
+  if (lane == 31) warp_sums[w] = inc;
+  __syncthreads();
+  if (w == 0) {
+    uint32_t ws = (lane < (int)(blockDim.x >> 5)) ? warp_sums[lane] : 0u;
+    uint32_t wi = ws;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t y = __shfl_up_sync(kFull, wi, o);
+      if (lane >= o) wi += y;
+    }
+    warp_sums[lane] = wi - ws;
+    if (lane == 31) total_s = wi;
+  }
+  __syncthreads();
+  uint32_t run = warp_sums[w] + inc - sum;
+  for (int k = b; k < e; ++k) {
+    const uint32_t c = count[k];
+    start[k] = run;
+    run += c;
+    count[k] = 0u;
+  }
+  if (t == 0) start[n] = total_s;
+}
+
+// ---------------------------------------------------------------------------------- K3
+// Place each agent's record at cell_start[cell] + slot (arrival order within a cell).
+template <int ENV>
+__global__ void __launch_bounds__(256) k_scatter(
+    Params P, const float4* __restrict__ state, const uint32_t* __restrict__ cell_id,
+    const uint32_t* __restrict__ slot, const uint32_t* __restrict__ cell_start,
+    float4* __restrict__ tmp_rec, uint32_t* __restrict__ tmp_id) {
+  const long long gi = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (gi >= P.total) return;
+  const int r = (int)(gi / P.N);
+  const int i = (int)(gi - (long long)r * P.N);
+  const uint32_t pos = cell_start[(size_t)r * P.G2 + cell_id[gi]] + slot[gi];
+  float4 s = state[gi];
+  if (ENV == kTag) s.w = (i >= P.first_chaser) ? 1.f : 0.f;   // type in the sorted record
+  tmp_rec[pos] = s;
+  tmp_id[pos] = (uint32_t)i;
+}
+
+// --------------------------------------------------------------------------------- K3b
+// One warp per cell: rank each member by agent id (ids are unique within a replica) and
+// write it to its stable slot ("ascending order (determinism anchor)").
+__global__ void __launch_bounds__(256) k_cell_sort(
+    int n_cells, const uint32_t* __restrict__ cell_start, const float4* __restrict__ tmp_rec,
+    const uint32_t* __restrict__ tmp_id, float4* __restrict__ sorted,
+    uint32_t* __restrict__ perm) {
+  const int cell = (int)(((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5);
+  const int lane = threadIdx.x & 31;
+  if (cell >= n_cells) return;
+  const uint32_t b = cell_start[cell];
+  const int m = (int)(cell_start[cell + 1] - b);
+  for (int base = 0; base < m; base += 32) {
+    const int idx = base + lane;
+    const bool valid = idx < m;
+    const uint32_t id = valid ? tmp_id[b + idx] : 0xffffffffu;
+    int rank = 0;
+    for (int jb = 0; jb < m; jb += 32) {
+      const uint32_t other = (jb + lane < m) ? tmp_id[b + jb + lane] : 0xffffffffu;
+#pragma unroll 8
+      for (int t = 0; t < 32; ++t) rank += (__shfl_sync(kFull, other, t) < id) ? 1 : 0;
+    }
+    if (valid) {
+      sorted[b + rank] = tmp_rec[b + idx];
+      perm[b + rank] = id;
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------------- K4
+// One CTA per (replica, cell); warp w handles the cell's query agents w, w+W, ...  Each
+// query scans the 3x3 cell stencil (<= 6 contiguous sorted segments) for neighbours
+// within d_v, compacts them with ballot/popc into a per-warp queue, and
+// processes 32 at a time: contact test, reward term (fixed point, A16b), bearing, sector
+// and per-sector nearest distance by shared-memory atomicMin on the float bits (A2, A3).
+constexpr int kSenseWarps = 4;
+
+template <int ENV, bool VISION>
+__global__ void __launch_bounds__(kSenseWarps * 32) k_sense(
+    Params P, const uint32_t* __restrict__ cell_start, const float4* __restrict__ sorted,
+    const uint32_t* __restrict__ perm, Outs O) {
+  __shared__ uint32_t s_min[kSenseWarps][kMaxViewSlots];
+  __shared__ float4 s_q[kSenseWarps][64];
+  __shared__ uint32_t s_seg[12];
+  __shared__ int s_nseg;
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int c = blockIdx.x;
+  const int r = c / P.G2;
+  const int cl = c - r * P.G2;
+  const int cy = cl / P.G, cx = cl - cy * P.G;
+  const uint32_t* cs = cell_start + (size_t)r * P.G2;
+
+  if (threadIdx.x == 0) {
+    int ns = 0;
+    for (int dy = -1; dy <= 1; ++dy) {
+      int yy = cy + dy;
+      yy += (yy < 0) ? P.G : 0;
+      yy -= (yy >= P.G) ? P.G : 0;
+      const int row = yy * P.G;
+      if (cx >= 1 && cx <= P.G - 2) {
+        s_seg[2 * ns] = cs[row + cx - 1]; s_seg[2 * ns + 1] = cs[row + cx + 2]; ++ns;
+      } else if (cx == 0) {                       // cells G-1 | 0, 1
+        s_seg[2 * ns] = cs[row + P.G - 1]; s_seg[2 * ns + 1] = cs[row + P.G]; ++ns;
+        s_seg[2 * ns] = cs[row]; s_seg[2 * ns + 1] = cs[row + 2]; ++ns;
+      } else {                                    // cells G-2, G-1 | 0
+        s_seg[2 * ns] = cs[row + P.G - 2]; s_seg[2 * ns + 1] = cs[row + P.G]; ++ns;
+        s_seg[2 * ns] = cs[row]; s_seg[2 * ns + 1] = cs[row + 1]; ++ns;
+      }
+    }
+    s_nseg = ns;
+  }
+  __syncthreads();
+  const int nseg = s_nseg;
+  const uint32_t qb = cs[cl], qe = cs[cl + 1];
+  const unsigned lt_mask = (1u << lane) - 1u;
+  uint32_t* my_min = s_min[warp];
+  float4* my_q = s_q[warp];
+
+  for (uint32_t q = qb + warp; q < qe; q += kSenseWarps) {
+    const float4 me = sorted[q];
+    const int tq = (ENV == kTag) ? (int)me.w : 0;
+    float sn = 0.f, csn = 0.f;
+    if (VISION) {
+      sincosf(me.z, &sn, &csn);
+      for (int k = lane; k < P.view_slots; k += 32) my_min[k] = kOneBits;
+    }
+    uint32_t nn = 0, ncol = 0, ntouch = 0;
+    long long rs = 0;
+    int nq = 0;
+    __syncwarp();
+
+    auto process = [&](const float4 e) {
+      const float d2 = e.z;
+      const bool contact = d2 <= P.contact2;                       // A6 (inclusive)
+      const float d = sqrtf(d2);
+      const int tj = (ENV == kTag) ? (int)e.w : 0;
+      // Eq. 1 / Fig. 4 (A5): -c_collide at contact, else rising then falling bonus.
+      const float f = contact ? -P.c_collide
+                              : ((d <= P.d_peak) ? P.k_rise * (d - P.two_dr)
+                                                 : P.k_fall * (P.d_v - d));
+      if (ENV == kFlock) {
+        rs += __float2ll_rn(f * kFix);
+        ncol += contact ? 1u : 0u;
+      } else {
+        if (contact) {
+          if (tj == tq) ++ncol; else ++ntouch;
+        }
+        if (tq == 0 && tj == 0) rs += __float2ll_rn((P.w_prox * f) * kFix);
+      }
+      if (VISION) {
+        // Bearing in the agent frame (A3): phi = atan2(h x d, h . d), CCW-positive.
+        const float fwd = csn * e.x + sn * e.y;
+        const float left = csn * e.y - sn * e.x;
+        const float phi = atan2f(left, fwd);
+        const float u = (phi + P.half_fov) * P.inv_fov;           // fraction of the fov
+        if (u >= 0.f && u < 1.f) {
+          const int k = min((int)(u * P.fv), P.v - 1);
+          const float val = fminf(d * P.inv_dv, kBelowOne);
+          atomicMin(&my_min[tj * P.v + k], __float_as_uint(val));
+        }
+      }
+    };
+
+    for (int sgi = 0; sgi < nseg; ++sgi) {
+      const uint32_t sb = s_seg[2 * sgi], se = s_seg[2 * sgi + 1];
+      for (uint32_t p0 = sb; p0 < se; p0 += 32) {
+        const uint32_t p = p0 + lane;
+        const bool valid = p < se;
+        float4 o = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (valid) o = __ldg(&sorted[p]);
+        // Minimal image with Sterbenz ordering (A11).
+        float dx = o.x - me.x;
+        if (dx > P.half_L) dx = (o.x - P.L) - me.x;
+        else if (dx < -P.half_L) dx = o.x - (me.x - P.L);
+        float dy = o.y - me.y;
+        if (dy > P.half_L) dy = (o.y - P.L) - me.y;
+        else if (dy < -P.half_L) dy = o.y - (me.y - P.L);
+        const float d2 = dx * dx + dy * dy;
+        const bool in = valid && (p != q) && (d2 < P.dv2);          // Eq. 1: d < d_v
+        const unsigned bal = __ballot_sync(kFull, in);
+        if (in) my_q[nq + __popc(bal & lt_mask)] = make_float4(dx, dy, d2, o.w);
+        const int cnt = __popc(bal);
+        nq += cnt;
+        nn += (uint32_t)cnt;
+        if (nq >= 32) {
+          __syncwarp();
+          process(my_q[lane]);
+          __syncwarp();
+          if (lane < nq - 32) my_q[lane] = my_q[lane + 32];
+          __syncwarp();
+          nq -= 32;
+        }
+      }
+    }
+    __syncwarp();
+    if (lane < nq) process(my_q[lane]);
+
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      ncol += __shfl_xor_sync(kFull, ncol, o);
+      if (ENV == kTag) ntouch += __shfl_xor_sync(kFull, ntouch, o);
+      rs += __shfl_xor_sync(kFull, rs, o);
+    }
+    if (ENV == kTag) {
+      const long long t = (long long)ntouch * P.touch_fix;
+      rs += (tq == 1) ? t : -t;                                     // P:194 touch rule
+    }
+    const size_t row = (size_t)r * P.N + perm[q];
+    if (lane == 0) {
+      if (O.reward) O.reward[row] = __ll2float_rn(rs) * kFixInv;
+      if (O.n_neigh) O.n_neigh[row] = nn;
+      if (O.n_collide) O.n_collide[row] = ncol;
+      if (ENV == kTag && O.n_touch) O.n_touch[row] = ntouch;
+    }
+    if (VISION) {
+      __syncwarp();
+      if (O.obs) {
+        float* orow = O.obs + row * (size_t)P.obs_dim;
+        for (int k = lane; k < P.view_slots; k += 32) orow[k] = __uint_as_float(my_min[k]);
+        if (ENV == kFlock && lane == 0) orow[P.view_slots] = __fdiv_rn(me.w, P.s_max);  // A24
+      }
+      if (O.occ) {
+        for (int w = 0; w < P.occ_words; ++w) {
+          const int k = 32 * w + lane;
+          const unsigned bits = __ballot_sync(kFull, k < P.view_slots && my_min[k] < kOneBits);
+          if (lane == 0) O.occ[row * (size_t)P.occ_words + w] = bits;
+        }
+      }
+    }
+    __syncwarp();
+  }
+}
+
+}  // namespace vg

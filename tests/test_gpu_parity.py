@@ -1,0 +1,323 @@
+"""GPU parity: the CUDA path (through the C ABI, via the ctypes binding) against the fp64
+oracle on the same seeded inputs, one step at a time (SURVEY.md §8c protocol): the oracle
+integrates the GPU's fp32 state of step t and senses the GPU's fp32 state of step t+1, so
+fp32/fp64 drift never compounds."""
+import math
+
+import numpy as np
+import pytest
+
+import oracle
+import vg_inputs as vi
+import vg_parity as parity
+
+pytestmark = pytest.mark.gpu
+
+
+def _torch():
+    import torch
+    return torch
+
+
+def dev(a):
+    torch = _torch()
+    return torch.from_numpy(np.ascontiguousarray(a)).cuda()
+
+
+def host(t):
+    return t.detach().cpu().numpy()
+
+
+def outs_np(out, r):
+    d = {}
+    for k in ("obs", "reward", "n_neigh", "n_collide", "n_touch", "sector_occ"):
+        t = getattr(out, k)
+        if t is not None:
+            a = host(t[r])
+            d[k] = a.view(np.uint32) if a.dtype == np.int32 else a
+    return d
+
+
+def make_world(p):
+    import paper_2207_03945_b200 as vg
+    return vg.World(p)
+
+
+def run_and_check(p, state0, n_steps, replicas=None, rows=None, seed=0, check_bins=True):
+    """Step the GPU world n_steps with seeded actions; check every step against the oracle."""
+    torch = _torch()
+    w = make_world(p)
+    out = w.alloc_outputs()
+    st = dev(state0)
+    stats = []
+    reps = range(p.n_replicas) if replicas is None else replicas
+    for t in range(n_steps):
+        prev = host(st)
+        act = vi.actions(p, seed=seed, step=t)
+        w.step(st, dev(act), out)
+        torch.cuda.synchronize()
+        assert w.sync_errors() == -1
+        cur = host(st)
+        ref_state = oracle.integrate(p, prev, act)
+        parity.check_integrate(p, cur, ref_state)
+        if check_bins:
+            bins = {k: host(v) for k, v in w.get_bins().items()}
+            parity.check_bins(p, bins, cur)
+        for r in reps:
+            stats.append(parity.check_sense(p, cur[r], outs_np(out, r), rows=rows))
+    w.close()
+    return stats
+
+
+def test_c1_100_steps(cuda):
+    # configs[0]: flock, 100 agents, 100 steps with seeded random actions — every row, step.
+    p = vi.workload("c1")
+    stats = run_and_check(p, vi.init_state(p, seed=0), 100)
+    assert sum(s["rows"] for s in stats) == 100 * 100
+
+
+def test_c2_flock_5000(cuda):
+    p = vi.workload("c2")
+    stats = run_and_check(p, vi.init_state(p, seed=0), 3)
+    print(stats)
+
+
+def test_c3_tag_10000(cuda):
+    p = vi.workload("c3")
+    stats = run_and_check(p, vi.init_state(p, seed=0), 2)
+    print(stats)
+
+
+def test_c4_full_size_sampled_replicas(cuda):
+    # configs[3] at its full size (the bench launch configuration), replicas {0,1,511,1023}.
+    p = vi.workload("c4")
+    st0 = vi.init_state(p, seed=0)
+    run_and_check(p, st0, 1, replicas=[0, 1, 511, 1023])
+
+
+def test_c5_full_size_sampled_rows(cuda):
+    # configs[4]: 1M-agent world; bins bit-exact in full, sensing on sampled rows against
+    # all N, plus size-independent properties (sum rule, closed-form expectations).
+    torch = _torch()
+    p = vi.workload("c5")
+    w = make_world(p)
+    out = w.alloc_outputs()
+    st = dev(vi.init_state(p, seed=0))
+    prev = host(st)
+    act = vi.actions(p, seed=0, step=0)
+    w.step(st, dev(act), out)
+    torch.cuda.synchronize()
+    cur = host(st)
+    parity.check_integrate(p, cur, oracle.integrate(p, prev, act))
+    parity.check_bins(p, {k: host(v) for k, v in w.get_bins().items()}, cur)
+    rows = np.random.default_rng(1).choice(p.n_agents, 96, replace=False)
+    parity.check_sense(p, cur[0], outs_np(out, 0), rows=rows)
+    nn = host(out.n_neigh).astype(np.int64)
+    assert nn.sum() % 2 == 0
+    e = (p.n_agents - 1) * math.pi * p.d_v ** 2 / p.width ** 2
+    assert nn.mean() == pytest.approx(e, rel=5e-3)
+    occ = np.unpackbits(host(out.sector_occ).view(np.uint8), bitorder="little").mean()
+    pocc = 1 - (1 - (p.fov / p.v) * p.d_v ** 2 / (2 * p.width ** 2)) ** (p.n_agents - 1)
+    assert occ == pytest.approx(pocc, abs=3e-3)
+    w.close()
+
+
+@pytest.mark.parametrize("case", ["lone", "pair", "sparse", "g3", "many_replicas",
+                                  "clustered", "tag_no_chasers", "tag_all_chasers"])
+def test_edge_cases(cuda, case):
+    if case == "lone":
+        p = vi.flock_params(1)
+    elif case == "pair":
+        p = vi.flock_params(2, width=30.0)
+    elif case == "sparse":
+        p = vi.flock_params(37, width=400.0, d_v=10.0)        # mostly empty cells
+    elif case == "g3":
+        p = vi.flock_params(300, width=30.1, d_v=10.0)        # G = 3, the minimum
+    elif case == "many_replicas":
+        p = vi.flock_params(7, n_replicas=3000, width=40.0)
+    elif case == "clustered":
+        p = vi.flock_params(4000)
+    elif case == "tag_no_chasers":
+        p = vi.tag_params(500, n_chasers=0, width=60.0)
+    else:
+        p = vi.tag_params(500, n_chasers=500, width=60.0)
+    st0 = vi.clustered_state(p, seed=3, n_clusters=3, sigma=1.5) if case == "clustered" \
+        else vi.init_state(p, seed=5)
+    if case == "g3":
+        assert oracle.grid_size(p) == 3
+    reps = [0, 1, 2999] if case == "many_replicas" else None
+    run_and_check(p, st0, 3, replicas=reps)
+
+
+def test_dyadic_world_bit_exact_thresholds(cuda):
+    # On a 2^-8 lattice with L = 128 every difference and d^2 is exact in fp32 and fp64:
+    # radius and contact decisions must agree exactly, even for pairs exactly on them.
+    torch = _torch()
+    p = vi.flock_params(400, width=128.0, d_v=8.0)
+    rng = np.random.default_rng(4)
+    q = rng.integers(0, 128 * 256, size=(400, 2))
+    q[1] = q[0] + [8 * 256, 0]
+    q[3] = q[2] + [0, 128]
+    q[5] = (q[4] + [127 * 256 + 200, 0]) % (128 * 256)        # wrapped pair
+    q %= 128 * 256
+    st = np.zeros((1, 400, 4), np.float32)
+    st[0, :, :2] = q / 256.0
+    st[0, :, 2] = (rng.random(400) * 6.0).astype(np.float32)
+    st[0, :, 3] = 0.275
+    w = make_world(p)
+    out = w.alloc_outputs()
+    x = dev(st)
+    w.bin(x)
+    w.sense(out)
+    torch.cuda.synchronize()
+    ref = oracle.sense_rows(p, st[0], np.arange(400))
+    assert np.array_equal(host(out.n_neigh)[0], ref["n_neigh"])
+    assert np.array_equal(host(out.n_collide)[0], ref["n_collide"])
+    parity.check_sense(p, st[0], outs_np(out, 0))
+    w.close()
+
+
+def test_reward_kernel_matches_sense(cuda):
+    torch = _torch()
+    for p in (vi.workload("c2"), vi.tag_params(3000, width=60.0)):
+        w = make_world(p)
+        a, b = w.alloc_outputs(), w.alloc_outputs()
+        st = dev(vi.init_state(p, seed=2))
+        w.bin(st)
+        w.sense(a)
+        w.reward(b)
+        torch.cuda.synchronize()
+        for k in ("reward", "n_neigh", "n_collide", "n_touch"):
+            if getattr(a, k) is not None:
+                assert torch.equal(getattr(a, k), getattr(b, k)), k
+        w.close()
+
+
+def test_integrate_then_bin_sense_equals_step(cuda):
+    torch = _torch()
+    p = vi.workload("c2")
+    w = make_world(p)
+    s1, s2 = dev(vi.init_state(p, seed=1)), dev(vi.init_state(p, seed=1))
+    act = dev(vi.actions(p, seed=1, step=0))
+    o1, o2 = w.alloc_outputs(), w.alloc_outputs()
+    w.step(s1, act, o1)
+    w.integrate(s2, act)
+    w.bin(s2)
+    w.sense(o2)
+    torch.cuda.synchronize()
+    assert torch.equal(s1, s2)
+    for k in ("obs", "reward", "n_neigh", "n_collide", "sector_occ"):
+        assert torch.equal(getattr(o1, k), getattr(o2, k)), k
+    w.close()
+
+
+def test_determinism_bitwise(cuda):
+    torch = _torch()
+    p = vi.workload("c2")
+    res = []
+    for _ in range(2):
+        w = make_world(p)
+        st = dev(vi.init_state(p, seed=0))
+        out = w.alloc_outputs()
+        for t in range(5):
+            w.step(st, dev(vi.actions(p, seed=0, step=t)), out)
+        torch.cuda.synchronize()
+        res.append((st.clone(), out.obs.clone(), out.reward.clone(), out.sector_occ.clone()))
+        w.close()
+    for a, b in zip(*res):
+        assert torch.equal(a, b)
+
+
+def test_step_host_matches_step(cuda):
+    torch = _torch()
+    p = vi.workload("c2")
+    w = make_world(p)
+    s1, s2 = dev(vi.init_state(p, seed=1)), dev(vi.init_state(p, seed=1))
+    o1, o2 = w.alloc_outputs(), w.alloc_outputs()
+    act = vi.actions(p, seed=1, step=0)
+    act_h = torch.from_numpy(act).pin_memory()
+    rew_h = torch.empty((1, p.n_agents), dtype=torch.float32).pin_memory()
+    w.step(s1, dev(act), o1)
+    w.step_host(s2, act_h, o2, rew_h)
+    torch.cuda.synchronize()
+    assert torch.equal(s1, s2) and torch.equal(o1.obs, o2.obs)
+    assert torch.equal(o1.reward.cpu(), rew_h)
+    w.close()
+
+
+def test_cuda_graph_capture(cuda):
+    torch = _torch()
+    p = vi.workload("c2")
+    w = make_world(p)
+    st = dev(vi.init_state(p, seed=0))
+    ref_st = st.clone()
+    act = dev(vi.actions(p, seed=0, step=0))
+    out, ref = w.alloc_outputs(), w.alloc_outputs()
+    w.step(ref_st, act, ref)          # eager reference
+    g = torch.cuda.CUDAGraph()
+    s = torch.cuda.Stream()
+    s.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(s):
+        with torch.cuda.graph(g, stream=s):
+            w.step(st, act, out)
+    g.replay()
+    torch.cuda.synchronize()
+    assert torch.equal(st, ref_st) and torch.equal(out.obs, ref.obs)
+    assert torch.equal(out.reward, ref.reward)
+    w.close()
+
+
+def test_free_running_drift_c1(cuda):
+    # Open-loop actions: positions do not depend on observations, so the oracle's own fp64
+    # trajectory stays within the integrate tolerance of the fp32 GPU one for 100 steps.
+    torch = _torch()
+    p = vi.workload("c1")
+    w = make_world(p)
+    st = dev(vi.init_state(p, seed=0))
+    ref = vi.init_state(p, seed=0).astype(np.float64)
+    out = w.alloc_outputs()
+    for t in range(100):
+        act = vi.actions(p, seed=0, step=t)
+        w.step(st, dev(act), out)
+        ref = oracle.integrate(p, ref, act)
+    torch.cuda.synchronize()
+    parity.check_integrate(p, host(st), ref)
+    w.close()
+
+
+@pytest.mark.parametrize("what", ["nan_action", "pos_out_of_range", "bad_heading"])
+def test_device_errors(cuda, what):
+    import paper_2207_03945_b200 as vg
+    torch = _torch()
+    p = vi.workload("c2")
+    w = make_world(p)
+    st = vi.init_state(p, seed=0)
+    act = vi.actions(p, seed=0, step=0)
+    bad = 1234
+    if what == "nan_action":
+        act[0, bad, 1] = np.nan
+    elif what == "pos_out_of_range":
+        st[0, bad, 0] = p.width
+    else:
+        st[0, bad, 2] = -0.5
+    x = dev(st)
+    w.step(x, dev(act), w.alloc_outputs())
+    with pytest.raises(vg.VgError) as ei:
+        w.sync_errors()
+    assert ei.value.bad_agent == bad and "VG_ESTATE" in str(ei.value)
+    assert w.sync_errors() == -1                      # cleared
+    w.close()
+    torch.cuda.synchronize()
+
+
+def test_out_of_box_actions_are_clamped(cuda):
+    torch = _torch()
+    p = vi.workload("c2")
+    w = make_world(p)
+    st = dev(vi.init_state(p, seed=0))
+    prev = host(st)
+    act = vi.actions(p, seed=0, step=0) * 25.0
+    w.integrate(st, dev(act))
+    torch.cuda.synchronize()
+    parity.check_integrate(p, host(st), oracle.integrate(p, prev, act))
+    w.close()
