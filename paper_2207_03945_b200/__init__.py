@@ -63,7 +63,7 @@ class _CudaArray:
     """Borrowed device buffer exposed through __cuda_array_interface__ (zero copy)."""
 
     def __init__(self, ptr: int, shape, typestr: str, owner):
-        self.__cuda_array_interface__ = {"data": (ptr, True), "shape": tuple(shape),
+        self.__cuda_array_interface__ = {"data": (ptr, False), "shape": tuple(shape),
                                          "typestr": typestr, "version": 3, "strides": None}
         self._owner = owner
 
