@@ -51,6 +51,7 @@ struct vg_world {
   uint32_t* perm = nullptr;        // [R*N]         stable order
   float4* tmp_rec = nullptr;       // [R*N]
   float4* sorted = nullptr;        // [R*N]
+  float2* sorted_xy = nullptr;     // [R*N]         positions of `sorted` (K4 candidate reads)
   float2* act_dev = nullptr;       // [R*N]         staging for vg_step_host
   unsigned long long* err_dev = nullptr;  // smallest bad agent index (device word)
   uint32_t* err_flag = nullptr;    // mapped pinned host flag (set by kernels)
@@ -148,6 +149,9 @@ vg::Params derive(const vg_config& c, int g) {
   P.k_rise = c.c_near / (c.d_peak - P.two_dr);
   P.k_fall = c.c_near / (c.d_v - c.d_peak);
   P.w_prox = c.w_prox;
+  P.b_rise = -P.k_rise * P.two_dr;
+  P.nk_fall = -P.k_fall;
+  P.b_fall = P.k_fall * c.d_v;
   P.touch_fix = (long long)std::llrint((double)c.r_touch * 4294967296.0);
   return P;
 }
@@ -192,7 +196,7 @@ vg_status bin_rest(vg_world* w, const float4* state, cudaStream_t s, bool prof =
   if (prof) prof_mark(w, 3, s);
   const long long threads = (long long)w->n_cells * 32;
   vg::k_cell_sort<<<(unsigned)((threads + 255) / 256), 256, 0, s>>>(
-      w->n_cells, w->cell_start, w->tmp_rec, w->tmp_id, w->sorted, w->perm);
+      w->n_cells, w->cell_start, w->tmp_rec, w->tmp_id, w->sorted, w->perm, w->sorted_xy);
   if (vg_status st = launch_check("k_cell_sort")) return st;
   if (prof) prof_mark(w, 4, s);
   w->binned = true;
@@ -217,10 +221,10 @@ vg_status launch_sense(vg_world* w, const vg_outputs* outs, cudaStream_t s) {
   const vg::Outs O = to_outs(outs);
   if (w->P.env == vg::kFlock)
     vg::k_sense<vg::kFlock, VISION><<<w->n_cells, vg::kSenseWarps * 32, 0, s>>>(
-        w->P, w->cell_start, w->sorted, w->perm, O);
+        w->P, w->cell_start, w->sorted, w->sorted_xy, w->perm, O);
   else
     vg::k_sense<vg::kTag, VISION><<<w->n_cells, vg::kSenseWarps * 32, 0, s>>>(
-        w->P, w->cell_start, w->sorted, w->perm, O);
+        w->P, w->cell_start, w->sorted, w->sorted_xy, w->perm, O);
   return launch_check("k_sense");
 }
 
@@ -267,6 +271,7 @@ vg_status vg_world_create(const vg_config* cfg, vg_world** out) {
   if (!st) st = dalloc(w, &w->perm, n);
   if (!st) st = dalloc(w, &w->tmp_rec, n);
   if (!st) st = dalloc(w, &w->sorted, n);
+  if (!st) st = dalloc(w, &w->sorted_xy, n);
   if (!st) st = dalloc(w, &w->act_dev, n);
   if (!st) st = dalloc(w, &w->err_dev, 1);
   if (!st) {
@@ -300,6 +305,7 @@ void vg_world_destroy(vg_world* w) {
   cudaFree(w->perm);
   cudaFree(w->tmp_rec);
   cudaFree(w->sorted);
+  cudaFree(w->sorted_xy);
   cudaFree(w->act_dev);
   cudaFree(w->err_dev);
   if (w->err_flag) cudaFreeHost(w->err_flag);

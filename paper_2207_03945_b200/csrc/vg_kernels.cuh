@@ -35,6 +35,7 @@ struct Params {
   float d_v, dv2, inv_dv, contact2, two_dr;
   float half_fov, inv_fov, fv;  // fov/2, 1/fov, float(v)
   float c_collide, d_peak, k_rise, k_fall, w_prox;
+  float b_rise, nk_fall, b_fall;   // f = min(k_rise d + b_rise, nk_fall d + b_fall) (A5)
   long long touch_fix;         // r_touch * 2^32
 };
 
@@ -203,7 +204,7 @@ __global__ void __launch_bounds__(256) k_scatter(
 __global__ void __launch_bounds__(256) k_cell_sort(
     int n_cells, const uint32_t* __restrict__ cell_start, const float4* __restrict__ tmp_rec,
     const uint32_t* __restrict__ tmp_id, float4* __restrict__ sorted,
-    uint32_t* __restrict__ perm) {
+    uint32_t* __restrict__ perm, float2* __restrict__ sorted_xy) {
   const int cell = (int)(((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5);
   const int lane = threadIdx.x & 31;
   if (cell >= n_cells) return;
@@ -220,27 +221,61 @@ __global__ void __launch_bounds__(256) k_cell_sort(
       for (int t = 0; t < 32; ++t) rank += (__shfl_sync(kFull, other, t) < id) ? 1 : 0;
     }
     if (valid) {
-      sorted[b + rank] = tmp_rec[b + idx];
+      const float4 rec = tmp_rec[b + idx];
+      sorted[b + rank] = rec;
       perm[b + rank] = id;
+      sorted_xy[b + rank] = make_float2(rec.x, rec.y);   // compact positions for K4
     }
   }
 }
 
 // ---------------------------------------------------------------------------------- K4
 // One CTA per (replica, cell); warp w handles the cell's query agents w, w+W, ...  Each
-// query scans the 3x3 cell stencil (<= 6 contiguous sorted segments) for neighbours
-// within d_v, compacts them with ballot/popc into a per-warp queue, and
-// processes 32 at a time: contact test, reward term (fixed point, A16b), bearing, sector
-// and per-sector nearest distance by shared-memory atomicMin on the float bits (A2, A3).
+// query scans the 3x3 cell stencil — up to 6 contiguous runs of the sorted arrays, each
+// with a uniform torus image shift — for neighbours within d_v, compacts
+// them with ballot/popc into a per-warp queue, and processes full warps of 32 pairs:
+// contact test, reward term (fixed point, A16b), bearing, sector, and the per-sector
+// nearest distance by shared-memory atomicMin on the float bits (A2, A3).
 constexpr int kSenseWarps = 4;
+constexpr int kQueue = 96;          // 31 carried + 2 x 32 pushed per iteration
+
+// atan2(y, x) in (-pi, pi] with |error| <~ 2.5e-7 rad: octant reduction,
+// t = min/max by the hardware reciprocal, degree-8 minimax polynomial in t^2 for atan(t)/t
+// on [0, 1] (max error 9e-8 in fp32), then the quadrant fix-ups; atan2(+-0, +-0) = +-0.
+__device__ __forceinline__ float vg_atan2(float y, float x) {
+  const float ax = fabsf(x), ay = fabsf(y);
+  const float mx = fmaxf(ax, ay), mn = fminf(ax, ay);
+  float t = mn * __frcp_rn(mx);
+  t = (mx > 0.f) ? t : 0.f;
+  const float s = t * t;
+  float p = 0.0024567253421992064f;
+  p = fmaf(p, s, -0.01440136507153511f);
+  p = fmaf(p, s, 0.03978124260902405f);
+  p = fmaf(p, s, -0.07234859466552734f);
+  p = fmaf(p, s, 0.10498947650194168f);
+  p = fmaf(p, s, -0.14161229133605957f);
+  p = fmaf(p, s, 0.19985906779766083f);
+  p = fmaf(p, s, -0.33332598209381104f);
+  p = fmaf(p, s, 0.9999998807907104f);
+  float r = p * t;
+  r = (ay > ax) ? (1.5707963705062866f - r) : r;
+  r = (x < 0.f) ? (3.1415927410125732f - r) : r;
+  return copysignf(r, y);
+}
+
+struct Seg {
+  uint32_t b, e;     // run [b, e) of the sorted arrays
+  float csx, csy;    // candidate image shift (0 or -L; exact by Sterbenz, A11)
+  float qsx, qsy;    // query image shift (0 or -L)
+};
 
 template <int ENV, bool VISION>
-__global__ void __launch_bounds__(kSenseWarps * 32) k_sense(
+__global__ void __launch_bounds__(kSenseWarps * 32, 8) k_sense(
     Params P, const uint32_t* __restrict__ cell_start, const float4* __restrict__ sorted,
-    const uint32_t* __restrict__ perm, Outs O) {
+    const float2* __restrict__ sorted_xy, const uint32_t* __restrict__ perm, Outs O) {
   __shared__ uint32_t s_min[kSenseWarps][kMaxViewSlots];
-  __shared__ float4 s_q[kSenseWarps][64];
-  __shared__ uint32_t s_seg[12];
+  __shared__ float4 s_q[kSenseWarps][kQueue];
+  __shared__ Seg s_seg[6];
   __shared__ int s_nseg;
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -252,19 +287,21 @@ __global__ void __launch_bounds__(kSenseWarps * 32) k_sense(
 
   if (threadIdx.x == 0) {
     int ns = 0;
+    const float mL = -P.L;
     for (int dy = -1; dy <= 1; ++dy) {
       int yy = cy + dy;
-      yy += (yy < 0) ? P.G : 0;
-      yy -= (yy >= P.G) ? P.G : 0;
+      float csy = 0.f, qsy = 0.f;
+      if (yy < 0) { yy += P.G; csy = mL; }           // candidate row G-1 seen from row 0
+      if (yy >= P.G) { yy -= P.G; qsy = mL; }        // candidate row 0 seen from row G-1
       const int row = yy * P.G;
       if (cx >= 1 && cx <= P.G - 2) {
-        s_seg[2 * ns] = cs[row + cx - 1]; s_seg[2 * ns + 1] = cs[row + cx + 2]; ++ns;
-      } else if (cx == 0) {                       // cells G-1 | 0, 1
-        s_seg[2 * ns] = cs[row + P.G - 1]; s_seg[2 * ns + 1] = cs[row + P.G]; ++ns;
-        s_seg[2 * ns] = cs[row]; s_seg[2 * ns + 1] = cs[row + 2]; ++ns;
-      } else {                                    // cells G-2, G-1 | 0
-        s_seg[2 * ns] = cs[row + P.G - 2]; s_seg[2 * ns + 1] = cs[row + P.G]; ++ns;
-        s_seg[2 * ns] = cs[row]; s_seg[2 * ns + 1] = cs[row + 1]; ++ns;
+        s_seg[ns++] = Seg{cs[row + cx - 1], cs[row + cx + 2], 0.f, csy, 0.f, qsy};
+      } else if (cx == 0) {                          // cells G-1 | 0, 1
+        s_seg[ns++] = Seg{cs[row + P.G - 1], cs[row + P.G], mL, csy, 0.f, qsy};
+        s_seg[ns++] = Seg{cs[row], cs[row + 2], 0.f, csy, 0.f, qsy};
+      } else {                                       // cells G-2, G-1 | 0
+        s_seg[ns++] = Seg{cs[row + P.G - 2], cs[row + P.G], 0.f, csy, 0.f, qsy};
+        s_seg[ns++] = Seg{cs[row], cs[row + 1], 0.f, csy, mL, qsy};
       }
     }
     s_nseg = ns;
@@ -278,26 +315,29 @@ __global__ void __launch_bounds__(kSenseWarps * 32) k_sense(
 
   for (uint32_t q = qb + warp; q < qe; q += kSenseWarps) {
     const float4 me = sorted[q];
-    const int tq = (ENV == kTag) ? (int)me.w : 0;
+    const uint32_t tq = (ENV == kTag) ? (uint32_t)me.w : 0u;
     float sn = 0.f, csn = 0.f;
     if (VISION) {
       sincosf(me.z, &sn, &csn);
       for (int k = lane; k < P.view_slots; k += 32) my_min[k] = kOneBits;
     }
-    uint32_t nn = 0, ncol = 0, ntouch = 0;
+    uint32_t pushed = 0, ncol = 0, ntouch = 0;
     long long rs = 0;
     int nq = 0;
     __syncwarp();
 
+    // Pair pass over one queue entry (dx, dy, d^2, index | type << 31).
     auto process = [&](const float4 e) {
+      const uint32_t tagbits = __float_as_uint(e.w);
+      if ((tagbits & 0x7fffffffu) == q) return;                      // j != i
+      const uint32_t tj = tagbits >> 31;
       const float d2 = e.z;
-      const bool contact = d2 <= P.contact2;                       // A6 (inclusive)
-      const float d = sqrtf(d2);
-      const int tj = (ENV == kTag) ? (int)e.w : 0;
-      // Eq. 1 / Fig. 4 (A5): -c_collide at contact, else rising then falling bonus.
+      const bool contact = d2 <= P.contact2;                          // A6 (inclusive)
+      const float rsq = rsqrtf(d2);
+      const float d = (d2 > 0.f) ? d2 * rsq : 0.f;
+      // Eq. 1 / Fig. 4 (A5): contact -> -c_collide, else the tent min(rise, fall).
       const float f = contact ? -P.c_collide
-                              : ((d <= P.d_peak) ? P.k_rise * (d - P.two_dr)
-                                                 : P.k_fall * (P.d_v - d));
+                              : fminf(fmaf(P.k_rise, d, P.b_rise), fmaf(P.nk_fall, d, P.b_fall));
       if (ENV == kFlock) {
         rs += __float2ll_rn(f * kFix);
         ncol += contact ? 1u : 0u;
@@ -305,14 +345,13 @@ __global__ void __launch_bounds__(kSenseWarps * 32) k_sense(
         if (contact) {
           if (tj == tq) ++ncol; else ++ntouch;
         }
-        if (tq == 0 && tj == 0) rs += __float2ll_rn((P.w_prox * f) * kFix);
+        if (tq == 0u && tj == 0u) rs += __float2ll_rn((P.w_prox * f) * kFix);
       }
       if (VISION) {
         // Bearing in the agent frame (A3): phi = atan2(h x d, h . d), CCW-positive.
-        const float fwd = csn * e.x + sn * e.y;
-        const float left = csn * e.y - sn * e.x;
-        const float phi = atan2f(left, fwd);
-        const float u = (phi + P.half_fov) * P.inv_fov;           // fraction of the fov
+        const float fwd = fmaf(csn, e.x, sn * e.y);
+        const float left = fmaf(csn, e.y, -sn * e.x);
+        const float u = fmaf(vg_atan2(left, fwd), P.inv_fov, 0.5f);   // fraction of the fov
         if (u >= 0.f && u < 1.f) {
           const int k = min((int)(u * P.fv), P.v - 1);
           const float val = fminf(d * P.inv_dv, kBelowOne);
@@ -322,69 +361,92 @@ __global__ void __launch_bounds__(kSenseWarps * 32) k_sense(
     };
 
     for (int sgi = 0; sgi < nseg; ++sgi) {
-      const uint32_t sb = s_seg[2 * sgi], se = s_seg[2 * sgi + 1];
-      for (uint32_t p0 = sb; p0 < se; p0 += 32) {
-        const uint32_t p = p0 + lane;
-        const bool valid = p < se;
-        float4 o = make_float4(0.f, 0.f, 0.f, 0.f);
-        if (valid) o = __ldg(&sorted[p]);
-        // Minimal image with Sterbenz ordering (A11).
-        float dx = o.x - me.x;
-        if (dx > P.half_L) dx = (o.x - P.L) - me.x;
-        else if (dx < -P.half_L) dx = o.x - (me.x - P.L);
-        float dy = o.y - me.y;
-        if (dy > P.half_L) dy = (o.y - P.L) - me.y;
-        else if (dy < -P.half_L) dy = o.y - (me.y - P.L);
-        const float d2 = dx * dx + dy * dy;
-        const bool in = valid && (p != q) && (d2 < P.dv2);          // Eq. 1: d < d_v
-        const unsigned bal = __ballot_sync(kFull, in);
-        if (in) my_q[nq + __popc(bal & lt_mask)] = make_float4(dx, dy, d2, o.w);
-        const int cnt = __popc(bal);
-        nq += cnt;
-        nn += (uint32_t)cnt;
-        if (nq >= 32) {
+      const Seg sg = s_seg[sgi];
+      const float qx = me.x + sg.qsx, qy = me.y + sg.qsy;            // exact (Sterbenz)
+      for (uint32_t p0 = sg.b; p0 < sg.e; p0 += 64) {
+        const uint32_t pa = p0 + lane, pb = p0 + 32 + lane;
+        const bool va = pa < sg.e, vb = pb < sg.e;
+        float ax = 0.f, ay = 0.f, bx = 0.f, by = 0.f;
+        uint32_t ta = 0u, tb = 0u;
+        if (ENV == kFlock) {
+          if (va) { const float2 o = __ldg(&sorted_xy[pa]); ax = o.x; ay = o.y; }
+          if (vb) { const float2 o = __ldg(&sorted_xy[pb]); bx = o.x; by = o.y; }
+        } else {
+          if (va) { const float4 o = __ldg(&sorted[pa]); ax = o.x; ay = o.y; ta = (uint32_t)o.w << 31; }
+          if (vb) { const float4 o = __ldg(&sorted[pb]); bx = o.x; by = o.y; tb = (uint32_t)o.w << 31; }
+        }
+        const float dxa = (ax + sg.csx) - qx, dya = (ay + sg.csy) - qy;
+        const float dxb = (bx + sg.csx) - qx, dyb = (by + sg.csy) - qy;
+        const float d2a = fmaf(dxa, dxa, dya * dya);
+        const float d2b = fmaf(dxb, dxb, dyb * dyb);
+        const bool ia = va && d2a < P.dv2;                             // Eq. 1: d < d_v
+        const bool ib = vb && d2b < P.dv2;
+        const unsigned bala = __ballot_sync(kFull, ia);
+        const unsigned balb = __ballot_sync(kFull, ib);
+        if (ia) my_q[nq + __popc(bala & lt_mask)] = make_float4(dxa, dya, d2a, __uint_as_float(pa | ta));
+        nq += __popc(bala);
+        if (ib) my_q[nq + __popc(balb & lt_mask)] = make_float4(dxb, dyb, d2b, __uint_as_float(pb | tb));
+        nq += __popc(balb);
+        while (nq >= 32) {
           __syncwarp();
           process(my_q[lane]);
-          __syncwarp();
-          if (lane < nq - 32) my_q[lane] = my_q[lane + 32];
-          __syncwarp();
           nq -= 32;
+          pushed += 32;
+          __syncwarp();
+          const float4 m0 = my_q[32 + lane], m1 = my_q[64 + lane];
+          __syncwarp();
+          if (lane < nq) my_q[lane] = m0;
+          if (lane + 32 < nq) my_q[32 + lane] = m1;
+          __syncwarp();
         }
       }
     }
     __syncwarp();
     if (lane < nq) process(my_q[lane]);
+    const uint32_t nn = pushed + (uint32_t)nq - 1u;                  // minus the self pair
 
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-      ncol += __shfl_xor_sync(kFull, ncol, o);
-      if (ENV == kTag) ntouch += __shfl_xor_sync(kFull, ntouch, o);
-      rs += __shfl_xor_sync(kFull, rs, o);
-    }
+    // Warp reductions (REDUX): the int64 reward sum split into exact 32-bit partial sums.
+    ncol = __reduce_add_sync(kFull, ncol);
+    if (ENV == kTag) ntouch = __reduce_add_sync(kFull, ntouch);
+    const unsigned long long ur = (unsigned long long)rs;
+    const uint32_t s_lo = __reduce_add_sync(kFull, (uint32_t)(ur & 0xffffu));
+    const uint32_t s_mid = __reduce_add_sync(kFull, (uint32_t)((ur >> 16) & 0xffffu));
+    const int s_hi = __reduce_add_sync(kFull, (int)(uint32_t)(ur >> 32));
+    long long rsum = ((long long)s_hi << 32) + ((long long)s_mid << 16) + (long long)s_lo;
     if (ENV == kTag) {
       const long long t = (long long)ntouch * P.touch_fix;
-      rs += (tq == 1) ? t : -t;                                     // P:194 touch rule
+      rsum += (tq == 1u) ? t : -t;                                    // P:194 touch rule
     }
     const size_t row = (size_t)r * P.N + perm[q];
     if (lane == 0) {
-      if (O.reward) O.reward[row] = __ll2float_rn(rs) * kFixInv;
+      if (O.reward) O.reward[row] = __ll2float_rn(rsum) * kFixInv;
       if (O.n_neigh) O.n_neigh[row] = nn;
       if (O.n_collide) O.n_collide[row] = ncol;
       if (ENV == kTag && O.n_touch) O.n_touch[row] = ntouch;
     }
     if (VISION) {
       __syncwarp();
+      uint32_t vals[kMaxViewSlots / 32];
+#pragma unroll
+      for (int w = 0; w < kMaxViewSlots / 32; ++w) {
+        const int k = 32 * w + lane;
+        vals[w] = (k < P.view_slots) ? my_min[k] : kOneBits;
+      }
       if (O.obs) {
         float* orow = O.obs + row * (size_t)P.obs_dim;
-        for (int k = lane; k < P.view_slots; k += 32) orow[k] = __uint_as_float(my_min[k]);
+#pragma unroll
+        for (int w = 0; w < kMaxViewSlots / 32; ++w)
+          if (32 * w + lane < P.view_slots) orow[32 * w + lane] = __uint_as_float(vals[w]);
         if (ENV == kFlock && lane == 0) orow[P.view_slots] = __fdiv_rn(me.w, P.s_max);  // A24
       }
       if (O.occ) {
-        for (int w = 0; w < P.occ_words; ++w) {
-          const int k = 32 * w + lane;
-          const unsigned bits = __ballot_sync(kFull, k < P.view_slots && my_min[k] < kOneBits);
-          if (lane == 0) O.occ[row * (size_t)P.occ_words + w] = bits;
+        uint32_t mine = 0u;
+#pragma unroll
+        for (int w = 0; w < kMaxViewSlots / 32; ++w) {
+          const unsigned bits = __ballot_sync(kFull, vals[w] < kOneBits);
+          if (lane == w) mine = bits;
         }
+        if (lane < P.occ_words) O.occ[row * (size_t)P.occ_words + lane] = mine;
       }
     }
     __syncwarp();
