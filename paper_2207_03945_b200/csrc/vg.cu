@@ -7,6 +7,7 @@
 #include <cstdarg>
 #include <cstdio>
 #include <cstring>
+#include <algorithm>
 #include <climits>
 #include <new>
 #include <vector>
@@ -216,14 +217,26 @@ vg::Outs to_outs(const vg_outputs* o) {
   return r;
 }
 
+// Query chunks per cell: enough CTAs to give ~32 resident warps per SM when the world has
+// few cells (C1-C3), 1 for large worlds.  Any value >= 1 is correct (grid-stride loop).
+int sense_chunks(const vg_world* w) {
+  const long long target_warps = 148LL * 32;
+  const long long warps = (long long)w->n_cells * vg::kSenseWarps;
+  const long long per_cell = (w->P.total + w->n_cells - 1) / w->n_cells;
+  long long ch = (target_warps + warps - 1) / warps;
+  ch = std::min(ch, std::max(1LL, (per_cell + vg::kSenseWarps - 1) / vg::kSenseWarps));
+  return (int)std::max(1LL, std::min(ch, 1024LL));
+}
+
 template <bool VISION>
 vg_status launch_sense(vg_world* w, const vg_outputs* outs, cudaStream_t s) {
   const vg::Outs O = to_outs(outs);
+  const dim3 grid((unsigned)w->n_cells, (unsigned)sense_chunks(w));
   if (w->P.env == vg::kFlock)
-    vg::k_sense<vg::kFlock, VISION><<<w->n_cells, vg::kSenseWarps * 32, 0, s>>>(
+    vg::k_sense<vg::kFlock, VISION><<<grid, vg::kSenseWarps * 32, 0, s>>>(
         w->P, w->cell_start, w->sorted, w->sorted_xy, w->perm, O);
   else
-    vg::k_sense<vg::kTag, VISION><<<w->n_cells, vg::kSenseWarps * 32, 0, s>>>(
+    vg::k_sense<vg::kTag, VISION><<<grid, vg::kSenseWarps * 32, 0, s>>>(
         w->P, w->cell_start, w->sorted, w->sorted_xy, w->perm, O);
   return launch_check("k_sense");
 }

@@ -245,8 +245,9 @@ constexpr int kQueue = 96;          // 31 carried + 2 x 32 pushed per iteration
 __device__ __forceinline__ float vg_atan2(float y, float x) {
   const float ax = fabsf(x), ay = fabsf(y);
   const float mx = fmaxf(ax, ay), mn = fminf(ax, ay);
-  float t = mn * __frcp_rn(mx);
-  t = (mx > 0.f) ? t : 0.f;
+  float rc;
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(rc) : "f"(mx));       // <= 1 ulp
+  const float t = (mx > 0.f) ? mn * rc : 0.f;
   const float s = t * t;
   float p = 0.0024567253421992064f;
   p = fmaf(p, s, -0.01440136507153511f);
@@ -313,13 +314,17 @@ __global__ void __launch_bounds__(kSenseWarps * 32, 8) k_sense(
   uint32_t* my_min = s_min[warp];
   float4* my_q = s_q[warp];
 
-  for (uint32_t q = qb + warp; q < qe; q += kSenseWarps) {
+  // Queries of this cell handled by this CTA: chunk blockIdx.y of gridDim.y (small worlds
+  // spread one cell's queries over several CTAs to fill the GPU).
+  const uint32_t qstride = kSenseWarps * gridDim.y;
+  for (uint32_t q = qb + blockIdx.y * kSenseWarps + warp; q < qe; q += qstride) {
     const float4 me = sorted[q];
     const uint32_t tq = (ENV == kTag) ? (uint32_t)me.w : 0u;
     float sn = 0.f, csn = 0.f;
     if (VISION) {
       sincosf(me.z, &sn, &csn);
-      for (int k = lane; k < P.view_slots; k += 32) my_min[k] = kOneBits;
+#pragma unroll
+      for (int w = 0; w < kMaxViewSlots / 32; ++w) my_min[32 * w + lane] = kOneBits;
     }
     uint32_t pushed = 0, ncol = 0, ntouch = 0;
     long long rs = 0;

@@ -1,0 +1,71 @@
+#!/usr/bin/env python
+"""Summarize ncu captures into profiles/ (run here, on the CPU box, after gpurun).
+
+  python tools/ncu_summary.py launches <launches.csv>          # per-kernel share of a launch list
+  python tools/ncu_summary.py full <report.ncu-rep> [config]   # key metrics per profiled kernel
+"""
+import collections
+import csv
+import json
+import subprocess
+import sys
+
+KEYS = [
+    "gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum",
+    "smsp__inst_executed.sum", "smsp__issue_active.avg.pct_of_peak_sustained_active",
+    "sm__throughput.avg.pct_of_peak_sustained_elapsed",
+    "gpu__compute_memory_throughput.avg.pct_of_peak_sustained_elapsed",
+    "dram__throughput.avg.pct_of_peak_sustained_elapsed",
+    "sm__warps_active.avg.per_cycle_active", "launch__registers_per_thread",
+    "sm__inst_executed_pipe_fma.avg.pct_of_peak_sustained_active",
+    "sm__inst_executed_pipe_alu.avg.pct_of_peak_sustained_active",
+    "sm__inst_executed_pipe_xu.avg.pct_of_peak_sustained_active",
+    "sm__inst_executed_pipe_lsu.avg.pct_of_peak_sustained_active",
+    "l1tex__t_sector_hit_rate.pct", "lts__t_sector_hit_rate.pct",
+    "launch__grid_size", "launch__block_size",
+]
+
+
+def launches(path):
+    rows = [r for r in csv.reader(open(path)) if len(r) > 5]
+    hdr = rows[0]
+    ki, vi = hdr.index("Kernel Name"), hdr.index("Metric Value")
+    d = collections.defaultdict(list)
+    for r in rows[1:]:
+        d[r[ki].split("(")[0][:70]].append(float(r[vi].replace(",", "")))
+    tot = sum(sum(v) for v in d.values())
+    out = ["| kernel | launches | mean us | share of all GPU time |", "|---|---|---|---|"]
+    for k, v in sorted(d.items(), key=lambda x: -sum(x[1])):
+        out.append(f"| `{k}` | {len(v)} | {sum(v) / len(v) / 1e3:.2f} | {sum(v) / tot:.3f} |")
+    return "\n".join(out)
+
+
+def full(path, config=None):
+    raw = subprocess.run(["ncu", "-i", path, "--page", "raw", "--csv"], capture_output=True,
+                         text=True, check=True).stdout.splitlines()
+    rows = list(csv.reader(raw))
+    hdr, units = rows[0], rows[1]
+    out, traffic = [], {}
+    for r in rows[2:]:
+        name = r[hdr.index("Kernel Name")].split("(")[0]
+        out.append(f"### `{name}`")
+        out.append("| metric | value |\n|---|---|")
+        for k in KEYS:
+            if k in hdr:
+                i = hdr.index(k)
+                out.append(f"| {k} | {r[i]} {units[i]} |")
+        i, j = hdr.index("dram__bytes_read.sum"), hdr.index("dram__bytes_write.sum")
+        scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
+        b = float(r[i]) * scale.get(units[i], 1) + float(r[j]) * scale.get(units[j], 1)
+        traffic.setdefault(name, b)
+    if config:
+        for name, b in traffic.items():
+            if "k_sense" in name:
+                json.dump({"config": config, "kernel": name, "bytes_per_launch": b,
+                           "source": path}, open("profiles/sense_traffic.json", "w"), indent=1)
+    return "\n".join(out)
+
+
+if __name__ == "__main__":
+    mode, path = sys.argv[1], sys.argv[2]
+    print(launches(path) if mode == "launches" else full(path, sys.argv[3] if len(sys.argv) > 3 else None))
