@@ -70,7 +70,7 @@ typedef enum { VG_SHARD_REPLICA = 0, VG_SHARD_SLAB = 1 } vg_shard;
 typedef struct {
   int32_t env;          /* vg_env                                                          */
   int32_t vision;       /* vg_vision: must be VG_VISION_SECTOR                             */
-  int32_t shard;        /* vg_shard: VG_SHARD_REPLICA (slab mode: not in this build)       */
+  int32_t shard;        /* vg_shard: VG_SHARD_REPLICA, or VG_SHARD_SLAB (see slab mode)     */
   int32_t n_agents;     /* N > 0, agents per replica                               */
   int32_t n_replicas;   /* R > 0; R*N < 2^31                                               */
   float width;          /* L, square torus side (A9)                           [100]       */
@@ -90,8 +90,8 @@ typedef struct {
   float r_touch;        /* tag touch reward magnitude                          [1.0]       */
   float w_prox;         /* tag runner proximity weight                         [0.1]       */
   float s_max_chaser;   /* tag chaser move bound (runners use s_max)           [0.375]     */
-  int32_t rank, world_size, halo_capacity; /* slab mode (reserved)                        */
-  const void* nccl_unique_id;              /* slab mode (reserved)                        */
+  int32_t rank, world_size, halo_capacity; /* slab mode: this rank, P, records/message   */
+  const void* nccl_unique_id;              /* reserved (the exchange is the caller's)     */
 } vg_config;
 
 /* Caller-owned device output buffers; a NULL pointer means "do not write".  Rows are in
@@ -107,7 +107,7 @@ typedef struct {
   uint32_t* n_touch;    /* [R][N] tag only: opposite-type contacts (d <= 2 d_r)           */
   uint32_t* sector_occ; /* [R][N][occ_words] bit (c*v + k) set iff sector k of channel c
                            holds a visible neighbour; occ_words = ceil(channels*v/32)     */
-  uint32_t* agent_id;   /* slab mode (reserved)                                           */
+  uint32_t* agent_id;   /* slab mode: [N] global agent id of each output row                */
 } vg_outputs;
 
 typedef struct {
@@ -170,6 +170,48 @@ vg_status vg_get_bins(const vg_world* w, const uint32_t** cell_id, const uint32_
 /* Synchronize `stream`, read and clear the device error word.  *bad_agent = -1 if clean,
  * else the smallest offending global agent index (and VG_ESTATE is returned). */
 vg_status vg_sync_errors(vg_world* w, void* stream, int64_t* bad_agent);
+
+/* ---------------------------------------------------------------- slab mode
+ * One world (n_replicas = 1, N = n_agents global) split over world_size = P ranks by
+ * x-slabs of whole cell columns: rank g owns global columns [g G/P, (g+1) G/P) (P | G,
+ * >= 2 columns per rank, and the largest move per step < cell size so an agent crosses
+ * at most one column).  Each step:
+ *   vg_slab_begin   integrate the owned rows and route them: stay, migrate (<= 1 slab), or
+ *                   copy as a ghost (boundary column) into two messages (left, right);
+ *   exchange        the caller moves send_left -> left rank's recv_right and send_right ->
+ *                   right rank's recv_left (torch.distributed P2P over NCCL, or
+ *                   vg_slab_exchange_loopback for P worlds in one process);
+ *   vg_slab_finish  append received records, bin owned + ghost agents (stable by global
+ *                   id), sense + reward the owned cells.
+ * Output rows are the owned agents in sorted (local cell, global id) order; outs->agent_id
+ * gives each row's global id; the next vg_slab_begin takes actions[row] in that order.
+ * Every per-agent result is bitwise identical to the single-world (replica) path.
+ * Buffers: outputs need capacity N rows.  Messages: {u32 count, 3 x u32}, float4 rec[cap],
+ * u32 id[cap], cap = halo_capacity (0 = auto: 4 N/G + 256, >= 1024).  A message or local
+ * overflow is reported as VG_EOVERFLOW by vg_sync_errors. */
+typedef struct {
+  void* send_left;
+  void* send_right;
+  void* recv_left;
+  void* recv_right;
+  int64_t message_bytes;   /* bytes of each of the four message buffers              */
+  int32_t left_rank, right_rank;
+  int32_t lo, hi;          /* owned global cell columns [lo, hi)                      */
+  int64_t capacity_rows;   /* output rows to allocate (= N)                           */
+} vg_slab_io;
+
+/* Host-only: plan[0..3] = lo, hi, left rank, right rank of `rank` (no device needed). */
+vg_status vg_slab_plan(int32_t grid, int32_t world_size, int32_t rank, int32_t* plan);
+/* Select this rank's owned + ghost agents from the full global state [N][4] (device) and
+ * bin them (step 0); vg_slab_sense then gives the initial observation. */
+vg_status vg_slab_load(vg_world* w, const float* state_global, void* stream);
+vg_status vg_slab_sense(vg_world* w, const vg_outputs* outs, void* stream);
+vg_status vg_slab_begin(vg_world* w, const float* actions, void* stream);
+vg_status vg_slab_get_io(vg_world* w, vg_slab_io* io);
+vg_status vg_slab_exchange_loopback(vg_world* const* worlds, int32_t n, void* stream);
+vg_status vg_slab_finish(vg_world* w, const vg_outputs* outs, void* stream);
+/* Synchronizes `stream`; *n_own = number of owned agents (valid output rows). */
+vg_status vg_slab_own_count(vg_world* w, void* stream, int64_t* n_own);
 
 /* Phase timing for measurement.  After vg_profile_begin(w, max_steps), each of the next
  * max_steps vg_step calls records CUDA events on its stream between its phases

@@ -27,12 +27,18 @@ __all__ = ["World", "Outputs", "VgError", "config_from_params"]
 _ENV = {"flock": _lib.ENV_FLOCK, "tag": _lib.ENV_TAG}
 
 
-def config_from_params(p) -> _lib.VgConfig:
-    """Build a vg_config from an EnvParams-like object (same field names)."""
+def config_from_params(p, slab: dict | None = None) -> _lib.VgConfig:
+    """Build a vg_config from an EnvParams-like object (same field names).  ``slab`` =
+    {"rank": g, "world_size": P, "halo_capacity": 0} selects slab mode (one world split
+    over P ranks by x-slabs)."""
     c = _lib.VgConfig()
     c.env = _ENV[p.env]
     c.vision = 0
-    c.shard = 0
+    c.shard = 1 if slab else 0
+    if slab:
+        c.rank = int(slab["rank"])
+        c.world_size = int(slab["world_size"])
+        c.halo_capacity = int(slab.get("halo_capacity", 0))
     c.n_agents = int(p.n_agents)
     c.n_replicas = int(p.n_replicas)
     for f in ("width", "d_v", "d_r", "fov", "s_min", "s_max", "a_max", "theta_max",
@@ -53,6 +59,7 @@ class Outputs:
     n_collide: torch.Tensor | None = None
     n_touch: torch.Tensor | None = None
     sector_occ: torch.Tensor | None = None
+    agent_id: torch.Tensor | None = None      # slab mode: global id of each row
 
 
 def _ptr(t: torch.Tensor | None) -> int | None:
@@ -69,14 +76,16 @@ class _CudaArray:
 
 
 class World:
-    def __init__(self, params, device: int | torch.device | None = None):
+    def __init__(self, params, device: int | torch.device | None = None,
+                 slab: dict | None = None):
         self.params = params
+        self.slab = dict(slab) if slab else None
         dev = torch.device("cuda", torch.cuda.current_device()) if device is None \
             else torch.device(device)
         if dev.type != "cuda":
             raise ValueError("World needs a CUDA device (there is no CPU path)")
         self.device = dev
-        self._cfg = config_from_params(params)
+        self._cfg = config_from_params(params, slab)
         self._h = c_void_p()
         with torch.cuda.device(dev):
             torch.cuda.init()
@@ -92,6 +101,14 @@ class World:
         self.scratch_bytes = info.scratch_bytes
         self.R, self.N = int(params.n_replicas), int(params.n_agents)
         self.is_tag = params.env == "tag"
+        if self.slab:
+            io = _lib.VgSlabIo()
+            check(_lib.lib.vg_slab_get_io(self._h, byref(io)))
+            self.slab_io = io
+            mk = lambda p: torch.as_tensor(  # noqa: E731
+                _CudaArray(p, (io.message_bytes,), "|u1", self), device=self.device)
+            self.messages = {"send_left": mk(io.send_left), "send_right": mk(io.send_right),
+                             "recv_left": mk(io.recv_left), "recv_right": mk(io.recv_right)}
 
     # ------------------------------------------------------------------ lifecycle
     def close(self) -> None:
@@ -127,7 +144,8 @@ class World:
                 "reward": ((R, N), torch.float32),
                 "n_neigh": ((R, N), torch.int32), "n_collide": ((R, N), torch.int32),
                 "n_touch": ((R, N), torch.int32),
-                "sector_occ": ((R, N, self.occ_words), torch.int32)}
+                "sector_occ": ((R, N, self.occ_words), torch.int32),
+                "agent_id": ((R, N), torch.int32)}
         o = _lib.VgOutputs()
         for name, (shape, dt) in spec.items():
             t = getattr(out, name)
@@ -148,6 +166,7 @@ class World:
             n_collide=z(R, N, dt=torch.int32) if counts else None,
             n_touch=z(R, N, dt=torch.int32) if (counts and self.is_tag) else None,
             sector_occ=z(R, N, self.occ_words, dt=torch.int32) if sector_occ else None,
+            agent_id=z(R, N, dt=torch.int32) if self.slab else None,
         )
 
     # ------------------------------------------------------------------ the ABI
@@ -191,16 +210,50 @@ class World:
                                     byref(o), _ptr(reward_host), self._stream()))
 
     def get_bins(self) -> dict:
-        """Zero-copy views of the last binning (valid until the next bin/step)."""
+        """Zero-copy views of the last binning (valid until the next bin/step).  Slab mode:
+        the local set (owned + ghosts) on the column-major local grid; perm = global ids."""
         ptrs = [c_void_p() for _ in range(4)]
         check(_lib.lib.vg_get_bins(self._h, *[byref(p) for p in ptrs]))
         R, N = self.R, self.N
+        if self.slab:
+            R, N = 1, self.N + 2 * ((self.slab_io.message_bytes - 16) // 20)
         mk = lambda p, shape, ts: torch.as_tensor(  # noqa: E731
             _CudaArray(p.value, shape, ts, self), device=self.device)
         return {"cell_id": mk(ptrs[0], (R, N), "<i4"),
                 "cell_start": mk(ptrs[1], (self.n_cells + 1,), "<i4"),
                 "perm": mk(ptrs[2], (R, N), "<i4"),
                 "sorted": mk(ptrs[3], (R, N, 4), "<f4")}
+
+    # ------------------------------------------------------------------ slab mode
+    def slab_load(self, state_global: torch.Tensor) -> None:
+        """Take this rank's owned + ghost agents from the full state [1, N, 4] and bin them."""
+        self._check_tensor(state_global, "state_global", (1, self.N, 4))
+        check(_lib.lib.vg_slab_load(self._h, state_global.data_ptr(), self._stream()))
+
+    def slab_sense(self, out: Outputs) -> None:
+        o = self._outs(out)
+        check(_lib.lib.vg_slab_sense(self._h, byref(o), self._stream()))
+
+    def slab_begin(self, actions: torch.Tensor) -> None:
+        """Integrate the owned rows with actions[row] (rows of the last output) and route."""
+        self._check_tensor(actions, "actions", (1, self.N, 2))
+        check(_lib.lib.vg_slab_begin(self._h, actions.data_ptr(), self._stream()))
+
+    def slab_finish(self, out: Outputs) -> None:
+        o = self._outs(out)
+        check(_lib.lib.vg_slab_finish(self._h, byref(o), self._stream()))
+
+    def slab_owned(self) -> tuple:
+        """(global ids [n_own], state records [n_own, 4]) of the owned agents, row order."""
+        n = self.slab_own_count()
+        b = self.get_bins()
+        own_b = int(b["cell_start"][self.grid].item())
+        return b["perm"][0, own_b:own_b + n].clone(), b["sorted"][0, own_b:own_b + n].clone()
+
+    def slab_own_count(self) -> int:
+        n = c_int64(0)
+        check(_lib.lib.vg_slab_own_count(self._h, self._stream(), byref(n)))
+        return n.value
 
     def profile_begin(self, max_steps: int) -> None:
         """Record per-phase CUDA events for the next max_steps vg_step calls."""

@@ -41,6 +41,15 @@ class VgOutputs(ctypes.Structure):
     ]
 
 
+class VgSlabIo(ctypes.Structure):
+    _fields_ = [
+        ("send_left", c_void_p), ("send_right", c_void_p),
+        ("recv_left", c_void_p), ("recv_right", c_void_p),
+        ("message_bytes", c_int64), ("left_rank", c_int32), ("right_rank", c_int32),
+        ("lo", c_int32), ("hi", c_int32), ("capacity_rows", c_int64),
+    ]
+
+
 class VgWorldInfo(ctypes.Structure):
     _fields_ = [
         ("grid", c_int32), ("cell_size", c_float), ("n_cells", c_int32),
@@ -66,6 +75,14 @@ SIGNATURES = {
     "vg_get_bins": (c_int32, [c_void_p, POINTER(c_void_p), POINTER(c_void_p),
                               POINTER(c_void_p), POINTER(c_void_p)]),
     "vg_sync_errors": (c_int32, [c_void_p, c_void_p, POINTER(c_int64)]),
+    "vg_slab_plan": (c_int32, [c_int32, c_int32, c_int32, POINTER(c_int32)]),
+    "vg_slab_load": (c_int32, [c_void_p, c_void_p, c_void_p]),
+    "vg_slab_sense": (c_int32, [c_void_p, POINTER(VgOutputs), c_void_p]),
+    "vg_slab_begin": (c_int32, [c_void_p, c_void_p, c_void_p]),
+    "vg_slab_get_io": (c_int32, [c_void_p, POINTER(VgSlabIo)]),
+    "vg_slab_exchange_loopback": (c_int32, [POINTER(c_void_p), c_int32, c_void_p]),
+    "vg_slab_finish": (c_int32, [c_void_p, POINTER(VgOutputs), c_void_p]),
+    "vg_slab_own_count": (c_int32, [c_void_p, c_void_p, POINTER(c_int64)]),
     "vg_profile_begin": (c_int32, [c_void_p, c_int32]),
     "vg_profile_end": (c_int32, [c_void_p, c_void_p, POINTER(ctypes.c_double),
                                  POINTER(c_int32)]),

@@ -56,6 +56,15 @@ struct vg_world {
   float2* act_dev = nullptr;       // [R*N]         staging for vg_step_host
   unsigned long long* err_dev = nullptr;  // smallest bad agent index (device word)
   uint32_t* err_flag = nullptr;    // mapped pinned host flag (set by kernels)
+  // slab mode (shard = VG_SHARD_SLAB)
+  bool slab = false;
+  vg::Slab SL{};
+  vg::SlabBufs SB{};
+  uint32_t* loc_n = nullptr;       // device counter (SB.n_loc)
+  uint32_t* slab_ovf = nullptr;    // device overflow flag (SB.overflow)
+  unsigned char* msg = nullptr;    // 4 messages: send_l, send_r, recv_l, recv_r
+  size_t msg_bytes = 0;
+  int left = -1, right = -1;
   // phase timing (vg_profile_begin/end): VG_N_PHASES + 1 events per recorded step
   std::vector<cudaEvent_t> prof_ev;
   int prof_max = 0, prof_n = 0;
@@ -75,7 +84,7 @@ vg_status validate(const vg_config& c, int* grid_out) {
   const double PI = 3.14159265358979323846;
   if (c.env != VG_ENV_FLOCK && c.env != VG_ENV_TAG) return fail(VG_EINVAL, "env: must be 0 (flock) or 1 (tag)");
   if (c.vision != VG_VISION_SECTOR) return fail(VG_EINVAL, "vision: only VG_VISION_SECTOR is built (reading A1)");
-  if (c.shard != VG_SHARD_REPLICA) return fail(VG_EINVAL, "shard: only VG_SHARD_REPLICA is built");
+  if (c.shard != VG_SHARD_REPLICA && c.shard != VG_SHARD_SLAB) return fail(VG_EINVAL, "shard: must be 0 (replica) or 1 (slab)");
   if (c.n_agents <= 0) return fail(VG_EINVAL, "n_agents: must be > 0 (S:241)");
   if (c.n_replicas <= 0) return fail(VG_EINVAL, "n_replicas: must be > 0");
   if ((long long)c.n_agents * c.n_replicas >= (1LL << 31)) return fail(VG_EINVAL, "n_agents*n_replicas: must be < 2^31");
@@ -106,6 +115,16 @@ vg_status validate(const vg_config& c, int* grid_out) {
   if (g < 3) return fail(VG_EINVAL, "grid: G = %d, need G >= 3 (3x3 stencil must not alias)", g);
   if ((double)c.width / g < need) return fail(VG_EINVAL, "grid: cell size L/G = %g must be >= d_v (1 + 2^-12) = %g (A16)", (double)c.width / g, need);
   if ((long long)g * g * c.n_replicas >= (1LL << 31)) return fail(VG_EINVAL, "grid: n_replicas * G^2 must be < 2^31");
+  if (c.shard == VG_SHARD_SLAB) {
+    if (c.world_size < 2) return fail(VG_EINVAL, "world_size: slab mode needs world_size >= 2");
+    if (c.rank < 0 || c.rank >= c.world_size) return fail(VG_EINVAL, "rank: must satisfy 0 <= rank < world_size");
+    if (c.n_replicas != 1) return fail(VG_EINVAL, "n_replicas: slab mode splits one world (n_replicas = 1)");
+    if (g % c.world_size != 0) return fail(VG_EINVAL, "grid: slab mode needs world_size | G (G = %d)", g);
+    if (g / c.world_size < 2) return fail(VG_EINVAL, "world_size: slab mode needs >= 2 cell columns per rank");
+    const double move = (c.env == VG_ENV_TAG) ? std::max((double)c.s_max, (double)c.s_max_chaser) : (double)c.s_max;
+    if (!(move < (double)c.width / g)) return fail(VG_EINVAL, "s_max: slab mode needs the largest move < cell size (one column per step)");
+    if (c.halo_capacity < 0) return fail(VG_EINVAL, "halo_capacity: must be >= 0 (0 = auto)");
+  }
   *grid_out = g;
   return VG_OK;
 }
@@ -213,6 +232,7 @@ vg::Outs to_outs(const vg_outputs* o) {
     r.n_collide = o->n_collide;
     r.n_touch = o->n_touch;
     r.occ = o->sector_occ;
+    r.agent_id = o->agent_id;
   }
   return r;
 }
@@ -231,14 +251,54 @@ int sense_chunks(const vg_world* w) {
 template <bool VISION>
 vg_status launch_sense(vg_world* w, const vg_outputs* outs, cudaStream_t s) {
   const vg::Outs O = to_outs(outs);
+  if (w->slab) {                      // owned cells only: local columns 1..W
+    const dim3 grid((unsigned)(w->SL.W * w->P.G), 1);
+    if (w->P.env == vg::kFlock)
+      vg::k_sense<vg::kFlock, VISION, true><<<grid, vg::kSenseWarps * 32, 0, s>>>(
+          w->P, w->cell_start, w->sorted, w->sorted_xy, w->perm, O, w->SL);
+    else
+      vg::k_sense<vg::kTag, VISION, true><<<grid, vg::kSenseWarps * 32, 0, s>>>(
+          w->P, w->cell_start, w->sorted, w->sorted_xy, w->perm, O, w->SL);
+    return launch_check("k_sense(slab)");
+  }
   const dim3 grid((unsigned)w->n_cells, (unsigned)sense_chunks(w));
   if (w->P.env == vg::kFlock)
-    vg::k_sense<vg::kFlock, VISION><<<grid, vg::kSenseWarps * 32, 0, s>>>(
-        w->P, w->cell_start, w->sorted, w->sorted_xy, w->perm, O);
+    vg::k_sense<vg::kFlock, VISION, false><<<grid, vg::kSenseWarps * 32, 0, s>>>(
+        w->P, w->cell_start, w->sorted, w->sorted_xy, w->perm, O, w->SL);
   else
-    vg::k_sense<vg::kTag, VISION><<<grid, vg::kSenseWarps * 32, 0, s>>>(
-        w->P, w->cell_start, w->sorted, w->sorted_xy, w->perm, O);
+    vg::k_sense<vg::kTag, VISION, false><<<grid, vg::kSenseWarps * 32, 0, s>>>(
+        w->P, w->cell_start, w->sorted, w->sorted_xy, w->perm, O, w->SL);
   return launch_check("k_sense");
+}
+
+unsigned stride_blocks(size_t n) {
+  return (unsigned)std::max<size_t>(1, std::min<size_t>((n + 255) / 256, 148 * 8));
+}
+
+// Bin the slab's local set (owned + ghosts) on the column-major local grid.
+template <int ENV>
+vg_status slab_bin(vg_world* w, cudaStream_t s) {
+  const unsigned nb = stride_blocks(w->SB.cap_loc);
+  vg::k_slab_keys<<<nb, 256, 0, s>>>(w->P, w->SL, w->SB, w->cell_id, w->slot, w->count);
+  if (vg_status st = launch_check("k_slab_keys")) return st;
+  vg::k_scan_cells<<<1, 1024, 0, s>>>(w->count, w->cell_start, w->n_cells);
+  if (vg_status st = launch_check("k_scan_cells")) return st;
+  vg::k_slab_scatter<ENV><<<nb, 256, 0, s>>>(w->P, w->SB, w->cell_id, w->slot, w->cell_start,
+                                              w->tmp_rec, w->tmp_id);
+  if (vg_status st = launch_check("k_slab_scatter")) return st;
+  const long long threads = (long long)w->n_cells * 32;
+  vg::k_cell_sort<<<(unsigned)((threads + 255) / 256), 256, 0, s>>>(
+      w->n_cells, w->cell_start, w->tmp_rec, w->tmp_id, w->sorted, w->perm, w->sorted_xy);
+  if (vg_status st = launch_check("k_cell_sort")) return st;
+  w->binned = true;
+  return VG_OK;
+}
+
+vg_status need_slab(const vg_world* w, bool slab, const char* fn) {
+  if (!w) return fail(VG_EINVAL, "%s: world NULL", fn);
+  if (w->slab != slab)
+    return fail(VG_EINVAL, slab ? "%s: needs a slab-mode world" : "%s: not available in slab mode (use vg_slab_*)", fn);
+  return VG_OK;
 }
 
 template <typename T>
@@ -274,8 +334,39 @@ vg_status vg_world_create(const vg_config* cfg, vg_world** out) {
   w->P = derive(*cfg, g);
   w->n_cells = g * g * cfg->n_replicas;
   cudaGetDevice(&w->device);
-  const size_t n = (size_t)w->P.total;
+  size_t n = (size_t)w->P.total;
   vg_status st = VG_OK;
+  if (cfg->shard == VG_SHARD_SLAB) {
+    const int P = cfg->world_size, W = g / P;
+    w->slab = true;
+    w->SL = vg::Slab{cfg->rank * W, (cfg->rank + 1) * W, W, (W + 2) * g};
+    w->n_cells = w->SL.n_lcells;
+    w->left = (cfg->rank + P - 1) % P;
+    w->right = (cfg->rank + 1) % P;
+    const long long col = ((long long)cfg->n_agents + g - 1) / g;
+    const uint32_t cap_msg = cfg->halo_capacity > 0 ? (uint32_t)cfg->halo_capacity
+                                                    : (uint32_t)std::max(1024LL, 4 * col + 256);
+    w->SB.cap_msg = cap_msg;
+    w->SB.cap_loc = (uint32_t)(cfg->n_agents + 2ull * cap_msg);
+    w->msg_bytes = 16 + 20 * (size_t)cap_msg;
+    n = w->SB.cap_loc;
+    if (!st) st = dalloc(w, &w->loc_n, 1);
+    if (!st) st = dalloc(w, &w->slab_ovf, 1);
+    if (!st) st = dalloc(w, &w->SB.loc_rec, n);
+    if (!st) st = dalloc(w, &w->SB.loc_id, n);
+    if (!st) st = dalloc(w, &w->msg, 4 * w->msg_bytes);
+    if (!st) {
+      w->SB.n_loc = w->loc_n;
+      w->SB.overflow = w->slab_ovf;
+      w->SB.send_l = w->msg;
+      w->SB.send_r = w->msg + w->msg_bytes;
+      w->SB.recv_l = w->msg + 2 * w->msg_bytes;
+      w->SB.recv_r = w->msg + 3 * w->msg_bytes;
+      cudaError_t e = cudaMemset(w->msg, 0, 4 * w->msg_bytes);
+      if (e == cudaSuccess) e = cudaMemset(w->slab_ovf, 0, sizeof(uint32_t));
+      if (e != cudaSuccess) st = fail(VG_ECUDA, "slab init: %s", cudaGetErrorString(e));
+    }
+  }
   if (!st) st = dalloc(w, &w->count, w->n_cells);
   if (!st) st = dalloc(w, &w->cell_start, w->n_cells + 1);
   if (!st) st = dalloc(w, &w->cell_id, n);
@@ -321,6 +412,11 @@ void vg_world_destroy(vg_world* w) {
   cudaFree(w->sorted_xy);
   cudaFree(w->act_dev);
   cudaFree(w->err_dev);
+  cudaFree(w->loc_n);
+  cudaFree(w->slab_ovf);
+  cudaFree(w->SB.loc_rec);
+  cudaFree(w->SB.loc_id);
+  cudaFree(w->msg);
   if (w->err_flag) cudaFreeHost(w->err_flag);
   delete w;
 }
@@ -340,6 +436,7 @@ vg_status vg_world_query(const vg_world* w, vg_world_info* info) {
 
 vg_status vg_bin(vg_world* w, const float* state, void* stream) {
   if (!w || !state) return fail(VG_EINVAL, "world/state: NULL");
+  if (vg_status st = need_slab(w, false, "vg_bin")) return st;
   if (vg_status st = check_pending(w)) return st;
   cudaStream_t s = as_stream(stream);
   const float4* in = reinterpret_cast<const float4*>(state);
@@ -370,6 +467,7 @@ vg_status vg_reward(vg_world* w, const vg_outputs* outs, void* stream) {
 
 vg_status vg_integrate(vg_world* w, float* state, const float* actions, void* stream) {
   if (!w || !state || !actions) return fail(VG_EINVAL, "world/state/actions: NULL");
+  if (vg_status st = need_slab(w, false, "vg_integrate")) return st;
   if (vg_status st = check_pending(w)) return st;
   cudaStream_t s = as_stream(stream);
   float4* io = reinterpret_cast<float4*>(state);
@@ -382,6 +480,7 @@ vg_status vg_integrate(vg_world* w, float* state, const float* actions, void* st
 vg_status vg_step(vg_world* w, float* state, const float* actions, const vg_outputs* outs,
                   void* stream) {
   if (!w || !state || !actions || !outs) return fail(VG_EINVAL, "world/state/actions/outs: NULL");
+  if (vg_status st = need_slab(w, false, "vg_step")) return st;
   if (vg_status st = check_pending(w)) return st;
   cudaStream_t s = as_stream(stream);
   float4* io = reinterpret_cast<float4*>(state);
@@ -427,6 +526,128 @@ vg_status vg_get_bins(const vg_world* w, const uint32_t** cell_id, const uint32_
   return VG_OK;
 }
 
+vg_status vg_slab_plan(int32_t grid, int32_t world_size, int32_t rank, int32_t* plan) {
+  if (!plan || world_size < 2 || rank < 0 || rank >= world_size || grid % world_size ||
+      grid / world_size < 2)
+    return fail(VG_EINVAL, "vg_slab_plan: need world_size >= 2, 0 <= rank < world_size, world_size | grid, grid/world_size >= 2");
+  const int W = grid / world_size;
+  plan[0] = rank * W;
+  plan[1] = (rank + 1) * W;
+  plan[2] = (rank + world_size - 1) % world_size;
+  plan[3] = (rank + 1) % world_size;
+  return VG_OK;
+}
+
+vg_status vg_slab_load(vg_world* w, const float* state_global, void* stream) {
+  if (vg_status st = need_slab(w, true, "vg_slab_load")) return st;
+  if (!state_global) return fail(VG_EINVAL, "state_global: NULL");
+  if (vg_status st = check_pending(w)) return st;
+  cudaStream_t s = as_stream(stream);
+  VG_CUDA(cudaMemsetAsync(w->loc_n, 0, sizeof(uint32_t), s));
+  const float4* st4 = reinterpret_cast<const float4*>(state_global);
+  const unsigned nb = stride_blocks((size_t)w->P.N);
+  if (w->P.env == vg::kFlock) {
+    vg::k_slab_load<vg::kFlock><<<nb, 256, 0, s>>>(w->P, w->SL, w->SB, st4, w->err_dev, w->err_flag);
+    if (vg_status st = launch_check("k_slab_load")) return st;
+    return slab_bin<vg::kFlock>(w, s);
+  }
+  vg::k_slab_load<vg::kTag><<<nb, 256, 0, s>>>(w->P, w->SL, w->SB, st4, w->err_dev, w->err_flag);
+  if (vg_status st = launch_check("k_slab_load")) return st;
+  return slab_bin<vg::kTag>(w, s);
+}
+
+vg_status vg_slab_begin(vg_world* w, const float* actions, void* stream) {
+  if (vg_status st = need_slab(w, true, "vg_slab_begin")) return st;
+  if (!actions) return fail(VG_EINVAL, "actions: NULL");
+  if (!w->binned) return fail(VG_EINVAL, "vg_slab_begin: call vg_slab_load first");
+  if (vg_status st = check_pending(w)) return st;
+  cudaStream_t s = as_stream(stream);
+  prof_mark(w, 0, s);
+  VG_CUDA(cudaMemsetAsync(w->loc_n, 0, sizeof(uint32_t), s));
+  VG_CUDA(cudaMemsetAsync(w->SB.send_l, 0, 16, s));
+  VG_CUDA(cudaMemsetAsync(w->SB.send_r, 0, 16, s));
+  const unsigned nb = stride_blocks((size_t)w->P.N / w->cfg.world_size + 1);
+  const float2* a = reinterpret_cast<const float2*>(actions);
+  if (w->P.env == vg::kFlock)
+    vg::k_slab_begin<vg::kFlock><<<nb, 256, 0, s>>>(w->P, w->SL, w->SB, w->cell_start, w->sorted,
+                                                     w->perm, a, w->err_dev, w->err_flag);
+  else
+    vg::k_slab_begin<vg::kTag><<<nb, 256, 0, s>>>(w->P, w->SL, w->SB, w->cell_start, w->sorted,
+                                                   w->perm, a, w->err_dev, w->err_flag);
+  vg_status st = launch_check("k_slab_begin");
+  prof_mark(w, 1, s);
+  return st;
+}
+
+vg_status vg_slab_get_io(vg_world* w, vg_slab_io* io) {
+  if (vg_status st = need_slab(w, true, "vg_slab_get_io")) return st;
+  if (!io) return fail(VG_EINVAL, "io: NULL");
+  io->send_left = w->SB.send_l;
+  io->send_right = w->SB.send_r;
+  io->recv_left = const_cast<unsigned char*>(w->SB.recv_l);
+  io->recv_right = const_cast<unsigned char*>(w->SB.recv_r);
+  io->message_bytes = (int64_t)w->msg_bytes;
+  io->left_rank = w->left;
+  io->right_rank = w->right;
+  io->lo = w->SL.lo;
+  io->hi = w->SL.hi;
+  io->capacity_rows = (int64_t)w->P.N;
+  return VG_OK;
+}
+
+vg_status vg_slab_exchange_loopback(vg_world* const* ws, int32_t n, void* stream) {
+  if (!ws || n < 2) return fail(VG_EINVAL, "vg_slab_exchange_loopback: need >= 2 worlds");
+  for (int g = 0; g < n; ++g) {
+    if (vg_status st = need_slab(ws[g], true, "vg_slab_exchange_loopback")) return st;
+    if (ws[g]->cfg.world_size != n || ws[g]->cfg.rank != g || ws[g]->msg_bytes != ws[0]->msg_bytes)
+      return fail(VG_EINVAL, "vg_slab_exchange_loopback: worlds must be ranks 0..n-1 of one slab group");
+  }
+  cudaStream_t s = as_stream(stream);
+  for (int g = 0; g < n; ++g) {
+    vg_world* w = ws[g];
+    VG_CUDA(cudaMemcpyAsync(const_cast<unsigned char*>(ws[w->left]->SB.recv_r), w->SB.send_l,
+                            w->msg_bytes, cudaMemcpyDeviceToDevice, s));
+    VG_CUDA(cudaMemcpyAsync(const_cast<unsigned char*>(ws[w->right]->SB.recv_l), w->SB.send_r,
+                            w->msg_bytes, cudaMemcpyDeviceToDevice, s));
+  }
+  return VG_OK;
+}
+
+vg_status vg_slab_finish(vg_world* w, const vg_outputs* outs, void* stream) {
+  if (vg_status st = need_slab(w, true, "vg_slab_finish")) return st;
+  if (!outs) return fail(VG_EINVAL, "outs: NULL");
+  cudaStream_t s = as_stream(stream);
+  vg::k_slab_unpack<<<stride_blocks(2ull * w->SB.cap_msg), 256, 0, s>>>(w->SB);
+  if (vg_status st = launch_check("k_slab_unpack")) return st;
+  prof_mark(w, 2, s);
+  vg_status st = (w->P.env == vg::kFlock) ? slab_bin<vg::kFlock>(w, s) : slab_bin<vg::kTag>(w, s);
+  if (st) return st;
+  prof_mark(w, 3, s);
+  prof_mark(w, 4, s);
+  st = launch_sense<true>(w, outs, s);
+  prof_mark(w, 5, s);
+  if (w->prof_n < w->prof_max) ++w->prof_n;
+  return st;
+}
+
+vg_status vg_slab_sense(vg_world* w, const vg_outputs* outs, void* stream) {
+  if (vg_status st = need_slab(w, true, "vg_slab_sense")) return st;
+  if (!outs) return fail(VG_EINVAL, "outs: NULL");
+  if (!w->binned) return fail(VG_EINVAL, "vg_slab_sense: call vg_slab_load first");
+  return launch_sense<true>(w, outs, as_stream(stream));
+}
+
+vg_status vg_slab_own_count(vg_world* w, void* stream, int64_t* n_own) {
+  if (vg_status st = need_slab(w, true, "vg_slab_own_count")) return st;
+  if (!n_own) return fail(VG_EINVAL, "n_own: NULL");
+  VG_CUDA(cudaStreamSynchronize(as_stream(stream)));
+  uint32_t a = 0, b = 0;
+  VG_CUDA(cudaMemcpy(&a, w->cell_start + w->P.G, 4, cudaMemcpyDeviceToHost));
+  VG_CUDA(cudaMemcpy(&b, w->cell_start + (size_t)(w->SL.W + 1) * w->P.G, 4, cudaMemcpyDeviceToHost));
+  *n_own = (int64_t)b - (int64_t)a;
+  return VG_OK;
+}
+
 vg_status vg_profile_begin(vg_world* w, int32_t max_steps) {
   if (!w || max_steps < 0 || max_steps > (1 << 20)) return fail(VG_EINVAL, "world/max_steps");
   const size_t need = (size_t)max_steps * (VG_N_PHASES + 1);
@@ -464,6 +685,14 @@ vg_status vg_sync_errors(vg_world* w, void* stream, int64_t* bad_agent) {
   unsigned long long v = 0;
   VG_CUDA(cudaMemcpy(&v, w->err_dev, sizeof(v), cudaMemcpyDeviceToHost));
   if (bad_agent) *bad_agent = (v == ~0ull) ? -1 : (int64_t)v;
+  if (w->slab) {
+    uint32_t ovf = 0;
+    VG_CUDA(cudaMemcpy(&ovf, w->slab_ovf, 4, cudaMemcpyDeviceToHost));
+    if (ovf) {
+      VG_CUDA(cudaMemset(w->slab_ovf, 0, 4));
+      return fail(VG_EOVERFLOW, "slab halo/local capacity overflow (raise halo_capacity)");
+    }
+  }
   if (v != ~0ull) {
     const unsigned long long none = ~0ull;
     VG_CUDA(cudaMemcpy(w->err_dev, &none, sizeof(none), cudaMemcpyHostToDevice));

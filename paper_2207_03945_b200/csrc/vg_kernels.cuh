@@ -46,6 +46,15 @@ struct Outs {
   uint32_t* n_collide;
   uint32_t* n_touch;
   uint32_t* occ;
+  uint32_t* agent_id;   // slab mode: global id of each output row
+};
+
+// Slab mode: this rank owns global cell columns [lo, hi), W = hi - lo >= 2.
+// The local grid has W + 2 columns (ghost columns 0 and W+1) x G rows, column-major:
+// local cell = lcx * G + cy, so the owned agents are the contiguous sorted range
+// [cell_start[G], cell_start[(W+1) G]).
+struct Slab {
+  int lo, hi, W, n_lcells;
 };
 
 // Record the smallest offending global agent index (S:59 error convention) and raise the
@@ -270,10 +279,10 @@ struct Seg {
   float qsx, qsy;    // query image shift (0 or -L)
 };
 
-template <int ENV, bool VISION>
+template <int ENV, bool VISION, bool SLAB>
 __global__ void __launch_bounds__(kSenseWarps * 32, 8) k_sense(
     Params P, const uint32_t* __restrict__ cell_start, const float4* __restrict__ sorted,
-    const float2* __restrict__ sorted_xy, const uint32_t* __restrict__ perm, Outs O) {
+    const float2* __restrict__ sorted_xy, const uint32_t* __restrict__ perm, Outs O, Slab SL) {
   __shared__ uint32_t s_min[kSenseWarps][kMaxViewSlots];
   __shared__ float4 s_q[kSenseWarps][kQueue];
   __shared__ Seg s_seg[6];
@@ -281,12 +290,37 @@ __global__ void __launch_bounds__(kSenseWarps * 32, 8) k_sense(
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int c = blockIdx.x;
-  const int r = c / P.G2;
-  const int cl = c - r * P.G2;
-  const int cy = cl / P.G, cx = cl - cy * P.G;
+  // Replica layout: cell = r G^2 + cy G + cx.  Slab layout: owned local column lcx = 1 + c/G.
+  const int r = SLAB ? 0 : c / P.G2;
+  const int cl = SLAB ? (1 + c / P.G) * P.G + c % P.G : c - r * P.G2;
+  const int cy = SLAB ? c % P.G : cl / P.G;
+  const int cx = SLAB ? 1 + c / P.G : cl - cy * P.G;
   const uint32_t* cs = cell_start + (size_t)r * P.G2;
 
-  if (threadIdx.x == 0) {
+  if (threadIdx.x == 0 && SLAB) {
+    // Stencil columns lcx-1..lcx+1 of the local grid (no x-wrap: ghost columns hold the
+    // neighbours).  Ghost column 0 of rank 0 is global column G-1 (candidate shift -L);
+    // ghost column W+1 of the last rank is global column 0 (query shift -L) (A11).
+    int ns = 0;
+    const float mL = -P.L;
+    for (int dxc = -1; dxc <= 1; ++dxc) {
+      const int col = cx + dxc;
+      const float csx = (col == 0 && SL.lo == 0) ? mL : 0.f;
+      const float qsx = (col == SL.W + 1 && SL.hi == P.G) ? mL : 0.f;
+      const int base = col * P.G;
+      if (cy >= 1 && cy <= P.G - 2) {
+        s_seg[ns++] = Seg{cs[base + cy - 1], cs[base + cy + 2], csx, 0.f, qsx, 0.f};
+      } else if (cy == 0) {                          // rows G-1 | 0, 1
+        s_seg[ns++] = Seg{cs[base + P.G - 1], cs[base + P.G], csx, mL, qsx, 0.f};
+        s_seg[ns++] = Seg{cs[base], cs[base + 2], csx, 0.f, qsx, 0.f};
+      } else {                                       // rows G-2, G-1 | 0
+        s_seg[ns++] = Seg{cs[base + P.G - 2], cs[base + P.G], csx, 0.f, qsx, 0.f};
+        s_seg[ns++] = Seg{cs[base], cs[base + 1], csx, 0.f, qsx, mL};
+      }
+    }
+    s_nseg = ns;
+  }
+  if (threadIdx.x == 0 && !SLAB) {
     int ns = 0;
     const float mL = -P.L;
     for (int dy = -1; dy <= 1; ++dy) {
@@ -422,8 +456,9 @@ __global__ void __launch_bounds__(kSenseWarps * 32, 8) k_sense(
       const long long t = (long long)ntouch * P.touch_fix;
       rsum += (tq == 1u) ? t : -t;                                    // P:194 touch rule
     }
-    const size_t row = (size_t)r * P.N + perm[q];
+    const size_t row = SLAB ? (size_t)(q - cs[P.G]) : (size_t)r * P.N + perm[q];
     if (lane == 0) {
+      if (SLAB && O.agent_id) O.agent_id[row] = perm[q];
       if (O.reward) O.reward[row] = __ll2float_rn(rsum) * kFixInv;
       if (O.n_neigh) O.n_neigh[row] = nn;
       if (O.n_collide) O.n_collide[row] = ncol;
@@ -455,6 +490,171 @@ __global__ void __launch_bounds__(kSenseWarps * 32, 8) k_sense(
       }
     }
     __syncwarp();
+  }
+}
+
+
+// ------------------------------------------------------------------------- slab mode
+// One world split over P ranks by x-slabs of cell columns.
+// Message = {u32 count, u32 pad[3]} + float4 rec[cap] + u32 id[cap] (global agent ids).
+struct SlabBufs {
+  uint32_t* n_loc;         // local set size (owned + ghosts), device counter
+  float4* loc_rec;         // [cap_loc]
+  uint32_t* loc_id;        // [cap_loc] global agent id
+  uint32_t cap_loc;
+  unsigned char* send_l;   // message to the left neighbour (global columns lo-1, lo)
+  unsigned char* send_r;   // message to the right neighbour (global columns hi-1, hi)
+  const unsigned char* recv_l;
+  const unsigned char* recv_r;
+  uint32_t cap_msg;        // records per message
+  uint32_t* overflow;      // device flag (VG_EOVERFLOW)
+};
+
+__device__ __forceinline__ uint32_t* msg_count(unsigned char* m) { return reinterpret_cast<uint32_t*>(m); }
+__device__ __forceinline__ float4* msg_rec(unsigned char* m) { return reinterpret_cast<float4*>(m + 16); }
+__device__ __forceinline__ uint32_t* msg_id(unsigned char* m, uint32_t cap) {
+  return reinterpret_cast<uint32_t*>(m + 16 + 16 * (size_t)cap);
+}
+
+__device__ __forceinline__ void loc_append(const SlabBufs& B, float4 s, uint32_t id) {
+  const uint32_t k = atomicAdd(B.n_loc, 1u);
+  if (k < B.cap_loc) { B.loc_rec[k] = s; B.loc_id[k] = id; }
+  else atomicExch(B.overflow, 1u);
+}
+
+__device__ __forceinline__ void msg_append(unsigned char* m, uint32_t cap, uint32_t* ovf,
+                                           float4 s, uint32_t id) {
+  const uint32_t k = atomicAdd(msg_count(m), 1u);
+  if (k < cap) { msg_rec(m)[k] = s; msg_id(m, cap)[k] = id; }
+  else atomicExch(ovf, 1u);
+}
+
+__device__ __forceinline__ int global_col(const Params& P, float x) {
+  return min(max(__float2int_rz(__fmul_rn(x, P.gs)), 0), P.G - 1);   // A16
+}
+
+// Route one post-integrate agent of this rank: owned columns stay local; columns lo-1 / hi
+// (migrants, <= 1 column per step since s_max < cell size) stay local as ghosts and go to
+// the neighbour that now owns them; boundary columns lo / hi-1 go to the neighbour as ghosts.
+__device__ __forceinline__ void slab_route(const Params& P, const Slab& SL, const SlabBufs& B,
+                                           float4 s, uint32_t id, unsigned long long* err,
+                                           volatile uint32_t* flag) {
+  const int d = (global_col(P, s.x) - SL.lo + P.G) % P.G;   // column offset from lo
+  if (d > SL.W && d != P.G - 1) {                            // moved more than one column
+    report_bad(err, flag, id);
+    return;
+  }
+  loc_append(B, s, id);
+  if (d == 0 || d == P.G - 1) msg_append(B.send_l, B.cap_msg, B.overflow, s, id);
+  if (d == SL.W - 1 || d == SL.W) msg_append(B.send_r, B.cap_msg, B.overflow, s, id);
+}
+
+// Begin a slab step: integrate the owned rows (the previous binning's owned range, in row
+// order; actions[row]) exactly as K1 does, then route them.
+template <int ENV>
+__global__ void __launch_bounds__(256) k_slab_begin(
+    Params P, Slab SL, SlabBufs B, const uint32_t* __restrict__ cell_start,
+    const float4* __restrict__ sorted, const uint32_t* __restrict__ perm,
+    const float2* __restrict__ actions, unsigned long long* err, volatile uint32_t* flag) {
+  const uint32_t own_b = cell_start[P.G];
+  const uint32_t n_own = cell_start[(SL.W + 1) * P.G] - own_b;
+  for (uint32_t row = blockIdx.x * blockDim.x + threadIdx.x; row < n_own;
+       row += gridDim.x * blockDim.x) {
+    float4 s = sorted[own_b + row];
+    const uint32_t id = perm[own_b + row];
+    const float2 a = actions[row];
+    bool bad = isnan(a.x) || isnan(a.y);
+    float turn, dist;
+    if (ENV == kFlock) {
+      const float acc = fminf(fmaxf(a.x, -P.a_max), P.a_max);
+      turn = fminf(fmaxf(a.y, -P.theta_max), P.theta_max);
+      const float sp = fminf(fmaxf(__fadd_rn(s.w, acc), P.s_min), P.s_max);
+      s.w = sp;
+      dist = sp;
+    } else {
+      turn = fminf(fmaxf(a.x, -P.theta_max), P.theta_max);
+      const float smax = (id >= (uint32_t)P.first_chaser) ? P.s_max_chaser : P.s_max;
+      dist = fminf(fmaxf(a.y, 0.f), smax);
+    }
+    s.z = wrap_heading(__fadd_rn(s.z, turn), P.two_pi);
+    float sn, cs;
+    sincosf(s.z, &sn, &cs);
+    s.x = wrap_pos(s.x, __fmul_rn(dist, cs), P.L);
+    s.y = wrap_pos(s.y, __fmul_rn(dist, sn), P.L);
+    if (bad) report_bad(err, flag, id);
+    slab_route(P, SL, B, s, id, err, flag);
+  }
+}
+
+// Initial distribution: every rank reads the full global state and keeps what it owns
+// plus its two ghost columns (no exchange needed).
+template <int ENV>
+__global__ void __launch_bounds__(256) k_slab_load(Params P, Slab SL, SlabBufs B,
+                                                   const float4* __restrict__ state,
+                                                   unsigned long long* err,
+                                                   volatile uint32_t* flag) {
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < (uint32_t)P.N;
+       i += gridDim.x * blockDim.x) {
+    const float4 s = state[i];
+    bool bad = !(s.x >= 0.f && s.x < P.L && s.y >= 0.f && s.y < P.L && s.z >= 0.f &&
+                 s.z < P.two_pi);
+    if (ENV == kFlock) bad |= !isfinite(s.w);
+    if (bad) { report_bad(err, flag, i); continue; }
+    const int d = (global_col(P, s.x) - SL.lo + P.G) % P.G;
+    if (d <= SL.W || d == P.G - 1) loc_append(B, s, i);
+  }
+}
+
+// Append the records received from both neighbours to the local set.
+__global__ void __launch_bounds__(256) k_slab_unpack(SlabBufs B) {
+  const uint32_t nl = min(*reinterpret_cast<const uint32_t*>(B.recv_l), B.cap_msg);
+  const uint32_t nr = min(*reinterpret_cast<const uint32_t*>(B.recv_r), B.cap_msg);
+  if (*reinterpret_cast<const uint32_t*>(B.recv_l) > B.cap_msg ||
+      *reinterpret_cast<const uint32_t*>(B.recv_r) > B.cap_msg) {
+    if (blockIdx.x == 0 && threadIdx.x == 0) atomicExch(B.overflow, 1u);
+  }
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < nl + nr;
+       i += gridDim.x * blockDim.x) {
+    const unsigned char* m = (i < nl) ? B.recv_l : B.recv_r;
+    const uint32_t k = (i < nl) ? i : i - nl;
+    loc_append(B, reinterpret_cast<const float4*>(m + 16)[k],
+               reinterpret_cast<const uint32_t*>(m + 16 + 16 * (size_t)B.cap_msg)[k]);
+  }
+}
+
+// Local cell ids (column-major, A16 global formula) + histogram slot of the local set.
+__global__ void __launch_bounds__(256) k_slab_keys(Params P, Slab SL, SlabBufs B,
+                                                   uint32_t* __restrict__ cell_id,
+                                                   uint32_t* __restrict__ slot,
+                                                   uint32_t* __restrict__ count) {
+  const uint32_t n = min(*B.n_loc, B.cap_loc);
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += gridDim.x * blockDim.x) {
+    const float4 s = B.loc_rec[i];
+    const int gx = global_col(P, s.x), gy = global_col(P, s.y);
+    const int lcx = min((gx - SL.lo + 1 + P.G) % P.G, SL.W + 1);
+    const uint32_t c = (uint32_t)(lcx * P.G + gy);
+    cell_id[i] = c;
+    slot[i] = atomicAdd(&count[c], 1u);
+  }
+}
+
+template <int ENV>
+__global__ void __launch_bounds__(256) k_slab_scatter(Params P, SlabBufs B,
+                                                      const uint32_t* __restrict__ cell_id,
+                                                      const uint32_t* __restrict__ slot,
+                                                      const uint32_t* __restrict__ cell_start,
+                                                      float4* __restrict__ tmp_rec,
+                                                      uint32_t* __restrict__ tmp_id) {
+  const uint32_t n = min(*B.n_loc, B.cap_loc);
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += gridDim.x * blockDim.x) {
+    const uint32_t pos = cell_start[cell_id[i]] + slot[i];
+    float4 s = B.loc_rec[i];
+    const uint32_t id = B.loc_id[i];
+    if (ENV == kTag) s.w = (id >= (uint32_t)P.first_chaser) ? 1.f : 0.f;
+    tmp_rec[pos] = s;
+    tmp_id[pos] = id;
   }
 }
 
