@@ -7,8 +7,8 @@ Metric (BASELINE.json): agent-steps/s of vg_step = integrate + bin + sense + rew
     python bench.py [--gpus N] [--steps K] [--warmup W] [--config c5] [--impl ours|reference]
 
 N > 1: launched by torchrun, one process per GPU.  Replica workloads (c1-c4) shard the
-replicas over ranks with no collective ("replicas only"); c5 (one 1M-agent world) runs an
-independent world per rank until slab mode exists.  Rank 0 prints one JSON
+replicas over ranks with no collective ("replicas only"); c5 (one 1M-agent world) is split
+into x-slabs with a one-column halo exchanged over NCCL each step.  Rank 0 prints one JSON
 line.  Timing: W untimed warm-up steps; K timed steps, each bracketed by CUDA events on
 the launching stream with a 256 MiB L2 flush between steps (outside the events);
 barrier + synchronize around the timed region; max over ranks.
@@ -199,6 +199,60 @@ def run_reference(args):
 
 
 # ---------------------------------------------------------------------------- our leg
+class ReplicaRunner:
+    """Replica workloads (and c5 at N = 1): one libvg world per rank, vg_step."""
+
+    def __init__(self, p, device, rank, torch, vg):
+        self.p, self.torch = p, torch
+        self.w = vg.World(p, device=device)
+        self.out = self.w.alloc_outputs()
+        self.state = torch.from_numpy(vi.init_state(p, seed=1000 * rank)).to(device)
+        self.launches = 5
+        self.phase_names = {"integrate_bin": "integrate_bin", "scan_cells": "scan_cells",
+                            "scatter": "scatter", "cell_sort": "cell_sort", "sense": "sense"}
+
+    def step(self, acts):
+        self.w.step(self.state, acts, self.out)
+
+    def step_host(self, acts_h, rew_h):
+        self.w.step_host(self.state, acts_h, self.out, rew_h)
+
+    def pairs_local(self):
+        return float(self.out.n_neigh.sum(dtype=self.torch.float64).item())
+
+
+class SlabRunner:
+    """c5 at N > 1: one world split into x-slabs (vg_slab_*), halo exchanged with
+    torch.distributed P2P over NCCL every step."""
+
+    def __init__(self, p, device, rank, world, torch, vg):
+        from paper_2207_03945_b200 import slab
+        self.p, self.torch, self.slab = p, torch, slab
+        self.w = vg.World(p, device=device, slab={"rank": rank, "world_size": world})
+        self.out = self.w.alloc_outputs()
+        full = torch.from_numpy(vi.init_state(p, seed=0)).to(device)   # same world everywhere
+        self.w.slab_load(full)
+        self.w.slab_sense(self.out)
+        del full
+        self.act_dev = torch.zeros((1, p.n_agents, 2), dtype=torch.float32, device=device)
+        self.launches = 7   # begin, unpack, keys, scan, scatter, cell_sort, sense
+        self.phase_names = {"integrate_bin": "begin (integrate+route)",
+                            "scan_cells": "exchange+unpack", "scatter": "bin local set",
+                            "cell_sort": "-", "sense": "sense"}
+
+    def step(self, acts):
+        self.slab.slab_step_dist(self.w, acts, self.out)
+
+    def step_host(self, acts_h, rew_h):
+        self.act_dev.copy_(acts_h, non_blocking=True)
+        self.slab.slab_step_dist(self.w, self.act_dev, self.out)
+        rew_h.copy_(self.out.reward, non_blocking=True)
+
+    def pairs_local(self):
+        n = self.w.slab_own_count()
+        return float(self.out.n_neigh[0, :n].sum(dtype=self.torch.float64).item())
+
+
 def run_ours(args):
     import torch
     import torch.distributed as dist
@@ -210,15 +264,19 @@ def run_ours(args):
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     device = torch.device("cuda", local)
     torch.cuda.set_device(device)
-    p, scaling = local_params(args.config, world, rank)
-    w = vg.World(p, device=device)
-    out = w.alloc_outputs()
-    state = torch.from_numpy(vi.init_state(p, seed=1000 * rank)).to(device)
+    slab_mode = args.config == "c5" and world > 1
+    if slab_mode:
+        p, scaling = vi.workload("c5"), "strong"
+        run = SlabRunner(p, device, rank, world, torch, vg)
+    else:
+        p, scaling = local_params(args.config, world, rank)
+        run = ReplicaRunner(p, device, rank, torch, vg)
+    w = run.w
     acts = action_pool(p, torch, device, seed=rank)
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=device)
 
     for k in range(args.warmup):
-        w.step(state, acts[k % len(acts)], out)
+        run.step(acts[k % len(acts)])
     torch.cuda.synchronize()
     w.sync_errors()
 
@@ -228,15 +286,13 @@ def run_ours(args):
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
-    nn_sum = torch.zeros((), dtype=torch.float64, device=device)
     with ClockSampler(local) as clk:
         w.profile_begin(K)
         for k in range(K):
             flush.fill_(k & 0xFF)                 # evict L2 between steps (not timed)
             ev0[k].record()
-            w.step(state, acts[k % len(acts)], out)
+            run.step(acts[k % len(acts)])
             ev1[k].record()
-            nn_sum += out.n_neigh.sum(dtype=torch.float64)   # pairs evaluated (not timed)
         torch.cuda.synchronize()
         phases, nrec = w.profile_end()
     if world > 1:
@@ -248,24 +304,24 @@ def run_ours(args):
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     max_ms = float(t.item())
-    agents_local = p.total_agents
-    agents_all = agents_local * world
+    agents_all = p.n_agents if slab_mode else p.total_agents * world
     value = agents_all * K / (max_ms / 1e3)
+    pairs_local = run.pairs_local()            # in-radius pairs of the last step (this rank)
 
-    # ---- end to end through the public API with host buffers (vg_step_host)
+    # ---- end to end through the public API with host buffers
     e2e = None
     if not args.no_e2e:
         acts_h = [a.cpu().pin_memory() for a in acts[:2]]
-        rew_h = torch.empty((p.n_replicas, p.n_agents), dtype=torch.float32).pin_memory()
+        rew_h = torch.empty(tuple(run.out.reward.shape), dtype=torch.float32).pin_memory()
         stream = torch.cuda.current_stream(device)
         for k in range(2):
-            w.step_host(state, acts_h[k % 2], out, rew_h)
+            run.step_host(acts_h[k % 2], rew_h)
         stream.synchronize()
         if world > 1:
             dist.barrier()
         t0 = time.perf_counter()
         for k in range(K):
-            w.step_host(state, acts_h[k % 2], out, rew_h)
+            run.step_host(acts_h[k % 2], rew_h)
             stream.synchronize()               # the step's reward is readable on the host
         e2e_s = time.perf_counter() - t0
         te = torch.tensor([e2e_s], dtype=torch.float64, device=device)
@@ -274,31 +330,33 @@ def run_ours(args):
         e2e = {"value": agents_all * K / float(te.item()), "unit": UNIT,
                "h2d_bytes_per_step": int(acts_h[0].numel() * 4),
                "d2h_bytes_per_step": int(rew_h.numel() * 4),
-               "note": "vg_step_host: actions H2D from pinned host, reward D2H, stream sync per step, wall clock"}
+               "note": ("vg_step_host" if not slab_mode else "actions H2D + slab step + reward D2H")
+                       + ": pinned host buffers, stream sync per step, wall clock, max over ranks"}
 
     if rank == 0:
         peaks, peak_src = measured_peaks()
         hbm = float(peaks.get("hbm_gbs", 6441.6))
         sm_mhz = float(peaks.get("sm_max_mhz", 1965.0))
         alu_peak = 148 * 128 * sm_mhz * 1e6 / 1e12      # fp32 lane-ops/s, TFLOP/s-equivalent
-        pairs_per_step = float(nn_sum.item()) / K
         sense_s = phases["sense"] / 1e3 / nrec
-        achieved = ALG_OPS_PER_PAIR * pairs_per_step / sense_s / 1e12
-        n = agents_local
+        achieved = ALG_OPS_PER_PAIR * pairs_local / sense_s / 1e12
+        n = p.total_agents if not slab_mode else p.n_agents // world
         obs_b = 4 * w.obs_dim + 4 * w.occ_words + SENSE_BYTES_FIXED
         stage_bytes = {"integrate_bin": 48 * n, "scan_cells": 8 * w.n_cells,
                        "scatter": 44 * n, "cell_sort": 40 * n, "sense": obs_b * n}
         stages = {}
+        tot_ph = sum(phases.values()) or 1.0
         for k2, ms in phases.items():
             avg = ms / nrec
             gbs = stage_bytes[k2] / (avg / 1e3) / 1e9 if avg > 0 else None
-            stages[k2] = {"ms": round(avg, 5), "alg_bytes": stage_bytes[k2],
-                          "GBps": round(gbs, 1) if gbs else None,
-                          "hbm_frac": round(gbs / hbm, 4) if gbs else None,
-                          "share": round(ms / sum(phases.values()), 4)}
+            stages[run.phase_names[k2]] = {
+                "ms": round(avg, 5), "alg_bytes": stage_bytes[k2],
+                "GBps": round(gbs, 1) if gbs else None,
+                "hbm_frac": round(gbs / hbm, 4) if gbs else None,
+                "share": round(ms / tot_ph, 4)}
         traffic = None
         tpath = os.path.join(ROOT, "profiles", "sense_traffic.json")
-        if os.path.exists(tpath):
+        if os.path.exists(tpath) and world == 1:
             try:
                 tj = json.load(open(tpath))
                 if tj.get("config") == args.config:
@@ -310,24 +368,30 @@ def run_ours(args):
             rate, sample, cores = oracle_rate(p, args.cpu_seconds)
             cpu = {"value": rate, "unit": UNIT, "cores": cores, "kind": "oracle",
                    "sample": sample}
+        if slab_mode:
+            par = f"slab{world}: x-slabs of {w.grid // world} cell columns + halo over NCCL"
+        elif world > 1:
+            par = f"replicas over {world} ranks (no collective)"
+        else:
+            par = "single GPU"
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": K,
             "warmup": args.warmup, "ms_per_step": max_ms / K, "higher_is_better": True,
             "scaling": scaling, "vs_baseline": None, "dtype": "f32", "data": "synthetic",
             "config": {"workload": args.config, "desc": vi.WORKLOAD_DESCRIPTIONS[args.config],
                        "R_per_gpu": p.n_replicas, "N": p.n_agents, "G": w.grid,
-                       "parallelism": ("replicas" if world > 1 else "single"),
+                       "parallelism": par,
                        "l2": "256 MiB buffer written between timed steps (outside events)"},
             "roofline": {"kernel": "k_sense (sector vision + reward)", "bound": "alu",
                          "achieved": achieved, "peak": alu_peak, "unit": "TFLOP/s",
                          "frac": achieved / alu_peak, "traffic": traffic,
-                         "basis": f"{ALG_OPS_PER_PAIR} fp32 ops x {pairs_per_step:.4g} "
+                         "basis": f"{ALG_OPS_PER_PAIR} fp32 ops x {pairs_local:.4g} "
                                   f"in-radius pairs per launch / mean k_sense time; peak = "
                                   f"148 SM x 128 lanes x {sm_mhz:.0f} MHz (1 op/lane/clk)"},
             "stages": stages,
             "hbm_peak_gbs": hbm, "peak_source": peak_src,
             "e2e": e2e,
-            "gpu_launches": 5 * K,
+            "gpu_launches": run.launches * K,
             "clocks": clk.summary(),
             "cpu_baseline": cpu,
             "context": PAPER_CONTEXT,
