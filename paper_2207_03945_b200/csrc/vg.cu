@@ -244,7 +244,7 @@ int sense_chunks(const vg_world* w) {
   const long long warps = (long long)w->n_cells * vg::kSenseWarps;
   const long long per_cell = (w->P.total + w->n_cells - 1) / w->n_cells;
   long long ch = (target_warps + warps - 1) / warps;
-  ch = std::min(ch, std::max(1LL, (per_cell + vg::kSenseWarps - 1) / vg::kSenseWarps));
+  ch = std::min(ch, std::max(1LL, (per_cell + 2 * vg::kSenseWarps - 1) / (2 * vg::kSenseWarps)));
   return (int)std::max(1LL, std::min(ch, 1024LL));
 }
 
@@ -375,7 +375,7 @@ vg_status vg_world_create(const vg_config* cfg, vg_world** out) {
   if (!st) st = dalloc(w, &w->perm, n);
   if (!st) st = dalloc(w, &w->tmp_rec, n);
   if (!st) st = dalloc(w, &w->sorted, n);
-  if (!st) st = dalloc(w, &w->sorted_xy, n);
+  if (!st) st = dalloc(w, &w->sorted_xy, n + 64);   // padded: unpredicated K4 loads
   if (!st) st = dalloc(w, &w->act_dev, n);
   if (!st) st = dalloc(w, &w->err_dev, 1);
   if (!st) {

@@ -283,8 +283,8 @@ template <int ENV, bool VISION, bool SLAB>
 __global__ void __launch_bounds__(kSenseWarps * 32, 8) k_sense(
     Params P, const uint32_t* __restrict__ cell_start, const float4* __restrict__ sorted,
     const float2* __restrict__ sorted_xy, const uint32_t* __restrict__ perm, Outs O, Slab SL) {
-  __shared__ uint32_t s_min[kSenseWarps][kMaxViewSlots];
-  __shared__ float4 s_q[kSenseWarps][kQueue];
+  __shared__ uint32_t s_min[kSenseWarps][2][kMaxViewSlots];
+  __shared__ float4 s_q[kSenseWarps][2][kQueue];
   __shared__ Seg s_seg[6];
   __shared__ int s_nseg;
 
@@ -344,31 +344,41 @@ __global__ void __launch_bounds__(kSenseWarps * 32, 8) k_sense(
   __syncthreads();
   const int nseg = s_nseg;
   const uint32_t qb = cs[cl], qe = cs[cl + 1];
-  const unsigned lt_mask = (1u << lane) - 1u;
-  uint32_t* my_min = s_min[warp];
-  float4* my_q = s_q[warp];
-
-  // Queries of this cell handled by this CTA: chunk blockIdx.y of gridDim.y (small worlds
-  // spread one cell's queries over several CTAs to fill the GPU).
-  const uint32_t qstride = kSenseWarps * gridDim.y;
-  for (uint32_t q = qb + blockIdx.y * kSenseWarps + warp; q < qe; q += qstride) {
-    const float4 me = sorted[q];
-    const uint32_t tq = (ENV == kTag) ? (uint32_t)me.w : 0u;
-    float sn = 0.f, csn = 0.f;
-    if (VISION) {
-      sincosf(me.z, &sn, &csn);
+  unsigned lt_mask;
+  asm("mov.u32 %0, %%lanemask_lt;" : "=r"(lt_mask));
+  // Each warp senses NQ = 2 queries of this cell at once: every candidate load, image
+  // shift and loop step is shared; each query has its own ballot, queue, sector row and
+  // accumulators.  A missing second query gets a NaN position (never a neighbour).
+  constexpr int NQ = 2;
+  const uint32_t qstride = NQ * kSenseWarps * gridDim.y;
+  for (uint32_t q0 = qb + NQ * (blockIdx.y * kSenseWarps + warp); q0 < qe; q0 += qstride) {
+    float4 me[NQ];
+    bool live[NQ];
+    uint32_t tq[NQ], pushed[NQ], ncol[NQ], ntouch[NQ];
+    float sn[NQ], csn[NQ];
+    long long rs[NQ];
+    int nq[NQ];
 #pragma unroll
-      for (int w = 0; w < kMaxViewSlots / 32; ++w) my_min[32 * w + lane] = kOneBits;
+    for (int t = 0; t < NQ; ++t) {
+      live[t] = q0 + t < qe;
+      me[t] = live[t] ? sorted[q0 + t] : make_float4(__int_as_float(0x7fc00000), 0.f, 0.f, 0.f);
+      tq[t] = (ENV == kTag) ? (uint32_t)me[t].w : 0u;
+      sn[t] = csn[t] = 0.f;
+      if (VISION) {
+        sincosf(me[t].z, &sn[t], &csn[t]);
+#pragma unroll
+        for (int w = 0; w < kMaxViewSlots / 32; ++w) s_min[warp][t][32 * w + lane] = kOneBits;
+      }
+      pushed[t] = ncol[t] = ntouch[t] = 0u;
+      rs[t] = 0;
+      nq[t] = 0;
     }
-    uint32_t pushed = 0, ncol = 0, ntouch = 0;
-    long long rs = 0;
-    int nq = 0;
     __syncwarp();
 
-    // Pair pass over one queue entry (dx, dy, d^2, index | type << 31).
-    auto process = [&](const float4 e) {
+    // Pair pass over one queue entry (dx, dy, d^2, index | type << 31) of query t.
+    auto process = [&](const int t, const float4 e) {
       const uint32_t tagbits = __float_as_uint(e.w);
-      if ((tagbits & 0x7fffffffu) == q) return;                      // j != i
+      if ((tagbits & 0x7fffffffu) == q0 + t) return;                 // j != i
       const uint32_t tj = tagbits >> 31;
       const float d2 = e.z;
       const bool contact = d2 <= P.contact2;                          // A6 (inclusive)
@@ -378,115 +388,140 @@ __global__ void __launch_bounds__(kSenseWarps * 32, 8) k_sense(
       const float f = contact ? -P.c_collide
                               : fminf(fmaf(P.k_rise, d, P.b_rise), fmaf(P.nk_fall, d, P.b_fall));
       if (ENV == kFlock) {
-        rs += __float2ll_rn(f * kFix);
-        ncol += contact ? 1u : 0u;
+        rs[t] += __float2ll_rn(f * kFix);
+        ncol[t] += contact ? 1u : 0u;
       } else {
         if (contact) {
-          if (tj == tq) ++ncol; else ++ntouch;
+          if (tj == tq[t]) ++ncol[t]; else ++ntouch[t];
         }
-        if (tq == 0u && tj == 0u) rs += __float2ll_rn((P.w_prox * f) * kFix);
+        if (tq[t] == 0u && tj == 0u) rs[t] += __float2ll_rn((P.w_prox * f) * kFix);
       }
       if (VISION) {
         // Bearing in the agent frame (A3): phi = atan2(h x d, h . d), CCW-positive.
-        const float fwd = fmaf(csn, e.x, sn * e.y);
-        const float left = fmaf(csn, e.y, -sn * e.x);
+        const float fwd = fmaf(csn[t], e.x, sn[t] * e.y);
+        const float left = fmaf(csn[t], e.y, -sn[t] * e.x);
         const float u = fmaf(vg_atan2(left, fwd), P.inv_fov, 0.5f);   // fraction of the fov
         if (u >= 0.f && u < 1.f) {
           const int k = min((int)(u * P.fv), P.v - 1);
           const float val = fminf(d * P.inv_dv, kBelowOne);
-          atomicMin(&my_min[tj * P.v + k], __float_as_uint(val));
+          atomicMin(&s_min[warp][t][tj * P.v + k], __float_as_uint(val));
         }
       }
     };
 
     for (int sgi = 0; sgi < nseg; ++sgi) {
       const Seg sg = s_seg[sgi];
-      const float qx = me.x + sg.qsx, qy = me.y + sg.qsy;            // exact (Sterbenz)
+      float qx[NQ], qy[NQ];
+#pragma unroll
+      for (int t = 0; t < NQ; ++t) {
+        qx[t] = me[t].x + sg.qsx;                                     // exact (Sterbenz)
+        qy[t] = me[t].y + sg.qsy;
+      }
       for (uint32_t p0 = sg.b; p0 < sg.e; p0 += 64) {
         const uint32_t pa = p0 + lane, pb = p0 + 32 + lane;
         const bool va = pa < sg.e, vb = pb < sg.e;
-        float ax = 0.f, ay = 0.f, bx = 0.f, by = 0.f;
+        float ax, ay, bx, by;
         uint32_t ta = 0u, tb = 0u;
-        if (ENV == kFlock) {
-          if (va) { const float2 o = __ldg(&sorted_xy[pa]); ax = o.x; ay = o.y; }
-          if (vb) { const float2 o = __ldg(&sorted_xy[pb]); bx = o.x; by = o.y; }
+        if (ENV == kFlock) {                 // sorted_xy is padded by 64: no predicate
+          const float2 oa = __ldg(&sorted_xy[pa]), ob = __ldg(&sorted_xy[pb]);
+          ax = oa.x; ay = oa.y; bx = ob.x; by = ob.y;
         } else {
+          ax = ay = bx = by = 0.f;
           if (va) { const float4 o = __ldg(&sorted[pa]); ax = o.x; ay = o.y; ta = (uint32_t)o.w << 31; }
           if (vb) { const float4 o = __ldg(&sorted[pb]); bx = o.x; by = o.y; tb = (uint32_t)o.w << 31; }
         }
-        const float dxa = (ax + sg.csx) - qx, dya = (ay + sg.csy) - qy;
-        const float dxb = (bx + sg.csx) - qx, dyb = (by + sg.csy) - qy;
-        const float d2a = fmaf(dxa, dxa, dya * dya);
-        const float d2b = fmaf(dxb, dxb, dyb * dyb);
-        const bool ia = va && d2a < P.dv2;                             // Eq. 1: d < d_v
-        const bool ib = vb && d2b < P.dv2;
-        const unsigned bala = __ballot_sync(kFull, ia);
-        const unsigned balb = __ballot_sync(kFull, ib);
-        if (ia) my_q[nq + __popc(bala & lt_mask)] = make_float4(dxa, dya, d2a, __uint_as_float(pa | ta));
-        nq += __popc(bala);
-        if (ib) my_q[nq + __popc(balb & lt_mask)] = make_float4(dxb, dyb, d2b, __uint_as_float(pb | tb));
-        nq += __popc(balb);
-        while (nq >= 32) {
-          __syncwarp();
-          process(my_q[lane]);
-          nq -= 32;
-          pushed += 32;
-          __syncwarp();
-          const float4 m0 = my_q[32 + lane], m1 = my_q[64 + lane];
-          __syncwarp();
-          if (lane < nq) my_q[lane] = m0;
-          if (lane + 32 < nq) my_q[32 + lane] = m1;
-          __syncwarp();
+        // Slots past the run end get a NaN position: never within d_v of anyone.
+        ax = va ? ax + sg.csx : __int_as_float(0x7fc00000);          // exact (Sterbenz)
+        bx = vb ? bx + sg.csx : __int_as_float(0x7fc00000);
+        ay += sg.csy; by += sg.csy;
+#pragma unroll
+        for (int t = 0; t < NQ; ++t) {
+          const float dxa = ax - qx[t], dya = ay - qy[t];
+          const float dxb = bx - qx[t], dyb = by - qy[t];
+          const float d2a = fmaf(dxa, dxa, dya * dya);
+          const float d2b = fmaf(dxb, dxb, dyb * dyb);
+          const bool ia = d2a < P.dv2;                                 // Eq. 1: d < d_v
+          const bool ib = d2b < P.dv2;
+          const unsigned bala = __ballot_sync(kFull, ia);
+          const unsigned balb = __ballot_sync(kFull, ib);
+          float4* qq = s_q[warp][t];
+          if (ia) qq[nq[t] + __popc(bala & lt_mask)] = make_float4(dxa, dya, d2a, __uint_as_float(pa | ta));
+          nq[t] += __popc(bala);
+          if (ib) qq[nq[t] + __popc(balb & lt_mask)] = make_float4(dxb, dyb, d2b, __uint_as_float(pb | tb));
+          nq[t] += __popc(balb);
+        }
+#pragma unroll
+        for (int t = 0; t < NQ; ++t) {
+          float4* qq = s_q[warp][t];
+          while (nq[t] >= 32) {
+            __syncwarp();
+            process(t, qq[lane]);
+            nq[t] -= 32;
+            pushed[t] += 32;
+            __syncwarp();
+            const float4 m0 = qq[32 + lane], m1 = qq[64 + lane];
+            __syncwarp();
+            if (lane < nq[t]) qq[lane] = m0;
+            if (lane + 32 < nq[t]) qq[32 + lane] = m1;
+            __syncwarp();
+          }
         }
       }
     }
     __syncwarp();
-    if (lane < nq) process(my_q[lane]);
-    const uint32_t nn = pushed + (uint32_t)nq - 1u;                  // minus the self pair
+#pragma unroll
+    for (int t = 0; t < NQ; ++t)
+      if (lane < nq[t]) process(t, s_q[warp][t][lane]);
+    __syncwarp();
 
-    // Warp reductions (REDUX): the int64 reward sum split into exact 32-bit partial sums.
-    ncol = __reduce_add_sync(kFull, ncol);
-    if (ENV == kTag) ntouch = __reduce_add_sync(kFull, ntouch);
-    const unsigned long long ur = (unsigned long long)rs;
-    const uint32_t s_lo = __reduce_add_sync(kFull, (uint32_t)(ur & 0xffffu));
-    const uint32_t s_mid = __reduce_add_sync(kFull, (uint32_t)((ur >> 16) & 0xffffu));
-    const int s_hi = __reduce_add_sync(kFull, (int)(uint32_t)(ur >> 32));
-    long long rsum = ((long long)s_hi << 32) + ((long long)s_mid << 16) + (long long)s_lo;
-    if (ENV == kTag) {
-      const long long t = (long long)ntouch * P.touch_fix;
-      rsum += (tq == 1u) ? t : -t;                                    // P:194 touch rule
-    }
-    const size_t row = SLAB ? (size_t)(q - cs[P.G]) : (size_t)r * P.N + perm[q];
-    if (lane == 0) {
-      if (SLAB && O.agent_id) O.agent_id[row] = perm[q];
-      if (O.reward) O.reward[row] = __ll2float_rn(rsum) * kFixInv;
-      if (O.n_neigh) O.n_neigh[row] = nn;
-      if (O.n_collide) O.n_collide[row] = ncol;
-      if (ENV == kTag && O.n_touch) O.n_touch[row] = ntouch;
-    }
-    if (VISION) {
-      __syncwarp();
-      uint32_t vals[kMaxViewSlots / 32];
 #pragma unroll
-      for (int w = 0; w < kMaxViewSlots / 32; ++w) {
-        const int k = 32 * w + lane;
-        vals[w] = (k < P.view_slots) ? my_min[k] : kOneBits;
+    for (int t = 0; t < NQ; ++t) {
+      if (!live[t]) continue;                                        // warp-uniform
+      const uint32_t q = q0 + t;
+      const uint32_t nn = pushed[t] + (uint32_t)nq[t] - 1u;          // minus the self pair
+      // Warp reductions (REDUX): the int64 reward sum as exact 32-bit partial sums.
+      const uint32_t nc = __reduce_add_sync(kFull, ncol[t]);
+      const uint32_t nt = (ENV == kTag) ? __reduce_add_sync(kFull, ntouch[t]) : 0u;
+      const unsigned long long ur = (unsigned long long)rs[t];
+      const uint32_t s_lo = __reduce_add_sync(kFull, (uint32_t)(ur & 0xffffu));
+      const uint32_t s_mid = __reduce_add_sync(kFull, (uint32_t)((ur >> 16) & 0xffffu));
+      const int s_hi = __reduce_add_sync(kFull, (int)(uint32_t)(ur >> 32));
+      long long rsum = ((long long)s_hi << 32) + ((long long)s_mid << 16) + (long long)s_lo;
+      if (ENV == kTag) {
+        const long long tt = (long long)nt * P.touch_fix;
+        rsum += (tq[t] == 1u) ? tt : -tt;                             // P:194 touch rule
       }
-      if (O.obs) {
-        float* orow = O.obs + row * (size_t)P.obs_dim;
-#pragma unroll
-        for (int w = 0; w < kMaxViewSlots / 32; ++w)
-          if (32 * w + lane < P.view_slots) orow[32 * w + lane] = __uint_as_float(vals[w]);
-        if (ENV == kFlock && lane == 0) orow[P.view_slots] = __fdiv_rn(me.w, P.s_max);  // A24
+      const size_t row = SLAB ? (size_t)(q - cs[P.G]) : (size_t)r * P.N + perm[q];
+      if (lane == 0) {
+        if (SLAB && O.agent_id) O.agent_id[row] = perm[q];
+        if (O.reward) O.reward[row] = __ll2float_rn(rsum) * kFixInv;
+        if (O.n_neigh) O.n_neigh[row] = nn;
+        if (O.n_collide) O.n_collide[row] = nc;
+        if (ENV == kTag && O.n_touch) O.n_touch[row] = nt;
       }
-      if (O.occ) {
-        uint32_t mine = 0u;
+      if (VISION) {
+        uint32_t vals[kMaxViewSlots / 32];
 #pragma unroll
         for (int w = 0; w < kMaxViewSlots / 32; ++w) {
-          const unsigned bits = __ballot_sync(kFull, vals[w] < kOneBits);
-          if (lane == w) mine = bits;
+          const int k = 32 * w + lane;
+          vals[w] = (k < P.view_slots) ? s_min[warp][t][k] : kOneBits;
         }
-        if (lane < P.occ_words) O.occ[row * (size_t)P.occ_words + lane] = mine;
+        if (O.obs) {
+          float* orow = O.obs + row * (size_t)P.obs_dim;
+#pragma unroll
+          for (int w = 0; w < kMaxViewSlots / 32; ++w)
+            if (32 * w + lane < P.view_slots) orow[32 * w + lane] = __uint_as_float(vals[w]);
+          if (ENV == kFlock && lane == 0) orow[P.view_slots] = __fdiv_rn(me[t].w, P.s_max);  // A24
+        }
+        if (O.occ) {
+          uint32_t mine = 0u;
+#pragma unroll
+          for (int w = 0; w < kMaxViewSlots / 32; ++w) {
+            const unsigned bits = __ballot_sync(kFull, vals[w] < kOneBits);
+            if (lane == w) mine = bits;
+          }
+          if (lane < P.occ_words) O.occ[row * (size_t)P.occ_words + lane] = mine;
+        }
       }
     }
     __syncwarp();
