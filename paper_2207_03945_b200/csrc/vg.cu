@@ -6,6 +6,7 @@
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <algorithm>
 #include <climits>
@@ -68,6 +69,21 @@ struct vg_world {
   // phase timing (vg_profile_begin/end): VG_N_PHASES + 1 events per recorded step
   std::vector<cudaEvent_t> prof_ev;
   int prof_max = 0, prof_n = 0;
+  // vg_step CUDA graphs, keyed by the (state, actions, outputs) pointers: one graph launch
+  // per step instead of five kernel launches (launch-bound small worlds).  Captured on a
+  // private stream, launched on the caller's.  Disabled while profiling, inside a caller's
+  // capture, or with VG_NO_GRAPH=1.
+  struct GraphEntry {
+    const void* state;
+    const void* actions;
+    vg_outputs outs;
+    cudaGraphExec_t exec;
+    unsigned long long last_use;
+  };
+  std::vector<GraphEntry> graphs;
+  unsigned long long graph_clock = 0;
+  cudaStream_t cap_stream = nullptr;
+  bool graphs_enabled = true;
 };
 
 namespace {
@@ -332,6 +348,10 @@ vg_status vg_world_create(const vg_config* cfg, vg_world** out) {
   if (!w) return fail(VG_ENOMEM, "host allocation failed");
   w->cfg = *cfg;
   w->P = derive(*cfg, g);
+  {
+    const char* ng = std::getenv("VG_NO_GRAPH");
+    w->graphs_enabled = !(ng && ng[0] && ng[0] != '0');
+  }
   w->n_cells = g * g * cfg->n_replicas;
   cudaGetDevice(&w->device);
   size_t n = (size_t)w->P.total;
@@ -400,6 +420,8 @@ vg_status vg_world_create(const vg_config* cfg, vg_world** out) {
 
 void vg_world_destroy(vg_world* w) {
   if (!w) return;
+  for (auto& g : w->graphs) cudaGraphExecDestroy(g.exec);
+  if (w->cap_stream) cudaStreamDestroy(w->cap_stream);
   for (cudaEvent_t e : w->prof_ev) cudaEventDestroy(e);
   cudaFree(w->count);
   cudaFree(w->cell_start);
@@ -477,14 +499,10 @@ vg_status vg_integrate(vg_world* w, float* state, const float* actions, void* st
   return launch_k1<vg::kTag, true, false>(w, io, nullptr, a, s);
 }
 
-vg_status vg_step(vg_world* w, float* state, const float* actions, const vg_outputs* outs,
-                  void* stream) {
-  if (!w || !state || !actions || !outs) return fail(VG_EINVAL, "world/state/actions/outs: NULL");
-  if (vg_status st = need_slab(w, false, "vg_step")) return st;
-  if (vg_status st = check_pending(w)) return st;
-  cudaStream_t s = as_stream(stream);
-  float4* io = reinterpret_cast<float4*>(state);
-  const float2* a = reinterpret_cast<const float2*>(actions);
+namespace {
+
+vg_status launch_step(vg_world* w, float4* io, const float2* a, const vg_outputs* outs,
+                      cudaStream_t s) {
   prof_mark(w, 0, s);
   if (w->P.env == vg::kFlock) {
     if (vg_status st = launch_k1<vg::kFlock, true, true>(w, io, nullptr, a, s)) return st;
@@ -497,6 +515,70 @@ vg_status vg_step(vg_world* w, float* state, const float* actions, const vg_outp
   }
   vg_status st = launch_sense<true>(w, outs, s);
   prof_mark(w, 5, s);
+  return st;
+}
+
+bool same_outs(const vg_outputs& a, const vg_outputs& b) {
+  return a.obs == b.obs && a.reward == b.reward && a.n_neigh == b.n_neigh &&
+         a.n_collide == b.n_collide && a.n_touch == b.n_touch && a.sector_occ == b.sector_occ &&
+         a.agent_id == b.agent_id;
+}
+
+vg_status step_graph(vg_world* w, float4* io, const float2* a, const vg_outputs* outs,
+                     cudaStream_t s) {
+  for (auto& g : w->graphs) {
+    if (g.state == io && g.actions == a && same_outs(g.outs, *outs)) {
+      g.last_use = ++w->graph_clock;
+      VG_CUDA(cudaGraphLaunch(g.exec, s));
+      w->binned = true;
+      return VG_OK;
+    }
+  }
+  if (!w->cap_stream) VG_CUDA(cudaStreamCreateWithFlags(&w->cap_stream, cudaStreamNonBlocking));
+  VG_CUDA(cudaStreamBeginCapture(w->cap_stream, cudaStreamCaptureModeThreadLocal));
+  vg_status st = launch_step(w, io, a, outs, w->cap_stream);
+  cudaGraph_t graph = nullptr;
+  cudaError_t e = cudaStreamEndCapture(w->cap_stream, &graph);
+  if (st) {
+    if (graph) cudaGraphDestroy(graph);
+    return st;
+  }
+  if (e != cudaSuccess) return fail(VG_ECUDA, "vg_step graph capture: %s", cudaGetErrorString(e));
+  cudaGraphExec_t exec = nullptr;
+  e = cudaGraphInstantiate(&exec, graph, 0);
+  cudaGraphDestroy(graph);
+  if (e != cudaSuccess) return fail(VG_ECUDA, "vg_step graph instantiate: %s", cudaGetErrorString(e));
+  if (w->graphs.size() >= 16) {                     // evict the least recently used
+    size_t lru = 0;
+    for (size_t i = 1; i < w->graphs.size(); ++i)
+      if (w->graphs[i].last_use < w->graphs[lru].last_use) lru = i;
+    cudaGraphExecDestroy(w->graphs[lru].exec);
+    w->graphs.erase(w->graphs.begin() + lru);
+  }
+  w->graphs.push_back({io, a, *outs, exec, ++w->graph_clock});
+  VG_CUDA(cudaGraphLaunch(exec, s));
+  w->binned = true;
+  return VG_OK;
+}
+
+}  // namespace
+
+vg_status vg_step(vg_world* w, float* state, const float* actions, const vg_outputs* outs,
+                  void* stream) {
+  if (!w || !state || !actions || !outs) return fail(VG_EINVAL, "world/state/actions/outs: NULL");
+  if (vg_status st = need_slab(w, false, "vg_step")) return st;
+  if (vg_status st = check_pending(w)) return st;
+  cudaStream_t s = as_stream(stream);
+  float4* io = reinterpret_cast<float4*>(state);
+  const float2* a = reinterpret_cast<const float2*>(actions);
+  cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+  if (cudaStreamIsCapturing(s, &cap) != cudaSuccess) {
+    cudaGetLastError();
+    cap = cudaStreamCaptureStatusActive;            // unknown: stay on the eager path
+  }
+  if (w->graphs_enabled && w->prof_n >= w->prof_max && cap == cudaStreamCaptureStatusNone)
+    return step_graph(w, io, a, outs, s);
+  vg_status st = launch_step(w, io, a, outs, s);
   if (w->prof_n < w->prof_max) ++w->prof_n;
   return st;
 }
