@@ -213,3 +213,26 @@ def actions(p: EnvParams, seed: int = 0, step: int = 0,
         u = rng.random((p.n_agents, 2))
         out[k] = (lo + u * (hi - lo)).astype(np.float32)
     return out
+
+
+# --------------------------------------------------------------------------------------
+# Shared-policy weights ("two hidden layers with 64 nodes")
+# --------------------------------------------------------------------------------------
+POLICY_KEYS = ("W1", "b1", "W2", "b2", "W3", "b3", "log_std", "V1", "c1", "V2", "c2", "V3", "c3")
+
+
+def policy_weights(obs_dim: int, seed: int = 0, hidden: int = 64, act_dim: int = 2,
+                   log_std: float = -1.0) -> dict:
+    """Seeded fp32 actor/critic weights, uniform in +-1/sqrt(fan_in) (random init)."""
+    rng = np.random.default_rng(seed)
+
+    def u(*shape, fan):
+        return (rng.uniform(-1.0, 1.0, shape) / math.sqrt(fan)).astype(np.float32)
+
+    return {"W1": u(hidden, obs_dim, fan=obs_dim), "b1": u(hidden, fan=obs_dim),
+            "W2": u(hidden, hidden, fan=hidden), "b2": u(hidden, fan=hidden),
+            "W3": u(act_dim, hidden, fan=hidden), "b3": u(act_dim, fan=hidden),
+            "log_std": np.full(act_dim, log_std, np.float32),
+            "V1": u(hidden, obs_dim, fan=obs_dim), "c1": u(hidden, fan=obs_dim),
+            "V2": u(hidden, hidden, fan=hidden), "c2": u(hidden, fan=hidden),
+            "V3": u(1, hidden, fan=hidden), "c3": u(1, fan=hidden)}
