@@ -213,6 +213,35 @@ vg_status vg_slab_finish(vg_world* w, const vg_outputs* outs, void* stream);
 /* Synchronizes `stream`; *n_own = number of owned agents (valid output rows). */
 vg_status vg_slab_own_count(vg_world* w, void* stream, int64_t* n_own);
 
+/* ------------------------------------------- shared policy forward
+ * The actor-critic MLP of P:212 ("two hidden layers with 64 nodes each", tanh)
+ * over all agents, on the tcgen05 tensor cores (fp16 operands, fp32 accumulation in TMEM),
+ * followed by the Gaussian action sample of P:198 / S:355-372: a = clip(mean +
+ * exp(log_std) eps, box), log-prob of the unclipped sample, eps from Philox4x32-10
+ * (key = seed, counter = (row, step)) + Box-Muller. */
+typedef struct vg_policy vg_policy;
+typedef struct {
+  int32_t obs_dim;         /* 1..144 (129 flock, 128 tag)                                  */
+  float act_lo[2];         /* action box (flock: (-a_max, -theta_max); tag: (-theta_max, 0)) */
+  float act_hi[2];
+} vg_policy_config;
+typedef struct {           /* caller-owned device buffers, NULL = not written              */
+  float* mean;             /* [rows][2] actor mean                                          */
+  float* value;            /* [rows]    critic value                                        */
+  float* action;           /* [rows][2] clipped sample (also needs the sampling to run)     */
+  float* logp;             /* [rows]    log-prob of the unclipped sample                    */
+} vg_policy_outputs;
+vg_status vg_policy_create(const vg_policy_config* cfg, vg_policy** out);
+void vg_policy_destroy(vg_policy* p);
+/* Upload weights: 13 fp32 device arrays, nn.Linear layout [out][in], in the order
+ * W1[64][d] b1[64] W2[64][64] b2[64] W3[2][64] b3[2] log_std[2]
+ * V1[64][d] c1[64] V2[64][64] c2[64] V3[1][64] c3[1]  (actor W*, critic V*). */
+vg_status vg_policy_set_weights(vg_policy* p, const float* const* weights, void* stream);
+/* obs: device [rows][obs_dim] fp32 (e.g. vg_outputs.obs).  Asynchronous on `stream`. */
+vg_status vg_policy_forward(vg_policy* p, const float* obs, int64_t rows,
+                            const vg_policy_outputs* outs, uint64_t seed, uint64_t step,
+                            void* stream);
+
 /* Phase timing for measurement.  After vg_profile_begin(w, max_steps), each of the next
  * max_steps vg_step calls records CUDA events on its stream between its phases
  * (VG_N_PHASES: integrate+cell-id+histogram, cell scan, scatter, cell sort, sense+reward).

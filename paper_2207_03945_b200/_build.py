@@ -10,7 +10,8 @@ ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 LIB = os.path.join(PKG, "libvg.so")
 SOURCES = [os.path.join(CSRC, "vg.cu")]
-HEADERS = [os.path.join(CSRC, "vg_kernels.cuh"), os.path.join(ROOT, "include", "vg.h")]
+HEADERS = [os.path.join(CSRC, "vg_kernels.cuh"), os.path.join(CSRC, "vg_policy.cuh"),
+           os.path.join(ROOT, "include", "vg.h")]
 
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",

@@ -50,6 +50,14 @@ class VgSlabIo(ctypes.Structure):
     ]
 
 
+class VgPolicyConfig(ctypes.Structure):
+    _fields_ = [("obs_dim", c_int32), ("act_lo", c_float * 2), ("act_hi", c_float * 2)]
+
+
+class VgPolicyOutputs(ctypes.Structure):
+    _fields_ = [("mean", c_void_p), ("value", c_void_p), ("action", c_void_p), ("logp", c_void_p)]
+
+
 class VgWorldInfo(ctypes.Structure):
     _fields_ = [
         ("grid", c_int32), ("cell_size", c_float), ("n_cells", c_int32),
@@ -83,6 +91,11 @@ SIGNATURES = {
     "vg_slab_exchange_loopback": (c_int32, [POINTER(c_void_p), c_int32, c_void_p]),
     "vg_slab_finish": (c_int32, [c_void_p, POINTER(VgOutputs), c_void_p]),
     "vg_slab_own_count": (c_int32, [c_void_p, c_void_p, POINTER(c_int64)]),
+    "vg_policy_create": (c_int32, [POINTER(VgPolicyConfig), POINTER(c_void_p)]),
+    "vg_policy_destroy": (None, [c_void_p]),
+    "vg_policy_set_weights": (c_int32, [c_void_p, POINTER(c_void_p), c_void_p]),
+    "vg_policy_forward": (c_int32, [c_void_p, c_void_p, c_int64, POINTER(VgPolicyOutputs),
+                                    ctypes.c_uint64, ctypes.c_uint64, c_void_p]),
     "vg_profile_begin": (c_int32, [c_void_p, c_int32]),
     "vg_profile_end": (c_int32, [c_void_p, c_void_p, POINTER(ctypes.c_double),
                                  POINTER(c_int32)]),

@@ -15,6 +15,7 @@
 
 #include "vg.h"
 #include "vg_kernels.cuh"
+#include "vg_policy.cuh"
 
 namespace {
 
@@ -728,6 +729,81 @@ vg_status vg_slab_own_count(vg_world* w, void* stream, int64_t* n_own) {
   VG_CUDA(cudaMemcpy(&b, w->cell_start + (size_t)(w->SL.W + 1) * w->P.G, 4, cudaMemcpyDeviceToHost));
   *n_own = (int64_t)b - (int64_t)a;
   return VG_OK;
+}
+
+// ------------------------------------------------------------------ shared policy (K7)
+}  // extern "C"
+
+struct vg_policy {
+  vg_policy_config cfg;
+  vg::PolicyPacked pk{};
+  bool have_weights = false;
+  int n_sm = 148;
+};
+
+extern "C" {
+
+vg_status vg_policy_create(const vg_policy_config* cfg, vg_policy** out) {
+  if (!out) return fail(VG_EINVAL, "out: NULL");
+  *out = nullptr;
+  if (!cfg) return fail(VG_EINVAL, "cfg: NULL");
+  if (cfg->obs_dim < 1 || cfg->obs_dim > vg::kPolK1) return fail(VG_EINVAL, "obs_dim: must be in [1, 144]");
+  for (int d = 0; d < 2; ++d)
+    if (!(cfg->act_lo[d] <= cfg->act_hi[d])) return fail(VG_EINVAL, "act_lo/act_hi: need lo <= hi");
+  vg_policy* p = new (std::nothrow) vg_policy();
+  if (!p) return fail(VG_ENOMEM, "host allocation failed");
+  p->cfg = *cfg;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&p->n_sm, cudaDevAttrMultiProcessorCount, dev);
+  cudaError_t e = cudaMalloc(reinterpret_cast<void**>(&p->pk.B1), vg::kPolN * vg::kPolK1 * 2);
+  if (e == cudaSuccess) e = cudaMalloc(reinterpret_cast<void**>(&p->pk.B2), vg::kPolN * vg::kPolK2 * 2);
+  if (e == cudaSuccess) e = cudaMalloc(reinterpret_cast<void**>(&p->pk.consts), vg::kConstFloats * 4);
+  if (e == cudaSuccess)
+    e = cudaFuncSetAttribute(vg::k_policy, cudaFuncAttributeMaxDynamicSharedMemorySize, vg::kPolSmem);
+  if (e != cudaSuccess) {
+    vg_policy_destroy(p);
+    return fail(VG_ECUDA, "vg_policy_create: %s", cudaGetErrorString(e));
+  }
+  *out = p;
+  return VG_OK;
+}
+
+void vg_policy_destroy(vg_policy* p) {
+  if (!p) return;
+  cudaFree(p->pk.B1);
+  cudaFree(p->pk.B2);
+  cudaFree(p->pk.consts);
+  delete p;
+}
+
+vg_status vg_policy_set_weights(vg_policy* p, const float* const* w, void* stream) {
+  if (!p || !w) return fail(VG_EINVAL, "policy/weights: NULL");
+  for (int i = 0; i < 13; ++i)
+    if (!w[i]) return fail(VG_EINVAL, "weights[%d]: NULL", i);
+  const int n = vg::kPolN * vg::kPolK1;
+  vg::k_policy_pack<<<(n + 255) / 256, 256, 0, as_stream(stream)>>>(
+      p->cfg.obs_dim, w[0], w[1], w[2], w[3], w[4], w[5], w[6], w[7], w[8], w[9], w[10], w[11],
+      w[12], p->cfg.act_lo[0], p->cfg.act_lo[1], p->cfg.act_hi[0], p->cfg.act_hi[1], p->pk);
+  if (vg_status st = launch_check("k_policy_pack")) return st;
+  p->have_weights = true;
+  return VG_OK;
+}
+
+vg_status vg_policy_forward(vg_policy* p, const float* obs, int64_t rows,
+                            const vg_policy_outputs* outs, uint64_t seed, uint64_t step,
+                            void* stream) {
+  if (!p || !obs || !outs) return fail(VG_EINVAL, "policy/obs/outs: NULL");
+  if (!p->have_weights) return fail(VG_EINVAL, "vg_policy_forward: call vg_policy_set_weights first");
+  if (rows < 0) return fail(VG_EINVAL, "rows: must be >= 0");
+  if (rows == 0) return VG_OK;
+  vg::PolicyOut o{outs->mean, outs->value, outs->action, outs->logp};
+  const int64_t tiles = (rows + vg::kPolTile - 1) / vg::kPolTile;
+  const unsigned grid = (unsigned)std::min<int64_t>(tiles, p->n_sm);
+  vg::k_policy<<<grid, vg::kPolThreads, vg::kPolSmem, as_stream(stream)>>>(
+      obs, rows, p->cfg.obs_dim, p->pk, o, (uint32_t)seed, (uint32_t)(seed >> 32),
+      (uint32_t)step, (uint32_t)(step >> 32));
+  return launch_check("k_policy");
 }
 
 vg_status vg_profile_begin(vg_world* w, int32_t max_steps) {

@@ -1,0 +1,331 @@
+// vg_policy.cuh — K7: shared-policy actor-critic forward on the sm_100a tensor cores.
+//
+// P:212 "The actor and critic PPO networks had two hidden layers with 64 nodes each";
+// P:198 shared policy, continuous actions; S:329-333 MLPPolicy (obs -> 64 -> 64 -> out,
+// tanh hidden, linear out, state-independent log_std); S:355-372 Gaussian sample, clip to
+// the action box, log-prob of the unclipped sample.  SURVEY.md §8f NEXT #1.
+//
+// Tile of 128 agents per step of a persistent CTA (one per SM, 8 warps):
+//   layer 1  D[128 x 128] = A1[128 x 144] . B1^T   (actor | critic hidden, fp16 in, fp32 acc)
+//   layer 2  D[128 x 128] = A2[128 x 128] . B2^T   (B2 block-diagonal: actor | critic)
+//   layer 3  mean (2) and value (1): fp32 FMAs in the epilogue; then Philox4x32-10 +
+//            Box-Muller noise, clip, log-prob.
+// Operands live in shared memory in the canonical K-major no-swizzle layout (8 x 16-byte
+// core matrices: SBO = 128 B between 8-row groups, LBO = R x 16 B between 8-column groups),
+// tcgen05.mma is issued by one thread, the fp32 accumulator lives in TMEM (128 columns) and
+// is read back with tcgen05.ld.32x32b (warp w reads TMEM lanes 32 (w % 4) ..).
+#pragma once
+
+#include <cstdint>
+#include <cuda_fp16.h>
+#include <cuda_runtime.h>
+
+namespace vg {
+
+constexpr int kPolTile = 128;      // agents per tile (MMA M)
+constexpr int kPolHidden = 64;
+constexpr int kPolN = 128;         // actor | critic concatenated (MMA N)
+constexpr int kPolK1 = 144;        // obs_dim padded to a multiple of 16 (<= 144)
+constexpr int kPolK2 = 128;        // hidden actor | critic
+constexpr int kPolThreads = 256;
+
+// Shared-memory carve-up (bytes).
+constexpr int kOffB1 = 0;
+constexpr int kOffB2 = kOffB1 + kPolN * kPolK1 * 2;        // 36864
+constexpr int kOffA1 = kOffB2 + kPolN * kPolK2 * 2;        // +32768
+constexpr int kOffA2 = kOffA1 + kPolTile * kPolK1 * 2;     // +36864
+constexpr int kOffC = kOffA2 + kPolTile * kPolK2 * 2;      // +32768 : fp32 constants
+constexpr int kConstFloats = 128 + 128 + 3 * 128 + 4 + 2 + 4;   // b1, b2, W3|V3, b3|c3, log_std, box
+constexpr int kOffBar = kOffC + ((kConstFloats * 4 + 15) / 16) * 16;
+constexpr int kPolSmem = kOffBar + 16;
+
+// Packed weights on the device (written once by k_policy_pack).
+struct PolicyPacked {
+  __half* B1;        // [kPolN x kPolK1] core-matrix layout
+  __half* B2;        // [kPolN x kPolK2] core-matrix layout (block diagonal)
+  float* consts;     // kConstFloats: b1[128] b2[128] W3[3][128] b3[3] pad log_std[2] lo[2] hi[2]
+};
+
+struct PolicyOut {
+  float* mean;       // [M][2]
+  float* value;      // [M]
+  float* action;     // [M][2] clipped sample (NULL: skip sampling)
+  float* logp;       // [M]
+};
+
+// Element offset of (r, k) in an R-row K-major core-matrix operand.
+__host__ __device__ __forceinline__ int cm_offset(int r, int k, int R) {
+  return ((k >> 3) * (R >> 3) + (r >> 3)) * 64 + (r & 7) * 8 + (k & 7);
+}
+
+// UMMA shared-memory descriptor: K-major, no swizzle, version 1 (sm_100).
+__device__ __forceinline__ uint64_t umma_desc(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
+  return (uint64_t)((saddr >> 4) & 0x3FFF) | ((uint64_t)((lbo >> 4) & 0x3FFF) << 16) |
+         ((uint64_t)((sbo >> 4) & 0x3FFF) << 32) | (1ull << 46);
+}
+
+// Instruction descriptor, kind::f16: D fp32, A/B fp16, both K-major, M = 128, N = 128.
+constexpr uint32_t kPolIdesc = (1u << 4) | ((uint32_t)(kPolN >> 3) << 17) | ((uint32_t)(kPolTile >> 4) << 24);
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+
+__device__ __forceinline__ void mma_f16(uint32_t tmem_d, uint64_t a, uint64_t b, uint32_t idesc,
+                                        uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}\n" ::"r"(tmem_d),
+      "l"(a), "l"(b), "r"(idesc), "r"(accumulate));
+}
+
+__device__ __forceinline__ void mma_commit(uint32_t bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(bar)
+               : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred done;\n"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 done, [%0], %1;\n\t"
+      "@!done bra WAIT_%=;\n\t}\n" ::"r"(bar),
+      "r"(parity)
+      : "memory");
+}
+
+// tanh(x) = sign(x) (1 - 2 / (exp(2|x|) + 1)): MUFU ex2 + rcp, absolute error ~2e-7
+// (tanh.approx.f32 is ~1e-3 absolute, too coarse for the parity budget).
+__device__ __forceinline__ float tanh_fast(float x) {
+  const float e = __expf(2.f * fabsf(x));
+  float r;
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(e + 1.f));
+  return copysignf(fmaf(-2.f, r, 1.f), x);
+}
+
+// 32 consecutive TMEM columns of this thread's lane.
+__device__ __forceinline__ void tmem_ld32(uint32_t taddr, float* v) {
+  uint32_t r[32];
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,"
+      "%15,%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+        "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]),
+        "=r"(r[14]), "=r"(r[15]), "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]),
+        "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]), "=r"(r[25]),
+        "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+      : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+  for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
+}
+
+// Philox4x32-10 (Salmon et al. SC'11): the same counter-based generator as oracle/policy.py.
+__device__ __forceinline__ void philox4x32_10(uint32_t c[4], uint32_t k0, uint32_t k1) {
+#pragma unroll
+  for (int r = 0; r < 10; ++r) {
+    const uint32_t hi0 = __umulhi(0xD2511F53u, c[0]), lo0 = 0xD2511F53u * c[0];
+    const uint32_t hi1 = __umulhi(0xCD9E8D57u, c[2]), lo1 = 0xCD9E8D57u * c[2];
+    const uint32_t n0 = hi1 ^ c[1] ^ k0, n2 = hi0 ^ c[3] ^ k1;
+    c[0] = n0; c[1] = lo1; c[2] = n2; c[3] = lo0;
+    k0 += 0x9E3779B9u;
+    k1 += 0xBB67AE85u;
+  }
+}
+
+// Pack fp32 weights (nn.Linear layout [out][in]) into the resident operand layouts.
+__global__ void k_policy_pack(int obs_dim, const float* __restrict__ W1, const float* __restrict__ b1,
+                              const float* __restrict__ W2, const float* __restrict__ b2,
+                              const float* __restrict__ W3, const float* __restrict__ b3,
+                              const float* __restrict__ log_std, const float* __restrict__ V1,
+                              const float* __restrict__ c1, const float* __restrict__ V2,
+                              const float* __restrict__ c2, const float* __restrict__ V3,
+                              const float* __restrict__ c3, float lo0, float lo1, float hi0,
+                              float hi1, PolicyPacked pk) {
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t < kPolN * kPolK1) {                                   // B1: rows 0-63 actor, 64-127 critic
+    const int n = t / kPolK1, k = t % kPolK1;
+    float v = 0.f;
+    if (k < obs_dim) v = (n < kPolHidden) ? W1[n * obs_dim + k] : V1[(n - kPolHidden) * obs_dim + k];
+    pk.B1[cm_offset(n, k, kPolN)] = __float2half_rn(v);
+  }
+  if (t < kPolN * kPolK2) {                                   // B2: block diagonal
+    const int n = t / kPolK2, k = t % kPolK2;
+    float v = 0.f;
+    if (n < kPolHidden && k < kPolHidden) v = W2[n * kPolHidden + k];
+    if (n >= kPolHidden && k >= kPolHidden) v = V2[(n - kPolHidden) * kPolHidden + (k - kPolHidden)];
+    pk.B2[cm_offset(n, k, kPolN)] = __float2half_rn(v);
+  }
+  if (t < kPolN) {
+    pk.consts[t] = (t < kPolHidden) ? b1[t] : c1[t - kPolHidden];
+    pk.consts[128 + t] = (t < kPolHidden) ? b2[t] : c2[t - kPolHidden];
+    pk.consts[256 + t] = (t < kPolHidden) ? W3[t] : 0.f;                       // mean_0
+    pk.consts[384 + t] = (t < kPolHidden) ? W3[kPolHidden + t] : 0.f;          // mean_1
+    pk.consts[512 + t] = (t >= kPolHidden) ? V3[t - kPolHidden] : 0.f;         // value
+  }
+  if (t == 0) {
+    pk.consts[640] = b3[0]; pk.consts[641] = b3[1]; pk.consts[642] = c3[0]; pk.consts[643] = 0.f;
+    pk.consts[644] = log_std[0]; pk.consts[645] = log_std[1];
+    pk.consts[646] = lo0; pk.consts[647] = lo1; pk.consts[648] = hi0; pk.consts[649] = hi1;
+  }
+}
+
+__global__ void __launch_bounds__(kPolThreads, 1) k_policy(
+    const float* __restrict__ obs, int64_t M, int obs_dim, PolicyPacked pk, PolicyOut out,
+    uint32_t seed_lo, uint32_t seed_hi, uint32_t step_lo, uint32_t step_hi) {
+  extern __shared__ __align__(1024) unsigned char smem[];
+  __half* sB1 = reinterpret_cast<__half*>(smem + kOffB1);
+  __half* sB2 = reinterpret_cast<__half*>(smem + kOffB2);
+  __half* sA1 = reinterpret_cast<__half*>(smem + kOffA1);
+  __half* sA2 = reinterpret_cast<__half*>(smem + kOffA2);
+  float* sC = reinterpret_cast<float*>(smem + kOffC);
+  uint64_t* bar = reinterpret_cast<uint64_t*>(smem + kOffBar);
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + kOffBar + 8);
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+
+  // Resident weights: plain 16-byte copies of the packed operands.
+  {
+    const uint4* g1 = reinterpret_cast<const uint4*>(pk.B1);
+    const uint4* g2 = reinterpret_cast<const uint4*>(pk.B2);
+    uint4* s1 = reinterpret_cast<uint4*>(sB1);
+    uint4* s2 = reinterpret_cast<uint4*>(sB2);
+    for (int i = tid; i < kPolN * kPolK1 / 8; i += kPolThreads) s1[i] = g1[i];
+    for (int i = tid; i < kPolN * kPolK2 / 8; i += kPolThreads) s2[i] = g2[i];
+    for (int i = tid; i < kConstFloats; i += kPolThreads) sC[i] = pk.consts[i];
+  }
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                 "r"(128));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  if (tid == 0) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(bar)));
+    asm volatile("fence.mbarrier_init.release.cluster;");
+  }
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  asm volatile("tcgen05.fence::before_thread_sync;");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;");
+  const uint32_t tmem = *tmem_slot;
+  const uint32_t bar_a = smem_u32(bar);
+  const uint32_t a1 = smem_u32(sA1), a2 = smem_u32(sA2), b1 = smem_u32(sB1), b2 = smem_u32(sB2);
+  uint32_t phase = 0;
+
+  // Epilogue mapping: warp w reads TMEM lanes (rows) 32 (w % 4) .. and columns 64 (w / 4) ..
+  const int erow = 32 * (warp & 3) + lane;
+  const int ecol = 64 * (warp >> 2);
+  const uint32_t taddr = tmem + ((uint32_t)(32 * (warp & 3)) << 16) + (uint32_t)ecol;
+
+  const int64_t n_tiles = (M + kPolTile - 1) / kPolTile;
+  for (int64_t tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
+    const int64_t m0 = tile * kPolTile;
+    // ---- A1: obs rows -> fp16 core-matrix layout (zero pad rows >= M, cols >= obs_dim).
+    for (int it = tid; it < kPolTile * (kPolK1 / 8); it += kPolThreads) {
+      const int r = it % kPolTile, kc = it / kPolTile;
+      const int64_t gr = m0 + r;
+      const float* src = obs + gr * obs_dim + kc * 8;
+      __align__(16) __half h[8];
+#pragma unroll
+      for (int e = 0; e < 8; ++e) {
+        const int k = kc * 8 + e;
+        h[e] = __float2half_rn((gr < M && k < obs_dim) ? __ldg(src + e) : 0.f);
+      }
+      *reinterpret_cast<uint4*>(sA1 + cm_offset(r, kc * 8, kPolTile)) = *reinterpret_cast<uint4*>(h);
+    }
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    asm volatile("tcgen05.fence::before_thread_sync;");
+    __syncthreads();
+    // ---- layer 1 on the tensor cores
+    if (tid == 0) {
+      asm volatile("tcgen05.fence::after_thread_sync;");
+#pragma unroll
+      for (int s = 0; s < kPolK1 / 16; ++s)
+        mma_f16(tmem, umma_desc(a1 + s * 2 * (kPolTile * 16), kPolTile * 16, 128),
+                umma_desc(b1 + s * 2 * (kPolN * 16), kPolN * 16, 128), kPolIdesc, s > 0);
+      mma_commit(bar_a);
+    }
+    mbar_wait(bar_a, phase);
+    phase ^= 1u;
+    asm volatile("tcgen05.fence::after_thread_sync;");
+    // ---- epilogue 1: h1 = tanh(D + b1) -> fp16 A2
+#pragma unroll
+    for (int half = 0; half < 2; ++half) {
+      float v[32];
+      tmem_ld32(taddr + 32 * half, v);
+#pragma unroll
+      for (int g = 0; g < 4; ++g) {
+        __align__(16) __half h[8];
+#pragma unroll
+        for (int e = 0; e < 8; ++e) {
+          const int col = ecol + 32 * half + 8 * g + e;
+          h[e] = __float2half_rn(tanh_fast(v[8 * g + e] + sC[col]));
+        }
+        *reinterpret_cast<uint4*>(sA2 + cm_offset(erow, ecol + 32 * half + 8 * g, kPolTile)) =
+            *reinterpret_cast<uint4*>(h);
+      }
+    }
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    asm volatile("tcgen05.fence::before_thread_sync;");
+    __syncthreads();
+    // ---- layer 2
+    if (tid == 0) {
+      asm volatile("tcgen05.fence::after_thread_sync;");
+#pragma unroll
+      for (int s = 0; s < kPolK2 / 16; ++s)
+        mma_f16(tmem, umma_desc(a2 + s * 2 * (kPolTile * 16), kPolTile * 16, 128),
+                umma_desc(b2 + s * 2 * (kPolN * 16), kPolN * 16, 128), kPolIdesc, s > 0);
+      mma_commit(bar_a);
+    }
+    mbar_wait(bar_a, phase);
+    phase ^= 1u;
+    asm volatile("tcgen05.fence::after_thread_sync;");
+    // ---- epilogue 2: h2 = tanh(D + b2); layer 3 dot products (fp32)
+    float acc0 = 0.f, acc1 = 0.f, accv = 0.f;
+#pragma unroll
+    for (int half = 0; half < 2; ++half) {
+      float v[32];
+      tmem_ld32(taddr + 32 * half, v);
+#pragma unroll
+      for (int e = 0; e < 32; ++e) {
+        const int col = ecol + 32 * half + e;
+        const float h = tanh_fast(v[e] + sC[128 + col]);
+        acc0 = fmaf(sC[256 + col], h, acc0);
+        acc1 = fmaf(sC[384 + col], h, acc1);
+        accv = fmaf(sC[512 + col], h, accv);
+      }
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;");
+    const int64_t gr = m0 + erow;
+    if (gr < M) {
+      if (warp >= 4) {                                   // critic columns
+        if (out.value) out.value[gr] = accv + sC[642];
+      } else {                                           // actor columns
+        const float mu0 = acc0 + sC[640], mu1 = acc1 + sC[641];
+        if (out.mean) { out.mean[2 * gr] = mu0; out.mean[2 * gr + 1] = mu1; }
+        if (out.action) {
+          uint32_t c[4] = {(uint32_t)gr, step_lo, step_hi, 0u};
+          philox4x32_10(c, seed_lo, seed_hi);
+          const float u0 = ((float)(c[0] >> 8) + 0.5f) * 5.9604645e-8f;     // (0, 1)
+          const float u1 = ((float)(c[1] >> 8) + 0.5f) * 5.9604645e-8f;
+          const float rr = sqrtf(-2.f * logf(u0));
+          float sn, cs;
+          sincospif(2.f * u1, &sn, &cs);
+          const float e0 = rr * cs, e1 = rr * sn;
+          const float ls0 = sC[644], ls1 = sC[645];
+          const float r0 = fmaf(expf(ls0), e0, mu0), r1 = fmaf(expf(ls1), e1, mu1);
+          out.action[2 * gr] = fminf(fmaxf(r0, sC[646]), sC[648]);
+          out.action[2 * gr + 1] = fminf(fmaxf(r1, sC[647]), sC[649]);
+          if (out.logp)
+            out.logp[gr] = -0.5f * (e0 * e0 + e1 * e1) - ls0 - ls1 - 1.8378770664093453f;
+        }
+      }
+    }
+    __syncthreads();
+  }
+  asm volatile("tcgen05.fence::after_thread_sync;");
+  __syncthreads();
+  if (warp == 0)
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(128));
+}
+
+}  // namespace vg
