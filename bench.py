@@ -51,6 +51,7 @@ def parse():
                     help="bounded oracle sample for cpu_baseline (seconds of CPU work)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-policy", action="store_true")
     return ap.parse_args()
 
 
@@ -343,6 +344,39 @@ def run_ours(args):
                "note": ("vg_step_host" if not slab_mode else "actions H2D + slab step + reward D2H")
                        + ": pinned host buffers, stream sync per step, wall clock, max over ranks"}
 
+    # ---- K7: shared-policy forward + sampling over this rank's obs,
+    # timed separately (not part of the env-step metric)
+    policy = None
+    if not args.no_policy and run.out.obs is not None:
+        from paper_2207_03945_b200.policy import Policy, action_box
+        lo, hi = action_box(p)
+        pl = Policy(w.obs_dim, lo, hi, device=device)
+        pl.set_weights(vi.policy_weights(w.obs_dim, seed=0))
+        rows = run.out.obs.numel() // w.obs_dim
+        if slab_mode:
+            rows = w.slab_own_count()
+        obs2d = run.out.obs.view(-1, w.obs_dim)[:rows]
+        pout = pl.alloc(rows)
+        for k in range(3):
+            pl.forward(obs2d, pout, seed=1, step=k)
+        pe0 = [torch.cuda.Event(enable_timing=True) for _ in range(K)]
+        pe1 = [torch.cuda.Event(enable_timing=True) for _ in range(K)]
+        for k in range(K):
+            flush.fill_(k & 0xFF)
+            pe0[k].record()
+            pl.forward(obs2d, pout, seed=1, step=k)
+            pe1[k].record()
+        torch.cuda.synchronize()
+        pms = sum(a.elapsed_time(b) for a, b in zip(pe0, pe1)) / K
+        flops = 2.0 * rows * (144 * 128 + 128 * 128 + 3 * 128)
+        pbytes = rows * (4 * w.obs_dim + 4 * 6)
+        policy = {"kernel": "k_policy (tcgen05 kind::f16, TMEM accumulators)", "rows": rows,
+                  "ms": pms, "agents_per_s": rows / (pms / 1e3),
+                  "tensor_TFLOPs": flops / (pms / 1e3) / 1e12,
+                  "hbm_GBps": pbytes / (pms / 1e3) / 1e9,
+                  "bound": "hbm (obs read 4*obs_dim B/row)"}
+        pl.close()
+
     if rank == 0:
         peaks, peak_src = measured_peaks()
         hbm = float(peaks.get("hbm_gbs", 6441.6))
@@ -402,6 +436,7 @@ def run_ours(args):
             "hbm_peak_gbs": hbm, "peak_source": peak_src,
             "e2e": e2e,
             "gpu_launches": run.launches * K,
+            "policy": policy,
             "clocks": clk.summary(),
             "cpu_baseline": cpu,
             "context": PAPER_CONTEXT,

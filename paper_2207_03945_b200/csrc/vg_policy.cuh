@@ -36,8 +36,10 @@ constexpr int kOffA1 = kOffB2 + kPolN * kPolK2 * 2;        // +32768
 constexpr int kOffA2 = kOffA1 + kPolTile * kPolK1 * 2;     // +36864
 constexpr int kOffC = kOffA2 + kPolTile * kPolK2 * 2;      // +32768 : fp32 constants
 constexpr int kConstFloats = 128 + 128 + 3 * 128 + 4 + 2 + 4;   // b1, b2, W3|V3, b3|c3, log_std, box
-constexpr int kOffBar = kOffC + ((kConstFloats * 4 + 15) / 16) * 16;
-constexpr int kPolSmem = kOffBar + 16;
+constexpr int kOffBar = kOffC + ((kConstFloats * 4 + 15) / 16) * 16;   // 2 mbarriers + tmem slot
+constexpr int kOffStage = ((kOffBar + 32 + 127) / 128) * 128;            // raw fp32 obs tile (TMA)
+constexpr int kStageBytes = kPolTile * kPolK1 * 4;                       // >= 128 rows x obs_dim
+constexpr int kPolSmem = kOffStage + kStageBytes;
 
 // Packed weights on the device (written once by k_policy_pack).
 struct PolicyPacked {
@@ -66,6 +68,10 @@ __device__ __forceinline__ uint64_t umma_desc(uint32_t saddr, uint32_t lbo, uint
 
 // Instruction descriptor, kind::f16: D fp32, A/B fp16, both K-major, M = 128, N = 128.
 constexpr uint32_t kPolIdesc = (1u << 4) | ((uint32_t)(kPolN >> 3) << 17) | ((uint32_t)(kPolTile >> 4) << 24);
+
+__device__ __forceinline__ uint32_t h2_bits(__half2 h) {
+  return *reinterpret_cast<uint32_t*>(&h);
+}
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return (uint32_t)__cvta_generic_to_shared(p);
@@ -96,6 +102,17 @@ __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
 
 // tanh(x) = sign(x) (1 - 2 / (exp(2|x|) + 1)): MUFU ex2 + rcp, absolute error ~2e-7
 // (tanh.approx.f32 is ~1e-3 absolute, too coarse for the parity budget).
+// 1-D TMA bulk copy global -> shared, completion counted on an mbarrier (tx bytes).
+__device__ __forceinline__ void tma_load_1d(uint32_t dst, const void* src, uint32_t bytes,
+                                            uint32_t bar) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes)
+               : "memory");
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),
+      "l"(src), "r"(bytes), "r"(bar)
+      : "memory");
+}
+
 __device__ __forceinline__ float tanh_fast(float x) {
   const float e = __expf(2.f * fabsf(x));
   float r;
@@ -179,8 +196,9 @@ __global__ void __launch_bounds__(kPolThreads, 1) k_policy(
   __half* sA1 = reinterpret_cast<__half*>(smem + kOffA1);
   __half* sA2 = reinterpret_cast<__half*>(smem + kOffA2);
   float* sC = reinterpret_cast<float*>(smem + kOffC);
-  uint64_t* bar = reinterpret_cast<uint64_t*>(smem + kOffBar);
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + kOffBar + 8);
+  const float* sStage = reinterpret_cast<const float*>(smem + kOffStage);
+  uint64_t* bar = reinterpret_cast<uint64_t*>(smem + kOffBar);          // [0] MMA, [1] TMA
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + kOffBar + 16);
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
 
   // Resident weights: plain 16-byte copies of the packed operands.
@@ -199,7 +217,8 @@ __global__ void __launch_bounds__(kPolThreads, 1) k_policy(
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
   }
   if (tid == 0) {
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(bar)));
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&bar[0])));
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&bar[1])));
     asm volatile("fence.mbarrier_init.release.cluster;");
   }
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
@@ -207,9 +226,10 @@ __global__ void __launch_bounds__(kPolThreads, 1) k_policy(
   __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;");
   const uint32_t tmem = *tmem_slot;
-  const uint32_t bar_a = smem_u32(bar);
+  const uint32_t bar_mma = smem_u32(&bar[0]), bar_tma = smem_u32(&bar[1]);
+  const uint32_t stage = smem_u32(sStage);
   const uint32_t a1 = smem_u32(sA1), a2 = smem_u32(sA2), b1 = smem_u32(sB1), b2 = smem_u32(sB2);
-  uint32_t phase = 0;
+  uint32_t ph_mma = 0, ph_tma = 0;
 
   // Epilogue mapping: warp w reads TMEM lanes (rows) 32 (w % 4) .. and columns 64 (w / 4) ..
   const int erow = 32 * (warp & 3) + lane;
@@ -217,35 +237,67 @@ __global__ void __launch_bounds__(kPolThreads, 1) k_policy(
   const uint32_t taddr = tmem + ((uint32_t)(32 * (warp & 3)) << 16) + (uint32_t)ecol;
 
   const int64_t n_tiles = (M + kPolTile - 1) / kPolTile;
+  // A full tile is one contiguous, 16-byte aligned block of 128 x obs_dim floats (m0 is a
+  // multiple of 128): one TMA bulk copy.  The ragged last tile is read with plain loads.
+  const uint32_t tile_bytes = (uint32_t)(kPolTile * obs_dim * 4);
+  const bool bulk_ok = (tile_bytes % 16u) == 0u &&
+                       (reinterpret_cast<uintptr_t>(obs) % 16u) == 0u;
+  auto is_full = [&](int64_t t) { return bulk_ok && (t + 1) * kPolTile <= M; };
+  if (tid == 0 && blockIdx.x < n_tiles && is_full(blockIdx.x))
+    tma_load_1d(stage, obs + (int64_t)blockIdx.x * kPolTile * obs_dim, tile_bytes, bar_tma);
+
   for (int64_t tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
     const int64_t m0 = tile * kPolTile;
+    const bool full = is_full(tile);
     // ---- A1: obs rows -> fp16 core-matrix layout (zero pad rows >= M, cols >= obs_dim).
+    if (full) {
+      mbar_wait(bar_tma, ph_tma);                        // this tile's TMA has landed
+      ph_tma ^= 1u;
+    }
+    // Thread -> (row r, 8-column chunk kc); a warp shares kc, so the chunk bounds are uniform.
     for (int it = tid; it < kPolTile * (kPolK1 / 8); it += kPolThreads) {
       const int r = it % kPolTile, kc = it / kPolTile;
+      const int nv = obs_dim - kc * 8;                    // valid columns in this chunk
       const int64_t gr = m0 + r;
-      const float* src = obs + gr * obs_dim + kc * 8;
-      __align__(16) __half h[8];
+      float x[8];
+      if (full) {
+        const float* src = sStage + r * obs_dim + kc * 8;
+        if (nv >= 8) {
 #pragma unroll
-      for (int e = 0; e < 8; ++e) {
-        const int k = kc * 8 + e;
-        h[e] = __float2half_rn((gr < M && k < obs_dim) ? __ldg(src + e) : 0.f);
+          for (int e = 0; e < 8; ++e) x[e] = src[e];
+        } else {
+#pragma unroll
+          for (int e = 0; e < 8; ++e) x[e] = (e < nv) ? src[e] : 0.f;
+        }
+      } else {
+        const float* src = obs + gr * obs_dim + kc * 8;
+#pragma unroll
+        for (int e = 0; e < 8; ++e) x[e] = (gr < M && e < nv) ? __ldg(src + e) : 0.f;
       }
-      *reinterpret_cast<uint4*>(sA1 + cm_offset(r, kc * 8, kPolTile)) = *reinterpret_cast<uint4*>(h);
+      uint4 pkd;
+      pkd.x = h2_bits(__floats2half2_rn(x[0], x[1]));
+      pkd.y = h2_bits(__floats2half2_rn(x[2], x[3]));
+      pkd.z = h2_bits(__floats2half2_rn(x[4], x[5]));
+      pkd.w = h2_bits(__floats2half2_rn(x[6], x[7]));
+      *reinterpret_cast<uint4*>(sA1 + cm_offset(r, kc * 8, kPolTile)) = pkd;
     }
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
     asm volatile("tcgen05.fence::before_thread_sync;");
     __syncthreads();
-    // ---- layer 1 on the tensor cores
+    // ---- prefetch the next tile (overlaps the MMAs and epilogues); layer 1 on the tensor cores
     if (tid == 0) {
+      const int64_t nt = tile + gridDim.x;
+      if (nt < n_tiles && is_full(nt))
+        tma_load_1d(stage, obs + nt * kPolTile * obs_dim, tile_bytes, bar_tma);
       asm volatile("tcgen05.fence::after_thread_sync;");
 #pragma unroll
       for (int s = 0; s < kPolK1 / 16; ++s)
         mma_f16(tmem, umma_desc(a1 + s * 2 * (kPolTile * 16), kPolTile * 16, 128),
                 umma_desc(b1 + s * 2 * (kPolN * 16), kPolN * 16, 128), kPolIdesc, s > 0);
-      mma_commit(bar_a);
+      mma_commit(bar_mma);
     }
-    mbar_wait(bar_a, phase);
-    phase ^= 1u;
+    mbar_wait(bar_mma, ph_mma);
+    ph_mma ^= 1u;
     asm volatile("tcgen05.fence::after_thread_sync;");
     // ---- epilogue 1: h1 = tanh(D + b1) -> fp16 A2
 #pragma unroll
@@ -254,14 +306,16 @@ __global__ void __launch_bounds__(kPolThreads, 1) k_policy(
       tmem_ld32(taddr + 32 * half, v);
 #pragma unroll
       for (int g = 0; g < 4; ++g) {
-        __align__(16) __half h[8];
+        const int c0 = ecol + 32 * half + 8 * g;
+        float t[8];
 #pragma unroll
-        for (int e = 0; e < 8; ++e) {
-          const int col = ecol + 32 * half + 8 * g + e;
-          h[e] = __float2half_rn(tanh_fast(v[8 * g + e] + sC[col]));
-        }
-        *reinterpret_cast<uint4*>(sA2 + cm_offset(erow, ecol + 32 * half + 8 * g, kPolTile)) =
-            *reinterpret_cast<uint4*>(h);
+        for (int e = 0; e < 8; ++e) t[e] = tanh_fast(v[8 * g + e] + sC[c0 + e]);
+        uint4 pkd;
+        pkd.x = h2_bits(__floats2half2_rn(t[0], t[1]));
+        pkd.y = h2_bits(__floats2half2_rn(t[2], t[3]));
+        pkd.z = h2_bits(__floats2half2_rn(t[4], t[5]));
+        pkd.w = h2_bits(__floats2half2_rn(t[6], t[7]));
+        *reinterpret_cast<uint4*>(sA2 + cm_offset(erow, c0, kPolTile)) = pkd;
       }
     }
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
@@ -274,10 +328,10 @@ __global__ void __launch_bounds__(kPolThreads, 1) k_policy(
       for (int s = 0; s < kPolK2 / 16; ++s)
         mma_f16(tmem, umma_desc(a2 + s * 2 * (kPolTile * 16), kPolTile * 16, 128),
                 umma_desc(b2 + s * 2 * (kPolN * 16), kPolN * 16, 128), kPolIdesc, s > 0);
-      mma_commit(bar_a);
+      mma_commit(bar_mma);
     }
-    mbar_wait(bar_a, phase);
-    phase ^= 1u;
+    mbar_wait(bar_mma, ph_mma);
+    ph_mma ^= 1u;
     asm volatile("tcgen05.fence::after_thread_sync;");
     // ---- epilogue 2: h2 = tanh(D + b2); layer 3 dot products (fp32)
     float acc0 = 0.f, acc1 = 0.f, accv = 0.f;
