@@ -246,7 +246,7 @@ __global__ void __launch_bounds__(256) k_cell_sort(
 // contact test, reward term (fixed point, A16b), bearing, sector, and the per-sector
 // nearest distance by shared-memory atomicMin on the float bits (A2, A3).
 constexpr int kSenseWarps = 4;
-constexpr int kQueue = 96;          // 31 carried + 2 x 32 pushed per iteration
+constexpr int kQueue = 128;         // ring (power of 2) >= 31 carried + 2 x 32 pushed
 
 // atan2(y, x) in (-pi, pi] with |error| <~ 2.5e-7 rad: octant reduction,
 // t = min/max by the hardware reciprocal, degree-8 minimax polynomial in t^2 for atan(t)/t
@@ -280,7 +280,7 @@ struct Seg {
 };
 
 template <int ENV, bool VISION, bool SLAB>
-__global__ void __launch_bounds__(kSenseWarps * 32, 8) k_sense(
+__global__ void __launch_bounds__(kSenseWarps * 32, 6) k_sense(
     Params P, const uint32_t* __restrict__ cell_start, const float4* __restrict__ sorted,
     const float2* __restrict__ sorted_xy, const uint32_t* __restrict__ perm, Outs O, Slab SL) {
   __shared__ uint32_t s_min[kSenseWarps][2][kMaxViewSlots];
@@ -354,10 +354,9 @@ __global__ void __launch_bounds__(kSenseWarps * 32, 8) k_sense(
   for (uint32_t q0 = qb + NQ * (blockIdx.y * kSenseWarps + warp); q0 < qe; q0 += qstride) {
     float4 me[NQ];
     bool live[NQ];
-    uint32_t tq[NQ], pushed[NQ], ncol[NQ], ntouch[NQ];
+    uint32_t tq[NQ], head[NQ], tail[NQ], ncol[NQ], ntouch[NQ];
     float sn[NQ], csn[NQ];
     long long rs[NQ];
-    int nq[NQ];
 #pragma unroll
     for (int t = 0; t < NQ; ++t) {
       live[t] = q0 + t < qe;
@@ -365,13 +364,15 @@ __global__ void __launch_bounds__(kSenseWarps * 32, 8) k_sense(
       tq[t] = (ENV == kTag) ? (uint32_t)me[t].w : 0u;
       sn[t] = csn[t] = 0.f;
       if (VISION) {
-        sincosf(me[t].z, &sn[t], &csn[t]);
+        // heading in [-pi, pi) for the MUFU sin/cos (abs error ~4e-7 rad, inside the band
+        // budget of 4.4e-6 rad); the subtraction is exact (Sterbenz).
+        const float th = (me[t].z >= 3.14159265f) ? me[t].z - P.two_pi : me[t].z;
+        __sincosf(th, &sn[t], &csn[t]);
 #pragma unroll
         for (int w = 0; w < kMaxViewSlots / 32; ++w) s_min[warp][t][32 * w + lane] = kOneBits;
       }
-      pushed[t] = ncol[t] = ntouch[t] = 0u;
+      head[t] = tail[t] = ncol[t] = ntouch[t] = 0u;
       rs[t] = 0;
-      nq[t] = 0;
     }
     __syncwarp();
 
@@ -445,40 +446,36 @@ __global__ void __launch_bounds__(kSenseWarps * 32, 8) k_sense(
           const unsigned bala = __ballot_sync(kFull, ia);
           const unsigned balb = __ballot_sync(kFull, ib);
           float4* qq = s_q[warp][t];
-          if (ia) qq[nq[t] + __popc(bala & lt_mask)] = make_float4(dxa, dya, d2a, __uint_as_float(pa | ta));
-          nq[t] += __popc(bala);
-          if (ib) qq[nq[t] + __popc(balb & lt_mask)] = make_float4(dxb, dyb, d2b, __uint_as_float(pb | tb));
-          nq[t] += __popc(balb);
+          if (ia) qq[(tail[t] + __popc(bala & lt_mask)) & (kQueue - 1)] =
+              make_float4(dxa, dya, d2a, __uint_as_float(pa | ta));
+          tail[t] += __popc(bala);
+          if (ib) qq[(tail[t] + __popc(balb & lt_mask)) & (kQueue - 1)] =
+              make_float4(dxb, dyb, d2b, __uint_as_float(pb | tb));
+          tail[t] += __popc(balb);
         }
 #pragma unroll
         for (int t = 0; t < NQ; ++t) {
           float4* qq = s_q[warp][t];
-          while (nq[t] >= 32) {
+          while (tail[t] - head[t] >= 32u) {
             __syncwarp();
-            process(t, qq[lane]);
-            nq[t] -= 32;
-            pushed[t] += 32;
-            __syncwarp();
-            const float4 m0 = qq[32 + lane], m1 = qq[64 + lane];
-            __syncwarp();
-            if (lane < nq[t]) qq[lane] = m0;
-            if (lane + 32 < nq[t]) qq[32 + lane] = m1;
-            __syncwarp();
+            process(t, qq[(head[t] + lane) & (kQueue - 1)]);
+            head[t] += 32u;
           }
         }
+        __syncwarp();                       // ring slots read above may be rewritten next
       }
     }
     __syncwarp();
 #pragma unroll
     for (int t = 0; t < NQ; ++t)
-      if (lane < nq[t]) process(t, s_q[warp][t][lane]);
+      if (lane < tail[t] - head[t]) process(t, s_q[warp][t][(head[t] + lane) & (kQueue - 1)]);
     __syncwarp();
 
 #pragma unroll
     for (int t = 0; t < NQ; ++t) {
       if (!live[t]) continue;                                        // warp-uniform
       const uint32_t q = q0 + t;
-      const uint32_t nn = pushed[t] + (uint32_t)nq[t] - 1u;          // minus the self pair
+      const uint32_t nn = tail[t] - 1u;                             // minus the self pair
       // Warp reductions (REDUX): the int64 reward sum as exact 32-bit partial sums.
       const uint32_t nc = __reduce_add_sync(kFull, ncol[t]);
       const uint32_t nt = (ENV == kTag) ? __reduce_add_sync(kFull, ntouch[t]) : 0u;
