@@ -51,7 +51,8 @@ def parse():
                     help="bounded oracle sample for cpu_baseline (seconds of CPU work)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
-    ap.add_argument("--no-policy", action="store_true")
+    ap.add_argument("--no-policy", action="store_true",
+                    help="skip the NEXT-row measurements (policy, GAE, opinion dynamics)")
     return ap.parse_args()
 
 
@@ -377,6 +378,50 @@ def run_ours(args):
                   "bound": "hbm (obs read 4*obs_dim B/row)"}
         pl.close()
 
+    # ---- K8 GAE (NEXT #3) over an n x 128 trajectory buffer and K9 opinion dynamics
+    # (NEXT #4, Listing 1) on a 10^6-node, degree-16 graph: measured separately.
+    gae_m = opin_m = None
+    if not args.no_policy and rank == 0:
+        from paper_2207_03945_b200 import rl
+        n_g, t_g = min(p.total_agents, 1_000_000), 128
+        gr = torch.randn((t_g, n_g), device=device)
+        gv = torch.randn((t_g + 1, n_g), device=device)
+        ga, gt = torch.empty_like(gr), torch.empty_like(gr)
+        for _ in range(3):
+            rl.gae(gr, gv, ga, gt)
+        ge = [torch.cuda.Event(enable_timing=True) for _ in range(2 * K)]
+        for k in range(K):
+            flush.fill_(k & 0xFF)
+            ge[2 * k].record()
+            rl.gae(gr, gv, ga, gt)
+            ge[2 * k + 1].record()
+        torch.cuda.synchronize()
+        gms = sum(ge[2 * k].elapsed_time(ge[2 * k + 1]) for k in range(K)) / K
+        gbytes = 4 * n_g * (4 * t_g + 1)
+        gae_m = {"kernel": "k_gae", "n": n_g, "t": t_g, "ms": gms,
+                 "GBps": gbytes / (gms / 1e3) / 1e9, "bound": "hbm",
+                 "alg_bytes": gbytes}
+        del gr, gv, ga, gt
+        og = vi.opinion_graph_fast(1_000_000, 16, seed=0)
+        od = {k: torch.from_numpy(v).to(device) for k, v in og.items()}
+        onext = torch.empty_like(od["op"])
+        for _ in range(3):
+            rl.opinion_step(od["row_ptr"], od["col"], od["weight"], od["op"], onext, 0.3, 0.5)
+        oe = [torch.cuda.Event(enable_timing=True) for _ in range(2 * K)]
+        for k in range(K):
+            flush.fill_(k & 0xFF)
+            oe[2 * k].record()
+            rl.opinion_step(od["row_ptr"], od["col"], od["weight"], od["op"], onext, 0.3, 0.5)
+            oe[2 * k + 1].record()
+        torch.cuda.synchronize()
+        oms = sum(oe[2 * k].elapsed_time(oe[2 * k + 1]) for k in range(K)) / K
+        n_e = int(og["col"].size)
+        obytes = 12 * n_e + 12 * 1_000_000
+        opin_m = {"kernel": "k_opinion", "nodes": 1_000_000, "edges": n_e, "ms": oms,
+                  "edges_per_s": n_e / (oms / 1e3), "GBps": obytes / (oms / 1e3) / 1e9,
+                  "bound": "hbm/L2 gather", "alg_bytes": obytes}
+        del od, onext
+
     if rank == 0:
         peaks, peak_src = measured_peaks()
         hbm = float(peaks.get("hbm_gbs", 6441.6))
@@ -437,6 +482,8 @@ def run_ours(args):
             "e2e": e2e,
             "gpu_launches": run.launches * K,
             "policy": policy,
+            "gae": gae_m,
+            "opinion": opin_m,
             "clocks": clk.summary(),
             "cpu_baseline": cpu,
             "context": PAPER_CONTEXT,

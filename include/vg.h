@@ -242,6 +242,24 @@ vg_status vg_policy_forward(vg_policy* p, const float* obs, int64_t rows,
                             const vg_policy_outputs* outs, uint64_t seed, uint64_t step,
                             void* stream);
 
+/* ------------------------------------------------- GAE over the trajectory buffer (§8f #3)
+ * Generalized advantage estimation for n agents x t steps, continuing task
+ * (no terminal flags; the value array carries the bootstrap row t).  Time-major device
+ * arrays: reward [t][n], value [t+1][n] -> adv [t][n], ret [t][n] (adv + value).
+ * A[k] = sum_l (gamma lambda)^l delta[k+l], delta[k] = r[k] + gamma V[k+1] - V[k]. */
+vg_status vg_gae(const float* reward, const float* value, int64_t n, int32_t t, float gamma,
+                 float lambda, float* adv, float* ret, void* stream);
+
+/* --------------------------------------- opinion dynamics, Listing 1 (§8f #4)
+ * One step of the bounded-confidence graph interaction + self interaction: for each node
+ * (me), over its out-edges in CSR order (sorted by (src, dst), row_ptr [n+1], col [E] =
+ * dst, weight [E] >= 0): if |op[me] - op[you]| < threshold then w = strength weight,
+ * new = (1 - w) new + w op[you]; new starts at op[me]; op_out[me] = new.  op_in and
+ * op_out are distinct device arrays [n] (simultaneous update). */
+vg_status vg_opinion_step(const int32_t* row_ptr, const int32_t* col, const float* weight,
+                          int32_t n, const float* op_in, float* op_out, float threshold,
+                          float strength, void* stream);
+
 /* Phase timing for measurement.  After vg_profile_begin(w, max_steps), each of the next
  * max_steps vg_step calls records CUDA events on its stream between its phases
  * (VG_N_PHASES: integrate+cell-id+histogram, cell scan, scatter, cell sort, sense+reward).

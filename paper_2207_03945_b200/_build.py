@@ -11,6 +11,7 @@ CSRC = os.path.join(PKG, "csrc")
 LIB = os.path.join(PKG, "libvg.so")
 SOURCES = [os.path.join(CSRC, "vg.cu")]
 HEADERS = [os.path.join(CSRC, "vg_kernels.cuh"), os.path.join(CSRC, "vg_policy.cuh"),
+           os.path.join(CSRC, "vg_rl.cuh"),
            os.path.join(ROOT, "include", "vg.h")]
 
 NVCC_FLAGS = [

@@ -16,6 +16,7 @@
 #include "vg.h"
 #include "vg_kernels.cuh"
 #include "vg_policy.cuh"
+#include "vg_rl.cuh"
 
 namespace {
 
@@ -804,6 +805,32 @@ vg_status vg_policy_forward(vg_policy* p, const float* obs, int64_t rows,
       obs, rows, p->cfg.obs_dim, p->pk, o, (uint32_t)seed, (uint32_t)(seed >> 32),
       (uint32_t)step, (uint32_t)(step >> 32));
   return launch_check("k_policy");
+}
+
+vg_status vg_gae(const float* reward, const float* value, int64_t n, int32_t t, float gamma,
+                 float lambda, float* adv, float* ret, void* stream) {
+  if (!reward || !value || !adv || !ret) return fail(VG_EINVAL, "vg_gae: NULL pointer");
+  if (n < 0 || t < 1) return fail(VG_EINVAL, "vg_gae: need n >= 0 and t >= 1");
+  if (!(gamma >= 0.f && gamma <= 1.f) || !(lambda >= 0.f && lambda <= 1.f))
+    return fail(VG_EINVAL, "vg_gae: gamma and lambda must be in [0, 1]");
+  if (n == 0) return VG_OK;
+  const unsigned blocks = (unsigned)std::min<int64_t>((n + 255) / 256, 1 << 20);
+  vg::k_gae<<<blocks, 256, 0, as_stream(stream)>>>(reward, value, n, t, gamma, gamma * lambda,
+                                                    adv, ret);
+  return launch_check("k_gae");
+}
+
+vg_status vg_opinion_step(const int32_t* row_ptr, const int32_t* col, const float* weight,
+                          int32_t n, const float* op_in, float* op_out, float threshold,
+                          float strength, void* stream) {
+  if (!row_ptr || !op_in || !op_out) return fail(VG_EINVAL, "vg_opinion_step: NULL pointer");
+  if (n < 0) return fail(VG_EINVAL, "vg_opinion_step: n must be >= 0");
+  if (op_in == op_out) return fail(VG_EINVAL, "vg_opinion_step: op_in and op_out must differ (simultaneous update)");
+  if (!(threshold >= 0.f) || !(strength >= 0.f)) return fail(VG_EINVAL, "vg_opinion_step: threshold, strength must be >= 0");
+  if (n == 0) return VG_OK;
+  vg::k_opinion<<<(unsigned)((n + 255) / 256), 256, 0, as_stream(stream)>>>(
+      row_ptr, col, weight, n, op_in, op_out, threshold, strength);
+  return launch_check("k_opinion");
 }
 
 vg_status vg_profile_begin(vg_world* w, int32_t max_steps) {

@@ -236,3 +236,36 @@ def policy_weights(obs_dim: int, seed: int = 0, hidden: int = 64, act_dim: int =
             "V1": u(hidden, obs_dim, fan=obs_dim), "c1": u(hidden, fan=obs_dim),
             "V2": u(hidden, hidden, fan=hidden), "c2": u(hidden, fan=hidden),
             "V3": u(1, hidden, fan=hidden), "c3": u(1, fan=hidden)}
+
+
+# --------------------------------------------------------------------------------------
+# Opinion-dynamics graph (Listing 1)
+# --------------------------------------------------------------------------------------
+def opinion_graph(n: int, degree: int, seed: int = 0) -> dict:
+    """Random directed graph, `degree` distinct out-neighbours per node (no self loops),
+    CSR sorted by (src, dst); weights U[0, 1]; opinions U[0, 1] (fp32)."""
+    rng = np.random.Generator(np.random.PCG64(seed))
+    deg = min(degree, n - 1)
+    cols = []
+    for i in range(n):
+        c = rng.choice(n - 1, deg, replace=False) if deg > 0 else np.zeros(0, np.int64)
+        c = c + (c >= i)                     # skip the self loop
+        cols.append(np.sort(c))
+    col = np.concatenate(cols).astype(np.int32) if cols else np.zeros(0, np.int32)
+    row_ptr = (np.arange(n + 1) * deg).astype(np.int32)
+    weight = rng.random(len(col)).astype(np.float32)
+    op = rng.random(n).astype(np.float32)
+    return {"row_ptr": row_ptr, "col": col, "weight": weight, "op": op}
+
+
+def opinion_graph_fast(n: int, degree: int, seed: int = 0) -> dict:
+    """Large-n variant (bench): out-neighbours drawn with replacement then de-duplicated
+    per row is avoided — uniform random dst != src, sorted per row, duplicates allowed."""
+    rng = np.random.Generator(np.random.PCG64(seed))
+    dst = rng.integers(0, n - 1, size=(n, degree))
+    dst = dst + (dst >= np.arange(n)[:, None])
+    dst.sort(axis=1)
+    return {"row_ptr": (np.arange(n + 1) * degree).astype(np.int32),
+            "col": dst.reshape(-1).astype(np.int32),
+            "weight": rng.random(n * degree).astype(np.float32),
+            "op": rng.random(n).astype(np.float32)}
