@@ -263,8 +263,10 @@ def run_ours(args):
 
     rank, local, world = rank_info()
     if world > 1:
+        import datetime
         torch.cuda.set_device(local)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local),
+                                timeout=datetime.timedelta(seconds=300))
     device = torch.device("cuda", local)
     torch.cuda.set_device(device)
     slab_mode = args.config == "c5" and world > 1
