@@ -47,6 +47,8 @@ def parse():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--config", default="c5", choices=["c1", "c2", "c3", "c4", "c5"])
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--vision", default="sector", choices=["sector", "ray"],
+                    help="vision model (reading A1): sector bins (default) or ray-disc (NEXT #2)")
     ap.add_argument("--cpu-seconds", type=float, default=15.0,
                     help="bounded oracle sample for cpu_baseline (seconds of CPU work)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -271,10 +273,11 @@ def run_ours(args):
     torch.cuda.set_device(device)
     slab_mode = args.config == "c5" and world > 1
     if slab_mode:
-        p, scaling = vi.workload("c5"), "strong"
+        p, scaling = vi.workload("c5").replace(vision=args.vision), "strong"
         run = SlabRunner(p, device, rank, world, torch, vg)
     else:
         p, scaling = local_params(args.config, world, rank)
+        p = p.replace(vision=args.vision)
         run = ReplicaRunner(p, device, rank, torch, vg)
     w = run.w
     acts = action_pool(p, torch, device, seed=rank)
@@ -471,6 +474,7 @@ def run_ours(args):
             "scaling": scaling, "vs_baseline": None, "dtype": "f32", "data": "synthetic",
             "config": {"workload": args.config, "desc": vi.WORKLOAD_DESCRIPTIONS[args.config],
                        "R_per_gpu": p.n_replicas, "N": p.n_agents, "G": w.grid,
+                       "vision": args.vision,
                        "parallelism": par,
                        "l2": "256 MiB buffer written between timed steps (outside events)"},
             "roofline": {"kernel": "k_sense (sector vision + reward)", "bound": "alu",

@@ -61,7 +61,10 @@ typedef enum {
 } vg_status;
 
 typedef enum { VG_ENV_FLOCK = 0, VG_ENV_TAG = 1 } vg_env;
-typedef enum { VG_VISION_SECTOR = 0 /* hot path (A1) */, VG_VISION_RAY = 1 /* not built */ } vg_vision;
+/* Vision model (reading A1): SECTOR bins neighbour centres by bearing (hot path); RAY casts
+ * one ray per sector centre against neighbour discs of radius d_r (NEXT #2;
+ * needs cell size >= (d_v + d_r)(1 + 2^-12)). */
+typedef enum { VG_VISION_SECTOR = 0, VG_VISION_RAY = 1 } vg_vision;
 typedef enum { VG_SHARD_REPLICA = 0, VG_SHARD_SLAB = 1 } vg_shard;
 
 /* World configuration.  All floats are authoritative fp32 values (A12).  Defaults in
@@ -69,7 +72,7 @@ typedef enum { VG_SHARD_REPLICA = 0, VG_SHARD_SLAB = 1 } vg_shard;
  * fov ~ 250 deg, v = 128 / 2 x 64 and obs_dim 129 / 128. */
 typedef struct {
   int32_t env;          /* vg_env                                                          */
-  int32_t vision;       /* vg_vision: must be VG_VISION_SECTOR                             */
+  int32_t vision;       /* vg_vision: VG_VISION_SECTOR (default) or VG_VISION_RAY          */
   int32_t shard;        /* vg_shard: VG_SHARD_REPLICA, or VG_SHARD_SLAB (see slab mode)     */
   int32_t n_agents;     /* N > 0, agents per replica                               */
   int32_t n_replicas;   /* R > 0; R*N < 2^31                                               */

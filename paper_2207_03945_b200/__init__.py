@@ -33,7 +33,7 @@ def config_from_params(p, slab: dict | None = None) -> _lib.VgConfig:
     over P ranks by x-slabs)."""
     c = _lib.VgConfig()
     c.env = _ENV[p.env]
-    c.vision = 0
+    c.vision = {"sector": 0, "ray": 1}[getattr(p, "vision", "sector")]
     c.shard = 1 if slab else 0
     if slab:
         c.rank = int(slab["rank"])

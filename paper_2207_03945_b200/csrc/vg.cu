@@ -56,6 +56,7 @@ struct vg_world {
   float4* tmp_rec = nullptr;       // [R*N]
   float4* sorted = nullptr;        // [R*N]
   float2* sorted_xy = nullptr;     // [R*N]         positions of `sorted` (K4 candidate reads)
+  float2* ray_dir = nullptr;       // [v] ray vision: sector-centre ray directions (agent frame)
   float2* act_dev = nullptr;       // [R*N]         staging for vg_step_host
   unsigned long long* err_dev = nullptr;  // smallest bad agent index (device word)
   uint32_t* err_flag = nullptr;    // mapped pinned host flag (set by kernels)
@@ -101,7 +102,7 @@ int auto_grid(double L, double dv) {
 vg_status validate(const vg_config& c, int* grid_out) {
   const double PI = 3.14159265358979323846;
   if (c.env != VG_ENV_FLOCK && c.env != VG_ENV_TAG) return fail(VG_EINVAL, "env: must be 0 (flock) or 1 (tag)");
-  if (c.vision != VG_VISION_SECTOR) return fail(VG_EINVAL, "vision: only VG_VISION_SECTOR is built (reading A1)");
+  if (c.vision != VG_VISION_SECTOR && c.vision != VG_VISION_RAY) return fail(VG_EINVAL, "vision: must be 0 (sector) or 1 (ray-disc)");
   if (c.shard != VG_SHARD_REPLICA && c.shard != VG_SHARD_SLAB) return fail(VG_EINVAL, "shard: must be 0 (replica) or 1 (slab)");
   if (c.n_agents <= 0) return fail(VG_EINVAL, "n_agents: must be > 0 (S:241)");
   if (c.n_replicas <= 0) return fail(VG_EINVAL, "n_replicas: must be > 0");
@@ -132,6 +133,10 @@ vg_status validate(const vg_config& c, int* grid_out) {
   if (g == 0) g = auto_grid(c.width, c.d_v);
   if (g < 3) return fail(VG_EINVAL, "grid: G = %d, need G >= 3 (3x3 stencil must not alias)", g);
   if ((double)c.width / g < need) return fail(VG_EINVAL, "grid: cell size L/G = %g must be >= d_v (1 + 2^-12) = %g (A16)", (double)c.width / g, need);
+  if (c.vision == VG_VISION_RAY && (double)c.width / g < ((double)c.d_v + c.d_r) * (1.0 + std::ldexp(1.0, -12)))
+    return fail(VG_EINVAL, "grid: ray vision needs cell size >= (d_v + d_r)(1 + 2^-12) (S:178)");
+  if (c.vision == VG_VISION_RAY && !(2.0 * ((double)c.d_v + c.d_r) < c.width))
+    return fail(VG_EINVAL, "d_v: ray vision needs d_v + d_r < width/2");
   if ((long long)g * g * c.n_replicas >= (1LL << 31)) return fail(VG_EINVAL, "grid: n_replicas * G^2 must be < 2^31");
   if (c.shard == VG_SHARD_SLAB) {
     if (c.world_size < 2) return fail(VG_EINVAL, "world_size: slab mode needs world_size >= 2");
@@ -187,6 +192,12 @@ vg::Params derive(const vg_config& c, int g) {
   P.k_rise = c.c_near / (c.d_peak - P.two_dr);
   P.k_fall = c.c_near / (c.d_v - c.d_peak);
   P.w_prox = c.w_prox;
+  P.d_r = c.d_r;
+  {
+    volatile float reach = c.d_v + c.d_r;
+    P.cand2 = reach * reach;
+  }
+  P.inv_w = (float)c.v / c.fov;
   P.b_rise = -P.k_rise * P.two_dr;
   P.nk_fall = -P.k_fall;
   P.b_fall = P.k_fall * c.d_v;
@@ -266,26 +277,28 @@ int sense_chunks(const vg_world* w) {
   return (int)std::max(1LL, std::min(ch, 1024LL));
 }
 
+template <int ENV, bool VISION, bool SLAB>
+void sense_kernel(vg_world* w, dim3 grid, const vg::Outs& O, cudaStream_t s) {
+  if (w->cfg.vision == VG_VISION_RAY)
+    vg::k_sense<ENV, VISION, SLAB, true><<<grid, vg::kSenseWarps * 32, 0, s>>>(
+        w->P, w->cell_start, w->sorted, w->sorted_xy, w->perm, O, w->SL, w->ray_dir);
+  else
+    vg::k_sense<ENV, VISION, SLAB, false><<<grid, vg::kSenseWarps * 32, 0, s>>>(
+        w->P, w->cell_start, w->sorted, w->sorted_xy, w->perm, O, w->SL, w->ray_dir);
+}
+
 template <bool VISION>
 vg_status launch_sense(vg_world* w, const vg_outputs* outs, cudaStream_t s) {
   const vg::Outs O = to_outs(outs);
   if (w->slab) {                      // owned cells only: local columns 1..W
     const dim3 grid((unsigned)(w->SL.W * w->P.G), 1);
-    if (w->P.env == vg::kFlock)
-      vg::k_sense<vg::kFlock, VISION, true><<<grid, vg::kSenseWarps * 32, 0, s>>>(
-          w->P, w->cell_start, w->sorted, w->sorted_xy, w->perm, O, w->SL);
-    else
-      vg::k_sense<vg::kTag, VISION, true><<<grid, vg::kSenseWarps * 32, 0, s>>>(
-          w->P, w->cell_start, w->sorted, w->sorted_xy, w->perm, O, w->SL);
+    if (w->P.env == vg::kFlock) sense_kernel<vg::kFlock, VISION, true>(w, grid, O, s);
+    else sense_kernel<vg::kTag, VISION, true>(w, grid, O, s);
     return launch_check("k_sense(slab)");
   }
   const dim3 grid((unsigned)w->n_cells, (unsigned)sense_chunks(w));
-  if (w->P.env == vg::kFlock)
-    vg::k_sense<vg::kFlock, VISION, false><<<grid, vg::kSenseWarps * 32, 0, s>>>(
-        w->P, w->cell_start, w->sorted, w->sorted_xy, w->perm, O, w->SL);
-  else
-    vg::k_sense<vg::kTag, VISION, false><<<grid, vg::kSenseWarps * 32, 0, s>>>(
-        w->P, w->cell_start, w->sorted, w->sorted_xy, w->perm, O, w->SL);
+  if (w->P.env == vg::kFlock) sense_kernel<vg::kFlock, VISION, false>(w, grid, O, s);
+  else sense_kernel<vg::kTag, VISION, false>(w, grid, O, s);
   return launch_check("k_sense");
 }
 
@@ -398,6 +411,17 @@ vg_status vg_world_create(const vg_config* cfg, vg_world** out) {
   if (!st) st = dalloc(w, &w->tmp_rec, n);
   if (!st) st = dalloc(w, &w->sorted, n);
   if (!st) st = dalloc(w, &w->sorted_xy, n + 64);   // padded: unpredicated K4 loads
+  if (!st) st = dalloc(w, &w->ray_dir, vg::kMaxViewSlots);
+  if (!st) {
+    // psi_k = -fov/2 + (k + 1/2) fov/v (orientation A3), in double, rounded once
+    float2 tab[vg::kMaxViewSlots] = {};
+    for (int k = 0; k < cfg->v; ++k) {
+      const double psi = -0.5 * (double)cfg->fov + (k + 0.5) * (double)cfg->fov / cfg->v;
+      tab[k] = make_float2((float)std::cos(psi), (float)std::sin(psi));
+    }
+    cudaError_t e = cudaMemcpy(w->ray_dir, tab, sizeof(tab), cudaMemcpyHostToDevice);
+    if (e != cudaSuccess) st = fail(VG_ECUDA, "ray table: %s", cudaGetErrorString(e));
+  }
   if (!st) st = dalloc(w, &w->act_dev, n);
   if (!st) st = dalloc(w, &w->err_dev, 1);
   if (!st) {
@@ -434,6 +458,7 @@ void vg_world_destroy(vg_world* w) {
   cudaFree(w->tmp_rec);
   cudaFree(w->sorted);
   cudaFree(w->sorted_xy);
+  cudaFree(w->ray_dir);
   cudaFree(w->act_dev);
   cudaFree(w->err_dev);
   cudaFree(w->loc_n);

@@ -36,6 +36,7 @@ struct Params {
   float half_fov, inv_fov, fv;  // fov/2, 1/fov, float(v)
   float c_collide, d_peak, k_rise, k_fall, w_prox;
   float b_rise, nk_fall, b_fall;   // f = min(k_rise d + b_rise, nk_fall d + b_fall) (A5)
+  float d_r, cand2, inv_w;         // ray vision: body radius, RN32((d_v + d_r)^2), v / fov
   long long touch_fix;         // r_touch * 2^32
 };
 
@@ -279,11 +280,16 @@ struct Seg {
   float qsx, qsy;    // query image shift (0 or -L)
 };
 
-template <int ENV, bool VISION, bool SLAB>
+// RAY: the ray-disc reading of the vision model (DESIGN.md
+// §6d): candidates within d_v + d_r, one ray per sector centre (table ray_dir, agent
+// frame), each neighbour a disc of radius d_r; counts and reward stay Eq. 1 (d < d_v).
+template <int ENV, bool VISION, bool SLAB, bool RAY>
 __global__ void __launch_bounds__(kSenseWarps * 32, 6) k_sense(
     Params P, const uint32_t* __restrict__ cell_start, const float4* __restrict__ sorted,
-    const float2* __restrict__ sorted_xy, const uint32_t* __restrict__ perm, Outs O, Slab SL) {
+    const float2* __restrict__ sorted_xy, const uint32_t* __restrict__ perm, Outs O, Slab SL,
+    const float2* __restrict__ ray_dir) {
   __shared__ uint32_t s_min[kSenseWarps][2][kMaxViewSlots];
+  __shared__ float2 s_ray[RAY ? kMaxViewSlots : 1];
   __shared__ float4 s_q[kSenseWarps][2][kQueue];
   __shared__ Seg s_seg[6];
   __shared__ int s_nseg;
@@ -341,6 +347,9 @@ __global__ void __launch_bounds__(kSenseWarps * 32, 6) k_sense(
     }
     s_nseg = ns;
   }
+  if (RAY) {
+    for (int k = threadIdx.x; k < P.v; k += blockDim.x) s_ray[k] = ray_dir[k];
+  }
   __syncthreads();
   const int nseg = s_nseg;
   const uint32_t qb = cs[cl], qe = cs[cl + 1];
@@ -354,7 +363,7 @@ __global__ void __launch_bounds__(kSenseWarps * 32, 6) k_sense(
   for (uint32_t q0 = qb + NQ * (blockIdx.y * kSenseWarps + warp); q0 < qe; q0 += qstride) {
     float4 me[NQ];
     bool live[NQ];
-    uint32_t tq[NQ], head[NQ], tail[NQ], ncol[NQ], ntouch[NQ];
+    uint32_t tq[NQ], head[NQ], tail[NQ], ncol[NQ], ntouch[NQ], nnb[NQ];
     float sn[NQ], csn[NQ];
     long long rs[NQ];
 #pragma unroll
@@ -371,7 +380,7 @@ __global__ void __launch_bounds__(kSenseWarps * 32, 6) k_sense(
 #pragma unroll
         for (int w = 0; w < kMaxViewSlots / 32; ++w) s_min[warp][t][32 * w + lane] = kOneBits;
       }
-      head[t] = tail[t] = ncol[t] = ntouch[t] = 0u;
+      head[t] = tail[t] = ncol[t] = ntouch[t] = nnb[t] = 0u;
       rs[t] = 0;
     }
     __syncwarp();
@@ -388,14 +397,50 @@ __global__ void __launch_bounds__(kSenseWarps * 32, 6) k_sense(
       // Eq. 1 / Fig. 4 (A5): contact -> -c_collide, else the tent min(rise, fall).
       const float f = contact ? -P.c_collide
                               : fminf(fmaf(P.k_rise, d, P.b_rise), fmaf(P.nk_fall, d, P.b_fall));
-      if (ENV == kFlock) {
-        rs[t] += __float2ll_rn(f * kFix);
-        ncol[t] += contact ? 1u : 0u;
-      } else {
-        if (contact) {
-          if (tj == tq[t]) ++ncol[t]; else ++ntouch[t];
+      if (!RAY || d2 < P.dv2) {                                       // Eq. 1: d < d_v
+        if (RAY) ++nnb[t];
+        if (ENV == kFlock) {
+          rs[t] += __float2ll_rn(f * kFix);
+          ncol[t] += contact ? 1u : 0u;
+        } else {
+          if (contact) {
+            if (tj == tq[t]) ++ncol[t]; else ++ntouch[t];
+          }
+          if (tq[t] == 0u && tj == 0u) rs[t] += __float2ll_rn((P.w_prox * f) * kFix);
         }
-        if (tq[t] == 0u && tj == 0u) rs[t] += __float2ll_rn((P.w_prox * f) * kFix);
+      }
+      if (VISION && RAY) {
+        const float fwd = fmaf(csn[t], e.x, sn[t] * e.y);
+        const float left = fmaf(csn[t], e.y, -sn[t] * e.x);
+        uint32_t* row = &s_min[warp][t][tj * P.v];
+        if (d <= P.d_r) {                          // origin inside the disc: every ray hits at 0
+          for (int k = 0; k < P.v; ++k) atomicMin(&row[k], 0u);
+          return;
+        }
+        const float phi = vg_atan2(left, fwd);
+        const float alpha = asinf(fminf(P.d_r * rsq, 1.f));
+        // Sectors whose centre ray may touch the disc: psi_k in [phi - alpha, phi + alpha]
+        // (also shifted by -+2 pi across the blind-spot seam), widened by one sector on each
+        // side; every ray in the range is then tested exactly.
+#pragma unroll 1
+        for (int wrap = -1; wrap <= 1; ++wrap) {
+          const float lo = phi - alpha + wrap * P.two_pi, hi = phi + alpha + wrap * P.two_pi;
+          if (hi < -P.half_fov - 0.1f || lo > P.half_fov + 0.1f) continue;
+          const int k0 = max(0, (int)floorf((lo + P.half_fov) * P.inv_w - 0.5f));
+          const int k1 = min(P.v - 1, (int)ceilf((hi + P.half_fov) * P.inv_w - 0.5f));
+          for (int k = k0; k <= k1; ++k) {
+            const float2 ud = s_ray[k];
+            const float bb = fmaf(ud.x, fwd, ud.y * left);       // along the ray
+            const float pp = fmaf(ud.x, left, -ud.y * fwd);      // perpendicular offset
+            const float h = (P.d_r - pp) * (P.d_r + pp);         // r^2 - p^2, well conditioned
+            if (h >= 0.f && bb > 0.f) {
+              const float tt = fmaxf(bb - sqrtf(h), 0.f);        // entry distance
+              if (tt < P.d_v)
+                atomicMin(&row[k], __float_as_uint(fminf(tt * P.inv_dv, kBelowOne)));
+            }
+          }
+        }
+        return;
       }
       if (VISION) {
         // Bearing in the agent frame (A3): phi = atan2(h x d, h . d), CCW-positive.
@@ -441,8 +486,8 @@ __global__ void __launch_bounds__(kSenseWarps * 32, 6) k_sense(
           const float dxb = bx - qx[t], dyb = by - qy[t];
           const float d2a = fmaf(dxa, dxa, dya * dya);
           const float d2b = fmaf(dxb, dxb, dyb * dyb);
-          const bool ia = d2a < P.dv2;                                 // Eq. 1: d < d_v
-          const bool ib = d2b < P.dv2;
+          const bool ia = d2a < (RAY ? P.cand2 : P.dv2);               // Eq. 1: d < d_v
+          const bool ib = d2b < (RAY ? P.cand2 : P.dv2);
           const unsigned bala = __ballot_sync(kFull, ia);
           const unsigned balb = __ballot_sync(kFull, ib);
           float4* qq = s_q[warp][t];
@@ -475,7 +520,8 @@ __global__ void __launch_bounds__(kSenseWarps * 32, 6) k_sense(
     for (int t = 0; t < NQ; ++t) {
       if (!live[t]) continue;                                        // warp-uniform
       const uint32_t q = q0 + t;
-      const uint32_t nn = tail[t] - 1u;                             // minus the self pair
+      const uint32_t nn = RAY ? __reduce_add_sync(kFull, nnb[t])
+                              : tail[t] - 1u;                   // minus the self pair
       // Warp reductions (REDUX): the int64 reward sum as exact 32-bit partial sums.
       const uint32_t nc = __reduce_add_sync(kFull, ncol[t]);
       const uint32_t nt = (ENV == kTag) ? __reduce_add_sync(kFull, ntouch[t]) : 0u;

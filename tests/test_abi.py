@@ -100,10 +100,15 @@ def test_unbuilt_modes_rejected():
     import paper_2207_03945_b200 as vg
     from paper_2207_03945_b200 import _lib
     c = vg.config_from_params(vi.workload("c2"))
-    c.vision = 1
+    c.vision = 2
     h = ctypes.c_void_p()
     assert _lib.lib.vg_world_create(ctypes.byref(c), ctypes.byref(h)) == _lib.VG_EINVAL
     assert "vision" in _lib.lib.vg_last_error().decode()
+    # ray vision needs cell size >= (d_v + d_r)(1 + 2^-12)
+    c = vg.config_from_params(vi.flock_params(100, width=100.0, d_v=10.0, grid=9, d_r=1.2,
+                                              vision="ray"))
+    assert _lib.lib.vg_world_create(ctypes.byref(c), ctypes.byref(h)) == _lib.VG_EINVAL
+    assert "ray vision" in _lib.lib.vg_last_error().decode()
 
 
 def test_null_arguments():

@@ -1,0 +1,90 @@
+"""GPU parity of the ray-disc vision variant (oracle/ray.py).
+
+Counts and reward are Eq. 1 as in the sector model (same contract); the view is checked
+against the oracle's per-sector interval [lo, hi] (1e-5 relative plus the fp32 sensitivity of
+near-grazing rays), and sector occupancy must agree with the view."""
+import math
+
+import numpy as np
+import pytest
+
+import oracle
+import vg_inputs as vi
+import vg_parity as parity
+from oracle.ray import ray_views
+
+pytestmark = pytest.mark.gpu
+
+
+def _run(p, st0, act=None):
+    import torch
+    import paper_2207_03945_b200 as vg
+    w = vg.World(p)
+    out = w.alloc_outputs()
+    st = torch.from_numpy(st0).cuda()
+    if act is None:
+        w.bin(st)
+        w.sense(out)
+    else:
+        w.step(st, torch.from_numpy(act).cuda(), out)
+    torch.cuda.synchronize()
+    res = {k: getattr(out, k)[0].cpu().numpy() for k in
+           ("obs", "reward", "n_neigh", "n_collide", "n_touch", "sector_occ")
+           if getattr(out, k) is not None}
+    cur = st.cpu().numpy()
+    w.close()
+    return res, cur
+
+
+def _check(p, g, state_r, rows):
+    nv = (1 if p.env == "flock" else 2) * p.v
+    # counts and reward: the sector-model contract (bands included), obs excluded
+    gg = {k: (v.view(np.uint32) if v.dtype == np.int32 else v) for k, v in g.items()
+          if k in ("reward", "n_neigh", "n_collide", "n_touch")}
+    parity.check_sense(p.replace(vision="sector"), state_r, gg, rows=rows)
+    view, lo, hi = ray_views(p, state_r, rows)
+    gv = g["obs"][rows, :nv].astype(np.float64)
+    assert np.all(gv >= lo - 1e-7) and np.all(gv <= hi + 1e-7), \
+        (np.max(lo - gv), np.max(gv - hi))
+    occ = np.unpackbits(g["sector_occ"][rows].view(np.uint8), axis=1, bitorder="little")[:, :nv]
+    assert np.array_equal(occ.astype(bool), gv < 1.0)
+    if p.env == "flock":
+        assert np.allclose(g["obs"][rows, nv], state_r[rows, 3] / p.s_max, rtol=1e-6)
+    return float(np.max(np.abs(gv - view)))
+
+
+@pytest.mark.parametrize("env", ["flock", "tag"])
+def test_ray_random_world(cuda, env):
+    p = (vi.flock_params(3000) if env == "flock" else vi.tag_params(3000)).replace(vision="ray")
+    st0 = vi.init_state(p, seed=4)
+    g, cur = _run(p, st0, vi.actions(p, seed=4))
+    print(_check(p, g, cur[0], np.arange(p.n_agents)))
+
+
+def test_ray_c5_full_size_sampled(cuda):
+    p = vi.workload("c5").replace(vision="ray")
+    g, cur = _run(p, vi.init_state(p, seed=1), vi.actions(p, seed=1))
+    rows = np.random.default_rng(2).choice(p.n_agents, 48, replace=False)
+    _check(p, g, cur[0], rows)
+
+
+def test_ray_closed_forms(cuda):
+    p = vi.flock_params(2).replace(vision="ray")
+    # dead ahead at 3: the central sectors read (3 - correction)/d_v; hit span ~ 2 asin(r/d)
+    g, _ = _run(p, np.array([[[50, 50, 0.0, 0.275], [53, 50, 0.0, 0.275]]], np.float32))
+    v = g["obs"][0, :128]
+    hits = np.nonzero(v < 1)[0]
+    assert 63 in hits and 64 in hits and v[63] == pytest.approx(v[64], rel=1e-6)
+    assert v[64] < 0.3 and v[64] > 0.275 - 1e-6
+    assert abs(len(hits) - 2 * math.asin(0.25 / 3) / (p.fov / 128)) <= 2
+    # origin inside the disc (d = 0.1 < d_r): every ray reads 0
+    g, _ = _run(p, np.array([[[50, 50, 0.0, 0.275], [50.1, 50, 2.0, 0.275]]], np.float32))
+    assert np.all(g["obs"][:, :128] == 0.0)
+    assert list(g["n_collide"]) == [1, 1]
+
+
+def test_ray_clustered(cuda):
+    p = vi.flock_params(2500).replace(vision="ray")
+    st0 = vi.clustered_state(p, seed=5, n_clusters=4, sigma=3.0)
+    g, cur = _run(p, st0)
+    _check(p, g, cur[0], np.arange(0, p.n_agents, 5))

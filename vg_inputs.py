@@ -51,6 +51,7 @@ class EnvParams:
     r_touch: float = 1.0
     w_prox: float = f32(0.1)
     s_max_chaser: float = 0.375  # 0.75 s_max
+    vision: str = "sector"      # "sector" (hot path) | "ray" (ray-disc reading, NEXT #2)
 
     @property
     def channels(self) -> int:
