@@ -383,6 +383,46 @@ def run_ours(args):
                   "bound": "hbm (obs read 4*obs_dim B/row)"}
         pl.close()
 
+    # ---- the paper's experience-collection loop (Fig. 5): vg_rollout of t = 16 steps
+    # (policy sample -> env step -> buffer, bootstrap value, GAE) replayed as one CUDA graph
+    roll_m = None
+    if not args.no_policy and not slab_mode and rank == 0:
+        from paper_2207_03945_b200 import rl
+        from paper_2207_03945_b200.policy import Policy, action_box
+        t_r = 16
+        M = p.total_agents
+        if M * (t_r + 1) * w.obs_dim * 4 < 40e9:
+            pol = Policy(w.obs_dim, *action_box(p), device=device)
+            pol.set_weights(vi.policy_weights(w.obs_dim, seed=0))
+            buf = rl.TrajectoryBuffer(M, t_r, w.obs_dim, device=device)
+            buf.obs[0].copy_(run.out.obs.view(M, -1))
+            rst = run.state.clone()
+            rl.rollout(w, pol, rst, buf, seed=3)
+            torch.cuda.synchronize()
+            g = torch.cuda.CUDAGraph()
+            cs = torch.cuda.Stream(device)
+            cs.wait_stream(torch.cuda.current_stream(device))
+            with torch.cuda.stream(cs):
+                with torch.cuda.graph(g, stream=cs):
+                    rl.rollout(w, pol, rst, buf, seed=3)
+            torch.cuda.current_stream(device).wait_stream(cs)
+            g.replay()
+            torch.cuda.synchronize()
+            re0 = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
+            re1 = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
+            for k in range(3):
+                buf.obs[0].copy_(buf.obs[t_r])        # continue from the last observation
+                re0[k].record()
+                g.replay()
+                re1[k].record()
+            torch.cuda.synchronize()
+            rms = sum(a.elapsed_time(b) for a, b in zip(re0, re1)) / 3
+            roll_m = {"what": "vg_rollout: t x (policy sample + env step) + bootstrap + GAE, one CUDA graph",
+                      "agents": M, "t": t_r, "ms": rms,
+                      "agent_steps_per_s": M * t_r / (rms / 1e3)}
+            del buf, pol
+            torch.cuda.empty_cache()
+
     # ---- K8 GAE (NEXT #3) over an n x 128 trajectory buffer and K9 opinion dynamics
     # (NEXT #4, Listing 1) on a 10^6-node, degree-16 graph: measured separately.
     gae_m = opin_m = None
@@ -489,6 +529,7 @@ def run_ours(args):
             "gpu_launches": run.launches * K,
             "policy": policy,
             "gae": gae_m,
+            "rollout": roll_m,
             "opinion": opin_m,
             "clocks": clk.summary(),
             "cpu_baseline": cpu,

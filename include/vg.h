@@ -253,6 +253,28 @@ vg_status vg_policy_forward(vg_policy* p, const float* obs, int64_t rows,
 vg_status vg_gae(const float* reward, const float* value, int64_t n, int32_t t, float gamma,
                  float lambda, float* adv, float* ret, void* stream);
 
+/* ------------------------------------------ experience collection (Fig. 5)
+ * t environment steps of the paper's loop, entirely on the device: for k = 0 .. t-1,
+ * the shared policy samples actions from obs[k] (value[k], action[k], logp[k]; noise
+ * counter step0 + k), then vg_step integrates them and writes obs[k+1] and reward[k];
+ * finally value[t] = V(obs[t]) (bootstrap) and GAE (vg_gae) fills adv / ret.
+ * Time-major device buffers for M = R*N agents: obs [t+1][M][obs_dim] (obs[0] from a prior
+ * vg_bin + vg_sense or the previous rollout's obs[t]), action [t][M][2], logp [t][M],
+ * reward [t][M], value [t+1][M], adv [t][M], ret [t][M].  Replica mode only.  No host
+ * synchronization: the whole call can be captured in one CUDA graph. */
+typedef struct {
+  float* obs;
+  float* action;
+  float* logp;
+  float* reward;
+  float* value;
+  float* adv;
+  float* ret;
+} vg_rollout_buffers;
+vg_status vg_rollout(vg_world* w, vg_policy* pol, float* state, const vg_rollout_buffers* buf,
+                     int32_t t, uint64_t seed, uint64_t step0, float gamma, float lambda,
+                     void* stream);
+
 /* --------------------------------------- opinion dynamics, Listing 1 (§8f #4)
  * One step of the bounded-confidence graph interaction + self interaction: for each node
  * (me), over its out-edges in CSR order (sorted by (src, dst), row_ptr [n+1], col [E] =

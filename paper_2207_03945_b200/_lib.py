@@ -58,6 +58,11 @@ class VgPolicyOutputs(ctypes.Structure):
     _fields_ = [("mean", c_void_p), ("value", c_void_p), ("action", c_void_p), ("logp", c_void_p)]
 
 
+class VgRolloutBuffers(ctypes.Structure):
+    _fields_ = [("obs", c_void_p), ("action", c_void_p), ("logp", c_void_p),
+                ("reward", c_void_p), ("value", c_void_p), ("adv", c_void_p), ("ret", c_void_p)]
+
+
 class VgWorldInfo(ctypes.Structure):
     _fields_ = [
         ("grid", c_int32), ("cell_size", c_float), ("n_cells", c_int32),
@@ -96,6 +101,8 @@ SIGNATURES = {
     "vg_policy_set_weights": (c_int32, [c_void_p, POINTER(c_void_p), c_void_p]),
     "vg_policy_forward": (c_int32, [c_void_p, c_void_p, c_int64, POINTER(VgPolicyOutputs),
                                     ctypes.c_uint64, ctypes.c_uint64, c_void_p]),
+    "vg_rollout": (c_int32, [c_void_p, c_void_p, c_void_p, POINTER(VgRolloutBuffers), c_int32,
+                             ctypes.c_uint64, ctypes.c_uint64, c_float, c_float, c_void_p]),
     "vg_gae": (c_int32, [c_void_p, c_void_p, c_int64, c_int32, c_float, c_float, c_void_p,
                          c_void_p, c_void_p]),
     "vg_opinion_step": (c_int32, [c_void_p, c_void_p, c_void_p, c_int32, c_void_p, c_void_p,

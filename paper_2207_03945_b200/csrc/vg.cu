@@ -858,6 +858,36 @@ vg_status vg_opinion_step(const int32_t* row_ptr, const int32_t* col, const floa
   return launch_check("k_opinion");
 }
 
+vg_status vg_rollout(vg_world* w, vg_policy* pol, float* state, const vg_rollout_buffers* b,
+                     int32_t t, uint64_t seed, uint64_t step0, float gamma, float lambda,
+                     void* stream) {
+  if (!w || !pol || !state || !b) return fail(VG_EINVAL, "vg_rollout: NULL argument");
+  if (vg_status st = need_slab(w, false, "vg_rollout")) return st;
+  if (!b->obs || !b->action || !b->reward || !b->value) return fail(VG_EINVAL, "vg_rollout: obs/action/reward/value buffers required");
+  if (t < 1) return fail(VG_EINVAL, "vg_rollout: t must be >= 1");
+  if (pol->cfg.obs_dim != w->P.obs_dim) return fail(VG_EINVAL, "vg_rollout: policy obs_dim %d != world obs_dim %d", pol->cfg.obs_dim, w->P.obs_dim);
+  if (vg_status st = check_pending(w)) return st;
+  cudaStream_t s = as_stream(stream);
+  const size_t M = (size_t)w->P.total;
+  float4* io = reinterpret_cast<float4*>(state);
+  for (int k = 0; k < t; ++k) {
+    const vg_policy_outputs po{nullptr, b->value + k * M, b->action + k * M * 2,
+                               b->logp ? b->logp + k * M : nullptr};
+    if (vg_status st = vg_policy_forward(pol, b->obs + k * M * w->P.obs_dim, (int64_t)M, &po,
+                                         seed, step0 + (uint64_t)k, stream)) return st;
+    vg_outputs o{};
+    o.obs = b->obs + (k + 1) * M * w->P.obs_dim;
+    o.reward = b->reward + k * M;
+    if (vg_status st = launch_step(w, io, reinterpret_cast<const float2*>(b->action + k * M * 2), &o, s)) return st;
+  }
+  const vg_policy_outputs pv{nullptr, b->value + (size_t)t * M, nullptr, nullptr};
+  if (vg_status st = vg_policy_forward(pol, b->obs + (size_t)t * M * w->P.obs_dim, (int64_t)M, &pv,
+                                       seed, step0 + (uint64_t)t, stream)) return st;
+  if (b->adv && b->ret)
+    return vg_gae(b->reward, b->value, (int64_t)M, t, gamma, lambda, b->adv, b->ret, stream);
+  return VG_OK;
+}
+
 vg_status vg_profile_begin(vg_world* w, int32_t max_steps) {
   if (!w || max_steps < 0 || max_steps > (1 << 20)) return fail(VG_EINVAL, "world/max_steps");
   const size_t need = (size_t)max_steps * (VG_N_PHASES + 1);

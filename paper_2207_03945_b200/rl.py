@@ -21,15 +21,16 @@ def _f32(t: torch.Tensor, name: str, shape=None):
 
 
 class TrajectoryBuffer:
-    """Time-major rollout storage for n agents x t steps: obs [t][n][obs_dim],
-    action [t][n][2], logp, reward [t][n], value [t+1][n] (bootstrap row), adv, ret.
-    vg_step / vg_policy_forward write straight into step k's slices (no copies)."""
+    """Time-major rollout storage for n agents x t steps: obs [t+1][n][obs_dim]
+    (obs[t] seeds the next rollout), action [t][n][2], logp, reward [t][n], value [t+1][n]
+    (bootstrap row), adv, ret.  vg_step / vg_policy_forward write straight into step k's
+    slices (no copies)."""
 
     def __init__(self, n: int, t: int, obs_dim: int, device=None):
         d = torch.device("cuda", torch.cuda.current_device()) if device is None else device
         z = lambda *s: torch.zeros(s, dtype=torch.float32, device=d)  # noqa: E731
         self.n, self.t = n, t
-        self.obs = z(t, n, obs_dim)
+        self.obs = z(t + 1, n, obs_dim)
         self.action = z(t, n, 2)
         self.logp = z(t, n)
         self.reward = z(t, n)
@@ -64,3 +65,18 @@ def opinion_step(row_ptr, col, weight, op_in, op_out, threshold: float, strength
     check(_lib.lib.vg_opinion_step(row_ptr.data_ptr(), col.data_ptr(), weight.data_ptr(), n,
                                    op_in.data_ptr(), op_out.data_ptr(), threshold, strength,
                                    _stream(op_in)))
+
+
+def rollout(world, policy, state: torch.Tensor, buf: TrajectoryBuffer, seed: int = 0,
+            step0: int = 0, gamma: float = 0.99, lam: float = 0.95) -> None:
+    """vg_rollout: t steps of the paper's experience-collection loop (Fig. 5) on device.
+    buf.obs[0] must hold the current observation (e.g. from world.bin + world.sense)."""
+    import ctypes
+    b = _lib.VgRolloutBuffers(buf.obs.data_ptr(), buf.action.data_ptr(), buf.logp.data_ptr(),
+                              buf.reward.data_ptr(), buf.value.data_ptr(), buf.adv.data_ptr(),
+                              buf.ret.data_ptr())
+    if buf.n != world.R * world.N or buf.obs.shape[2] != world.obs_dim:
+        raise ValueError("trajectory buffer does not match the world")
+    check(_lib.lib.vg_rollout(world._h, policy._h, state.data_ptr(), ctypes.byref(b), buf.t,
+                              ctypes.c_uint64(seed), ctypes.c_uint64(step0), gamma, lam,
+                              _stream(state)))
