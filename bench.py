@@ -212,8 +212,9 @@ class ReplicaRunner:
         self.w = vg.World(p, device=device)
         self.out = self.w.alloc_outputs()
         self.state = torch.from_numpy(vi.init_state(p, seed=1000 * rank)).to(device)
-        self.launches = 5
-        self.phase_names = {"integrate_bin": "integrate_bin", "scan_cells": "scan_cells",
+        self.launches = self.w.kernels_per_step
+        self.phase_names = {"integrate_bin": ("integrate+bin (fused K1-K3)" if self.launches == 2
+                                              else "integrate_bin"), "scan_cells": "scan_cells",
                             "scatter": "scatter", "cell_sort": "cell_sort", "sense": "sense"}
 
     def step(self, acts):
@@ -476,7 +477,8 @@ def run_ours(args):
         achieved = ALG_OPS_PER_PAIR * pairs_local / sense_s / 1e12
         n = p.total_agents if not slab_mode else p.n_agents // world
         obs_b = 4 * w.obs_dim + 4 * w.occ_words + SENSE_BYTES_FIXED
-        stage_bytes = {"integrate_bin": 48 * n, "scan_cells": 8 * w.n_cells,
+        fused = getattr(w, "kernels_per_step", 5) == 2
+        stage_bytes = {"integrate_bin": (72 if fused else 48) * n, "scan_cells": 8 * w.n_cells,
                        "scatter": 44 * n, "cell_sort": 40 * n, "sense": obs_b * n}
         stages = {}
         tot_ph = sum(phases.values()) or 1.0

@@ -122,6 +122,7 @@ typedef struct {
   int32_t occ_words;    /* ceil(channels * v / 32)                                         */
   int64_t total_agents; /* R * N                                                           */
   int64_t scratch_bytes;/* device bytes owned by the world                                 */
+  int32_t kernels_per_step; /* libvg kernels one vg_step (slab: begin + finish) launches   */
 } vg_world_info;
 
 typedef struct vg_world vg_world;

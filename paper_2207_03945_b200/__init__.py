@@ -99,6 +99,7 @@ class World:
         self.channels = info.channels
         self.occ_words = info.occ_words
         self.scratch_bytes = info.scratch_bytes
+        self.kernels_per_step = info.kernels_per_step
         self.R, self.N = int(params.n_replicas), int(params.n_agents)
         self.is_tag = params.env == "tag"
         if self.slab:

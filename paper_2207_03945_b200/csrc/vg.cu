@@ -46,6 +46,7 @@ struct vg_world {
   int device = -1;
   int n_cells = 0;
   bool binned = false;
+  bool fused_bin = false;          // K1-K3 fused per replica (small worlds)
   size_t scratch_bytes = 0;
   uint32_t* count = nullptr;       // [n_cells]     per-cell histogram (zero between uses)
   uint32_t* cell_start = nullptr;  // [n_cells + 1]
@@ -233,6 +234,17 @@ vg_status launch_k1(vg_world* w, float4* io, const float4* in, const float2* act
   return launch_check("k_integrate_bin");
 }
 
+template <int ENV, bool INTEGRATE>
+vg_status launch_fused_bin(vg_world* w, float4* io, const float4* in, const float2* act,
+                           cudaStream_t s) {
+  vg::k_replica_bin<ENV, INTEGRATE><<<w->P.R, vg::kRBThreads, 0, s>>>(
+      w->P, io, in, act, w->cell_id, w->cell_start, w->sorted, w->perm, w->sorted_xy,
+      w->err_dev, w->err_flag);
+  if (vg_status st = launch_check("k_replica_bin")) return st;
+  w->binned = true;
+  return VG_OK;
+}
+
 template <int ENV>
 vg_status bin_rest(vg_world* w, const float4* state, cudaStream_t s, bool prof = false) {
   const long long n = w->P.total;
@@ -363,6 +375,10 @@ vg_status vg_world_create(const vg_config* cfg, vg_world** out) {
   if (!w) return fail(VG_ENOMEM, "host allocation failed");
   w->cfg = *cfg;
   w->P = derive(*cfg, g);
+  // one CTA per replica: worth it when replicas fill the GPU or the world is tiny
+  w->fused_bin = cfg->shard == VG_SHARD_REPLICA && g * g <= vg::kRBMaxCells &&
+                 cfg->n_agents <= vg::kRBMaxAgents &&
+                 (cfg->n_replicas >= 64 || cfg->n_agents <= 1024);
   {
     const char* ng = std::getenv("VG_NO_GRAPH");
     w->graphs_enabled = !(ng && ng[0] && ng[0] != '0');
@@ -480,6 +496,7 @@ vg_status vg_world_query(const vg_world* w, vg_world_info* info) {
   info->occ_words = w->P.occ_words;
   info->total_agents = w->P.total;
   info->scratch_bytes = (int64_t)w->scratch_bytes;
+  info->kernels_per_step = w->slab ? 7 : (w->fused_bin ? 2 : 5);
   return VG_OK;
 }
 
@@ -489,6 +506,9 @@ vg_status vg_bin(vg_world* w, const float* state, void* stream) {
   if (vg_status st = check_pending(w)) return st;
   cudaStream_t s = as_stream(stream);
   const float4* in = reinterpret_cast<const float4*>(state);
+  if (w->fused_bin)
+    return (w->P.env == vg::kFlock) ? launch_fused_bin<vg::kFlock, false>(w, nullptr, in, nullptr, s)
+                                    : launch_fused_bin<vg::kTag, false>(w, nullptr, in, nullptr, s);
   if (w->P.env == vg::kFlock) {
     if (vg_status st = launch_k1<vg::kFlock, false, true>(w, nullptr, in, nullptr, s)) return st;
     return bin_rest<vg::kFlock>(w, in, s);
@@ -531,6 +551,15 @@ namespace {
 vg_status launch_step(vg_world* w, float4* io, const float2* a, const vg_outputs* outs,
                       cudaStream_t s) {
   prof_mark(w, 0, s);
+  if (w->fused_bin) {
+    vg_status st = (w->P.env == vg::kFlock) ? launch_fused_bin<vg::kFlock, true>(w, io, nullptr, a, s)
+                                            : launch_fused_bin<vg::kTag, true>(w, io, nullptr, a, s);
+    if (st) return st;
+    for (int k = 1; k <= 4; ++k) prof_mark(w, k, s);
+    st = launch_sense<true>(w, outs, s);
+    prof_mark(w, 5, s);
+    return st;
+  }
   if (w->P.env == vg::kFlock) {
     if (vg_status st = launch_k1<vg::kFlock, true, true>(w, io, nullptr, a, s)) return st;
     prof_mark(w, 1, s);

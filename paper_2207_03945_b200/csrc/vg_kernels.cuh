@@ -239,6 +239,147 @@ __global__ void __launch_bounds__(256) k_cell_sort(
   }
 }
 
+// ------------------------------------------------------------------------------ K1-K3 fused
+// Small replica worlds (G^2 <= 256 cells, N <= 32768, many replicas): one CTA of 1024
+// threads per replica integrates (optional), bins and stably scatters its agents — the same
+// results as K1 + K2 + K3 + K3b bit for bit (stable order = ascending agent id).
+// Warp w owns the contiguous agent range [w S, (w+1) S) and a private per-cell count row:
+//   pass 1  integrate, cell id (A16), warp-private histogram (match_any aggregated);
+//   scan    per cell an exclusive scan over the 32 warps (warp shuffles), then over cells;
+//   pass 2  each warp walks its range in order: position = cell start + earlier warps +
+//           earlier agents of this warp in the cell + lower lanes with the same cell.
+// Three block barriers in total.
+constexpr int kRBMaxCells = 256;
+constexpr int kRBMaxAgents = 32768;
+
+constexpr int kRBThreads = 1024;     // 32 warps per replica CTA, 2 CTAs per SM
+
+template <int ENV, bool INTEGRATE>
+__global__ void __launch_bounds__(kRBThreads, 2) k_replica_bin(
+    Params P, float4* __restrict__ state_io, const float4* __restrict__ state_in,
+    const float2* __restrict__ actions, uint32_t* __restrict__ cell_id,
+    uint32_t* __restrict__ cell_start, float4* __restrict__ sorted,
+    uint32_t* __restrict__ perm, float2* __restrict__ sorted_xy,
+    unsigned long long* __restrict__ err, volatile uint32_t* flag) {
+  constexpr int NW = kRBThreads / 32;
+  __shared__ uint32_t s_wc[NW][kRBMaxCells + 1];     // per-warp counts, then offsets (+1: banks)
+  __shared__ uint32_t s_tot[kRBMaxCells];
+  const int r = blockIdx.x, tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int N = P.N, C = P.G2;
+  const size_t base = (size_t)r * N;
+  const float4* src = INTEGRATE ? state_io : state_in;
+  const int span = (N + NW - 1) / NW;
+  const int i0 = min(N, warp * span), i1 = min(N, i0 + span);
+  unsigned lt;
+  asm("mov.u32 %0, %%lanemask_lt;" : "=r"(lt));
+  for (int c = lane; c < C; c += 32) s_wc[warp][c] = 0u;
+  __syncwarp();
+  // ---- pass 1: integrate + cell id + warp-private histogram
+  for (int b = i0; b < i1; b += 32) {
+    const int i = b + lane;
+    const bool valid = i < i1;
+    uint32_t c = 0xFFFFFFFFu;
+    if (valid) {
+      const size_t gi = base + i;
+      float4 s = src[gi];
+      bool bad = !(s.x >= 0.f && s.x < P.L && s.y >= 0.f && s.y < P.L && s.z >= 0.f &&
+                   s.z < P.two_pi);
+      if (ENV == kFlock) bad |= !isfinite(s.w);
+      if (INTEGRATE) {
+        const float2 a = actions[gi];
+        bad |= isnan(a.x) || isnan(a.y);
+        float turn, dist;
+        if (ENV == kFlock) {
+          const float acc = fminf(fmaxf(a.x, -P.a_max), P.a_max);
+          turn = fminf(fmaxf(a.y, -P.theta_max), P.theta_max);
+          const float sp = fminf(fmaxf(__fadd_rn(s.w, acc), P.s_min), P.s_max);
+          s.w = sp;
+          dist = sp;
+        } else {
+          turn = fminf(fmaxf(a.x, -P.theta_max), P.theta_max);
+          const float smax = (i >= P.first_chaser) ? P.s_max_chaser : P.s_max;
+          dist = fminf(fmaxf(a.y, 0.f), smax);
+        }
+        s.z = wrap_heading(__fadd_rn(s.z, turn), P.two_pi);
+        float sn, cs;
+        sincosf(s.z, &sn, &cs);
+        s.x = wrap_pos(s.x, __fmul_rn(dist, cs), P.L);
+        s.y = wrap_pos(s.y, __fmul_rn(dist, sn), P.L);
+        state_io[gi] = s;
+      }
+      if (bad) report_bad(err, flag, (unsigned long long)gi);
+      int cx = __float2int_rz(__fmul_rn(s.x, P.gs));
+      int cy = __float2int_rz(__fmul_rn(s.y, P.gs));
+      cx = min(max(cx, 0), P.G - 1);
+      cy = min(max(cy, 0), P.G - 1);
+      c = (uint32_t)(cy * P.G + cx);
+      cell_id[gi] = c;                                // re-read in pass 2 (same warp)
+    }
+    const unsigned grp = __match_any_sync(kFull, c);
+    if (valid && (grp & lt) == 0u) s_wc[warp][c] += __popc(grp);
+    __syncwarp();
+  }
+  __syncthreads();
+  // ---- per cell: exclusive scan over the NW warps; totals per cell
+  for (int cc = tid; cc < C; cc += kRBThreads) {
+    uint32_t run = 0;
+#pragma unroll
+    for (int w = 0; w < NW; ++w) {
+      const uint32_t t = s_wc[w][cc];
+      s_wc[w][cc] = run;
+      run += t;
+    }
+    s_tot[cc] = run;
+  }
+  __syncthreads();
+  // ---- exclusive scan over the (<= 256) cells by warp 0: 8 consecutive cells per lane
+  if (warp == 0) {
+    uint32_t v[8], sum = 0;
+#pragma unroll
+    for (int e = 0; e < 8; ++e) {
+      const int c = lane * 8 + e;
+      v[e] = (c < C) ? s_tot[c] : 0u;
+      sum += v[e];
+    }
+    uint32_t inc = sum;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t y = __shfl_up_sync(kFull, inc, o);
+      if (lane >= o) inc += y;
+    }
+    uint32_t run = inc - sum;
+#pragma unroll
+    for (int e = 0; e < 8; ++e) {
+      const int c = lane * 8 + e;
+      if (c < C) {
+        s_tot[c] = run;
+        cell_start[(size_t)r * C + c] = (uint32_t)base + run;
+      }
+      run += v[e];
+    }
+    if (r == (int)gridDim.x - 1 && lane == 0) cell_start[(size_t)P.R * C] = (uint32_t)P.total;
+  }
+  __syncthreads();
+  // ---- pass 2: in-order walk of this warp's range, stable positions, scatter
+  for (int b = i0; b < i1; b += 32) {
+    const int i = b + lane;
+    const bool valid = i < i1;
+    const uint32_t c = valid ? cell_id[base + i] : 0xFFFFFFFFu;
+    const unsigned grp = __match_any_sync(kFull, c);
+    if (valid) {
+      const uint32_t pos = (uint32_t)base + s_tot[c] + s_wc[warp][c] + __popc(grp & lt);
+      float4 s = src[base + i];
+      if (ENV == kTag) s.w = (i >= P.first_chaser) ? 1.f : 0.f;
+      sorted[pos] = s;
+      perm[pos] = (uint32_t)i;
+      sorted_xy[pos] = make_float2(s.x, s.y);
+    }
+    __syncwarp();
+    if (valid && (grp & lt) == 0u) s_wc[warp][c] += __popc(grp);
+    __syncwarp();
+  }
+}
+
 // ---------------------------------------------------------------------------------- K4
 // One CTA per (replica, cell); warp w handles the cell's query agents w, w+W, ...  Each
 // query scans the 3x3 cell stencil — up to 6 contiguous runs of the sorted arrays, each
