@@ -49,6 +49,7 @@ struct vg_world {
   bool fused_bin = false;          // K1-K3 fused per replica (small worlds)
   size_t scratch_bytes = 0;
   uint32_t* count = nullptr;       // [n_cells]     per-cell histogram (zero between uses)
+  uint32_t* tile_sum = nullptr;    // [n_cells / 4096 + 1] multi-CTA scan partials
   uint32_t* cell_start = nullptr;  // [n_cells + 1]
   uint32_t* cell_id = nullptr;     // [R*N]
   uint32_t* slot = nullptr;        // [R*N]         arrival slot within the cell
@@ -234,6 +235,20 @@ vg_status launch_k1(vg_world* w, float4* io, const float4* in, const float2* act
   return launch_check("k_integrate_bin");
 }
 
+// Exclusive scan of the cell counts into cell_start (re-zeroing the counts).
+vg_status scan_cells(vg_world* w, cudaStream_t s) {
+  const int n = w->n_cells;
+  if (n <= 2 * vg::kScanTile) {
+    vg::k_scan_cells<<<1, 1024, 0, s>>>(w->count, w->cell_start, n);
+    return launch_check("k_scan_cells");
+  }
+  const unsigned tiles = (unsigned)((n + vg::kScanTile - 1) / vg::kScanTile);
+  vg::k_scan_tiles<<<tiles, 1024, 0, s>>>(w->count, n, w->tile_sum);
+  if (vg_status st = launch_check("k_scan_tiles")) return st;
+  vg::k_scan_apply<<<tiles, 1024, 0, s>>>(w->count, w->cell_start, n, w->tile_sum);
+  return launch_check("k_scan_apply");
+}
+
 template <int ENV, bool INTEGRATE>
 vg_status launch_fused_bin(vg_world* w, float4* io, const float4* in, const float2* act,
                            cudaStream_t s) {
@@ -248,8 +263,7 @@ vg_status launch_fused_bin(vg_world* w, float4* io, const float4* in, const floa
 template <int ENV>
 vg_status bin_rest(vg_world* w, const float4* state, cudaStream_t s, bool prof = false) {
   const long long n = w->P.total;
-  vg::k_scan_cells<<<1, 1024, 0, s>>>(w->count, w->cell_start, w->n_cells);
-  if (vg_status st = launch_check("k_scan_cells")) return st;
+  if (vg_status st = scan_cells(w, s)) return st;
   if (prof) prof_mark(w, 2, s);
   vg::k_scatter<ENV><<<(unsigned)((n + 255) / 256), 256, 0, s>>>(
       w->P, state, w->cell_id, w->slot, w->cell_start, w->tmp_rec, w->tmp_id);
@@ -324,8 +338,7 @@ vg_status slab_bin(vg_world* w, cudaStream_t s) {
   const unsigned nb = stride_blocks(w->SB.cap_loc);
   vg::k_slab_keys<<<nb, 256, 0, s>>>(w->P, w->SL, w->SB, w->cell_id, w->slot, w->count);
   if (vg_status st = launch_check("k_slab_keys")) return st;
-  vg::k_scan_cells<<<1, 1024, 0, s>>>(w->count, w->cell_start, w->n_cells);
-  if (vg_status st = launch_check("k_scan_cells")) return st;
+  if (vg_status st = scan_cells(w, s)) return st;
   vg::k_slab_scatter<ENV><<<nb, 256, 0, s>>>(w->P, w->SB, w->cell_id, w->slot, w->cell_start,
                                               w->tmp_rec, w->tmp_id);
   if (vg_status st = launch_check("k_slab_scatter")) return st;
@@ -419,6 +432,7 @@ vg_status vg_world_create(const vg_config* cfg, vg_world** out) {
     }
   }
   if (!st) st = dalloc(w, &w->count, w->n_cells);
+  if (!st) st = dalloc(w, &w->tile_sum, w->n_cells / vg::kScanTile + 1);
   if (!st) st = dalloc(w, &w->cell_start, w->n_cells + 1);
   if (!st) st = dalloc(w, &w->cell_id, n);
   if (!st) st = dalloc(w, &w->slot, n);
@@ -466,6 +480,7 @@ void vg_world_destroy(vg_world* w) {
   if (w->cap_stream) cudaStreamDestroy(w->cap_stream);
   for (cudaEvent_t e : w->prof_ev) cudaEventDestroy(e);
   cudaFree(w->count);
+  cudaFree(w->tile_sum);
   cudaFree(w->cell_start);
   cudaFree(w->cell_id);
   cudaFree(w->slot);

@@ -190,6 +190,83 @@ __global__ void __launch_bounds__(1024) k_scan_cells(uint32_t* __restrict__ coun
   if (t == 0) start[n] = total_s;
 }
 
+// K2' (multi-CTA): tiles of 4096 counts.  k_scan_tiles sums each tile; k_scan_apply lets
+// every CTA add up the sums of the tiles before it (<= a few hundred) and scans its own
+// tile, writing start[] and re-zeroing the counts.  Same result as k_scan_cells.
+constexpr int kScanTile = 4096;
+
+__global__ void __launch_bounds__(1024) k_scan_tiles(const uint32_t* __restrict__ count, int n,
+                                                      uint32_t* __restrict__ tile_sum) {
+  __shared__ uint32_t ws[32];
+  const int t = threadIdx.x, base = blockIdx.x * kScanTile;
+  uint32_t s = 0;
+#pragma unroll
+  for (int e = 0; e < 4; ++e) {
+    const int k = base + e * 1024 + t;
+    s += (k < n) ? count[k] : 0u;
+  }
+  s = __reduce_add_sync(kFull, s);
+  if ((t & 31) == 0) ws[t >> 5] = s;
+  __syncthreads();
+  if (t < 32) {
+    const uint32_t v = __reduce_add_sync(kFull, ws[t]);
+    if (t == 0) tile_sum[blockIdx.x] = v;
+  }
+}
+
+__global__ void __launch_bounds__(1024) k_scan_apply(uint32_t* __restrict__ count,
+                                                      uint32_t* __restrict__ start, int n,
+                                                      const uint32_t* __restrict__ tile_sum) {
+  __shared__ uint32_t ws[32];
+  __shared__ uint32_t s_off;
+  const int t = threadIdx.x, lane = t & 31, w = t >> 5;
+  const int base = blockIdx.x * kScanTile;
+  if (w == 0) {                                           // offset = sum of earlier tiles
+    uint32_t o = 0;
+    for (int k = lane; k < (int)blockIdx.x; k += 32) o += tile_sum[k];
+    o = __reduce_add_sync(kFull, o);
+    if (lane == 0) s_off = o;
+  }
+  // 4 consecutive counts per thread (thread t owns base + 4t .. 4t+3)
+  uint32_t v[4], sum = 0;
+#pragma unroll
+  for (int e = 0; e < 4; ++e) {
+    const int k = base + 4 * t + e;
+    v[e] = (k < n) ? count[k] : 0u;
+    sum += v[e];
+  }
+  uint32_t inc = sum;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint32_t y = __shfl_up_sync(kFull, inc, o);
+    if (lane >= o) inc += y;
+  }
+  if (lane == 31) ws[w] = inc;
+  __syncthreads();
+  if (w == 0) {
+    const uint32_t x = ws[lane];
+    uint32_t xi = x;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t y = __shfl_up_sync(kFull, xi, o);
+      if (lane >= o) xi += y;
+    }
+    ws[lane] = xi - x;
+  }
+  __syncthreads();
+  uint32_t run = s_off + ws[w] + inc - sum;
+#pragma unroll
+  for (int e = 0; e < 4; ++e) {
+    const int k = base + 4 * t + e;
+    if (k < n) {
+      start[k] = run;
+      count[k] = 0u;
+    }
+    run += v[e];
+  }
+  if (blockIdx.x == gridDim.x - 1 && t == 1023) start[n] = run;
+}
+
 // ---------------------------------------------------------------------------------- K3
 // Place each agent's record at cell_start[cell] + slot (arrival order within a cell).
 template <int ENV>
