@@ -89,6 +89,7 @@ struct vg_world {
   unsigned long long graph_clock = 0;
   cudaStream_t cap_stream = nullptr;
   bool graphs_enabled = true;
+  int n_sm = 148;
 };
 
 namespace {
@@ -209,6 +210,18 @@ vg::Params derive(const vg_config& c, int g) {
 
 inline cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s); }
 
+// Runs an entry point on the device the object was created on, restoring the caller's.
+struct DeviceGuard {
+  int prev = -1;
+  explicit DeviceGuard(int dev) {
+    if (dev >= 0 && cudaGetDevice(&prev) == cudaSuccess && prev != dev) cudaSetDevice(dev);
+    else prev = -1;
+  }
+  ~DeviceGuard() {
+    if (prev >= 0) cudaSetDevice(prev);
+  }
+};
+
 // Record phase boundary `k` of the current profiled step (no-op when not profiling).
 inline void prof_mark(vg_world* w, int k, cudaStream_t s) {
   if (w->prof_n < w->prof_max) cudaEventRecord(w->prof_ev[(size_t)w->prof_n * (VG_N_PHASES + 1) + k], s);
@@ -295,7 +308,7 @@ vg::Outs to_outs(const vg_outputs* o) {
 // Query chunks per cell: enough CTAs to give ~32 resident warps per SM when the world has
 // few cells (C1-C3), 1 for large worlds.  Any value >= 1 is correct (grid-stride loop).
 int sense_chunks(const vg_world* w) {
-  const long long target_warps = 148LL * 32;
+  const long long target_warps = (long long)w->n_sm * 32;
   const long long warps = (long long)w->n_cells * vg::kSenseWarps;
   const long long per_cell = (w->P.total + w->n_cells - 1) / w->n_cells;
   long long ch = (target_warps + warps - 1) / warps;
@@ -329,7 +342,7 @@ vg_status launch_sense(vg_world* w, const vg_outputs* outs, cudaStream_t s) {
 }
 
 unsigned stride_blocks(size_t n) {
-  return (unsigned)std::max<size_t>(1, std::min<size_t>((n + 255) / 256, 148 * 8));
+  return (unsigned)std::max<size_t>(1, std::min<size_t>((n + 255) / 256, 148 * 8));   // grid-stride
 }
 
 // Bin the slab's local set (owned + ghosts) on the column-major local grid.
@@ -398,6 +411,7 @@ vg_status vg_world_create(const vg_config* cfg, vg_world** out) {
   }
   w->n_cells = g * g * cfg->n_replicas;
   cudaGetDevice(&w->device);
+  cudaDeviceGetAttribute(&w->n_sm, cudaDevAttrMultiProcessorCount, w->device);
   size_t n = (size_t)w->P.total;
   vg_status st = VG_OK;
   if (cfg->shard == VG_SHARD_SLAB) {
@@ -518,6 +532,7 @@ vg_status vg_world_query(const vg_world* w, vg_world_info* info) {
 vg_status vg_bin(vg_world* w, const float* state, void* stream) {
   if (!w || !state) return fail(VG_EINVAL, "world/state: NULL");
   if (vg_status st = need_slab(w, false, "vg_bin")) return st;
+  DeviceGuard dg_(w->device);
   if (vg_status st = check_pending(w)) return st;
   cudaStream_t s = as_stream(stream);
   const float4* in = reinterpret_cast<const float4*>(state);
@@ -535,6 +550,7 @@ vg_status vg_bin(vg_world* w, const float* state, void* stream) {
 vg_status vg_sense(vg_world* w, const vg_outputs* outs, void* stream) {
   if (!w || !outs) return fail(VG_EINVAL, "world/outs: NULL");
   if (!w->binned) return fail(VG_EINVAL, "vg_sense: no binned state (call vg_bin or vg_step first)");
+  DeviceGuard dg_(w->device);
   if (vg_status st = check_pending(w)) return st;
   return launch_sense<true>(w, outs, as_stream(stream));
 }
@@ -542,6 +558,7 @@ vg_status vg_sense(vg_world* w, const vg_outputs* outs, void* stream) {
 vg_status vg_reward(vg_world* w, const vg_outputs* outs, void* stream) {
   if (!w || !outs) return fail(VG_EINVAL, "world/outs: NULL");
   if (!w->binned) return fail(VG_EINVAL, "vg_reward: no binned state (call vg_bin or vg_step first)");
+  DeviceGuard dg_(w->device);
   if (vg_status st = check_pending(w)) return st;
   vg_outputs o = *outs;
   o.obs = nullptr;
@@ -552,6 +569,7 @@ vg_status vg_reward(vg_world* w, const vg_outputs* outs, void* stream) {
 vg_status vg_integrate(vg_world* w, float* state, const float* actions, void* stream) {
   if (!w || !state || !actions) return fail(VG_EINVAL, "world/state/actions: NULL");
   if (vg_status st = need_slab(w, false, "vg_integrate")) return st;
+  DeviceGuard dg_(w->device);
   if (vg_status st = check_pending(w)) return st;
   cudaStream_t s = as_stream(stream);
   float4* io = reinterpret_cast<float4*>(state);
@@ -638,6 +656,7 @@ vg_status vg_step(vg_world* w, float* state, const float* actions, const vg_outp
                   void* stream) {
   if (!w || !state || !actions || !outs) return fail(VG_EINVAL, "world/state/actions/outs: NULL");
   if (vg_status st = need_slab(w, false, "vg_step")) return st;
+  DeviceGuard dg_(w->device);
   if (vg_status st = check_pending(w)) return st;
   cudaStream_t s = as_stream(stream);
   float4* io = reinterpret_cast<float4*>(state);
@@ -657,6 +676,7 @@ vg_status vg_step(vg_world* w, float* state, const float* actions, const vg_outp
 vg_status vg_step_host(vg_world* w, float* state, const float* actions_host,
                        const vg_outputs* outs, float* reward_host, void* stream) {
   if (!w || !state || !actions_host || !outs) return fail(VG_EINVAL, "world/state/actions_host/outs: NULL");
+  DeviceGuard dg_(w->device);
   if (reward_host && !outs->reward) return fail(VG_EINVAL, "reward_host: needs outs->reward");
   cudaStream_t s = as_stream(stream);
   VG_CUDA(cudaMemcpyAsync(w->act_dev, actions_host, sizeof(float2) * (size_t)w->P.total,
@@ -693,6 +713,7 @@ vg_status vg_slab_plan(int32_t grid, int32_t world_size, int32_t rank, int32_t* 
 
 vg_status vg_slab_load(vg_world* w, const float* state_global, void* stream) {
   if (vg_status st = need_slab(w, true, "vg_slab_load")) return st;
+  DeviceGuard dg_(w->device);
   if (!state_global) return fail(VG_EINVAL, "state_global: NULL");
   if (vg_status st = check_pending(w)) return st;
   cudaStream_t s = as_stream(stream);
@@ -713,6 +734,7 @@ vg_status vg_slab_begin(vg_world* w, const float* actions, void* stream) {
   if (vg_status st = need_slab(w, true, "vg_slab_begin")) return st;
   if (!actions) return fail(VG_EINVAL, "actions: NULL");
   if (!w->binned) return fail(VG_EINVAL, "vg_slab_begin: call vg_slab_load first");
+  DeviceGuard dg_(w->device);
   if (vg_status st = check_pending(w)) return st;
   cudaStream_t s = as_stream(stream);
   prof_mark(w, 0, s);
@@ -768,6 +790,7 @@ vg_status vg_slab_exchange_loopback(vg_world* const* ws, int32_t n, void* stream
 
 vg_status vg_slab_finish(vg_world* w, const vg_outputs* outs, void* stream) {
   if (vg_status st = need_slab(w, true, "vg_slab_finish")) return st;
+  DeviceGuard dg_(w->device);
   if (!outs) return fail(VG_EINVAL, "outs: NULL");
   cudaStream_t s = as_stream(stream);
   vg::k_slab_unpack<<<stride_blocks(2ull * w->SB.cap_msg), 256, 0, s>>>(w->SB);
@@ -787,11 +810,13 @@ vg_status vg_slab_sense(vg_world* w, const vg_outputs* outs, void* stream) {
   if (vg_status st = need_slab(w, true, "vg_slab_sense")) return st;
   if (!outs) return fail(VG_EINVAL, "outs: NULL");
   if (!w->binned) return fail(VG_EINVAL, "vg_slab_sense: call vg_slab_load first");
+  DeviceGuard dg_(w->device);
   return launch_sense<true>(w, outs, as_stream(stream));
 }
 
 vg_status vg_slab_own_count(vg_world* w, void* stream, int64_t* n_own) {
   if (vg_status st = need_slab(w, true, "vg_slab_own_count")) return st;
+  DeviceGuard dg_(w->device);
   if (!n_own) return fail(VG_EINVAL, "n_own: NULL");
   VG_CUDA(cudaStreamSynchronize(as_stream(stream)));
   uint32_t a = 0, b = 0;
@@ -809,6 +834,7 @@ struct vg_policy {
   vg::PolicyPacked pk{};
   bool have_weights = false;
   int n_sm = 148;
+  int device = -1;
 };
 
 extern "C" {
@@ -825,6 +851,7 @@ vg_status vg_policy_create(const vg_policy_config* cfg, vg_policy** out) {
   p->cfg = *cfg;
   int dev = 0;
   cudaGetDevice(&dev);
+  p->device = dev;
   cudaDeviceGetAttribute(&p->n_sm, cudaDevAttrMultiProcessorCount, dev);
   cudaError_t e = cudaMalloc(reinterpret_cast<void**>(&p->pk.B1), vg::kPolN * vg::kPolK1 * 2);
   if (e == cudaSuccess) e = cudaMalloc(reinterpret_cast<void**>(&p->pk.B2), vg::kPolN * vg::kPolK2 * 2);
@@ -851,6 +878,7 @@ vg_status vg_policy_set_weights(vg_policy* p, const float* const* w, void* strea
   if (!p || !w) return fail(VG_EINVAL, "policy/weights: NULL");
   for (int i = 0; i < 13; ++i)
     if (!w[i]) return fail(VG_EINVAL, "weights[%d]: NULL", i);
+  DeviceGuard dg_(p->device);
   const int n = vg::kPolN * vg::kPolK1;
   vg::k_policy_pack<<<(n + 255) / 256, 256, 0, as_stream(stream)>>>(
       p->cfg.obs_dim, w[0], w[1], w[2], w[3], w[4], w[5], w[6], w[7], w[8], w[9], w[10], w[11],
@@ -867,6 +895,7 @@ vg_status vg_policy_forward(vg_policy* p, const float* obs, int64_t rows,
   if (!p->have_weights) return fail(VG_EINVAL, "vg_policy_forward: call vg_policy_set_weights first");
   if (rows < 0) return fail(VG_EINVAL, "rows: must be >= 0");
   if (rows == 0) return VG_OK;
+  DeviceGuard dg_(p->device);
   vg::PolicyOut o{outs->mean, outs->value, outs->action, outs->logp};
   const int64_t tiles = (rows + vg::kPolTile - 1) / vg::kPolTile;
   const unsigned grid = (unsigned)std::min<int64_t>(tiles, p->n_sm);
@@ -907,6 +936,7 @@ vg_status vg_rollout(vg_world* w, vg_policy* pol, float* state, const vg_rollout
                      void* stream) {
   if (!w || !pol || !state || !b) return fail(VG_EINVAL, "vg_rollout: NULL argument");
   if (vg_status st = need_slab(w, false, "vg_rollout")) return st;
+  DeviceGuard dg_(w->device);
   if (!b->obs || !b->action || !b->reward || !b->value) return fail(VG_EINVAL, "vg_rollout: obs/action/reward/value buffers required");
   if (t < 1) return fail(VG_EINVAL, "vg_rollout: t must be >= 1");
   if (pol->cfg.obs_dim != w->P.obs_dim) return fail(VG_EINVAL, "vg_rollout: policy obs_dim %d != world obs_dim %d", pol->cfg.obs_dim, w->P.obs_dim);
@@ -947,6 +977,7 @@ vg_status vg_profile_begin(vg_world* w, int32_t max_steps) {
 
 vg_status vg_profile_end(vg_world* w, void* stream, double* phase_ms, int32_t* n_steps) {
   if (!w || !phase_ms) return fail(VG_EINVAL, "world/phase_ms: NULL");
+  DeviceGuard dg_(w->device);
   VG_CUDA(cudaStreamSynchronize(as_stream(stream)));
   for (int k = 0; k < VG_N_PHASES; ++k) phase_ms[k] = 0.0;
   for (int i = 0; i < w->prof_n; ++i) {
@@ -965,6 +996,7 @@ vg_status vg_profile_end(vg_world* w, void* stream, double* phase_ms, int32_t* n
 
 vg_status vg_sync_errors(vg_world* w, void* stream, int64_t* bad_agent) {
   if (!w) return fail(VG_EINVAL, "world: NULL");
+  DeviceGuard dg_(w->device);
   VG_CUDA(cudaStreamSynchronize(as_stream(stream)));
   unsigned long long v = 0;
   VG_CUDA(cudaMemcpy(&v, w->err_dev, sizeof(v), cudaMemcpyDeviceToHost));
