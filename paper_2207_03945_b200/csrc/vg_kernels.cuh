@@ -636,16 +636,22 @@ __global__ void __launch_bounds__(kSenseWarps * 32, 6) k_sense(
           return;
         }
         const float phi = vg_atan2(left, fwd);
-        const float alpha = asinf(fminf(P.d_r * rsq, 1.f));
+        // Angular half-width of the disc, asin(d_r / d), bounded from above (the per-ray test
+        // below is exact, so the range only has to be conservative): for s = d_r/d <= 1/2,
+        // asin(s) <= s (1 + s^2 (1/6 + s^2/10)); nearer discs take asinf.
+        const float sr = fminf(P.d_r * rsq, 1.f);
+        const float alpha = (sr <= 0.5f)
+            ? fmaf(sr * sr * sr, fmaf(sr * sr, 0.1f, 0.16666667f), sr) + 1e-6f
+            : asinf(sr);
         // Sectors whose centre ray may touch the disc: psi_k in [phi - alpha, phi + alpha]
-        // (also shifted by -+2 pi across the blind-spot seam), widened by one sector on each
-        // side; every ray in the range is then tested exactly.
+        // (also shifted by -+2 pi across the blind-spot seam), with a 1e-4-sector margin for
+        // the fp32 error of phi and alpha; every ray in the range is then tested exactly.
 #pragma unroll 1
         for (int wrap = -1; wrap <= 1; ++wrap) {
           const float lo = phi - alpha + wrap * P.two_pi, hi = phi + alpha + wrap * P.two_pi;
           if (hi < -P.half_fov - 0.1f || lo > P.half_fov + 0.1f) continue;
-          const int k0 = max(0, (int)floorf((lo + P.half_fov) * P.inv_w - 0.5f));
-          const int k1 = min(P.v - 1, (int)ceilf((hi + P.half_fov) * P.inv_w - 0.5f));
+          const int k0 = max(0, (int)ceilf((lo + P.half_fov) * P.inv_w - 0.5f - 1e-4f));
+          const int k1 = min(P.v - 1, (int)floorf((hi + P.half_fov) * P.inv_w - 0.5f + 1e-4f));
           for (int k = k0; k <= k1; ++k) {
             const float2 ud = s_ray[k];
             const float bb = fmaf(ud.x, fwd, ud.y * left);       // along the ray
