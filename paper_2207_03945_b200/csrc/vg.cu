@@ -855,6 +855,7 @@ vg_status vg_policy_create(const vg_policy_config* cfg, vg_policy** out) {
   cudaDeviceGetAttribute(&p->n_sm, cudaDevAttrMultiProcessorCount, dev);
   cudaError_t e = cudaMalloc(reinterpret_cast<void**>(&p->pk.B1), vg::kPolN * vg::kPolK1 * 2);
   if (e == cudaSuccess) e = cudaMalloc(reinterpret_cast<void**>(&p->pk.B2), vg::kPolN * vg::kPolK2 * 2);
+  if (e == cudaSuccess) e = cudaMalloc(reinterpret_cast<void**>(&p->pk.B3), vg::kPolN3 * vg::kPolK2 * 2);
   if (e == cudaSuccess) e = cudaMalloc(reinterpret_cast<void**>(&p->pk.consts), vg::kConstFloats * 4);
   if (e == cudaSuccess)
     e = cudaFuncSetAttribute(vg::k_policy, cudaFuncAttributeMaxDynamicSharedMemorySize, vg::kPolSmem);
@@ -870,6 +871,7 @@ void vg_policy_destroy(vg_policy* p) {
   if (!p) return;
   cudaFree(p->pk.B1);
   cudaFree(p->pk.B2);
+  cudaFree(p->pk.B3);
   cudaFree(p->pk.consts);
   delete p;
 }

@@ -5,11 +5,11 @@
 // tanh hidden, linear out, state-independent log_std); S:355-372 Gaussian sample, clip to
 // the action box, log-prob of the unclipped sample.  SURVEY.md §8f NEXT #1.
 //
-// Tile of 128 agents per step of a persistent CTA (one per SM, 8 warps):
+// Tile of 128 agents per step of a persistent CTA (one per SM, 16 warps):
 //   layer 1  D[128 x 128] = A1[128 x 144] . B1^T   (actor | critic hidden, fp16 in, fp32 acc)
 //   layer 2  D[128 x 128] = A2[128 x 128] . B2^T   (B2 block-diagonal: actor | critic)
-//   layer 3  mean (2) and value (1): fp32 FMAs in the epilogue; then Philox4x32-10 +
-//            Box-Muller noise, clip, log-prob.
+//   layer 3  D[128 x 16]  = A3[128 x 128] . B3^T   (rows of B3: W3[0], W3[1], V3, zeros)
+//   then Philox4x32-10 + Box-Muller noise, clip, log-prob.
 // Operands live in shared memory in the canonical K-major no-swizzle layout (8 x 16-byte
 // core matrices: SBO = 128 B between 8-row groups, LBO = R x 16 B between 8-column groups),
 // tcgen05.mma is issued by one thread, the fp32 accumulator lives in TMEM (128 columns) and
@@ -27,15 +27,18 @@ constexpr int kPolHidden = 64;
 constexpr int kPolN = 128;         // actor | critic concatenated (MMA N)
 constexpr int kPolK1 = 144;        // obs_dim padded to a multiple of 16 (<= 144)
 constexpr int kPolK2 = 128;        // hidden actor | critic
-constexpr int kPolThreads = 256;
+constexpr int kPolN3 = 16;         // layer-3 MMA N: mean_0, mean_1, value, 13 zero rows
+constexpr int kPolThreads = 512;   // 16 warps: TMEM lane quadrant (w % 4) x 32-column group (w / 4)
 
-// Shared-memory carve-up (bytes).
+// Shared-memory carve-up (bytes).  A3 (layer-3 operand) aliases A1, free once MMA1 is done.
 constexpr int kOffB1 = 0;
 constexpr int kOffB2 = kOffB1 + kPolN * kPolK1 * 2;        // 36864
-constexpr int kOffA1 = kOffB2 + kPolN * kPolK2 * 2;        // +32768
+constexpr int kOffB3 = kOffB2 + kPolN * kPolK2 * 2;        // +32768
+constexpr int kOffA1 = kOffB3 + kPolN3 * kPolK2 * 2;       // +4096
 constexpr int kOffA2 = kOffA1 + kPolTile * kPolK1 * 2;     // +36864
 constexpr int kOffC = kOffA2 + kPolTile * kPolK2 * 2;      // +32768 : fp32 constants
-constexpr int kConstFloats = 128 + 128 + 3 * 128 + 4 + 2 + 4;   // b1, b2, W3|V3, b3|c3, log_std, box
+// consts: b1[128] b2[128] | b3_0 b3_1 c3 pad | log_std[2] | lo[2] hi[2]
+constexpr int kConstFloats = 128 + 128 + 4 + 2 + 4;
 constexpr int kOffBar = kOffC + ((kConstFloats * 4 + 15) / 16) * 16;   // 2 mbarriers + tmem slot
 constexpr int kOffStage = ((kOffBar + 32 + 127) / 128) * 128;            // raw fp32 obs tile (TMA)
 constexpr int kStageBytes = kPolTile * kPolK1 * 4;                       // >= 128 rows x obs_dim
@@ -45,7 +48,8 @@ constexpr int kPolSmem = kOffStage + kStageBytes;
 struct PolicyPacked {
   __half* B1;        // [kPolN x kPolK1] core-matrix layout
   __half* B2;        // [kPolN x kPolK2] core-matrix layout (block diagonal)
-  float* consts;     // kConstFloats: b1[128] b2[128] W3[3][128] b3[3] pad log_std[2] lo[2] hi[2]
+  __half* B3;        // [kPolN3 x kPolK2] core-matrix layout
+  float* consts;     // kConstFloats (see above)
 };
 
 struct PolicyOut {
@@ -66,8 +70,9 @@ __device__ __forceinline__ uint64_t umma_desc(uint32_t saddr, uint32_t lbo, uint
          ((uint64_t)((sbo >> 4) & 0x3FFF) << 32) | (1ull << 46);
 }
 
-// Instruction descriptor, kind::f16: D fp32, A/B fp16, both K-major, M = 128, N = 128.
+// Instruction descriptors, kind::f16: D fp32, A/B fp16, both K-major, M = 128, N = 128 / 16.
 constexpr uint32_t kPolIdesc = (1u << 4) | ((uint32_t)(kPolN >> 3) << 17) | ((uint32_t)(kPolTile >> 4) << 24);
+constexpr uint32_t kPolIdesc3 = (1u << 4) | ((uint32_t)(kPolN3 >> 3) << 17) | ((uint32_t)(kPolTile >> 4) << 24);
 
 __device__ __forceinline__ uint32_t h2_bits(__half2 h) {
   return *reinterpret_cast<uint32_t*>(&h);
@@ -137,6 +142,16 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, float* v) {
   for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
 }
 
+__device__ __forceinline__ void tmem_ld4(uint32_t taddr, float* v) {
+  uint32_t r0, r1, r2, r3;
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x4.b32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r0), "=r"(r1), "=r"(r2), "=r"(r3)
+               : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+  v[0] = __uint_as_float(r0); v[1] = __uint_as_float(r1);
+  v[2] = __uint_as_float(r2); v[3] = __uint_as_float(r3);
+}
+
 // Philox4x32-10 (Salmon et al. SC'11): the same counter-based generator as oracle/policy.py.
 __device__ __forceinline__ void philox4x32_10(uint32_t c[4], uint32_t k0, uint32_t k1) {
 #pragma unroll
@@ -173,17 +188,21 @@ __global__ void k_policy_pack(int obs_dim, const float* __restrict__ W1, const f
     if (n >= kPolHidden && k >= kPolHidden) v = V2[(n - kPolHidden) * kPolHidden + (k - kPolHidden)];
     pk.B2[cm_offset(n, k, kPolN)] = __float2half_rn(v);
   }
+  if (t < kPolN3 * kPolK2) {                                  // B3: W3[0], W3[1], V3, zeros
+    const int n = t / kPolK2, k = t % kPolK2;
+    float v = 0.f;
+    if (n < 2 && k < kPolHidden) v = W3[n * kPolHidden + k];
+    if (n == 2 && k >= kPolHidden) v = V3[k - kPolHidden];
+    pk.B3[cm_offset(n, k, kPolN3)] = __float2half_rn(v);
+  }
   if (t < kPolN) {
     pk.consts[t] = (t < kPolHidden) ? b1[t] : c1[t - kPolHidden];
     pk.consts[128 + t] = (t < kPolHidden) ? b2[t] : c2[t - kPolHidden];
-    pk.consts[256 + t] = (t < kPolHidden) ? W3[t] : 0.f;                       // mean_0
-    pk.consts[384 + t] = (t < kPolHidden) ? W3[kPolHidden + t] : 0.f;          // mean_1
-    pk.consts[512 + t] = (t >= kPolHidden) ? V3[t - kPolHidden] : 0.f;         // value
   }
   if (t == 0) {
-    pk.consts[640] = b3[0]; pk.consts[641] = b3[1]; pk.consts[642] = c3[0]; pk.consts[643] = 0.f;
-    pk.consts[644] = log_std[0]; pk.consts[645] = log_std[1];
-    pk.consts[646] = lo0; pk.consts[647] = lo1; pk.consts[648] = hi0; pk.consts[649] = hi1;
+    pk.consts[256] = b3[0]; pk.consts[257] = b3[1]; pk.consts[258] = c3[0]; pk.consts[259] = 0.f;
+    pk.consts[260] = log_std[0]; pk.consts[261] = log_std[1];
+    pk.consts[262] = lo0; pk.consts[263] = lo1; pk.consts[264] = hi0; pk.consts[265] = hi1;
   }
 }
 
@@ -193,8 +212,10 @@ __global__ void __launch_bounds__(kPolThreads, 1) k_policy(
   extern __shared__ __align__(1024) unsigned char smem[];
   __half* sB1 = reinterpret_cast<__half*>(smem + kOffB1);
   __half* sB2 = reinterpret_cast<__half*>(smem + kOffB2);
+  __half* sB3 = reinterpret_cast<__half*>(smem + kOffB3);
   __half* sA1 = reinterpret_cast<__half*>(smem + kOffA1);
   __half* sA2 = reinterpret_cast<__half*>(smem + kOffA2);
+  __half* sA3 = sA1;                                                    // alias (see above)
   float* sC = reinterpret_cast<float*>(smem + kOffC);
   const float* sStage = reinterpret_cast<const float*>(smem + kOffStage);
   uint64_t* bar = reinterpret_cast<uint64_t*>(smem + kOffBar);          // [0] MMA, [1] TMA
@@ -205,15 +226,18 @@ __global__ void __launch_bounds__(kPolThreads, 1) k_policy(
   {
     const uint4* g1 = reinterpret_cast<const uint4*>(pk.B1);
     const uint4* g2 = reinterpret_cast<const uint4*>(pk.B2);
+    const uint4* g3 = reinterpret_cast<const uint4*>(pk.B3);
     uint4* s1 = reinterpret_cast<uint4*>(sB1);
     uint4* s2 = reinterpret_cast<uint4*>(sB2);
+    uint4* s3 = reinterpret_cast<uint4*>(sB3);
     for (int i = tid; i < kPolN * kPolK1 / 8; i += kPolThreads) s1[i] = g1[i];
     for (int i = tid; i < kPolN * kPolK2 / 8; i += kPolThreads) s2[i] = g2[i];
+    for (int i = tid; i < kPolN3 * kPolK2 / 8; i += kPolThreads) s3[i] = g3[i];
     for (int i = tid; i < kConstFloats; i += kPolThreads) sC[i] = pk.consts[i];
   }
   if (warp == 0) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
-                 "r"(128));
+                 "r"(256));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
   }
   if (tid == 0) {
@@ -225,16 +249,17 @@ __global__ void __launch_bounds__(kPolThreads, 1) k_policy(
   asm volatile("tcgen05.fence::before_thread_sync;");
   __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;");
-  const uint32_t tmem = *tmem_slot;
+  const uint32_t tmem = *tmem_slot;                  // D1/D2: columns 0-127, D3: 128-143
   const uint32_t bar_mma = smem_u32(&bar[0]), bar_tma = smem_u32(&bar[1]);
   const uint32_t stage = smem_u32(sStage);
-  const uint32_t a1 = smem_u32(sA1), a2 = smem_u32(sA2), b1 = smem_u32(sB1), b2 = smem_u32(sB2);
+  const uint32_t a1 = smem_u32(sA1), a2 = smem_u32(sA2), a3 = smem_u32(sA3);
+  const uint32_t b1 = smem_u32(sB1), b2 = smem_u32(sB2), b3 = smem_u32(sB3);
   uint32_t ph_mma = 0, ph_tma = 0;
 
-  // Epilogue mapping: warp w reads TMEM lanes (rows) 32 (w % 4) .. and columns 64 (w / 4) ..
+  // Epilogue mapping: warp w reads TMEM lanes (rows) 32 (w % 4) .. and columns 32 (w / 4) ..
   const int erow = 32 * (warp & 3) + lane;
-  const int ecol = 64 * (warp >> 2);
-  const uint32_t taddr = tmem + ((uint32_t)(32 * (warp & 3)) << 16) + (uint32_t)ecol;
+  const int ecol = 32 * (warp >> 2);
+  const uint32_t tlane = (uint32_t)(32 * (warp & 3)) << 16;
 
   const int64_t n_tiles = (M + kPolTile - 1) / kPolTile;
   // A full tile is one contiguous, 16-byte aligned block of 128 x obs_dim floats (m0 is a
@@ -245,6 +270,36 @@ __global__ void __launch_bounds__(kPolThreads, 1) k_policy(
   auto is_full = [&](int64_t t) { return bulk_ok && (t + 1) * kPolTile <= M; };
   if (tid == 0 && blockIdx.x < n_tiles && is_full(blockIdx.x))
     tma_load_1d(stage, obs + (int64_t)blockIdx.x * kPolTile * obs_dim, tile_bytes, bar_tma);
+
+  // MMA issue (one thread): s K-steps of 16 from A (R = 128 rows) and B (RB rows).
+  auto issue = [&](uint32_t d, uint32_t a, uint32_t b, int ksteps, int rb, uint32_t idesc) {
+    asm volatile("tcgen05.fence::after_thread_sync;");
+    for (int k = 0; k < ksteps; ++k)
+      mma_f16(d, umma_desc(a + k * 2 * (kPolTile * 16), kPolTile * 16, 128),
+              umma_desc(b + k * 2 * (rb * 16), rb * 16, 128), idesc, k > 0);
+    mma_commit(bar_mma);
+  };
+  // Epilogue of a hidden layer: h = tanh(D + bias) -> fp16 operand of the next layer.
+  auto hidden_epilogue = [&](const float* bias, __half* dst) {
+    float v[32];
+    tmem_ld32(tmem + tlane + (uint32_t)ecol, v);
+#pragma unroll
+    for (int g = 0; g < 4; ++g) {
+      const int c0 = ecol + 8 * g;
+      float t[8];
+#pragma unroll
+      for (int e = 0; e < 8; ++e) t[e] = tanh_fast(v[8 * g + e] + bias[c0 + e]);
+      uint4 pkd;
+      pkd.x = h2_bits(__floats2half2_rn(t[0], t[1]));
+      pkd.y = h2_bits(__floats2half2_rn(t[2], t[3]));
+      pkd.z = h2_bits(__floats2half2_rn(t[4], t[5]));
+      pkd.w = h2_bits(__floats2half2_rn(t[6], t[7]));
+      *reinterpret_cast<uint4*>(dst + cm_offset(erow, c0, kPolTile)) = pkd;
+    }
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    asm volatile("tcgen05.fence::before_thread_sync;");
+    __syncthreads();
+  };
 
   for (int64_t tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
     const int64_t m0 = tile * kPolTile;
@@ -284,77 +339,35 @@ __global__ void __launch_bounds__(kPolThreads, 1) k_policy(
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
     asm volatile("tcgen05.fence::before_thread_sync;");
     __syncthreads();
-    // ---- prefetch the next tile (overlaps the MMAs and epilogues); layer 1 on the tensor cores
+    // ---- prefetch the next tile (overlaps the MMAs and epilogues); layer 1
     if (tid == 0) {
       const int64_t nt = tile + gridDim.x;
       if (nt < n_tiles && is_full(nt))
         tma_load_1d(stage, obs + nt * kPolTile * obs_dim, tile_bytes, bar_tma);
-      asm volatile("tcgen05.fence::after_thread_sync;");
-#pragma unroll
-      for (int s = 0; s < kPolK1 / 16; ++s)
-        mma_f16(tmem, umma_desc(a1 + s * 2 * (kPolTile * 16), kPolTile * 16, 128),
-                umma_desc(b1 + s * 2 * (kPolN * 16), kPolN * 16, 128), kPolIdesc, s > 0);
-      mma_commit(bar_mma);
+      issue(tmem, a1, b1, kPolK1 / 16, kPolN, kPolIdesc);
     }
     mbar_wait(bar_mma, ph_mma);
     ph_mma ^= 1u;
     asm volatile("tcgen05.fence::after_thread_sync;");
-    // ---- epilogue 1: h1 = tanh(D + b1) -> fp16 A2
-#pragma unroll
-    for (int half = 0; half < 2; ++half) {
-      float v[32];
-      tmem_ld32(taddr + 32 * half, v);
-#pragma unroll
-      for (int g = 0; g < 4; ++g) {
-        const int c0 = ecol + 32 * half + 8 * g;
-        float t[8];
-#pragma unroll
-        for (int e = 0; e < 8; ++e) t[e] = tanh_fast(v[8 * g + e] + sC[c0 + e]);
-        uint4 pkd;
-        pkd.x = h2_bits(__floats2half2_rn(t[0], t[1]));
-        pkd.y = h2_bits(__floats2half2_rn(t[2], t[3]));
-        pkd.z = h2_bits(__floats2half2_rn(t[4], t[5]));
-        pkd.w = h2_bits(__floats2half2_rn(t[6], t[7]));
-        *reinterpret_cast<uint4*>(sA2 + cm_offset(erow, c0, kPolTile)) = pkd;
-      }
-    }
-    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-    asm volatile("tcgen05.fence::before_thread_sync;");
-    __syncthreads();
+    hidden_epilogue(sC, sA2);                            // h1 -> A2
     // ---- layer 2
-    if (tid == 0) {
-      asm volatile("tcgen05.fence::after_thread_sync;");
-#pragma unroll
-      for (int s = 0; s < kPolK2 / 16; ++s)
-        mma_f16(tmem, umma_desc(a2 + s * 2 * (kPolTile * 16), kPolTile * 16, 128),
-                umma_desc(b2 + s * 2 * (kPolN * 16), kPolN * 16, 128), kPolIdesc, s > 0);
-      mma_commit(bar_mma);
-    }
+    if (tid == 0) issue(tmem, a2, b2, kPolK2 / 16, kPolN, kPolIdesc);
     mbar_wait(bar_mma, ph_mma);
     ph_mma ^= 1u;
     asm volatile("tcgen05.fence::after_thread_sync;");
-    // ---- epilogue 2: h2 = tanh(D + b2); layer 3 dot products (fp32)
-    float acc0 = 0.f, acc1 = 0.f, accv = 0.f;
-#pragma unroll
-    for (int half = 0; half < 2; ++half) {
-      float v[32];
-      tmem_ld32(taddr + 32 * half, v);
-#pragma unroll
-      for (int e = 0; e < 32; ++e) {
-        const int col = ecol + 32 * half + e;
-        const float h = tanh_fast(v[e] + sC[128 + col]);
-        acc0 = fmaf(sC[256 + col], h, acc0);
-        acc1 = fmaf(sC[384 + col], h, acc1);
-        accv = fmaf(sC[512 + col], h, accv);
-      }
-    }
-    asm volatile("tcgen05.fence::before_thread_sync;");
-    const int64_t gr = m0 + erow;
-    if (gr < M) {
-      if (warp >= 4) {                                   // critic columns
-        if (out.value) out.value[gr] = accv + sC[642];
-      } else {                                           // actor columns
-        const float mu0 = acc0 + sC[640], mu1 = acc1 + sC[641];
+    hidden_epilogue(sC + 128, sA3);                      // h2 -> A3 (aliases A1)
+    // ---- layer 3: mean_0, mean_1, value in TMEM columns 128..130
+    if (tid == 0) issue(tmem + 128, a3, b3, kPolK2 / 16, kPolN3, kPolIdesc3);
+    mbar_wait(bar_mma, ph_mma);
+    ph_mma ^= 1u;
+    asm volatile("tcgen05.fence::after_thread_sync;");
+    if (warp < 4) {                                      // one thread per row
+      float o[4];
+      tmem_ld4(tmem + tlane + 128u, o);
+      const int64_t gr = m0 + erow;
+      if (gr < M) {
+        const float mu0 = o[0] + sC[256], mu1 = o[1] + sC[257];
+        if (out.value) out.value[gr] = o[2] + sC[258];
         if (out.mean) { out.mean[2 * gr] = mu0; out.mean[2 * gr + 1] = mu1; }
         if (out.action) {
           uint32_t c[4] = {(uint32_t)gr, step_lo, step_hi, 0u};
@@ -365,21 +378,22 @@ __global__ void __launch_bounds__(kPolThreads, 1) k_policy(
           float sn, cs;
           sincospif(2.f * u1, &sn, &cs);
           const float e0 = rr * cs, e1 = rr * sn;
-          const float ls0 = sC[644], ls1 = sC[645];
+          const float ls0 = sC[260], ls1 = sC[261];
           const float r0 = fmaf(expf(ls0), e0, mu0), r1 = fmaf(expf(ls1), e1, mu1);
-          out.action[2 * gr] = fminf(fmaxf(r0, sC[646]), sC[648]);
-          out.action[2 * gr + 1] = fminf(fmaxf(r1, sC[647]), sC[649]);
+          out.action[2 * gr] = fminf(fmaxf(r0, sC[262]), sC[264]);
+          out.action[2 * gr + 1] = fminf(fmaxf(r1, sC[263]), sC[265]);
           if (out.logp)
             out.logp[gr] = -0.5f * (e0 * e0 + e1 * e1) - ls0 - ls1 - 1.8378770664093453f;
         }
       }
     }
+    asm volatile("tcgen05.fence::before_thread_sync;");
     __syncthreads();
   }
   asm volatile("tcgen05.fence::after_thread_sync;");
   __syncthreads();
   if (warp == 0)
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(128));
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(256));
 }
 
 }  // namespace vg
