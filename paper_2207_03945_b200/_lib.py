@@ -8,7 +8,11 @@ import os
 from ctypes import POINTER, c_char_p, c_float, c_int32, c_int64, c_uint32, c_void_p
 
 _PKG = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_PKG, "libvg.so")
+# VG_LIB_VARIANT=<name> loads build/variants/libvg_<name>.so (tuning experiments built by
+# tools/build_variants.py); unset = the in-tree libvg.so.
+LIB_PATH = (os.path.join(os.path.dirname(_PKG), "build", "variants",
+                         f"libvg_{os.environ['VG_LIB_VARIANT']}.so")
+            if os.environ.get("VG_LIB_VARIANT") else os.path.join(_PKG, "libvg.so"))
 
 VG_OK, VG_EINVAL, VG_ESTATE, VG_ECUDA, VG_ENCCL, VG_EOVERFLOW, VG_ENOMEM = range(7)
 N_PHASES = 5

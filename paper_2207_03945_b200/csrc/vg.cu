@@ -312,7 +312,7 @@ int sense_chunks(const vg_world* w) {
   const long long warps = (long long)w->n_cells * vg::kSenseWarps;
   const long long per_cell = (w->P.total + w->n_cells - 1) / w->n_cells;
   long long ch = (target_warps + warps - 1) / warps;
-  ch = std::min(ch, std::max(1LL, (per_cell + 2 * vg::kSenseWarps - 1) / (2 * vg::kSenseWarps)));
+  ch = std::min(ch, std::max(1LL, (per_cell + vg::kSenseNQ * vg::kSenseWarps - 1) / (vg::kSenseNQ * vg::kSenseWarps)));
   return (int)std::max(1LL, std::min(ch, 1024LL));
 }
 

@@ -464,7 +464,15 @@ __global__ void __launch_bounds__(kRBThreads, 2) k_replica_bin(
 // them with ballot/popc into a per-warp queue, and processes full warps of 32 pairs:
 // contact test, reward term (fixed point, A16b), bearing, sector, and the per-sector
 // nearest distance by shared-memory atomicMin on the float bits (A2, A3).
+#ifndef VG_SENSE_NQ
+#define VG_SENSE_NQ 2
+#endif
+#ifndef VG_SENSE_MINB
+#define VG_SENSE_MINB 6
+#endif
 constexpr int kSenseWarps = 4;
+constexpr int kSenseNQ = VG_SENSE_NQ;         // queries sensed together by one warp
+constexpr int kSenseMinBlocks = VG_SENSE_MINB;  // resident CTAs per SM
 constexpr int kQueue = 128;         // ring (power of 2) >= 31 carried + 2 x 32 pushed
 
 // atan2(y, x) in (-pi, pi] with |error| <~ 2.5e-7 rad: octant reduction,
@@ -492,6 +500,23 @@ __device__ __forceinline__ float vg_atan2(float y, float x) {
   return copysignf(r, y);
 }
 
+__device__ __forceinline__ uint32_t sh_addr(const void* p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void sts128(uint32_t a, float4 v) {
+  asm volatile("st.shared.v4.f32 [%0], {%1, %2, %3, %4};" ::"r"(a), "f"(v.x), "f"(v.y), "f"(v.z),
+               "f"(v.w)
+               : "memory");
+}
+__device__ __forceinline__ float4 lds128(uint32_t a) {
+  float4 v;
+  asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
+               : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
+               : "r"(a)
+               : "memory");
+  return v;
+}
+
 struct Seg {
   uint32_t b, e;     // run [b, e) of the sorted arrays
   float csx, csy;    // candidate image shift (0 or -L; exact by Sterbenz, A11)
@@ -502,13 +527,15 @@ struct Seg {
 // §6d): candidates within d_v + d_r, one ray per sector centre (table ray_dir, agent
 // frame), each neighbour a disc of radius d_r; counts and reward stay Eq. 1 (d < d_v).
 template <int ENV, bool VISION, bool SLAB, bool RAY>
-__global__ void __launch_bounds__(kSenseWarps * 32, 6) k_sense(
+__global__ void __launch_bounds__(kSenseWarps * 32, kSenseMinBlocks) k_sense(
     Params P, const uint32_t* __restrict__ cell_start, const float4* __restrict__ sorted,
     const float2* __restrict__ sorted_xy, const uint32_t* __restrict__ perm, Outs O, Slab SL,
     const float2* __restrict__ ray_dir) {
-  __shared__ uint32_t s_min[kSenseWarps][2][kMaxViewSlots];
+  __shared__ uint32_t s_min[kSenseWarps][kSenseNQ][kMaxViewSlots];
   __shared__ float2 s_ray[RAY ? kMaxViewSlots : 1];
-  __shared__ float4 s_q[kSenseWarps][2][kQueue];
+  // Ring queues, kQueue float4 each, at shared addresses aligned to the ring size (the
+  // shared window has a reserved prefix, so the alignment is done on the address).
+  __shared__ float4 s_q_raw[(kSenseWarps * kSenseNQ + 1) * kQueue];
   __shared__ Seg s_seg[6];
   __shared__ int s_nseg;
 
@@ -573,15 +600,17 @@ __global__ void __launch_bounds__(kSenseWarps * 32, 6) k_sense(
   const uint32_t qb = cs[cl], qe = cs[cl + 1];
   unsigned lt_mask;
   asm("mov.u32 %0, %%lanemask_lt;" : "=r"(lt_mask));
-  // Each warp senses NQ = 2 queries of this cell at once: every candidate load, image
-  // shift and loop step is shared; each query has its own ballot, queue, sector row and
-  // accumulators.  A missing second query gets a NaN position (never a neighbour).
-  constexpr int NQ = 2;
+  // Each warp senses NQ queries of this cell at once: every candidate load, image shift
+  // and loop step is shared; each query has its own ballot, queue, sector row and
+  // accumulators.  A missing query gets a NaN position (never a neighbour).
+  constexpr int NQ = kSenseNQ;
   const uint32_t qstride = NQ * kSenseWarps * gridDim.y;
   for (uint32_t q0 = qb + NQ * (blockIdx.y * kSenseWarps + warp); q0 < qe; q0 += qstride) {
     float4 me[NQ];
     bool live[NQ];
-    uint32_t tq[NQ], head[NQ], tail[NQ], ncol[NQ], ntouch[NQ], nnb[NQ];
+    // Ring queue of query t: kQueue float4 entries at byte address qbase[t] (aligned to the
+    // ring size, so slot addresses are qbase | (byte offset & mask)); head/tail in bytes.
+    uint32_t tq[NQ], head[NQ], tail[NQ], ncol[NQ], ntouch[NQ], nnb[NQ], qbase[NQ];
     float sn[NQ], csn[NQ];
     long long rs[NQ];
 #pragma unroll
@@ -599,6 +628,8 @@ __global__ void __launch_bounds__(kSenseWarps * 32, 6) k_sense(
         for (int w = 0; w < kMaxViewSlots / 32; ++w) s_min[warp][t][32 * w + lane] = kOneBits;
       }
       head[t] = tail[t] = ncol[t] = ntouch[t] = nnb[t] = 0u;
+      qbase[t] = ((sh_addr(s_q_raw) + (kQueue * 16 - 1)) & ~(uint32_t)(kQueue * 16 - 1)) +
+                 (uint32_t)((warp * NQ + t) * kQueue * 16);
       rs[t] = 0;
     }
     __syncwarp();
@@ -610,8 +641,9 @@ __global__ void __launch_bounds__(kSenseWarps * 32, 6) k_sense(
       const uint32_t tj = tagbits >> 31;
       const float d2 = e.z;
       const bool contact = d2 <= P.contact2;                          // A6 (inclusive)
-      const float rsq = rsqrtf(d2);
-      const float d = (d2 > 0.f) ? d2 * rsq : 0.f;
+      float rsq;                                   // MUFU.RSQ without the subnormal rescale:
+      asm("rsqrt.approx.ftz.f32 %0, %1;" : "=f"(rsq) : "f"(d2));
+      const float d = (d2 >= 1.17549435e-38f) ? d2 * rsq : 0.f;   // subnormal d^2 -> d = 0
       // Eq. 1 / Fig. 4 (A5): contact -> -c_collide, else the tent min(rise, fall).
       const float f = contact ? -P.c_collide
                               : fminf(fmaf(P.k_rise, d, P.b_rise), fmaf(P.nk_fall, d, P.b_fall));
@@ -690,6 +722,7 @@ __global__ void __launch_bounds__(kSenseWarps * 32, 6) k_sense(
       for (uint32_t p0 = sg.b; p0 < sg.e; p0 += 64) {
         const uint32_t pa = p0 + lane, pb = p0 + 32 + lane;
         const bool va = pa < sg.e, vb = pb < sg.e;
+        const bool two = p0 + 32 < sg.e;                             // warp-uniform
         float ax, ay, bx, by;
         uint32_t ta = 0u, tb = 0u;
         if (ENV == kFlock) {                 // sorted_xy is padded by 64: no predicate
@@ -704,31 +737,29 @@ __global__ void __launch_bounds__(kSenseWarps * 32, 6) k_sense(
         ax = va ? ax + sg.csx : __int_as_float(0x7fc00000);          // exact (Sterbenz)
         bx = vb ? bx + sg.csx : __int_as_float(0x7fc00000);
         ay += sg.csy; by += sg.csy;
+        // Ballot the in-radius candidates of one 32-slot half and append them to each
+        // query's ring (dx, dy, d^2, index | type << 31).
+        auto scan = [&](const float cx_, const float cy_, const uint32_t word) {
+#pragma unroll
+          for (int t = 0; t < NQ; ++t) {
+            const float dx = cx_ - qx[t], dy = cy_ - qy[t];
+            const float d2 = fmaf(dx, dx, dy * dy);
+            const bool in = d2 < (RAY ? P.cand2 : P.dv2);                // Eq. 1: d < d_v
+            const unsigned bal = __ballot_sync(kFull, in);
+            if (in)
+              sts128(qbase[t] | ((tail[t] + (__popc(bal & lt_mask) << 4)) & (kQueue * 16 - 16)),
+                     make_float4(dx, dy, d2, __uint_as_float(word)));
+            tail[t] += __popc(bal) << 4;
+          }
+        };
+        scan(ax, ay, pa | ta);
+        if (two) scan(bx, by, pb | tb);
 #pragma unroll
         for (int t = 0; t < NQ; ++t) {
-          const float dxa = ax - qx[t], dya = ay - qy[t];
-          const float dxb = bx - qx[t], dyb = by - qy[t];
-          const float d2a = fmaf(dxa, dxa, dya * dya);
-          const float d2b = fmaf(dxb, dxb, dyb * dyb);
-          const bool ia = d2a < (RAY ? P.cand2 : P.dv2);               // Eq. 1: d < d_v
-          const bool ib = d2b < (RAY ? P.cand2 : P.dv2);
-          const unsigned bala = __ballot_sync(kFull, ia);
-          const unsigned balb = __ballot_sync(kFull, ib);
-          float4* qq = s_q[warp][t];
-          if (ia) qq[(tail[t] + __popc(bala & lt_mask)) & (kQueue - 1)] =
-              make_float4(dxa, dya, d2a, __uint_as_float(pa | ta));
-          tail[t] += __popc(bala);
-          if (ib) qq[(tail[t] + __popc(balb & lt_mask)) & (kQueue - 1)] =
-              make_float4(dxb, dyb, d2b, __uint_as_float(pb | tb));
-          tail[t] += __popc(balb);
-        }
-#pragma unroll
-        for (int t = 0; t < NQ; ++t) {
-          float4* qq = s_q[warp][t];
-          while (tail[t] - head[t] >= 32u) {
+          while (tail[t] - head[t] >= 32u * 16u) {
             __syncwarp();
-            process(t, qq[(head[t] + lane) & (kQueue - 1)]);
-            head[t] += 32u;
+            process(t, lds128(qbase[t] | ((head[t] + lane * 16u) & (kQueue * 16 - 16))));
+            head[t] += 32u * 16u;
           }
         }
         __syncwarp();                       // ring slots read above may be rewritten next
@@ -737,7 +768,8 @@ __global__ void __launch_bounds__(kSenseWarps * 32, 6) k_sense(
     __syncwarp();
 #pragma unroll
     for (int t = 0; t < NQ; ++t)
-      if (lane < tail[t] - head[t]) process(t, s_q[warp][t][(head[t] + lane) & (kQueue - 1)]);
+      if (lane * 16u < tail[t] - head[t])
+        process(t, lds128(qbase[t] | ((head[t] + lane * 16u) & (kQueue * 16 - 16))));
     __syncwarp();
 
 #pragma unroll
@@ -745,7 +777,7 @@ __global__ void __launch_bounds__(kSenseWarps * 32, 6) k_sense(
       if (!live[t]) continue;                                        // warp-uniform
       const uint32_t q = q0 + t;
       const uint32_t nn = RAY ? __reduce_add_sync(kFull, nnb[t])
-                              : tail[t] - 1u;                   // minus the self pair
+                              : (tail[t] >> 4) - 1u;            // minus the self pair
       // Warp reductions (REDUX): the int64 reward sum as exact 32-bit partial sums.
       const uint32_t nc = __reduce_add_sync(kFull, ncol[t]);
       const uint32_t nt = (ENV == kTag) ? __reduce_add_sync(kFull, ntouch[t]) : 0u;
