@@ -245,7 +245,8 @@ class World:
         check(_lib.lib.vg_slab_finish(self._h, byref(o), self._stream()))
 
     def slab_owned(self) -> tuple:
-        """(global ids [n_own], state records [n_own, 4]) of the owned agents, row order."""
+        """(global ids [n_own], state records [n_own, 4]) of the owned agents in (cell, id)
+        order (vg_get_bins); output rows use the sense order — map them by outs.agent_id."""
         n = self.slab_own_count()
         b = self.get_bins()
         own_b = int(b["cell_start"][self.grid].item())

@@ -57,7 +57,10 @@ struct vg_world {
   uint32_t* perm = nullptr;        // [R*N]         stable order
   float4* tmp_rec = nullptr;       // [R*N]
   float4* sorted = nullptr;        // [R*N]
-  float2* sorted_xy = nullptr;     // [R*N]         positions of `sorted` (K4 candidate reads)
+  float4* xo_rec = nullptr;        // [R*N]         K4 sense order: within a cell by (axis key, id)
+  uint32_t* xo_perm = nullptr;     // [R*N]         agent ids in sense order
+  float2* xo_xy = nullptr;         // [R*N + 64]    positions in sense order (K4 candidate reads)
+  uint32_t* sub_tab = nullptr;     // [(n_cells + 1) * kSub] K4 window table (K3b)
   float2* ray_dir = nullptr;       // [v] ray vision: sector-centre ray directions (agent frame)
   float2* act_dev = nullptr;       // [R*N]         staging for vg_step_host
   unsigned long long* err_dev = nullptr;  // smallest bad agent index (device word)
@@ -205,6 +208,11 @@ vg::Params derive(const vg_config& c, int g) {
   P.nk_fall = -P.k_fall;
   P.b_fall = P.k_fall * c.d_v;
   P.touch_fix = (long long)std::llrint((double)c.r_touch * 4294967296.0);
+  P.cell = L / (float)g;
+  P.win_r2 = (c.vision == VG_VISION_RAY) ? P.cand2 : P.dv2;
+  // K4 windows only ever widen the candidate set: 1 % of the radius plus 2^-19 L covers the
+  // fp32 rounding of the keys, of the pair test and the fuzz of the A16 cell boundaries.
+  P.win_margin = 0.01f * std::sqrt(P.win_r2) + L * 1.9073486e-6f;
   return P;
 }
 
@@ -266,8 +274,8 @@ template <int ENV, bool INTEGRATE>
 vg_status launch_fused_bin(vg_world* w, float4* io, const float4* in, const float2* act,
                            cudaStream_t s) {
   vg::k_replica_bin<ENV, INTEGRATE><<<w->P.R, vg::kRBThreads, 0, s>>>(
-      w->P, io, in, act, w->cell_id, w->cell_start, w->sorted, w->perm, w->sorted_xy,
-      w->err_dev, w->err_flag);
+      w->P, io, in, act, w->cell_id, w->cell_start, w->sorted, w->perm, w->xo_rec, w->xo_perm,
+      w->xo_xy, w->sub_tab, w->err_dev, w->err_flag);
   if (vg_status st = launch_check("k_replica_bin")) return st;
   w->binned = true;
   return VG_OK;
@@ -282,9 +290,10 @@ vg_status bin_rest(vg_world* w, const float4* state, cudaStream_t s, bool prof =
       w->P, state, w->cell_id, w->slot, w->cell_start, w->tmp_rec, w->tmp_id);
   if (vg_status st = launch_check("k_scatter")) return st;
   if (prof) prof_mark(w, 3, s);
-  const long long threads = (long long)w->n_cells * 32;
+  const long long threads = (long long)(w->n_cells + 1) * 32;   // + the sentinel row
   vg::k_cell_sort<<<(unsigned)((threads + 255) / 256), 256, 0, s>>>(
-      w->n_cells, w->cell_start, w->tmp_rec, w->tmp_id, w->sorted, w->perm, w->sorted_xy);
+      w->P, w->n_cells, w->slab ? 1 : 0, w->cell_start, w->tmp_rec, w->tmp_id, w->sorted,
+      w->perm, w->xo_rec, w->xo_perm, w->xo_xy, w->sub_tab);
   if (vg_status st = launch_check("k_cell_sort")) return st;
   if (prof) prof_mark(w, 4, s);
   w->binned = true;
@@ -320,10 +329,10 @@ template <int ENV, bool VISION, bool SLAB>
 void sense_kernel(vg_world* w, dim3 grid, const vg::Outs& O, cudaStream_t s) {
   if (w->cfg.vision == VG_VISION_RAY)
     vg::k_sense<ENV, VISION, SLAB, true><<<grid, vg::kSenseWarps * 32, 0, s>>>(
-        w->P, w->cell_start, w->sorted, w->sorted_xy, w->perm, O, w->SL, w->ray_dir);
+        w->P, w->cell_start, w->xo_rec, w->xo_xy, w->xo_perm, O, w->SL, w->ray_dir, w->sub_tab);
   else
     vg::k_sense<ENV, VISION, SLAB, false><<<grid, vg::kSenseWarps * 32, 0, s>>>(
-        w->P, w->cell_start, w->sorted, w->sorted_xy, w->perm, O, w->SL, w->ray_dir);
+        w->P, w->cell_start, w->xo_rec, w->xo_xy, w->xo_perm, O, w->SL, w->ray_dir, w->sub_tab);
 }
 
 template <bool VISION>
@@ -355,9 +364,10 @@ vg_status slab_bin(vg_world* w, cudaStream_t s) {
   vg::k_slab_scatter<ENV><<<nb, 256, 0, s>>>(w->P, w->SB, w->cell_id, w->slot, w->cell_start,
                                               w->tmp_rec, w->tmp_id);
   if (vg_status st = launch_check("k_slab_scatter")) return st;
-  const long long threads = (long long)w->n_cells * 32;
+  const long long threads = (long long)(w->n_cells + 1) * 32;   // + the sentinel row
   vg::k_cell_sort<<<(unsigned)((threads + 255) / 256), 256, 0, s>>>(
-      w->n_cells, w->cell_start, w->tmp_rec, w->tmp_id, w->sorted, w->perm, w->sorted_xy);
+      w->P, w->n_cells, w->slab ? 1 : 0, w->cell_start, w->tmp_rec, w->tmp_id, w->sorted,
+      w->perm, w->xo_rec, w->xo_perm, w->xo_xy, w->sub_tab);
   if (vg_status st = launch_check("k_cell_sort")) return st;
   w->binned = true;
   return VG_OK;
@@ -454,7 +464,10 @@ vg_status vg_world_create(const vg_config* cfg, vg_world** out) {
   if (!st) st = dalloc(w, &w->perm, n);
   if (!st) st = dalloc(w, &w->tmp_rec, n);
   if (!st) st = dalloc(w, &w->sorted, n);
-  if (!st) st = dalloc(w, &w->sorted_xy, n + 64);   // padded: unpredicated K4 loads
+  if (!st) st = dalloc(w, &w->xo_rec, n);
+  if (!st) st = dalloc(w, &w->xo_perm, n);
+  if (!st) st = dalloc(w, &w->xo_xy, n + 64);       // padded: unpredicated K4 loads
+  if (!st) st = dalloc(w, &w->sub_tab, ((size_t)w->n_cells + 1) * vg::kSub);
   if (!st) st = dalloc(w, &w->ray_dir, vg::kMaxViewSlots);
   if (!st) {
     // psi_k = -fov/2 + (k + 1/2) fov/v (orientation A3), in double, rounded once
@@ -502,7 +515,10 @@ void vg_world_destroy(vg_world* w) {
   cudaFree(w->perm);
   cudaFree(w->tmp_rec);
   cudaFree(w->sorted);
-  cudaFree(w->sorted_xy);
+  cudaFree(w->xo_rec);
+  cudaFree(w->xo_perm);
+  cudaFree(w->xo_xy);
+  cudaFree(w->sub_tab);
   cudaFree(w->ray_dir);
   cudaFree(w->act_dev);
   cudaFree(w->err_dev);
@@ -744,11 +760,11 @@ vg_status vg_slab_begin(vg_world* w, const float* actions, void* stream) {
   const unsigned nb = stride_blocks((size_t)w->P.N / w->cfg.world_size + 1);
   const float2* a = reinterpret_cast<const float2*>(actions);
   if (w->P.env == vg::kFlock)
-    vg::k_slab_begin<vg::kFlock><<<nb, 256, 0, s>>>(w->P, w->SL, w->SB, w->cell_start, w->sorted,
-                                                     w->perm, a, w->err_dev, w->err_flag);
+    vg::k_slab_begin<vg::kFlock><<<nb, 256, 0, s>>>(w->P, w->SL, w->SB, w->cell_start, w->xo_rec,
+                                                     w->xo_perm, a, w->err_dev, w->err_flag);
   else
-    vg::k_slab_begin<vg::kTag><<<nb, 256, 0, s>>>(w->P, w->SL, w->SB, w->cell_start, w->sorted,
-                                                   w->perm, a, w->err_dev, w->err_flag);
+    vg::k_slab_begin<vg::kTag><<<nb, 256, 0, s>>>(w->P, w->SL, w->SB, w->cell_start, w->xo_rec,
+                                                   w->xo_perm, a, w->err_dev, w->err_flag);
   vg_status st = launch_check("k_slab_begin");
   prof_mark(w, 1, s);
   return st;

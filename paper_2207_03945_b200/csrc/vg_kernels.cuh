@@ -37,6 +37,8 @@ struct Params {
   float c_collide, d_peak, k_rise, k_fall, w_prox;
   float b_rise, nk_fall, b_fall;   // f = min(k_rise d + b_rise, nk_fall d + b_fall) (A5)
   float d_r, cand2, inv_w;         // ray vision: body radius, RN32((d_v + d_r)^2), v / fov
+  float cell;                      // RN32(L / G) (K4 windows only)
+  float win_r2, win_margin;        // K4 window: candidate radius^2, conservative margin
   long long touch_fix;         // r_touch * 2^32
 };
 
@@ -286,16 +288,95 @@ __global__ void __launch_bounds__(256) k_scatter(
 }
 
 // --------------------------------------------------------------------------------- K3b
+// Sub-bins for the K4 candidate windows: cell c, with axis index ca (cx on the
+// row-major replica grid, cy on the column-major slab grid), is cut along its axis into kSub
+// sub-bins; a record with axis key a lies in sub_bin(ca, a).  The K4 "sense order" (xo_*)
+// is, within each cell, ascending (sub-bin, id): along a run of cells of one grid row
+// (column) the sub-bins then ascend, and a window [klo, khi] of keys is covered by one
+// contiguous range, read from sub_tab[c kSub + s] = first sense-order index of cell c in
+// sub-bin >= s (sub_tab[(n_cells) kSub] = total, so sub_tab[c kSub + kSub] = next cell).
+// K4 maps klo / khi with the same monotone fp32 formulas, so no key in the window is
+// missed.  Outputs never depend on this order (fixed-point sums, min, counts).
+// With u = RN32(a G/L) (the A16 product, so ca = min(G-1, floor(u))), the sub-bin is
+// floor(kSub u) - kSub ca clamped to [0, kSub) (kSub u is exact): a monotone function of a.
+constexpr int kSub = 8;
+__device__ __forceinline__ int sub_bin(const Params& P, int ca, float a) {
+  const int sb = __float2int_rd(__fmul_rn(a, P.gs) * (float)kSub) - kSub * ca;
+  return min(max(sb, 0), kSub - 1);
+}
+
+// Sense order of one cell from its stable (id-ordered) records [b, b + m): a stable counting
+// sort by sub-bin, one warp.  Writes xo_* and the cell's kSub table entries.
+__device__ __forceinline__ void sense_order_cell(const Params& P, int ca, bool axis_y,
+                                                 uint32_t b, int m,
+                                                 const float4* sorted, const uint32_t* perm,
+                                                 float4* __restrict__ xo_rec,
+                                                 uint32_t* __restrict__ xo_perm,
+                                                 float2* __restrict__ xo_xy, uint32_t* tab,
+                                                 int lane, unsigned lt) {
+  uint32_t cnt = 0;                                       // lane s < kSub: records in sub-bin s
+  for (int ib = 0; ib < m; ib += 32) {
+    const bool valid = ib + lane < m;
+    int sb = kSub;
+    if (valid) {
+      const float4 rec = sorted[b + ib + lane];
+      sb = sub_bin(P, ca, axis_y ? rec.y : rec.x);
+    }
+#pragma unroll
+    for (int s = 0; s < kSub; ++s) {
+      const uint32_t n = __popc(__ballot_sync(kFull, sb == s));
+      if (lane == s) cnt += n;
+    }
+  }
+  uint32_t inc = cnt;                                     // exclusive scan over lanes 0..7
+#pragma unroll
+  for (int o = 1; o < kSub; o <<= 1) {
+    const uint32_t y = __shfl_up_sync(kFull, inc, o);
+    if (lane >= o) inc += y;
+  }
+  uint32_t run = inc - cnt;                               // lane s: records in sub-bins < s
+  if (lane < kSub) tab[lane] = b + run;
+  for (int ib = 0; ib < m; ib += 32) {
+    const bool valid = ib + lane < m;
+    float4 rec = make_float4(0.f, 0.f, 0.f, 0.f);
+    uint32_t id = 0u;
+    int sb = kSub;
+    if (valid) {
+      rec = sorted[b + ib + lane];
+      id = perm[b + ib + lane];
+      sb = sub_bin(P, ca, axis_y ? rec.y : rec.x);
+    }
+    const unsigned grp = __match_any_sync(kFull, sb);
+    const uint32_t pos = __shfl_sync(kFull, run, sb & (kSub - 1)) + __popc(grp & lt);
+    if (valid) {
+      xo_rec[b + pos] = rec;
+      xo_perm[b + pos] = id;
+      xo_xy[b + pos] = make_float2(rec.x, rec.y);        // compact positions for K4
+    }
+#pragma unroll
+    for (int s = 0; s < kSub; ++s) {
+      const uint32_t n = __popc(__ballot_sync(kFull, sb == s));
+      if (lane == s) run += n;
+    }
+  }
+}
+
 // One warp per cell: rank each member by agent id (ids are unique within a replica) and
-// write it to its stable slot ("ascending order (determinism anchor)").
+// write it to its stable slot ("ascending order (determinism anchor)"); then the
+// cell's sense order (above).  Warp n_cells writes the table sentinel.
 __global__ void __launch_bounds__(256) k_cell_sort(
-    int n_cells, const uint32_t* __restrict__ cell_start, const float4* __restrict__ tmp_rec,
-    const uint32_t* __restrict__ tmp_id, float4* __restrict__ sorted,
-    uint32_t* __restrict__ perm, float2* __restrict__ sorted_xy) {
+    Params P, int n_cells, int axis_y, const uint32_t* __restrict__ cell_start,
+    const float4* __restrict__ tmp_rec, const uint32_t* __restrict__ tmp_id,
+    float4* __restrict__ sorted, uint32_t* __restrict__ perm, float4* __restrict__ xo_rec,
+    uint32_t* __restrict__ xo_perm, float2* __restrict__ xo_xy, uint32_t* __restrict__ sub_tab) {
   const int cell = (int)(((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5);
   const int lane = threadIdx.x & 31;
-  if (cell >= n_cells) return;
+  if (cell > n_cells) return;
   const uint32_t b = cell_start[cell];
+  if (cell == n_cells) {
+    if (lane == 0) sub_tab[(size_t)n_cells * kSub] = b;
+    return;
+  }
   const int m = (int)(cell_start[cell + 1] - b);
   for (int base = 0; base < m; base += 32) {
     const int idx = base + lane;
@@ -308,12 +389,15 @@ __global__ void __launch_bounds__(256) k_cell_sort(
       for (int t = 0; t < 32; ++t) rank += (__shfl_sync(kFull, other, t) < id) ? 1 : 0;
     }
     if (valid) {
-      const float4 rec = tmp_rec[b + idx];
-      sorted[b + rank] = rec;
+      sorted[b + rank] = tmp_rec[b + idx];
       perm[b + rank] = id;
-      sorted_xy[b + rank] = make_float2(rec.x, rec.y);   // compact positions for K4
     }
   }
+  __syncwarp();                                         // this warp's writes are visible
+  unsigned lt;
+  asm("mov.u32 %0, %%lanemask_lt;" : "=r"(lt));
+  sense_order_cell(P, cell % P.G, axis_y != 0, b, m, sorted, perm, xo_rec, xo_perm, xo_xy,
+                   sub_tab + (size_t)cell * kSub, lane, lt);
 }
 
 // ------------------------------------------------------------------------------ K1-K3 fused
@@ -336,7 +420,8 @@ __global__ void __launch_bounds__(kRBThreads, 2) k_replica_bin(
     Params P, float4* __restrict__ state_io, const float4* __restrict__ state_in,
     const float2* __restrict__ actions, uint32_t* __restrict__ cell_id,
     uint32_t* __restrict__ cell_start, float4* __restrict__ sorted,
-    uint32_t* __restrict__ perm, float2* __restrict__ sorted_xy,
+    uint32_t* __restrict__ perm, float4* __restrict__ xo_rec, uint32_t* __restrict__ xo_perm,
+    float2* __restrict__ xo_xy, uint32_t* __restrict__ sub_tab,
     unsigned long long* __restrict__ err, volatile uint32_t* flag) {
   constexpr int NW = kRBThreads / 32;
   __shared__ uint32_t s_wc[NW][kRBMaxCells + 1];     // per-warp counts, then offsets (+1: banks)
@@ -449,12 +534,19 @@ __global__ void __launch_bounds__(kRBThreads, 2) k_replica_bin(
       if (ENV == kTag) s.w = (i >= P.first_chaser) ? 1.f : 0.f;
       sorted[pos] = s;
       perm[pos] = (uint32_t)i;
-      sorted_xy[pos] = make_float2(s.x, s.y);
     }
     __syncwarp();
     if (valid && (grp & lt) == 0u) s_wc[warp][c] += __popc(grp);
     __syncwarp();
   }
+  __syncthreads();                   // the block's sorted / perm writes are now visible
+  // ---- pass 3: K4 sense order of each cell (see K3b)
+  for (int c = warp; c < C; c += NW) {
+    const int m = ((c + 1 < C) ? (int)s_tot[c + 1] : N) - (int)s_tot[c];
+    sense_order_cell(P, c % P.G, false, (uint32_t)base + s_tot[c], m, sorted, perm, xo_rec,
+                     xo_perm, xo_xy, sub_tab + ((size_t)r * C + c) * kSub, lane, lt);
+  }
+  if (r == (int)gridDim.x - 1 && tid == 0) sub_tab[(size_t)P.R * C * kSub] = (uint32_t)P.total;
 }
 
 // ---------------------------------------------------------------------------------- K4
@@ -517,20 +609,22 @@ __device__ __forceinline__ float4 lds128(uint32_t a) {
   return v;
 }
 
-struct Seg {
-  uint32_t b, e;     // run [b, e) of the sorted arrays
+// A run of stencil cells along one grid row (replica) / column (slab): cells with axis
+// index a0..a1, linear ids cbase + a0 .. cbase + a1.
+struct __align__(16) Seg {
   float csx, csy;    // candidate image shift (0 or -L; exact by Sterbenz, A11)
   float qsx, qsy;    // query image shift (0 or -L)
+  float plo, phi;    // the run's extent across its axis (shifted frame, widened by the margin)
+  int cbase, a0, a1;
 };
 
-// RAY: the ray-disc reading of the vision model (DESIGN.md
-// §6d): candidates within d_v + d_r, one ray per sector centre (table ray_dir, agent
-// frame), each neighbour a disc of radius d_r; counts and reward stay Eq. 1 (d < d_v).
 template <int ENV, bool VISION, bool SLAB, bool RAY>
 __global__ void __launch_bounds__(kSenseWarps * 32, kSenseMinBlocks) k_sense(
     Params P, const uint32_t* __restrict__ cell_start, const float4* __restrict__ sorted,
     const float2* __restrict__ sorted_xy, const uint32_t* __restrict__ perm, Outs O, Slab SL,
-    const float2* __restrict__ ray_dir) {
+    const float2* __restrict__ ray_dir, const uint32_t* __restrict__ sub_tab) {
+  // sorted / sorted_xy / perm are the sense-order arrays (xo_* of K3b): within a cell the
+  // records ascend in x (replica grid, runs along rows) or y (slab grid, runs along columns).
   __shared__ uint32_t s_min[kSenseWarps][kSenseNQ][kMaxViewSlots];
   __shared__ float2 s_ray[RAY ? kMaxViewSlots : 1];
   // Ring queues, kQueue float4 each, at shared addresses aligned to the ring size (the
@@ -558,15 +652,19 @@ __global__ void __launch_bounds__(kSenseWarps * 32, kSenseMinBlocks) k_sense(
       const int col = cx + dxc;
       const float csx = (col == 0 && SL.lo == 0) ? mL : 0.f;
       const float qsx = (col == SL.W + 1 && SL.hi == P.G) ? mL : 0.f;
+      const int gcol = (SL.lo + col - 1 + P.G) % P.G;
+      const float plo = (float)gcol * P.cell + csx - P.win_margin;
+      const float phi = (float)(gcol + 1) * P.cell + csx + P.win_margin;
       const int base = col * P.G;
+      const int g1 = P.G - 1;
       if (cy >= 1 && cy <= P.G - 2) {
-        s_seg[ns++] = Seg{cs[base + cy - 1], cs[base + cy + 2], csx, 0.f, qsx, 0.f};
+        s_seg[ns++] = Seg{csx, 0.f, qsx, 0.f, plo, phi, base, cy - 1, cy + 1};
       } else if (cy == 0) {                          // rows G-1 | 0, 1
-        s_seg[ns++] = Seg{cs[base + P.G - 1], cs[base + P.G], csx, mL, qsx, 0.f};
-        s_seg[ns++] = Seg{cs[base], cs[base + 2], csx, 0.f, qsx, 0.f};
+        s_seg[ns++] = Seg{csx, mL, qsx, 0.f, plo, phi, base, g1, g1};
+        s_seg[ns++] = Seg{csx, 0.f, qsx, 0.f, plo, phi, base, 0, 1};
       } else {                                       // rows G-2, G-1 | 0
-        s_seg[ns++] = Seg{cs[base + P.G - 2], cs[base + P.G], csx, 0.f, qsx, 0.f};
-        s_seg[ns++] = Seg{cs[base], cs[base + 1], csx, 0.f, qsx, mL};
+        s_seg[ns++] = Seg{csx, 0.f, qsx, 0.f, plo, phi, base, P.G - 2, g1};
+        s_seg[ns++] = Seg{csx, 0.f, qsx, mL, plo, phi, base, 0, 0};
       }
     }
     s_nseg = ns;
@@ -580,14 +678,17 @@ __global__ void __launch_bounds__(kSenseWarps * 32, kSenseMinBlocks) k_sense(
       if (yy < 0) { yy += P.G; csy = mL; }           // candidate row G-1 seen from row 0
       if (yy >= P.G) { yy -= P.G; qsy = mL; }        // candidate row 0 seen from row G-1
       const int row = yy * P.G;
+      const float plo = (float)yy * P.cell + csy - P.win_margin;
+      const float phi = (float)(yy + 1) * P.cell + csy + P.win_margin;
+      const int g1 = P.G - 1;
       if (cx >= 1 && cx <= P.G - 2) {
-        s_seg[ns++] = Seg{cs[row + cx - 1], cs[row + cx + 2], 0.f, csy, 0.f, qsy};
+        s_seg[ns++] = Seg{0.f, csy, 0.f, qsy, plo, phi, row, cx - 1, cx + 1};
       } else if (cx == 0) {                          // cells G-1 | 0, 1
-        s_seg[ns++] = Seg{cs[row + P.G - 1], cs[row + P.G], mL, csy, 0.f, qsy};
-        s_seg[ns++] = Seg{cs[row], cs[row + 2], 0.f, csy, 0.f, qsy};
+        s_seg[ns++] = Seg{mL, csy, 0.f, qsy, plo, phi, row, g1, g1};
+        s_seg[ns++] = Seg{0.f, csy, 0.f, qsy, plo, phi, row, 0, 1};
       } else {                                       // cells G-2, G-1 | 0
-        s_seg[ns++] = Seg{cs[row + P.G - 2], cs[row + P.G], 0.f, csy, 0.f, qsy};
-        s_seg[ns++] = Seg{cs[row], cs[row + 1], 0.f, csy, mL, qsy};
+        s_seg[ns++] = Seg{0.f, csy, 0.f, qsy, plo, phi, row, P.G - 2, g1};
+        s_seg[ns++] = Seg{0.f, csy, mL, qsy, plo, phi, row, 0, 0};
       }
     }
     s_nseg = ns;
@@ -604,6 +705,12 @@ __global__ void __launch_bounds__(kSenseWarps * 32, kSenseMinBlocks) k_sense(
   // and loop step is shared; each query has its own ballot, queue, sector row and
   // accumulators.  A missing query gets a NaN position (never a neighbour).
   constexpr int NQ = kSenseNQ;
+  // Pair-pass constants pinned in registers (otherwise re-loaded per pair batch).
+  float c_contact2 = P.contact2, c_mcollide = -P.c_collide, c_k_rise = P.k_rise,
+        c_b_rise = P.b_rise, c_nk_fall = P.nk_fall, c_b_fall = P.b_fall, c_inv_fov = P.inv_fov,
+        c_fv = P.fv, c_inv_dv = P.inv_dv;
+  asm volatile("" : "+f"(c_contact2), "+f"(c_mcollide), "+f"(c_k_rise), "+f"(c_b_rise),
+               "+f"(c_nk_fall), "+f"(c_b_fall), "+f"(c_inv_fov), "+f"(c_fv), "+f"(c_inv_dv));
   const uint32_t qstride = NQ * kSenseWarps * gridDim.y;
   for (uint32_t q0 = qb + NQ * (blockIdx.y * kSenseWarps + warp); q0 < qe; q0 += qstride) {
     float4 me[NQ];
@@ -637,16 +744,16 @@ __global__ void __launch_bounds__(kSenseWarps * 32, kSenseMinBlocks) k_sense(
     // Pair pass over one queue entry (dx, dy, d^2, index | type << 31) of query t.
     auto process = [&](const int t, const float4 e) {
       const uint32_t tagbits = __float_as_uint(e.w);
-      if ((tagbits & 0x7fffffffu) == q0 + t) return;                 // j != i
-      const uint32_t tj = tagbits >> 31;
+      if (ENV == kFlock ? tagbits == q0 + t : (tagbits & 0x7fffffffu) == q0 + t) return;  // j != i
+      const uint32_t tj = (ENV == kTag) ? tagbits >> 31 : 0u;
       const float d2 = e.z;
-      const bool contact = d2 <= P.contact2;                          // A6 (inclusive)
+      const bool contact = d2 <= c_contact2;                          // A6 (inclusive)
       float rsq;                                   // MUFU.RSQ without the subnormal rescale:
       asm("rsqrt.approx.ftz.f32 %0, %1;" : "=f"(rsq) : "f"(d2));
       const float d = (d2 >= 1.17549435e-38f) ? d2 * rsq : 0.f;   // subnormal d^2 -> d = 0
       // Eq. 1 / Fig. 4 (A5): contact -> -c_collide, else the tent min(rise, fall).
-      const float f = contact ? -P.c_collide
-                              : fminf(fmaf(P.k_rise, d, P.b_rise), fmaf(P.nk_fall, d, P.b_fall));
+      const float f = contact ? c_mcollide
+                              : fminf(fmaf(c_k_rise, d, c_b_rise), fmaf(c_nk_fall, d, c_b_fall));
       if (!RAY || d2 < P.dv2) {                                       // Eq. 1: d < d_v
         if (RAY) ++nnb[t];
         if (ENV == kFlock) {
@@ -702,10 +809,10 @@ __global__ void __launch_bounds__(kSenseWarps * 32, kSenseMinBlocks) k_sense(
         // Bearing in the agent frame (A3): phi = atan2(h x d, h . d), CCW-positive.
         const float fwd = fmaf(csn[t], e.x, sn[t] * e.y);
         const float left = fmaf(csn[t], e.y, -sn[t] * e.x);
-        const float u = fmaf(vg_atan2(left, fwd), P.inv_fov, 0.5f);   // fraction of the fov
+        const float u = fmaf(vg_atan2(left, fwd), c_inv_fov, 0.5f);   // fraction of the fov
         if (u >= 0.f && u < 1.f) {
-          const int k = min((int)(u * P.fv), P.v - 1);
-          const float val = fminf(d * P.inv_dv, kBelowOne);
+          const int k = min((int)(u * c_fv), P.v - 1);
+          const float val = fminf(d * c_inv_dv, kBelowOne);
           atomicMin(&s_min[warp][t][tj * P.v + k], __float_as_uint(val));
         }
       }
@@ -719,10 +826,37 @@ __global__ void __launch_bounds__(kSenseWarps * 32, kSenseMinBlocks) k_sense(
         qx[t] = me[t].x + sg.qsx;                                     // exact (Sterbenz)
         qy[t] = me[t].y + sg.qsy;
       }
-      for (uint32_t p0 = sg.b; p0 < sg.e; p0 += 64) {
+      // Window of this run: the queries' distance across the run axis bounds
+      // the reach along it, sqrt(r^2 - dperp^2); keys in the candidates' raw frame.  A dead
+      // query (NaN) drops out of fminf / fmaxf (dperp -> 0: only ever wider).
+      float amin = SLAB ? qy[0] : qx[0], amax = amin, dperp = 3.0e38f;
+#pragma unroll
+      for (int t = 0; t < NQ; ++t) {
+        const float aq = SLAB ? qy[t] : qx[t], pq = SLAB ? qx[t] : qy[t];
+        amin = fminf(amin, aq);
+        amax = fmaxf(amax, aq);
+        dperp = fminf(dperp, fmaxf(fmaxf(sg.plo - pq, pq - sg.phi), 0.f));
+      }
+      const float h2 = fmaf(-dperp, dperp, P.win_r2);
+      if (!(h2 > 0.f)) continue;                                     // run out of reach
+      float wdt;
+      asm("sqrt.approx.ftz.f32 %0, %1;" : "=f"(wdt) : "f"(h2));
+      wdt += P.win_margin;
+      const float csa = SLAB ? sg.csy : sg.csx;
+      // Sub-bin lookups (K3b table): from the sub-bin holding klo to the one holding khi,
+      // clamped to the run's cells; the same monotone formula as sub_bin().
+      const float ulo = __fmul_rn(amin - csa - wdt, P.gs), uhi = __fmul_rn(amax - csa + wdt, P.gs);
+      const int ca_lo = min(max(__float2int_rd(ulo), sg.a0), sg.a1);
+      const int ca_hi = min(max(__float2int_rd(uhi), sg.a0), sg.a1);
+      const int g_lo = kSub * ca_lo + min(max(__float2int_rd(ulo * (float)kSub) - kSub * ca_lo, 0), kSub - 1);
+      const int g_hi = kSub * ca_hi + min(max(__float2int_rd(uhi * (float)kSub) - kSub * ca_hi, 0), kSub - 1);
+      const uint32_t* tb = sub_tab + (size_t)((SLAB ? 0 : r * P.G2) + sg.cbase) * kSub;
+      const uint32_t wb = __ldg(&tb[g_lo]);
+      const uint32_t we = __ldg(&tb[g_hi + 1]);
+      for (uint32_t p0 = wb; p0 < we; p0 += 64) {
         const uint32_t pa = p0 + lane, pb = p0 + 32 + lane;
-        const bool va = pa < sg.e, vb = pb < sg.e;
-        const bool two = p0 + 32 < sg.e;                             // warp-uniform
+        const bool va = pa < we, vb = pb < we;
+        const bool two = p0 + 32 < we;                               // warp-uniform
         float ax, ay, bx, by;
         uint32_t ta = 0u, tb = 0u;
         if (ENV == kFlock) {                 // sorted_xy is padded by 64: no predicate
@@ -754,10 +888,10 @@ __global__ void __launch_bounds__(kSenseWarps * 32, kSenseMinBlocks) k_sense(
         };
         scan(ax, ay, pa | ta);
         if (two) scan(bx, by, pb | tb);
+        __syncwarp();                       // ring pushes above are visible to the warp
 #pragma unroll
         for (int t = 0; t < NQ; ++t) {
           while (tail[t] - head[t] >= 32u * 16u) {
-            __syncwarp();
             process(t, lds128(qbase[t] | ((head[t] + lane * 16u) & (kQueue * 16 - 16))));
             head[t] += 32u * 16u;
           }

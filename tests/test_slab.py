@@ -126,10 +126,10 @@ def _compare_group(p, P, steps, state0, seed=0, halo=0):
                 a = getattr(o, k)[0, :n]
                 b = getattr(out_r, k)[0][ids]
                 assert torch.equal(a.view(torch.int32), b.view(torch.int32)), f"{tag}: {k} differs (P={P})"
-            oid, ost = w.slab_owned()
-            assert torch.equal(oid.long(), ids)
+            oid, ost = w.slab_owned()            # (cell, id) order; output rows: sense order
+            assert torch.equal(torch.sort(oid.long()).values, torch.sort(ids).values)
             cols = 4 if p.env == "flock" else 3
-            assert torch.equal(ost[:, :cols], st[0][ids][:, :cols]), f"{tag}: state differs"
+            assert torch.equal(ost[:, :cols], st[0][oid.long()][:, :cols]), f"{tag}: state differs"
         assert torch.equal(seen, torch.ones_like(seen)), "every agent owned exactly once"
 
     check("load")
