@@ -177,6 +177,29 @@ def test_dyadic_world_bit_exact_thresholds(cuda):
     w.close()
 
 
+@pytest.mark.parametrize("vision", ["sector", "ray"])
+def test_window_rim_neighbours(cuda, vision):
+    # K4 cuts each stencil run to a candidate window: neighbours on the rim
+    # of the view disc, at wrap edges and in the adjacent rows must all still be found.
+    torch = _torch()
+    p = vi.flock_params(3000, width=100.0, d_v=10.0, vision=vision)
+    st = vi.rim_state(p, 60, seed=9, radius=p.d_v + (p.d_r if vision == "ray" else 0.0))
+    w = make_world(p)
+    out = w.alloc_outputs()
+    w.bin(dev(st))
+    w.sense(out)
+    torch.cuda.synchronize()
+    rows = np.arange(60 * 17)                       # the queries and their rim neighbours
+    if vision == "ray":
+        import test_gpu_ray as tr
+        tr._check(p, outs_np(out, 0), st[0], rows)
+    else:
+        parity.check_sense(p, st[0], outs_np(out, 0), rows=rows)
+    if vision == "sector":
+        assert (host(out.n_neigh)[0][:60] >= 16).all()   # every ring member is in range
+    w.close()
+
+
 def test_reward_kernel_matches_sense(cuda):
     torch = _torch()
     for p in (vi.workload("c2"), vi.tag_params(3000, width=60.0)):

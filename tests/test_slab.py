@@ -156,6 +156,15 @@ def test_slab_bit_identical_flock(cuda, P):
 
 
 @pytest.mark.gpu
+@pytest.mark.parametrize("P", [2, 4])
+def test_slab_window_rim(cuda, P):
+    # K4 windows run along columns in slab mode: rim neighbours (vi.rim_state) at slab and
+    # wrap edges must give the single-world result bit for bit.
+    p = vi.flock_params(6000, width=170.0, d_v=10.0, grid=16)
+    _compare_group(p, P, 2, vi.rim_state(p, 150, seed=5, radius=p.d_v))
+
+
+@pytest.mark.gpu
 @pytest.mark.parametrize("P", [2, 3])
 def test_slab_bit_identical_tag(cuda, P):
     p = vi.tag_params(12000, width=120.0, d_v=10.0, grid=9 if P == 3 else 8)

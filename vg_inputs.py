@@ -270,3 +270,26 @@ def opinion_graph_fast(n: int, degree: int, seed: int = 0) -> dict:
             "col": dst.reshape(-1).astype(np.int32),
             "weight": rng.random(n * degree).astype(np.float32),
             "op": rng.random(n).astype(np.float32)}
+
+
+def rim_state(p: EnvParams, n_q: int, seed: int, radius: float) -> np.ndarray:
+    """Queries (a third of them within d_v of a wrap edge) each ringed by 16 neighbours just
+    inside the view radius (d = d_v (1 - 1e-4)), plus uniform background agents: every
+    window edge of K4 (along the run axis and at the chord limit of the adjacent rows) is hit."""
+    rng = np.random.default_rng(seed)
+    L = p.width
+    q = rng.random((n_q, 2)) * L
+    edge = rng.random(n_q) < 1 / 3
+    axis = rng.integers(0, 2, n_q)
+    for ax in (0, 1):
+        m = edge & (axis == ax)
+        q[m, ax] = rng.choice([0.3, L - 0.3], m.sum()) + rng.normal(0, 0.1, m.sum())
+    ang = rng.random((n_q, 1)) * 2 * np.pi + np.arange(16)[None, :] * (2 * np.pi / 16)
+    rim = q[:, None, :] + radius * (1 - 1e-4) * np.stack([np.cos(ang), np.sin(ang)], -1)
+    pts = np.concatenate([q, rim.reshape(-1, 2)])
+    pts = np.concatenate([pts, rng.random((p.n_agents - len(pts), 2)) * L]) % L
+    st = np.zeros((1, p.n_agents, 4), np.float32)
+    st[0, :, :2] = pts.astype(np.float32) % np.float32(L)
+    st[0, :, 2] = (rng.random(p.n_agents) * 6.28).astype(np.float32)
+    st[0, :, 3] = 0.275
+    return st
