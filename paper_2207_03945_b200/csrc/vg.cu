@@ -325,8 +325,25 @@ int sense_chunks(const vg_world* w) {
   return (int)std::max(1LL, std::min(ch, 1024LL));
 }
 
+// K4's candidate reads hit L1: cap the shared-memory carve-out so the resident CTAs' shared
+// memory leaves L1 room.  Set once per kernel instance.
+#ifndef VG_SENSE_CARVEOUT
+#define VG_SENSE_CARVEOUT 86
+#endif
+template <typename K>
+void sense_carveout(K* k) {
+  if (VG_SENSE_CARVEOUT >= 0)
+    cudaFuncSetAttribute(k, cudaFuncAttributePreferredSharedMemoryCarveout, VG_SENSE_CARVEOUT);
+}
+
 template <int ENV, bool VISION, bool SLAB>
 void sense_kernel(vg_world* w, dim3 grid, const vg::Outs& O, cudaStream_t s) {
+  static bool once = [] {
+    sense_carveout(vg::k_sense<ENV, VISION, SLAB, true>);
+    sense_carveout(vg::k_sense<ENV, VISION, SLAB, false>);
+    return true;
+  }();
+  (void)once;
   if (w->cfg.vision == VG_VISION_RAY)
     vg::k_sense<ENV, VISION, SLAB, true><<<grid, vg::kSenseWarps * 32, 0, s>>>(
         w->P, w->cell_start, w->xo_rec, w->xo_xy, w->xo_perm, O, w->SL, w->ray_dir, w->sub_tab);

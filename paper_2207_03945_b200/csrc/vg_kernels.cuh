@@ -560,12 +560,21 @@ __global__ void __launch_bounds__(kRBThreads, 2) k_replica_bin(
 #define VG_SENSE_NQ 2
 #endif
 #ifndef VG_SENSE_MINB
-#define VG_SENSE_MINB 6
+#define VG_SENSE_MINB 7
 #endif
-constexpr int kSenseWarps = 4;
+#ifndef VG_SENSE_WARPS
+#define VG_SENSE_WARPS 4
+#endif
+constexpr int kSenseWarps = VG_SENSE_WARPS;
 constexpr int kSenseNQ = VG_SENSE_NQ;         // queries sensed together by one warp
 constexpr int kSenseMinBlocks = VG_SENSE_MINB;  // resident CTAs per SM
-constexpr int kQueue = 128;         // ring (power of 2) >= 31 carried + 2 x 32 pushed
+// Ring (power of 2): >= 31 carried + 64 pushed, and large enough that one chunk's pushes
+// never reach the slots the previous drain read (carried + 64 + 2 x 32 <= kQueue), so one
+// warp sync per chunk (before the drain) orders all ring traffic.
+#ifndef VG_SENSE_QUEUE
+#define VG_SENSE_QUEUE 128
+#endif
+constexpr int kQueue = VG_SENSE_QUEUE;
 
 // atan2(y, x) in (-pi, pi] with |error| <~ 2.5e-7 rad: octant reduction,
 // t = min/max by the hardware reciprocal, degree-8 minimax polynomial in t^2 for atan(t)/t
@@ -818,41 +827,56 @@ __global__ void __launch_bounds__(kSenseWarps * 32, kSenseMinBlocks) k_sense(
       }
     };
 
+    // Run windows, lane-parallel: lane i < nseg computes run i's candidate window
+    // [wb, we) once per warp-iteration: the queries' distance dperp across the
+    // run axis bounds the reach along it to sqrt(r^2 - dperp^2); keys in the candidates' raw
+    // frame.  A dead query (NaN) drops out of fminf / fmaxf (dperp -> 0: only ever wider).
+    uint32_t my_wb = 0u, my_we = 0u;
+    float my_csx = 0.f, my_csy = 0.f, my_qsx = 0.f, my_qsy = 0.f;
+    if (lane < nseg) {
+      const Seg sg = s_seg[lane];
+      my_csx = sg.csx; my_csy = sg.csy; my_qsx = sg.qsx; my_qsy = sg.qsy;
+      float amin = 3.0e38f, amax = -3.0e38f, dperp = 3.0e38f;
+#pragma unroll
+      for (int t = 0; t < NQ; ++t) {
+        const float qxs = me[t].x + sg.qsx, qys = me[t].y + sg.qsy;   // exact (Sterbenz)
+        const float aq = SLAB ? qys : qxs, pq = SLAB ? qxs : qys;
+        amin = fminf(amin, aq);
+        amax = fmaxf(amax, aq);
+        dperp = fminf(dperp, fmaxf(fmaxf(sg.plo - pq, pq - sg.phi), 0.f));
+      }
+      const float h2 = fmaf(-dperp, dperp, P.win_r2);
+      if (h2 > 0.f) {                                                // else out of reach
+        float wdt;
+        asm("sqrt.approx.ftz.f32 %0, %1;" : "=f"(wdt) : "f"(h2));
+        wdt += P.win_margin;
+        const float csa = SLAB ? sg.csy : sg.csx;
+        // Sub-bin lookups (K3b table): from the sub-bin holding klo to the one holding khi,
+        // clamped to the run's cells; the same monotone formula as sub_bin().
+        const float ulo = __fmul_rn(amin - csa - wdt, P.gs), uhi = __fmul_rn(amax - csa + wdt, P.gs);
+        const int ca_lo = min(max(__float2int_rd(ulo), sg.a0), sg.a1);
+        const int ca_hi = min(max(__float2int_rd(uhi), sg.a0), sg.a1);
+        const int g_lo = kSub * ca_lo + min(max(__float2int_rd(ulo * (float)kSub) - kSub * ca_lo, 0), kSub - 1);
+        const int g_hi = kSub * ca_hi + min(max(__float2int_rd(uhi * (float)kSub) - kSub * ca_hi, 0), kSub - 1);
+        const uint32_t* tb = sub_tab + (size_t)((SLAB ? 0 : r * P.G2) + sg.cbase) * kSub;
+        my_wb = __ldg(&tb[g_lo]);
+        my_we = __ldg(&tb[g_hi + 1]);
+      }
+    }
     for (int sgi = 0; sgi < nseg; ++sgi) {
-      const Seg sg = s_seg[sgi];
+      const uint32_t wb = __shfl_sync(kFull, my_wb, sgi), we = __shfl_sync(kFull, my_we, sgi);
+      if (wb >= we) continue;                                        // warp-uniform
+      Seg sg;
+      sg.csx = __shfl_sync(kFull, my_csx, sgi);
+      sg.csy = __shfl_sync(kFull, my_csy, sgi);
+      sg.qsx = __shfl_sync(kFull, my_qsx, sgi);
+      sg.qsy = __shfl_sync(kFull, my_qsy, sgi);
       float qx[NQ], qy[NQ];
 #pragma unroll
       for (int t = 0; t < NQ; ++t) {
         qx[t] = me[t].x + sg.qsx;                                     // exact (Sterbenz)
         qy[t] = me[t].y + sg.qsy;
       }
-      // Window of this run: the queries' distance across the run axis bounds
-      // the reach along it, sqrt(r^2 - dperp^2); keys in the candidates' raw frame.  A dead
-      // query (NaN) drops out of fminf / fmaxf (dperp -> 0: only ever wider).
-      float amin = SLAB ? qy[0] : qx[0], amax = amin, dperp = 3.0e38f;
-#pragma unroll
-      for (int t = 0; t < NQ; ++t) {
-        const float aq = SLAB ? qy[t] : qx[t], pq = SLAB ? qx[t] : qy[t];
-        amin = fminf(amin, aq);
-        amax = fmaxf(amax, aq);
-        dperp = fminf(dperp, fmaxf(fmaxf(sg.plo - pq, pq - sg.phi), 0.f));
-      }
-      const float h2 = fmaf(-dperp, dperp, P.win_r2);
-      if (!(h2 > 0.f)) continue;                                     // run out of reach
-      float wdt;
-      asm("sqrt.approx.ftz.f32 %0, %1;" : "=f"(wdt) : "f"(h2));
-      wdt += P.win_margin;
-      const float csa = SLAB ? sg.csy : sg.csx;
-      // Sub-bin lookups (K3b table): from the sub-bin holding klo to the one holding khi,
-      // clamped to the run's cells; the same monotone formula as sub_bin().
-      const float ulo = __fmul_rn(amin - csa - wdt, P.gs), uhi = __fmul_rn(amax - csa + wdt, P.gs);
-      const int ca_lo = min(max(__float2int_rd(ulo), sg.a0), sg.a1);
-      const int ca_hi = min(max(__float2int_rd(uhi), sg.a0), sg.a1);
-      const int g_lo = kSub * ca_lo + min(max(__float2int_rd(ulo * (float)kSub) - kSub * ca_lo, 0), kSub - 1);
-      const int g_hi = kSub * ca_hi + min(max(__float2int_rd(uhi * (float)kSub) - kSub * ca_hi, 0), kSub - 1);
-      const uint32_t* tb = sub_tab + (size_t)((SLAB ? 0 : r * P.G2) + sg.cbase) * kSub;
-      const uint32_t wb = __ldg(&tb[g_lo]);
-      const uint32_t we = __ldg(&tb[g_hi + 1]);
       for (uint32_t p0 = wb; p0 < we; p0 += 64) {
         const uint32_t pa = p0 + lane, pb = p0 + 32 + lane;
         const bool va = pa < we, vb = pb < we;
@@ -896,7 +920,7 @@ __global__ void __launch_bounds__(kSenseWarps * 32, kSenseMinBlocks) k_sense(
             head[t] += 32u * 16u;
           }
         }
-        __syncwarp();                       // ring slots read above may be rewritten next
+        if (kQueue < 160) __syncwarp();     // small ring: drained slots may be rewritten next
       }
     }
     __syncwarp();
