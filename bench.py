@@ -203,6 +203,52 @@ def run_reference(args):
     return 0
 
 
+# --------------------------------------------------------------------- sanity (§8d)
+def closed_forms(p) -> dict:
+    """Per-agent expectations for iid uniform positions on the torus (d_v < L/2), the
+    SURVEY §8d sanity table: E[n_neigh], E[n_collide], E[reward] (flock, Eq. 1 with the A5
+    tent f) with Poisson variances, and P(sector occupied).  Bench-side host arithmetic on
+    the configuration only (numerical quadrature of f), not the oracle."""
+    rho = (p.n_agents - 1) / p.width ** 2
+    d = np.linspace(0.0, p.d_v, 400001)[1:-1]
+    two_dr = 2 * p.d_r
+    f = np.where(d <= two_dr, -p.c_collide,
+                 np.where(d <= p.d_peak, p.c_near * (d - two_dr) / (p.d_peak - two_dr),
+                          p.c_near * (p.d_v - d) / (p.d_v - p.d_peak)))
+    dd = d[1] - d[0]
+    m1 = float(np.sum(f * 2 * np.pi * d) * dd)
+    m2 = float(np.sum(f * f * 2 * np.pi * d) * dd)
+    e_nn = rho * np.pi * p.d_v ** 2
+    e_nc = rho * np.pi * two_dr ** 2
+    a_sec = (p.fov / p.v) * p.d_v ** 2 / (2 * p.width ** 2)
+    p_occ = 1 - (1 - a_sec) ** (p.n_agents - 1)
+    return {"n_neigh": (e_nn, e_nn), "n_collide": (e_nc, e_nc), "reward": (rho * m1, rho * m2),
+            "occupied": (p_occ, p_occ * (1 - p_occ))}
+
+
+def sanity(p, out, rows, torch) -> dict:
+    """Measured per-agent means of the last step vs closed_forms, with z-scores (sigma of the
+    mean from the per-agent variance; agents are weakly correlated, so |z| <~ 5 is fine)."""
+    cf = closed_forms(p)
+    o = out
+    nv = (1 if p.env == "flock" else 2) * p.v
+    meas = {"n_neigh": o.n_neigh.view(-1)[:rows].double().mean().item()}
+    if p.env == "flock":                  # tag: n_collide / reward follow the type rules
+        meas["n_collide"] = o.n_collide.view(-1)[:rows].double().mean().item()
+        meas["reward"] = o.reward.view(-1)[:rows].double().mean().item()
+    if o.obs is not None and p.env == "flock":
+        view = o.obs.view(-1, o.obs.shape[-1])[:rows, :nv]
+        meas["occupied"] = (view < 1.0).double().mean().item()
+    res = {}
+    for k, m in meas.items():
+        e, var = cf[k]
+        n = rows * (nv if k == "occupied" else 1)
+        z = (m - e) / math.sqrt(var / n) if var > 0 else 0.0
+        res[k] = {"measured": m, "closed_form": e, "z": z}
+    res["ok"] = all(abs(v["z"]) < 5 for v in res.values() if isinstance(v, dict))
+    return res
+
+
 # ---------------------------------------------------------------------------- our leg
 class ReplicaRunner:
     """Replica workloads (and c5 at N = 1): one libvg world per rank, vg_step."""
@@ -325,6 +371,10 @@ def run_ours(args):
     agents_all = p.n_agents if slab_mode else p.total_agents * world
     value = agents_all * K / (max_ms / 1e3)
     pairs_local = run.pairs_local()            # in-radius pairs of the last step (this rank)
+    san = None
+    if args.vision == "sector" and args.config in ("c2", "c3", "c4", "c5"):
+        rows = run.w.slab_own_count() if slab_mode else p.total_agents
+        san = sanity(p, run.out, rows, torch)
 
     # ---- end to end through the public API with host buffers
     e2e = None
@@ -526,6 +576,7 @@ def run_ours(args):
                                   f"in-radius pairs per launch / mean k_sense time; peak = "
                                   f"148 SM x 128 lanes x {sm_mhz:.0f} MHz (1 op/lane/clk)"},
             "stages": stages,
+            "sanity": san,
             "hbm_peak_gbs": hbm, "peak_source": peak_src,
             "e2e": e2e,
             "gpu_launches": run.launches * K,
