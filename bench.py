@@ -540,13 +540,20 @@ def run_ours(args):
                 "GBps": round(gbs, 1) if gbs else None,
                 "hbm_frac": round(gbs / hbm, 4) if gbs else None,
                 "share": round(ms / tot_ph, 4)}
-        traffic = None
+        traffic, issue = None, None
         tpath = os.path.join(ROOT, "profiles", "sense_traffic.json")
         if os.path.exists(tpath) and world == 1:
             try:
                 tj = json.load(open(tpath))
-                if tj.get("config") == args.config:
+                if tj.get("config") == args.config and args.vision == "sector":
                     traffic = tj.get("bytes_per_launch")
+                    wi = tj.get("warp_instructions")
+                    if wi:
+                        # issue-slot roofline of the same launch: warp instructions (ncu,
+                        # committed) / (live mean k_sense time x 148 SM x 4 issue/clk x clk)
+                        cap = 148 * 4 * sm_mhz * 1e6 * sense_s
+                        issue = {"warp_instructions": wi, "frac": wi / cap,
+                                 "peak": "148 SM x 4 schedulers x 1 warp-instr/clk"}
             except Exception:
                 pass
         cpu = None
@@ -571,7 +578,7 @@ def run_ours(args):
                        "l2": "256 MiB buffer written between timed steps (outside events)"},
             "roofline": {"kernel": "k_sense (sector vision + reward)", "bound": "alu",
                          "achieved": achieved, "peak": alu_peak, "unit": "TFLOP/s",
-                         "frac": achieved / alu_peak, "traffic": traffic,
+                         "frac": achieved / alu_peak, "traffic": traffic, "issue": issue,
                          "basis": f"{ALG_OPS_PER_PAIR} fp32 ops x {pairs_local:.4g} "
                                   f"in-radius pairs per launch / mean k_sense time; peak = "
                                   f"148 SM x 128 lanes x {sm_mhz:.0f} MHz (1 op/lane/clk)"},
