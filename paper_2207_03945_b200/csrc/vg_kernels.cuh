@@ -576,9 +576,10 @@ constexpr int kSenseMinBlocks = VG_SENSE_MINB;  // resident CTAs per SM
 #endif
 constexpr int kQueue = VG_SENSE_QUEUE;
 
-// atan2(y, x) in (-pi, pi] with |error| <~ 2.5e-7 rad: octant reduction,
-// t = min/max by the hardware reciprocal, degree-8 minimax polynomial in t^2 for atan(t)/t
-// on [0, 1] (max error 9e-8 in fp32), then the quadrant fix-ups; atan2(+-0, +-0) = +-0.
+// atan2(y, x) in (-pi, pi] with |error| <~ 3.3e-7 rad (the sector band is
+// 1e-6 fov = 4.4e-6 rad): octant reduction, t = min/max by the hardware reciprocal, a
+// degree-6 minimax polynomial in t^2 for atan(t)/t on [0, 1] (fit error 2.5e-7), then the
+// quadrant fix-ups; atan2(+-0, +-0) = +-0.
 __device__ __forceinline__ float vg_atan2(float y, float x) {
   const float ax = fabsf(x), ay = fabsf(y);
   const float mx = fmaxf(ax, ay), mn = fminf(ax, ay);
@@ -586,15 +587,13 @@ __device__ __forceinline__ float vg_atan2(float y, float x) {
   asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(rc) : "f"(mx));       // <= 1 ulp
   const float t = (mx > 0.f) ? mn * rc : 0.f;
   const float s = t * t;
-  float p = 0.0024567253421992064f;
-  p = fmaf(p, s, -0.01440136507153511f);
-  p = fmaf(p, s, 0.03978124260902405f);
-  p = fmaf(p, s, -0.07234859466552734f);
-  p = fmaf(p, s, 0.10498947650194168f);
-  p = fmaf(p, s, -0.14161229133605957f);
-  p = fmaf(p, s, 0.19985906779766083f);
-  p = fmaf(p, s, -0.33332598209381104f);
-  p = fmaf(p, s, 0.9999998807907104f);
+  float p = 0.006812420208007097f;
+  p = fmaf(p, s, -0.03360610455274582f);
+  p = fmaf(p, s, 0.07962583005428314f);
+  p = fmaf(p, s, -0.13233458995819092f);
+  p = fmaf(p, s, 0.198078453540802f);
+  p = fmaf(p, s, -0.3331737220287323f);
+  p = fmaf(p, s, 0.9999961256980896f);
   float r = p * t;
   r = (ay > ax) ? (1.5707963705062866f - r) : r;
   r = (x < 0.f) ? (3.1415927410125732f - r) : r;
