@@ -122,6 +122,15 @@ def test_c5_full_size_sampled_rows(cuda):
     w.close()
 
 
+@pytest.mark.parametrize("fov,v", [(2 * math.pi, 128), (0.5, 128), (1.0, 7), (4.36, 64)])
+def test_sector_model_variants(cuda, fov, v):
+    # fov = 2 pi (the seam at phi = pi), narrow sectors (atan2 path: sector-table bins would
+    # hold two boundaries), few wide sectors, tag-like v = 64: every sector decision agrees
+    # with the oracle up to the bands.
+    p = vi.flock_params(2500, width=70.0, d_v=7.0, fov=np.float32(fov), v=v)
+    run_and_check(p, vi.init_state(p, seed=11), 2)
+
+
 @pytest.mark.parametrize("case", ["lone", "pair", "sparse", "g3", "many_replicas",
                                   "clustered", "tag_no_chasers", "tag_all_chasers"])
 def test_edge_cases(cuda, case):
