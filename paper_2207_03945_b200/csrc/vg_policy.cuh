@@ -5,7 +5,10 @@
 // tanh hidden, linear out, state-independent log_std); S:355-372 Gaussian sample, clip to
 // the action box, log-prob of the unclipped sample.  SURVEY.md §8f NEXT #1.
 //
-// Tile of 128 agents per step of a persistent CTA (one per SM, 16 warps):
+// Tiles of 128 agents; a persistent CTA (one per SM, 16 warps) runs two tiles at once: warp
+// group g (8 warps) owns every other tile of the CTA, its own A operand buffer and its own
+// 256 TMEM columns, so one group's MMAs, TMA waits and epilogues overlap the other's.
+// Per tile:
 //   layer 1  D[128 x 128] = A1[128 x 144] . B1^T   (actor | critic hidden, fp16 in, fp32 acc)
 //   layer 2  D[128 x 128] = A2[128 x 128] . B2^T   (B2 block-diagonal: actor | critic)
 //   layer 3  D[128 x 16]  = A3[128 x 128] . B3^T   (rows of B3: W3[0], W3[1], V3, zeros)
@@ -13,7 +16,9 @@
 // Operands live in shared memory in the canonical K-major no-swizzle layout (8 x 16-byte
 // core matrices: SBO = 128 B between 8-row groups, LBO = R x 16 B between 8-column groups),
 // tcgen05.mma is issued by one thread, the fp32 accumulator lives in TMEM (128 columns) and
-// is read back with tcgen05.ld.32x32b (warp w reads TMEM lanes 32 (w % 4) ..).
+// is read back with tcgen05.ld.32x32b (warp w reads TMEM lanes 32 (w % 4) ..).  One fp32
+// staging buffer receives each tile by TMA; the group that owns the tile converts it to its
+// fp16 operand and then issues the TMA of the CTA's next tile (the other group's).
 #pragma once
 
 #include <cstdint>
@@ -28,19 +33,21 @@ constexpr int kPolN = 128;         // actor | critic concatenated (MMA N)
 constexpr int kPolK1 = 144;        // obs_dim padded to a multiple of 16 (<= 144)
 constexpr int kPolK2 = 128;        // hidden actor | critic
 constexpr int kPolN3 = 16;         // layer-3 MMA N: mean_0, mean_1, value, 13 zero rows
-constexpr int kPolThreads = 512;   // 16 warps: TMEM lane quadrant (w % 4) x 32-column group (w / 4)
+constexpr int kPolThreads = 512;   // 2 groups x 8 warps: TMEM lane quadrant (w % 4) x column half
+constexpr int kPolGroup = 256;     // threads per group
 
-// Shared-memory carve-up (bytes).  A3 (layer-3 operand) aliases A1, free once MMA1 is done.
+// Shared-memory carve-up (bytes).  Per group one operand buffer A: A1 (layer 1), A2 and A3
+// all alias it — each is written only after the MMA reading the previous one has completed.
 constexpr int kOffB1 = 0;
 constexpr int kOffB2 = kOffB1 + kPolN * kPolK1 * 2;        // 36864
 constexpr int kOffB3 = kOffB2 + kPolN * kPolK2 * 2;        // +32768
-constexpr int kOffA1 = kOffB3 + kPolN3 * kPolK2 * 2;       // +4096
-constexpr int kOffA2 = kOffA1 + kPolTile * kPolK1 * 2;     // +36864
-constexpr int kOffC = kOffA2 + kPolTile * kPolK2 * 2;      // +32768 : fp32 constants
+constexpr int kOffA = kOffB3 + kPolN3 * kPolK2 * 2;        // +4096: A[0], A[1]
+constexpr int kABytes = kPolTile * kPolK1 * 2;             // 36864
+constexpr int kOffC = kOffA + 2 * kABytes;                 // fp32 constants
 // consts: b1[128] b2[128] | b3_0 b3_1 c3 pad | log_std[2] | lo[2] hi[2]
 constexpr int kConstFloats = 128 + 128 + 4 + 2 + 4;
-constexpr int kOffBar = kOffC + ((kConstFloats * 4 + 15) / 16) * 16;   // 2 mbarriers + tmem slot
-constexpr int kOffStage = ((kOffBar + 32 + 127) / 128) * 128;            // raw fp32 obs tile (TMA)
+constexpr int kOffBar = kOffC + ((kConstFloats * 4 + 15) / 16) * 16;   // 4 mbarriers + tmem slot
+constexpr int kOffStage = ((kOffBar + 48 + 127) / 128) * 128;            // raw fp32 obs tile (TMA)
 constexpr int kStageBytes = kPolTile * kPolK1 * 4;                       // >= 128 rows x obs_dim
 constexpr int kPolSmem = kOffStage + kStageBytes;
 
@@ -206,6 +213,10 @@ __global__ void k_policy_pack(int obs_dim, const float* __restrict__ W1, const f
   }
 }
 
+__device__ __forceinline__ void group_sync(int g) {      // named barrier of one warp group
+  asm volatile("bar.sync %0, %1;" ::"r"(1 + g), "r"(kPolGroup) : "memory");
+}
+
 __global__ void __launch_bounds__(kPolThreads, 1) k_policy(
     const float* __restrict__ obs, int64_t M, int obs_dim, PolicyPacked pk, PolicyOut out,
     uint32_t seed_lo, uint32_t seed_hi, uint32_t step_lo, uint32_t step_hi) {
@@ -213,14 +224,15 @@ __global__ void __launch_bounds__(kPolThreads, 1) k_policy(
   __half* sB1 = reinterpret_cast<__half*>(smem + kOffB1);
   __half* sB2 = reinterpret_cast<__half*>(smem + kOffB2);
   __half* sB3 = reinterpret_cast<__half*>(smem + kOffB3);
-  __half* sA1 = reinterpret_cast<__half*>(smem + kOffA1);
-  __half* sA2 = reinterpret_cast<__half*>(smem + kOffA2);
-  __half* sA3 = sA1;                                                    // alias (see above)
   float* sC = reinterpret_cast<float*>(smem + kOffC);
   const float* sStage = reinterpret_cast<const float*>(smem + kOffStage);
-  uint64_t* bar = reinterpret_cast<uint64_t*>(smem + kOffBar);          // [0] MMA, [1] TMA
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + kOffBar + 16);
+  // mbarriers: [g] MMA completion of group g; [2 + g] TMA arrival of group g's tiles (a
+  // barrier per group keeps each one's phases in its own tile order).
+  uint64_t* bar = reinterpret_cast<uint64_t*>(smem + kOffBar);
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + kOffBar + 32);
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int g = warp >> 3, gw = warp & 7, gtid = tid & (kPolGroup - 1);
+  __half* sA = reinterpret_cast<__half*>(smem + kOffA + g * kABytes);
 
   // Resident weights: plain 16-byte copies of the packed operands.
   {
@@ -237,80 +249,94 @@ __global__ void __launch_bounds__(kPolThreads, 1) k_policy(
   }
   if (warp == 0) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
-                 "r"(256));
+                 "r"(512));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
   }
   if (tid == 0) {
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&bar[0])));
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&bar[1])));
+    for (int i = 0; i < 4; ++i)
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&bar[i])));
     asm volatile("fence.mbarrier_init.release.cluster;");
   }
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
   asm volatile("tcgen05.fence::before_thread_sync;");
   __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;");
-  const uint32_t tmem = *tmem_slot;                  // D1/D2: columns 0-127, D3: 128-143
-  const uint32_t bar_mma = smem_u32(&bar[0]), bar_tma = smem_u32(&bar[1]);
+  const uint32_t tmem = *tmem_slot + (uint32_t)(g * 256);   // D: +0..127, D3: +128..143
+  const uint32_t bar_mma = smem_u32(&bar[g]), bar_tma = smem_u32(&bar[2 + g]);
+  const uint32_t bar_tma_next = smem_u32(&bar[3 - g]);      // the other group's
   const uint32_t stage = smem_u32(sStage);
-  const uint32_t a1 = smem_u32(sA1), a2 = smem_u32(sA2), a3 = smem_u32(sA3);
+  const uint32_t a = smem_u32(sA);
   const uint32_t b1 = smem_u32(sB1), b2 = smem_u32(sB2), b3 = smem_u32(sB3);
-  uint32_t ph_mma = 0, ph_tma = 0;
+  uint32_t ph_mma = 0;
 
-  // Epilogue mapping: warp w reads TMEM lanes (rows) 32 (w % 4) .. and columns 32 (w / 4) ..
-  const int erow = 32 * (warp & 3) + lane;
-  const int ecol = 32 * (warp >> 2);
-  const uint32_t tlane = (uint32_t)(32 * (warp & 3)) << 16;
+  // Epilogue mapping: warp gw of the group reads TMEM lanes (rows) 32 (gw % 4) .. (the lane
+  // quadrant of its CTA warp id) and columns 64 (gw / 4) ..
+  const int erow = 32 * (gw & 3) + lane;
+  const int ecol = 64 * (gw >> 2);
+  const uint32_t tlane = (uint32_t)(32 * (gw & 3)) << 16;
 
   const int64_t n_tiles = (M + kPolTile - 1) / kPolTile;
   // A full tile is one contiguous, 16-byte aligned block of 128 x obs_dim floats (m0 is a
-  // multiple of 128): one TMA bulk copy.  The ragged last tile is read with plain loads.
+  // multiple of 128): one TMA bulk copy.  Only the last tile of the range can be ragged; it
+  // is read with plain loads (and, being the last, never precedes a TMA'd tile).
   const uint32_t tile_bytes = (uint32_t)(kPolTile * obs_dim * 4);
   const bool bulk_ok = (tile_bytes % 16u) == 0u &&
                        (reinterpret_cast<uintptr_t>(obs) % 16u) == 0u;
   auto is_full = [&](int64_t t) { return bulk_ok && (t + 1) * kPolTile <= M; };
-  if (tid == 0 && blockIdx.x < n_tiles && is_full(blockIdx.x))
+  if (tid == 0 && blockIdx.x < n_tiles && is_full(blockIdx.x))     // group 0's first tile
     tma_load_1d(stage, obs + (int64_t)blockIdx.x * kPolTile * obs_dim, tile_bytes, bar_tma);
 
-  // MMA issue (one thread): s K-steps of 16 from A (R = 128 rows) and B (RB rows).
-  auto issue = [&](uint32_t d, uint32_t a, uint32_t b, int ksteps, int rb, uint32_t idesc) {
+  // MMA issue (one thread per group): ksteps K-steps of 16 from A (128 rows), B (rb rows).
+  auto issue = [&](uint32_t d, uint32_t aa, uint32_t b, int ksteps, int rb, uint32_t idesc) {
     asm volatile("tcgen05.fence::after_thread_sync;");
     for (int k = 0; k < ksteps; ++k)
-      mma_f16(d, umma_desc(a + k * 2 * (kPolTile * 16), kPolTile * 16, 128),
+      mma_f16(d, umma_desc(aa + k * 2 * (kPolTile * 16), kPolTile * 16, 128),
               umma_desc(b + k * 2 * (rb * 16), rb * 16, 128), idesc, k > 0);
     mma_commit(bar_mma);
   };
-  // Epilogue of a hidden layer: h = tanh(D + bias) -> fp16 operand of the next layer.
-  auto hidden_epilogue = [&](const float* bias, __half* dst) {
-    float v[32];
-    tmem_ld32(tmem + tlane + (uint32_t)ecol, v);
+  auto wait_mma = [&]() {
+    mbar_wait(bar_mma, ph_mma);
+    ph_mma ^= 1u;
+    asm volatile("tcgen05.fence::after_thread_sync;");
+  };
+  // Epilogue of a hidden layer: h = tanh(D + bias) -> fp16 operand of the next layer (A).
+  auto hidden_epilogue = [&](const float* bias) {
 #pragma unroll
-    for (int g = 0; g < 4; ++g) {
-      const int c0 = ecol + 8 * g;
-      float t[8];
+    for (int half = 0; half < 2; ++half) {
+      float v[32];
+      const int cb = ecol + 32 * half;
+      tmem_ld32(tmem + tlane + (uint32_t)cb, v);
 #pragma unroll
-      for (int e = 0; e < 8; ++e) t[e] = tanh_fast(v[8 * g + e] + bias[c0 + e]);
-      uint4 pkd;
-      pkd.x = h2_bits(__floats2half2_rn(t[0], t[1]));
-      pkd.y = h2_bits(__floats2half2_rn(t[2], t[3]));
-      pkd.z = h2_bits(__floats2half2_rn(t[4], t[5]));
-      pkd.w = h2_bits(__floats2half2_rn(t[6], t[7]));
-      *reinterpret_cast<uint4*>(dst + cm_offset(erow, c0, kPolTile)) = pkd;
+      for (int q = 0; q < 4; ++q) {
+        const int c0 = cb + 8 * q;
+        float t[8];
+#pragma unroll
+        for (int e = 0; e < 8; ++e) t[e] = tanh_fast(v[8 * q + e] + bias[c0 + e]);
+        uint4 pkd;
+        pkd.x = h2_bits(__floats2half2_rn(t[0], t[1]));
+        pkd.y = h2_bits(__floats2half2_rn(t[2], t[3]));
+        pkd.z = h2_bits(__floats2half2_rn(t[4], t[5]));
+        pkd.w = h2_bits(__floats2half2_rn(t[6], t[7]));
+        *reinterpret_cast<uint4*>(sA + cm_offset(erow, c0, kPolTile)) = pkd;
+      }
     }
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
     asm volatile("tcgen05.fence::before_thread_sync;");
-    __syncthreads();
+    group_sync(g);
   };
 
-  for (int64_t tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
+  uint32_t ph_tma = 0;
+  for (int64_t tile = blockIdx.x + (int64_t)g * gridDim.x; tile < n_tiles;
+       tile += 2 * (int64_t)gridDim.x) {
     const int64_t m0 = tile * kPolTile;
     const bool full = is_full(tile);
     // ---- A1: obs rows -> fp16 core-matrix layout (zero pad rows >= M, cols >= obs_dim).
-    if (full) {
-      mbar_wait(bar_tma, ph_tma);                        // this tile's TMA has landed
+    if (full) {                                          // this tile's TMA has landed
+      mbar_wait(bar_tma, ph_tma);
       ph_tma ^= 1u;
     }
     // Thread -> (row r, 8-column chunk kc); a warp shares kc, so the chunk bounds are uniform.
-    for (int it = tid; it < kPolTile * (kPolK1 / 8); it += kPolThreads) {
+    for (int it = gtid; it < kPolTile * (kPolK1 / 8); it += kPolGroup) {
       const int r = it % kPolTile, kc = it / kPolTile;
       const int nv = obs_dim - kc * 8;                    // valid columns in this chunk
       const int64_t gr = m0 + r;
@@ -334,34 +360,28 @@ __global__ void __launch_bounds__(kPolThreads, 1) k_policy(
       pkd.y = h2_bits(__floats2half2_rn(x[2], x[3]));
       pkd.z = h2_bits(__floats2half2_rn(x[4], x[5]));
       pkd.w = h2_bits(__floats2half2_rn(x[6], x[7]));
-      *reinterpret_cast<uint4*>(sA1 + cm_offset(r, kc * 8, kPolTile)) = pkd;
+      *reinterpret_cast<uint4*>(sA + cm_offset(r, kc * 8, kPolTile)) = pkd;
     }
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
     asm volatile("tcgen05.fence::before_thread_sync;");
-    __syncthreads();
-    // ---- prefetch the next tile (overlaps the MMAs and epilogues); layer 1
-    if (tid == 0) {
+    group_sync(g);
+    // ---- the stage is free: load the CTA's next tile (the other group's); layer 1
+    if (gtid == 0) {
       const int64_t nt = tile + gridDim.x;
       if (nt < n_tiles && is_full(nt))
-        tma_load_1d(stage, obs + nt * kPolTile * obs_dim, tile_bytes, bar_tma);
-      issue(tmem, a1, b1, kPolK1 / 16, kPolN, kPolIdesc);
+        tma_load_1d(stage, obs + nt * kPolTile * obs_dim, tile_bytes, bar_tma_next);
+      issue(tmem, a, b1, kPolK1 / 16, kPolN, kPolIdesc);
     }
-    mbar_wait(bar_mma, ph_mma);
-    ph_mma ^= 1u;
-    asm volatile("tcgen05.fence::after_thread_sync;");
-    hidden_epilogue(sC, sA2);                            // h1 -> A2
+    wait_mma();
+    hidden_epilogue(sC);                                 // h1 -> A (A1 consumed)
     // ---- layer 2
-    if (tid == 0) issue(tmem, a2, b2, kPolK2 / 16, kPolN, kPolIdesc);
-    mbar_wait(bar_mma, ph_mma);
-    ph_mma ^= 1u;
-    asm volatile("tcgen05.fence::after_thread_sync;");
-    hidden_epilogue(sC + 128, sA3);                      // h2 -> A3 (aliases A1)
-    // ---- layer 3: mean_0, mean_1, value in TMEM columns 128..130
-    if (tid == 0) issue(tmem + 128, a3, b3, kPolK2 / 16, kPolN3, kPolIdesc3);
-    mbar_wait(bar_mma, ph_mma);
-    ph_mma ^= 1u;
-    asm volatile("tcgen05.fence::after_thread_sync;");
-    if (warp < 4) {                                      // one thread per row
+    if (gtid == 0) issue(tmem, a, b2, kPolK2 / 16, kPolN, kPolIdesc);
+    wait_mma();
+    hidden_epilogue(sC + 128);                           // h2 -> A (A2 consumed)
+    // ---- layer 3: mean_0, mean_1, value in TMEM columns +128..130
+    if (gtid == 0) issue(tmem + 128, a, b3, kPolK2 / 16, kPolN3, kPolIdesc3);
+    wait_mma();
+    if (gw < 4) {                                        // one thread per row
       float o[4];
       tmem_ld4(tmem + tlane + 128u, o);
       const int64_t gr = m0 + erow;
@@ -388,12 +408,12 @@ __global__ void __launch_bounds__(kPolThreads, 1) k_policy(
       }
     }
     asm volatile("tcgen05.fence::before_thread_sync;");
-    __syncthreads();
+    group_sync(g);                                       // TMEM / A free for the next tile
   }
   asm volatile("tcgen05.fence::after_thread_sync;");
   __syncthreads();
   if (warp == 0)
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(256));
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(*tmem_slot), "r"(512));
 }
 
 }  // namespace vg
