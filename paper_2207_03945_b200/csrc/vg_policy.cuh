@@ -112,8 +112,8 @@ __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
       : "memory");
 }
 
-// tanh(x) = sign(x) (1 - 2 / (exp(2|x|) + 1)): MUFU ex2 + rcp, absolute error ~2e-7
-// (tanh.approx.f32 is ~1e-3 absolute, too coarse for the parity budget).
+// tanh(x) = sign(x) (2 / (1 + exp(-2|x|)) - 1), absolute error ~2e-7 (tanh.approx.f32 is
+// ~1e-3 absolute, too coarse for the parity budget).
 // 1-D TMA bulk copy global -> shared, completion counted on an mbarrier (tx bytes).
 __device__ __forceinline__ void tma_load_1d(uint32_t dst, const void* src, uint32_t bytes,
                                             uint32_t bar) {
@@ -125,11 +125,27 @@ __device__ __forceinline__ void tma_load_1d(uint32_t dst, const void* src, uint3
       : "memory");
 }
 
+#ifndef VG_TANH_NEWTON
+#define VG_TANH_NEWTON 1
+#endif
 __device__ __forceinline__ float tanh_fast(float x) {
+#if VG_TANH_NEWTON
+  // One MUFU op: e = 2^(-2|x| log2 e) in (0, 1], y = 1 + e in (1, 2], 1/y from a linear
+  // start (|rel err| <= 0.09) and three Newton steps on the FMA pipe (9e-8), tanh|x| =
+  // 2/y - 1; the SFU (16 lanes/clk) was the K7 limiter with ex2 + rcp.  |error| ~2e-7.
+  float e;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(e) : "f"(fabsf(x) * -2.8853900817779268f));
+  const float y = 1.f + e;
+  float r = fmaf(-0.5f, y, 1.4571f);
+#pragma unroll
+  for (int i = 0; i < 3; ++i) r = fmaf(r, fmaf(-y, r, 1.f), r);
+  return copysignf(fmaf(2.f, r, -1.f), x);
+#else
   const float e = __expf(2.f * fabsf(x));
   float r;
   asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(e + 1.f));
   return copysignf(fmaf(-2.f, r, 1.f), x);
+#endif
 }
 
 // 32 consecutive TMEM columns of this thread's lane.

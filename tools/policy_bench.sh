@@ -1,0 +1,6 @@
+for v in - tanh2; do
+  if [ "$v" = "-" ]; then unset VG_LIB_VARIANT; else export VG_LIB_VARIANT=$v; fi
+  timeout 300 python bench.py --steps 10 --warmup 3 --no-cpu-baseline --no-e2e > gpurun_out/pb_$v.json 2>gpurun_out/pb_$v.err
+  python -c "
+import json; d=json.loads(open('gpurun_out/pb_$v.json').read().strip().splitlines()[-1]); print('$v', d['policy']['ms'], d['rollout']['ms'])"
+done
