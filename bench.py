@@ -556,6 +556,15 @@ def run_ours(args):
                                  "peak": "148 SM x 4 schedulers x 1 warp-instr/clk"}
             except Exception:
                 pass
+        parity_ev = None                 # committed GPU-vs-oracle statistics (tools/parity_stats.py)
+        ppath = os.path.join(ROOT, "profiles", "parity_stats.json")
+        if os.path.exists(ppath):
+            try:
+                pj = json.load(open(ppath))
+                if args.config in pj and args.vision == "sector":
+                    parity_ev = dict(pj[args.config], source="profiles/parity_stats.json")
+            except Exception:
+                pass
         cpu = None
         if world == 1 and not args.no_cpu_baseline:
             rate, sample, cores = oracle_rate(p, args.cpu_seconds)
@@ -584,6 +593,7 @@ def run_ours(args):
                                   f"148 SM x 128 lanes x {sm_mhz:.0f} MHz (1 op/lane/clk)"},
             "stages": stages,
             "sanity": san,
+            "parity": parity_ev,
             "hbm_peak_gbs": hbm, "peak_source": peak_src,
             "e2e": e2e,
             "gpu_launches": run.launches * K,
