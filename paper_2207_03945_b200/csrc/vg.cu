@@ -352,11 +352,23 @@ void sense_kernel(vg_world* w, dim3 grid, const vg::Outs& O, cudaStream_t s) {
         w->P, w->cell_start, w->xo_rec, w->xo_xy, w->xo_perm, O, w->SL, w->ray_dir, w->sub_tab);
 }
 
+// Slab mode senses only W x G owned cells (2312 at c5, P = 8): split each cell's queries
+// over enough CTAs for ~8 resident waves, or the last partial wave idles most SMs.
+int sense_chunks_slab(const vg_world* w) {
+  const long long cells = (long long)w->SL.W * w->P.G;
+  const long long target = (long long)w->n_sm * vg::kSenseMinBlocks * 8;
+  const long long per_cell = std::max(1LL, (long long)w->P.N / ((long long)w->P.G * w->P.G));
+  long long ch = (target + cells - 1) / cells;
+  ch = std::min(ch, std::max(1LL, (per_cell + vg::kSenseNQ * vg::kSenseWarps - 1) /
+                                      (vg::kSenseNQ * vg::kSenseWarps)));
+  return (int)std::max(1LL, std::min(ch, 64LL));
+}
+
 template <bool VISION>
 vg_status launch_sense(vg_world* w, const vg_outputs* outs, cudaStream_t s) {
   const vg::Outs O = to_outs(outs);
   if (w->slab) {                      // owned cells only: local columns 1..W
-    const dim3 grid((unsigned)(w->SL.W * w->P.G), 1);
+    const dim3 grid((unsigned)(w->SL.W * w->P.G), (unsigned)sense_chunks_slab(w));
     if (w->P.env == vg::kFlock) sense_kernel<vg::kFlock, VISION, true>(w, grid, O, s);
     else sense_kernel<vg::kTag, VISION, true>(w, grid, O, s);
     return launch_check("k_sense(slab)");
