@@ -1007,15 +1007,27 @@ __device__ __forceinline__ uint32_t* msg_id(unsigned char* m, uint32_t cap) {
   return reinterpret_cast<uint32_t*>(m + 16 + 16 * (size_t)cap);
 }
 
+// Appends are warp-aggregated: one atomic per converged group of lanes (the local set and
+// the messages are plain counters, hammered by every agent otherwise).
+__device__ __forceinline__ uint32_t warp_reserve(uint32_t* counter) {
+  const unsigned m = __activemask();
+  const int leader = __ffs(m) - 1;
+  const int lane = threadIdx.x & 31;
+  uint32_t base = 0u;
+  if (lane == leader) base = atomicAdd(counter, (uint32_t)__popc(m));
+  base = __shfl_sync(m, base, leader);
+  return base + (uint32_t)__popc(m & ((1u << lane) - 1u));
+}
+
 __device__ __forceinline__ void loc_append(const SlabBufs& B, float4 s, uint32_t id) {
-  const uint32_t k = atomicAdd(B.n_loc, 1u);
+  const uint32_t k = warp_reserve(B.n_loc);
   if (k < B.cap_loc) { B.loc_rec[k] = s; B.loc_id[k] = id; }
   else atomicExch(B.overflow, 1u);
 }
 
 __device__ __forceinline__ void msg_append(unsigned char* m, uint32_t cap, uint32_t* ovf,
                                            float4 s, uint32_t id) {
-  const uint32_t k = atomicAdd(msg_count(m), 1u);
+  const uint32_t k = warp_reserve(msg_count(m));
   if (k < cap) { msg_rec(m)[k] = s; msg_id(m, cap)[k] = id; }
   else atomicExch(ovf, 1u);
 }
@@ -1126,7 +1138,14 @@ __global__ void __launch_bounds__(256) k_slab_keys(Params P, Slab SL, SlabBufs B
     const int lcx = min((gx - SL.lo + 1 + P.G) % P.G, SL.W + 1);
     const uint32_t c = (uint32_t)(lcx * P.G + gy);
     cell_id[i] = c;
-    slot[i] = atomicAdd(&count[c], 1u);
+    // The local set is in the previous sense order (cell-major), so a warp's agents share
+    // few cells: one atomic per cell group (match_any), slots by lane rank within it.
+    const unsigned grp = __match_any_sync(__activemask(), c);
+    const int lane = threadIdx.x & 31, leader = __ffs(grp) - 1;
+    uint32_t base = 0u;
+    if (lane == leader) base = atomicAdd(&count[c], (uint32_t)__popc(grp));
+    base = __shfl_sync(grp, base, leader);
+    slot[i] = base + (uint32_t)__popc(grp & ((1u << lane) - 1u));
   }
 }
 
