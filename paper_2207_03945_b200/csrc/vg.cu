@@ -209,6 +209,7 @@ vg::Params derive(const vg_config& c, int g) {
   P.b_fall = P.k_fall * c.d_v;
   P.touch_fix = (long long)std::llrint((double)c.r_touch * 4294967296.0);
   P.cell = L / (float)g;
+  P.inv_smax = 1.0f / c.s_max;
   P.win_r2 = (c.vision == VG_VISION_RAY) ? P.cand2 : P.dv2;
   // K4 windows only ever widen the candidate set: 1 % of the radius plus 2^-19 L covers the
   // fp32 rounding of the keys, of the pair test and the fuzz of the A16 cell boundaries.

@@ -38,6 +38,7 @@ struct Params {
   float b_rise, nk_fall, b_fall;   // f = min(k_rise d + b_rise, nk_fall d + b_fall) (A5)
   float d_r, cand2, inv_w;         // ray vision: body radius, RN32((d_v + d_r)^2), v / fov
   float cell;                      // RN32(L / G) (K4 windows only)
+  float inv_smax;                  // RN32(1 / s_max): obs[v] = s / s_max to <= 1.5 ulp (A24)
   float win_r2, win_margin;        // K4 window: candidate radius^2, conservative margin
   long long touch_fix;         // r_touch * 2^32
 };
@@ -969,7 +970,7 @@ __global__ void __launch_bounds__(kSenseWarps * 32, kSenseMinBlocks) k_sense(
 #pragma unroll
           for (int w = 0; w < kMaxViewSlots / 32; ++w)
             if (32 * w + lane < P.view_slots) orow[32 * w + lane] = __uint_as_float(vals[w]);
-          if (ENV == kFlock && lane == 0) orow[P.view_slots] = __fdiv_rn(me[t].w, P.s_max);  // A24
+          if (ENV == kFlock && lane == 0) orow[P.view_slots] = me[t].w * P.inv_smax;  // A24
         }
         if (O.occ) {
           uint32_t mine = 0u;
