@@ -45,7 +45,7 @@ def full(path, config=None):
                          text=True, check=True).stdout.splitlines()
     rows = list(csv.reader(raw))
     hdr, units = rows[0], rows[1]
-    out, traffic = [], {}
+    out = []
     for r in rows[2:]:
         name = r[hdr.index("Kernel Name")].split("(")[0]
         out.append(f"### `{name}`")
@@ -54,15 +54,7 @@ def full(path, config=None):
             if k in hdr:
                 i = hdr.index(k)
                 out.append(f"| {k} | {r[i]} {units[i]} |")
-        i, j = hdr.index("dram__bytes_read.sum"), hdr.index("dram__bytes_write.sum")
-        scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
-        b = float(r[i]) * scale.get(units[i], 1) + float(r[j]) * scale.get(units[j], 1)
-        traffic.setdefault(name, b)
-    if config:
-        for name, b in traffic.items():
-            if "k_sense" in name:
-                json.dump({"config": config, "kernel": name, "bytes_per_launch": b,
-                           "source": path}, open("profiles/sense_traffic.json", "w"), indent=1)
+    # (profiles/sense_traffic.json is written by tools/update_profiles.py)
     return "\n".join(out)
 
 
