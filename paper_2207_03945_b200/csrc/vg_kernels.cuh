@@ -409,8 +409,8 @@ __global__ void __launch_bounds__(256) k_cell_sort(
 //   pass 1  integrate, cell id (A16), warp-private histogram (match_any aggregated);
 //   scan    per cell an exclusive scan over the 32 warps (warp shuffles), then over cells;
 //   pass 2  each warp walks its range in order: position = cell start + earlier warps +
-//           earlier agents of this warp in the cell + lower lanes with the same cell.
-// Three block barriers in total.
+//           earlier agents of this warp in the cell + lower lanes with the same cell;
+//   pass 3  warp per cell: the K4 sense order and window table (sense_order_cell, K3b).
 constexpr int kRBMaxCells = 256;
 constexpr int kRBMaxAgents = 32768;
 
