@@ -301,7 +301,7 @@ vg_status bin_rest(vg_world* w, const float4* state, cudaStream_t s, bool prof =
   return VG_OK;
 }
 
-vg::Outs to_outs(const vg_outputs* o) {
+vg::Outs to_outs(const vg_world* w, const vg_outputs* o) {
   vg::Outs r{};
   if (o) {
     r.obs = o->obs;
@@ -312,6 +312,10 @@ vg::Outs to_outs(const vg_outputs* o) {
     r.occ = o->sector_occ;
     r.agent_id = o->agent_id;
   }
+  const bool all = r.obs && r.reward && r.n_neigh && r.n_collide && r.occ &&
+                   (w->P.env != vg::kTag || r.n_touch) && (!w->slab || r.agent_id);
+  const long long rows = w->slab ? (long long)w->P.N : w->P.total;
+  r.fast = (all && rows * (w->P.obs_dim + 1) < (1LL << 31)) ? 1 : 0;
   return r;
 }
 
@@ -367,7 +371,7 @@ int sense_chunks_slab(const vg_world* w) {
 
 template <bool VISION>
 vg_status launch_sense(vg_world* w, const vg_outputs* outs, cudaStream_t s) {
-  const vg::Outs O = to_outs(outs);
+  const vg::Outs O = to_outs(w, outs);
   if (w->slab) {                      // owned cells only: local columns 1..W
     const dim3 grid((unsigned)(w->SL.W * w->P.G), (unsigned)sense_chunks_slab(w));
     if (w->P.env == vg::kFlock) sense_kernel<vg::kFlock, VISION, true>(w, grid, O, s);

@@ -11,6 +11,7 @@
 #pragma once
 
 #include <cstdint>
+#include <type_traits>
 #include <cuda_runtime.h>
 
 namespace vg {
@@ -51,6 +52,8 @@ struct Outs {
   uint32_t* n_touch;
   uint32_t* occ;
   uint32_t* agent_id;   // slab mode: global id of each output row
+  int fast;             // every output K4 writes is present and rows x obs_dim < 2^31:
+                        // K4 skips the NULL checks and indexes in 32 bits
 };
 
 // Slab mode: this rank owns global cell columns [lo, hi), W = hi - lo >= 2.
@@ -950,38 +953,44 @@ __global__ void __launch_bounds__(kSenseWarps * 32, kSenseMinBlocks) k_sense(
         const long long tt = (long long)nt * P.touch_fix;
         rsum += (tq[t] == 1u) ? tt : -tt;                             // P:194 touch rule
       }
-      const size_t row = SLAB ? (size_t)(q - cs[P.G]) : (size_t)r * P.N + perm[q];
-      if (lane == 0) {
-        if (SLAB && O.agent_id) O.agent_id[row] = perm[q];
-        if (O.reward) O.reward[row] = __ll2float_rn(rsum) * kFixInv;
-        if (O.n_neigh) O.n_neigh[row] = nn;
-        if (O.n_collide) O.n_collide[row] = nc;
-        if (ENV == kTag && O.n_touch) O.n_touch[row] = nt;
-      }
-      if (VISION) {
-        uint32_t vals[kMaxViewSlots / 32];
-#pragma unroll
-        for (int w = 0; w < kMaxViewSlots / 32; ++w) {
-          const int k = 32 * w + lane;
-          vals[w] = (k < P.view_slots) ? s_min[warp][t][k] : kOneBits;
+      auto emit = [&](auto fast_c) {
+        constexpr bool FAST = decltype(fast_c)::value;
+        using idx_t = typename std::conditional<FAST, uint32_t, size_t>::type;
+        const idx_t row = SLAB ? (idx_t)(q - cs[P.G]) : (idx_t)r * (idx_t)P.N + (idx_t)perm[q];
+        if (lane == 0) {
+          if (SLAB && (FAST || O.agent_id)) O.agent_id[row] = perm[q];
+          if (FAST || O.reward) O.reward[row] = __ll2float_rn(rsum) * kFixInv;
+          if (FAST || O.n_neigh) O.n_neigh[row] = nn;
+          if (FAST || O.n_collide) O.n_collide[row] = nc;
+          if (ENV == kTag && (FAST || O.n_touch)) O.n_touch[row] = nt;
         }
-        if (O.obs) {
-          float* orow = O.obs + row * (size_t)P.obs_dim;
-#pragma unroll
-          for (int w = 0; w < kMaxViewSlots / 32; ++w)
-            if (32 * w + lane < P.view_slots) orow[32 * w + lane] = __uint_as_float(vals[w]);
-          if (ENV == kFlock && lane == 0) orow[P.view_slots] = me[t].w * P.inv_smax;  // A24
-        }
-        if (O.occ) {
-          uint32_t mine = 0u;
+        if (VISION) {
+          uint32_t vals[kMaxViewSlots / 32];
 #pragma unroll
           for (int w = 0; w < kMaxViewSlots / 32; ++w) {
-            const unsigned bits = __ballot_sync(kFull, vals[w] < kOneBits);
-            if (lane == w) mine = bits;
+            const int k = 32 * w + lane;
+            vals[w] = (k < P.view_slots) ? s_min[warp][t][k] : kOneBits;
           }
-          if (lane < P.occ_words) O.occ[row * (size_t)P.occ_words + lane] = mine;
+          if (FAST || O.obs) {
+            float* orow = O.obs + row * (idx_t)P.obs_dim;
+#pragma unroll
+            for (int w = 0; w < kMaxViewSlots / 32; ++w)
+              if (32 * w + lane < P.view_slots) orow[32 * w + lane] = __uint_as_float(vals[w]);
+            if (ENV == kFlock && lane == 0) orow[P.view_slots] = me[t].w * P.inv_smax;  // A24
+          }
+          if (FAST || O.occ) {
+            uint32_t mine = 0u;
+#pragma unroll
+            for (int w = 0; w < kMaxViewSlots / 32; ++w) {
+              const unsigned bits = __ballot_sync(kFull, vals[w] < kOneBits);
+              if (lane == w) mine = bits;
+            }
+            if (lane < P.occ_words) O.occ[row * (idx_t)P.occ_words + lane] = mine;
+          }
         }
-      }
+      };
+      if (O.fast) emit(std::true_type{});
+      else emit(std::false_type{});
     }
     __syncwarp();
   }
