@@ -811,7 +811,9 @@ __global__ void __launch_bounds__(kSenseWarps * 32, kSenseMinBlocks) k_sense(
             const float pp = fmaf(ud.x, left, -ud.y * fwd);      // perpendicular offset
             const float h = (P.d_r - pp) * (P.d_r + pp);         // r^2 - p^2, well conditioned
             if (h >= 0.f && bb > 0.f) {
-              const float tt = fmaxf(bb - sqrtf(h), 0.f);        // entry distance
+              float sh;                                          // MUFU sqrt (~1 ulp): the
+              asm("sqrt.approx.ftz.f32 %0, %1;" : "=f"(sh) : "f"(h));   // IEEE sqrtf's slow path
+              const float tt = fmaxf(bb - sh, 0.f);              // entry distance
               if (tt < P.d_v)
                 atomicMin(&row[k], __float_as_uint(fminf(tt * P.inv_dv, kBelowOne)));
             }
