@@ -225,6 +225,30 @@ def test_reward_kernel_matches_sense(cuda):
         w.close()
 
 
+@pytest.mark.parametrize("which", ["no_obs", "no_occ", "only_obs", "no_counts"])
+def test_partial_outputs_equal_full(cuda, which):
+    # K4 has a fast path when every output is present and a NULL-checked path otherwise:
+    # any subset of outputs must equal the same outputs of a full run bit for bit.
+    torch = _torch()
+    for p in (vi.workload("c2"), vi.tag_params(3000, width=60.0)):
+        w = make_world(p)
+        st = dev(vi.init_state(p, seed=6))
+        full = w.alloc_outputs()
+        kw = {"no_obs": dict(obs=False), "no_occ": dict(sector_occ=False),
+              "only_obs": dict(reward=False, counts=False, sector_occ=False),
+              "no_counts": dict(counts=False)}[which]
+        part = w.alloc_outputs(**kw)
+        w.bin(st)
+        w.sense(full)
+        w.sense(part)
+        torch.cuda.synchronize()
+        for k in ("obs", "reward", "n_neigh", "n_collide", "n_touch", "sector_occ"):
+            a, b = getattr(part, k), getattr(full, k)
+            if a is not None and b is not None:
+                assert torch.equal(a.view(torch.int32), b.view(torch.int32)), (which, k)
+        w.close()
+
+
 def test_integrate_then_bin_sense_equals_step(cuda):
     torch = _torch()
     p = vi.workload("c2")
