@@ -165,6 +165,16 @@ def test_slab_window_rim(cuda, P):
 
 
 @pytest.mark.gpu
+@pytest.mark.parametrize("env", ["flock", "tag"])
+def test_slab_bit_identical_ray(cuda, env):
+    # the ray-disc vision variant (NEXT #2) through the slab path: windows of radius
+    # d_v + d_r along the columns, ghost columns, migrants — bit-identical to one world.
+    mk = vi.flock_params if env == "flock" else vi.tag_params
+    p = mk(12000, width=176.0, d_v=10.0, grid=16).replace(vision="ray")
+    _compare_group(p, 4, 2, vi.init_state(p, seed=8))
+
+
+@pytest.mark.gpu
 @pytest.mark.parametrize("P", [2, 3])
 def test_slab_bit_identical_tag(cuda, P):
     p = vi.tag_params(12000, width=120.0, d_v=10.0, grid=9 if P == 3 else 8)
