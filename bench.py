@@ -425,13 +425,19 @@ def run_ours(args):
             pe1[k].record()
         torch.cuda.synchronize()
         pms = sum(a.elapsed_time(b) for a, b in zip(pe0, pe1)) / K
-        flops = 2.0 * rows * (144 * 128 + 128 * 128 + 3 * 128)
+        # algorithmic MACs per row: obs_dim x 64 x 2 (actor, critic), 64 x 64 x 2, 64 x 3
+        flops = 2.0 * rows * (w.obs_dim * 128 + 2 * 64 * 64 + 3 * 64)
         pbytes = rows * (4 * w.obs_dim + 4 * 6)
+        pk = measured_peaks()[0]
+        tf_peak = float(pk.get("bf16_tflops", 1674.4))       # fp16 dense = bf16 dense rate
+        gbs = pbytes / (pms / 1e3) / 1e9
+        tfs = flops / (pms / 1e3) / 1e12
         policy = {"kernel": "k_policy (tcgen05 kind::f16, TMEM accumulators)", "rows": rows,
                   "ms": pms, "agents_per_s": rows / (pms / 1e3),
-                  "tensor_TFLOPs": flops / (pms / 1e3) / 1e12,
-                  "hbm_GBps": pbytes / (pms / 1e3) / 1e9,
-                  "bound": "hbm (obs read 4*obs_dim B/row)"}
+                  "tensor_TFLOPs": tfs, "tensor_frac": tfs / tf_peak,
+                  "hbm_GBps": gbs, "hbm_frac": gbs / float(pk.get("hbm_gbs", 6441.6)),
+                  "limiter": "issue / SFU of the fp32-accurate tanh epilogue (ncu, DESIGN.md "
+                             "6b); HBM floor = 4 obs_dim B per row"}
         pl.close()
 
     # ---- the paper's experience-collection loop (Fig. 5): vg_rollout of t = 16 steps
