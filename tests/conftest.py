@@ -9,6 +9,21 @@ for _p in (ROOT, os.path.join(ROOT, "tests")):
         sys.path.insert(0, _p)
 
 
+def _ensure_library():
+    """Build libvg.so in-tree if it is missing or older than its sources (nvcc is in the
+    image here and on the GPU box); a failed build fails the tests loudly at import."""
+    import importlib.util
+    spec = importlib.util.spec_from_file_location(
+        "_vg_build", os.path.join(ROOT, "paper_2207_03945_b200", "_build.py"))
+    mod = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(mod)
+    if mod.needs_build():
+        mod.build()
+
+
+_ensure_library()
+
+
 def pytest_configure(config):
     config.addinivalue_line("markers", "gpu: needs a CUDA device (B200, sm_100a)")
     config.addinivalue_line("markers", "slow: longer CPU test")
