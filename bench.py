@@ -306,8 +306,14 @@ class SlabRunner:
 
 
 def run_ours(args):
+    import importlib.util
     import torch
     import torch.distributed as dist
+    spec = importlib.util.spec_from_file_location(      # compile libvg.so if this checkout
+        "_vg_build", os.path.join(ROOT, "paper_2207_03945_b200", "_build.py"))   # lacks it
+    _b = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(_b)
+    _b.build()
     import paper_2207_03945_b200 as vg
 
     rank, local, world = rank_info()
