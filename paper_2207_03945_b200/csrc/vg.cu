@@ -260,8 +260,8 @@ vg_status launch_k1(vg_world* w, float4* io, const float4* in, const float2* act
 // Exclusive scan of the cell counts into cell_start (re-zeroing the counts).
 vg_status scan_cells(vg_world* w, cudaStream_t s) {
   const int n = w->n_cells;
-  if (n <= 2 * vg::kScanTile) {
-    vg::k_scan_cells<<<1, 1024, 0, s>>>(w->count, w->cell_start, n);
+  if (n <= vg::kScanSmallMax) {                 // (dynamic smem limit set at world creation)
+    vg::k_scan_cells<<<1, 1024, (size_t)n * 4, s>>>(w->count, w->cell_start, n);
     return launch_check("k_scan_cells");
   }
   const unsigned tiles = (unsigned)((n + vg::kScanTile - 1) / vg::kScanTile);
@@ -342,13 +342,27 @@ void sense_carveout(K* k) {
 }
 
 template <int ENV, bool VISION, bool SLAB>
+void sense_carveouts() {
+  sense_carveout(vg::k_sense<ENV, VISION, SLAB, true>);
+  sense_carveout(vg::k_sense<ENV, VISION, SLAB, false>);
+}
+
+// Function attributes apply to the current device: set them for every world created.
+void set_kernel_attributes() {
+  cudaFuncSetAttribute(vg::k_scan_cells, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       vg::kScanSmallMax * 4);
+  sense_carveouts<vg::kFlock, true, false>();
+  sense_carveouts<vg::kFlock, true, true>();
+  sense_carveouts<vg::kTag, true, false>();
+  sense_carveouts<vg::kTag, true, true>();
+  sense_carveouts<vg::kFlock, false, false>();
+  sense_carveouts<vg::kTag, false, false>();
+  sense_carveouts<vg::kFlock, false, true>();
+  sense_carveouts<vg::kTag, false, true>();
+}
+
+template <int ENV, bool VISION, bool SLAB>
 void sense_kernel(vg_world* w, dim3 grid, const vg::Outs& O, cudaStream_t s) {
-  static bool once = [] {
-    sense_carveout(vg::k_sense<ENV, VISION, SLAB, true>);
-    sense_carveout(vg::k_sense<ENV, VISION, SLAB, false>);
-    return true;
-  }();
-  (void)once;
   if (w->cfg.vision == VG_VISION_RAY)
     vg::k_sense<ENV, VISION, SLAB, true><<<grid, vg::kSenseWarps * 32, 0, s>>>(
         w->P, w->cell_start, w->xo_rec, w->xo_xy, w->xo_perm, O, w->SL, w->ray_dir, w->sub_tab);
@@ -456,6 +470,7 @@ vg_status vg_world_create(const vg_config* cfg, vg_world** out) {
   w->n_cells = g * g * cfg->n_replicas;
   cudaGetDevice(&w->device);
   cudaDeviceGetAttribute(&w->n_sm, cudaDevAttrMultiProcessorCount, w->device);
+  set_kernel_attributes();                         // per device (the current one)
   size_t n = (size_t)w->P.total;
   vg_status st = VG_OK;
   if (cfg->shard == VG_SHARD_SLAB) {
@@ -575,7 +590,8 @@ vg_status vg_world_query(const vg_world* w, vg_world_info* info) {
   info->occ_words = w->P.occ_words;
   info->total_agents = w->P.total;
   info->scratch_bytes = (int64_t)w->scratch_bytes;
-  info->kernels_per_step = w->slab ? 7 : (w->fused_bin ? 2 : 5);
+  const int scan_k = (w->n_cells > vg::kScanSmallMax) ? 2 : 1;
+  info->kernels_per_step = w->slab ? 6 + scan_k : (w->fused_bin ? 2 : 4 + scan_k);
   return VG_OK;
 }
 

@@ -156,16 +156,22 @@ __global__ void __launch_bounds__(256) k_integrate_bin(
 
 // ---------------------------------------------------------------------------------- K2
 // Exclusive scan of n counts into start[0..n] (start[n] = total) and re-zero the counts
-// for the next binning.  One CTA of 1024 threads, each owning a contiguous chunk.
+// for the next binning.  One CTA of 1024 threads: the counts are staged in shared memory
+// with coalesced loads, each thread scans a contiguous chunk there, and the results go
+// back out coalesced (n <= kScanSmallMax; larger grids use K2').
+constexpr int kScanSmallMax = 12288;   // 48 KB; above it the 2-kernel K2' is faster (c5: 18,496)
 __global__ void __launch_bounds__(1024) k_scan_cells(uint32_t* __restrict__ count,
                                                       uint32_t* __restrict__ start, int n) {
+  extern __shared__ uint32_t s_c[];                     // [n]
   __shared__ uint32_t warp_sums[32];
   __shared__ uint32_t total_s;
   const int t = threadIdx.x, lane = t & 31, w = t >> 5;
+  for (int k = t; k < n; k += blockDim.x) s_c[k] = count[k];
+  __syncthreads();
   const int per = (n + blockDim.x - 1) / blockDim.x;
   const int b = min(n, t * per), e = min(n, b + per);
   uint32_t sum = 0;
-  for (int k = b; k < e; ++k) sum += count[k];
+  for (int k = b; k < e; ++k) sum += s_c[k];
   uint32_t inc = sum;
 #pragma unroll
   for (int o = 1; o < 32; o <<= 1) {
@@ -188,9 +194,13 @@ __global__ void __launch_bounds__(1024) k_scan_cells(uint32_t* __restrict__ coun
   __syncthreads();
   uint32_t run = warp_sums[w] + inc - sum;
   for (int k = b; k < e; ++k) {
-    const uint32_t c = count[k];
-    start[k] = run;
+    const uint32_t c = s_c[k];
+    s_c[k] = run;
     run += c;
+  }
+  __syncthreads();
+  for (int k = t; k < n; k += blockDim.x) {
+    start[k] = s_c[k];
     count[k] = 0u;
   }
   if (t == 0) start[n] = total_s;
