@@ -1,8 +1,6 @@
 """Pins for oracle.grid_size / cell_ids / bins (a2) — SPEC examples, textbook sort, no GPU."""
-import math
 
 import numpy as np
-import pytest
 
 import oracle
 import vg_inputs as vi

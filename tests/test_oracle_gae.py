@@ -1,6 +1,5 @@
 """Pins for oracle.gae: single step, zeros, closed forms, library cumsum."""
 import numpy as np
-import pytest
 
 from oracle.gae import gae
 

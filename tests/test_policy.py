@@ -9,7 +9,6 @@ Two checks:
    activations, otherwise exact) within 2e-4 absolute — tight enough that any layout or
    indexing error (O(0.1)) fails.
 Actions/log-probs: the same Philox bits on both sides, fp32 Box-Muller (~1e-6 relative)."""
-import math
 
 import numpy as np
 import pytest

@@ -9,7 +9,7 @@ import torch
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path[:0] = [ROOT, os.path.join(ROOT, "tests")]
-import oracle  # noqa: E402
+
 import vg_inputs as vi  # noqa: E402
 import vg_parity as parity  # noqa: E402
 import paper_2207_03945_b200 as vg  # noqa: E402
