@@ -49,6 +49,9 @@ def parse():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--vision", default="sector", choices=["sector", "ray"],
                     help="vision model (reading A1): sector bins (default) or ray-disc (NEXT #2)")
+    ap.add_argument("--state", default="uniform", choices=["uniform", "clustered"],
+                    help="initial positions: iid uniform (the paper-shaped default) or the "
+                         "SURVEY 8d stress variant (16 Gaussian clusters, sigma = 2 d_v)")
     ap.add_argument("--cpu-seconds", type=float, default=15.0,
                     help="bounded oracle sample for cpu_baseline (seconds of CPU work)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -257,7 +260,8 @@ class ReplicaRunner:
         self.p, self.torch = p, torch
         self.w = vg.World(p, device=device)
         self.out = self.w.alloc_outputs()
-        self.state = torch.from_numpy(vi.init_state(p, seed=1000 * rank)).to(device)
+        init = vi.clustered_state if STATE == "clustered" else vi.init_state
+        self.state = torch.from_numpy(init(p, seed=1000 * rank)).to(device)
         self.launches = self.w.kernels_per_step
         self.phase_names = {"integrate_bin": ("integrate+bin (fused K1-K3)" if self.launches == 2
                                               else "integrate_bin"), "scan_cells": "scan_cells",
@@ -282,7 +286,8 @@ class SlabRunner:
         self.p, self.torch, self.slab = p, torch, slab
         self.w = vg.World(p, device=device, slab={"rank": rank, "world_size": world})
         self.out = self.w.alloc_outputs()
-        full = torch.from_numpy(vi.init_state(p, seed=0)).to(device)   # same world everywhere
+        init = vi.clustered_state if STATE == "clustered" else vi.init_state
+        full = torch.from_numpy(init(p, seed=0)).to(device)   # same world everywhere
         self.w.slab_load(full)
         self.w.slab_sense(self.out)
         del full
@@ -378,7 +383,7 @@ def run_ours(args):
     value = agents_all * K / (max_ms / 1e3)
     pairs_local = run.pairs_local()            # in-radius pairs of the last step (this rank)
     san = None
-    if args.vision == "sector" and args.config in ("c2", "c3", "c4", "c5"):
+    if args.vision == "sector" and args.config in ("c2", "c3", "c4", "c5") and STATE == "uniform":
         rows = run.w.slab_own_count() if slab_mode else p.total_agents
         san = sanity(p, run.out, rows, torch)
 
@@ -594,7 +599,7 @@ def run_ours(args):
             "scaling": scaling, "vs_baseline": None, "dtype": "f32", "data": "synthetic",
             "config": {"workload": args.config, "desc": vi.WORKLOAD_DESCRIPTIONS[args.config],
                        "R_per_gpu": p.n_replicas, "N": p.n_agents, "G": w.grid,
-                       "vision": args.vision,
+                       "vision": args.vision, "state": STATE,
                        "parallelism": par,
                        "l2": "256 MiB buffer written between timed steps (outside events)"},
             "roofline": {"kernel": "k_sense (sector vision + reward)", "bound": "alu",
@@ -624,8 +629,13 @@ def run_ours(args):
     return 0
 
 
+STATE = "uniform"
+
+
 def main():
+    global STATE
     args = parse()
+    STATE = args.state
     if args.impl == "reference":
         return run_reference(args)
     return run_ours(args)

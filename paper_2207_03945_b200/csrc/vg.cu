@@ -61,6 +61,9 @@ struct vg_world {
   uint32_t* xo_perm = nullptr;     // [R*N]         agent ids in sense order
   float2* xo_xy = nullptr;         // [R*N + 64]    positions in sense order (K4 candidate reads)
   uint32_t* sub_tab = nullptr;     // [(n_cells + 1) * kSub] K4 window table (K3b)
+  uint2* work = nullptr;           // [work_cap] K4 work items (cell, first query)
+  uint32_t* work_cnt = nullptr;    // [1] item count
+  long long work_cap = 0;
   float2* ray_dir = nullptr;       // [v] ray vision: sector-centre ray directions (agent frame)
   float2* act_dev = nullptr;       // [R*N]         staging for vg_step_host
   unsigned long long* err_dev = nullptr;  // smallest bad agent index (device word)
@@ -319,15 +322,17 @@ vg::Outs to_outs(const vg_world* w, const vg_outputs* o) {
   return r;
 }
 
-// Query chunks per cell: enough CTAs to give ~32 resident warps per SM when the world has
-// few cells (C1-C3), 1 for large worlds.  Any value >= 1 is correct (grid-stride loop).
-int sense_chunks(const vg_world* w) {
-  const long long target_warps = (long long)w->n_sm * 32;
-  const long long warps = (long long)w->n_cells * vg::kSenseWarps;
-  const long long per_cell = (w->P.total + w->n_cells - 1) / w->n_cells;
-  long long ch = (target_warps + warps - 1) / warps;
-  ch = std::min(ch, std::max(1LL, (per_cell + vg::kSenseNQ * vg::kSenseWarps - 1) / (vg::kSenseNQ * vg::kSenseWarps)));
-  return (int)std::max(1LL, std::min(ch, 1024LL));
+// K4 work items (k_sense_work): queries per item, chosen so a world has ~4 items per
+// resident CTA when it is small (c1-c3) and whole cells (~54 queries at c5) when it is
+// large; dense cells (clusters) are split into many items.
+int sense_chunk_q(const vg_world* w) {
+  const long long queries = w->slab ? (long long)w->P.N / w->cfg.world_size : w->P.total;
+  const long long slots = (long long)w->n_sm * vg::kSenseMinBlocks * 4;
+  long long q = (queries / slots) / 8 * 8;
+#ifndef VG_SENSE_CHUNK_MAX
+#define VG_SENSE_CHUNK_MAX 128
+#endif
+  return (int)std::max(8LL, std::min(q, (long long)VG_SENSE_CHUNK_MAX));
 }
 
 // K4's candidate reads hit L1: cap the shared-memory carve-out so the resident CTAs' shared
@@ -362,39 +367,35 @@ void set_kernel_attributes() {
 }
 
 template <int ENV, bool VISION, bool SLAB>
-void sense_kernel(vg_world* w, dim3 grid, const vg::Outs& O, cudaStream_t s) {
+void sense_kernel(vg_world* w, int cells, const vg::Outs& O, cudaStream_t s) {
+  const int cq = sense_chunk_q(w);
+  cudaMemsetAsync(w->work_cnt, 0, sizeof(uint32_t), s);
+  vg::k_sense_work<SLAB><<<(unsigned)((cells + 255) / 256), 256, 0, s>>>(
+      w->P, w->SL, w->cell_start, cells, cq, w->work, w->work_cnt);
+  // items <= cells + queries / chunk_q (+1): an upper bound, surplus CTAs exit at once
+  const long long queries = w->slab ? (long long)w->P.N : w->P.total;
+  const unsigned grid = (unsigned)std::min<long long>(cells + queries / cq + 1, w->work_cap);
   if (w->cfg.vision == VG_VISION_RAY)
     vg::k_sense<ENV, VISION, SLAB, true><<<grid, vg::kSenseWarps * 32, 0, s>>>(
-        w->P, w->cell_start, w->xo_rec, w->xo_xy, w->xo_perm, O, w->SL, w->ray_dir, w->sub_tab);
+        w->P, w->cell_start, w->xo_rec, w->xo_xy, w->xo_perm, O, w->SL, w->ray_dir, w->sub_tab,
+        w->work, w->work_cnt, cq);
   else
     vg::k_sense<ENV, VISION, SLAB, false><<<grid, vg::kSenseWarps * 32, 0, s>>>(
-        w->P, w->cell_start, w->xo_rec, w->xo_xy, w->xo_perm, O, w->SL, w->ray_dir, w->sub_tab);
-}
-
-// Slab mode senses only W x G owned cells (2312 at c5, P = 8): split each cell's queries
-// over enough CTAs for ~8 resident waves, or the last partial wave idles most SMs.
-int sense_chunks_slab(const vg_world* w) {
-  const long long cells = (long long)w->SL.W * w->P.G;
-  const long long target = (long long)w->n_sm * vg::kSenseMinBlocks * 8;
-  const long long per_cell = std::max(1LL, (long long)w->P.N / ((long long)w->P.G * w->P.G));
-  long long ch = (target + cells - 1) / cells;
-  ch = std::min(ch, std::max(1LL, (per_cell + vg::kSenseNQ * vg::kSenseWarps - 1) /
-                                      (vg::kSenseNQ * vg::kSenseWarps)));
-  return (int)std::max(1LL, std::min(ch, 64LL));
+        w->P, w->cell_start, w->xo_rec, w->xo_xy, w->xo_perm, O, w->SL, w->ray_dir, w->sub_tab,
+        w->work, w->work_cnt, cq);
 }
 
 template <bool VISION>
 vg_status launch_sense(vg_world* w, const vg_outputs* outs, cudaStream_t s) {
   const vg::Outs O = to_outs(w, outs);
   if (w->slab) {                      // owned cells only: local columns 1..W
-    const dim3 grid((unsigned)(w->SL.W * w->P.G), (unsigned)sense_chunks_slab(w));
-    if (w->P.env == vg::kFlock) sense_kernel<vg::kFlock, VISION, true>(w, grid, O, s);
-    else sense_kernel<vg::kTag, VISION, true>(w, grid, O, s);
+    const int cells = w->SL.W * w->P.G;
+    if (w->P.env == vg::kFlock) sense_kernel<vg::kFlock, VISION, true>(w, cells, O, s);
+    else sense_kernel<vg::kTag, VISION, true>(w, cells, O, s);
     return launch_check("k_sense(slab)");
   }
-  const dim3 grid((unsigned)w->n_cells, (unsigned)sense_chunks(w));
-  if (w->P.env == vg::kFlock) sense_kernel<vg::kFlock, VISION, false>(w, grid, O, s);
-  else sense_kernel<vg::kTag, VISION, false>(w, grid, O, s);
+  if (w->P.env == vg::kFlock) sense_kernel<vg::kFlock, VISION, false>(w, w->n_cells, O, s);
+  else sense_kernel<vg::kTag, VISION, false>(w, w->n_cells, O, s);
   return launch_check("k_sense");
 }
 
@@ -517,6 +518,11 @@ vg_status vg_world_create(const vg_config* cfg, vg_world** out) {
   if (!st) st = dalloc(w, &w->xo_perm, n);
   if (!st) st = dalloc(w, &w->xo_xy, n + 64);       // padded: unpredicated K4 loads
   if (!st) st = dalloc(w, &w->sub_tab, ((size_t)w->n_cells + 1) * vg::kSub);
+  if (!st) {
+    w->work_cap = (long long)w->n_cells + (long long)n / 8 + 1;       // chunk_q >= 8
+    st = dalloc(w, &w->work, (size_t)w->work_cap);
+  }
+  if (!st) st = dalloc(w, &w->work_cnt, 1);
   if (!st) st = dalloc(w, &w->ray_dir, vg::kMaxViewSlots);
   if (!st) {
     // psi_k = -fov/2 + (k + 1/2) fov/v (orientation A3), in double, rounded once
@@ -568,6 +574,8 @@ void vg_world_destroy(vg_world* w) {
   cudaFree(w->xo_perm);
   cudaFree(w->xo_xy);
   cudaFree(w->sub_tab);
+  cudaFree(w->work);
+  cudaFree(w->work_cnt);
   cudaFree(w->ray_dir);
   cudaFree(w->act_dev);
   cudaFree(w->err_dev);
@@ -591,7 +599,8 @@ vg_status vg_world_query(const vg_world* w, vg_world_info* info) {
   info->total_agents = w->P.total;
   info->scratch_bytes = (int64_t)w->scratch_bytes;
   const int scan_k = (w->n_cells > vg::kScanSmallMax) ? 2 : 1;
-  info->kernels_per_step = w->slab ? 6 + scan_k : (w->fused_bin ? 2 : 4 + scan_k);
+  // (+1: the K4 work list; the memset of its counters is not a kernel)
+  info->kernels_per_step = w->slab ? 7 + scan_k : (w->fused_bin ? 3 : 5 + scan_k);
   return VG_OK;
 }
 

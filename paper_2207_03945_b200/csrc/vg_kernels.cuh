@@ -640,11 +640,44 @@ struct __align__(16) Seg {
   int cbase, a0, a1;
 };
 
+// K4 work list: for every sensed cell (replica: all cells; slab: the owned W x G), items
+// (cell, first query) covering its queries in chunks of chunk_q; warp-aggregated append.
+template <bool SLAB>
+__global__ void __launch_bounds__(256) k_sense_work(Params P, Slab SL,
+                                                    const uint32_t* __restrict__ cell_start,
+                                                    int n_cells, int chunk_q,
+                                                    uint2* __restrict__ work,
+                                                    uint32_t* __restrict__ work_n) {
+  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  const int lane = threadIdx.x & 31;
+  uint32_t nch = 0u, qb = 0u;
+  if (c < n_cells) {
+    const int r = SLAB ? 0 : c / P.G2;
+    const int cl = SLAB ? (1 + c / P.G) * P.G + c % P.G : c - r * P.G2;
+    const uint32_t* cs = cell_start + (size_t)r * P.G2;
+    qb = cs[cl];
+    nch = (cs[cl + 1] - qb + (uint32_t)chunk_q - 1u) / (uint32_t)chunk_q;
+  }
+  uint32_t incl = nch;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint32_t y = __shfl_up_sync(kFull, incl, o);
+    if (lane >= o) incl += y;
+  }
+  uint32_t base = 0u;
+  if (lane == 31 && incl > 0u) base = atomicAdd(work_n, incl);
+  base = __shfl_sync(kFull, base, 31) + incl - nch;
+  for (uint32_t k = 0; k < nch; ++k)
+    work[base + k] = make_uint2((uint32_t)c, qb + k * (uint32_t)chunk_q);
+  (void)SL;
+}
+
 template <int ENV, bool VISION, bool SLAB, bool RAY>
 __global__ void __launch_bounds__(kSenseWarps * 32, kSenseMinBlocks) k_sense(
     Params P, const uint32_t* __restrict__ cell_start, const float4* __restrict__ sorted,
     const float2* __restrict__ sorted_xy, const uint32_t* __restrict__ perm, Outs O, Slab SL,
-    const float2* __restrict__ ray_dir, const uint32_t* __restrict__ sub_tab) {
+    const float2* __restrict__ ray_dir, const uint32_t* __restrict__ sub_tab,
+    const uint2* __restrict__ work, const uint32_t* __restrict__ work_n, int chunk_q) {
   // sorted / sorted_xy / perm are the sense-order arrays (xo_* of K3b): within a cell the
   // records ascend in x (replica grid, runs along rows) or y (slab grid, runs along columns).
   __shared__ uint32_t s_min[kSenseWarps][kSenseNQ][kMaxViewSlots];
@@ -656,7 +689,30 @@ __global__ void __launch_bounds__(kSenseWarps * 32, kSenseMinBlocks) k_sense(
   __shared__ int s_nseg;
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int c = blockIdx.x;
+  if (RAY) {
+    for (int k = threadIdx.x; k < P.v; k += blockDim.x) s_ray[k] = ray_dir[k];
+  }
+  unsigned lt_mask;
+  asm("mov.u32 %0, %%lanemask_lt;" : "=r"(lt_mask));
+  // Each warp senses NQ queries of this cell at once: every candidate load, image shift
+  // and loop step is shared; each query has its own ballot, queue, sector row and
+  // accumulators.  A missing query gets a NaN position (never a neighbour).
+  constexpr int NQ = kSenseNQ;
+  // Pair-pass constants.  (ptxas sees through this empty asm and re-loads them from the
+  // parameter bank per pair batch; forcing them into registers with an opaque add costs 8
+  // registers and measured 4 % slower, DESIGN.md §6.)
+  float c_contact2 = P.contact2, c_mcollide = -P.c_collide, c_k_rise = P.k_rise,
+        c_b_rise = P.b_rise, c_nk_fall = P.nk_fall, c_b_fall = P.b_fall, c_inv_fov = P.inv_fov,
+        c_fv = P.fv, c_inv_dv = P.inv_dv;
+  asm volatile("" : "+f"(c_contact2), "+f"(c_mcollide), "+f"(c_k_rise), "+f"(c_b_rise),
+               "+f"(c_nk_fall), "+f"(c_b_fall), "+f"(c_inv_fov), "+f"(c_fv), "+f"(c_inv_dv));
+  // One CTA per work item of k_sense_work: item = (cell, first query), up to chunk_q
+  // queries of that cell — dense cells are split over many CTAs.  The grid is an upper
+  // bound on the item count (cells + queries / chunk_q); surplus CTAs exit at once.
+  {
+    if (blockIdx.x >= *work_n) return;
+    const uint2 item = work[blockIdx.x];
+    const int c = (int)item.x;
   // Replica layout: cell = r G^2 + cy G + cx.  Slab layout: owned local column lcx = 1 + c/G.
   const int r = SLAB ? 0 : c / P.G2;
   const int cl = SLAB ? (1 + c / P.G) * P.G + c % P.G : c - r * P.G2;
@@ -715,28 +771,11 @@ __global__ void __launch_bounds__(kSenseWarps * 32, kSenseMinBlocks) k_sense(
     }
     s_nseg = ns;
   }
-  if (RAY) {
-    for (int k = threadIdx.x; k < P.v; k += blockDim.x) s_ray[k] = ray_dir[k];
-  }
-  __syncthreads();
-  const int nseg = s_nseg;
-  const uint32_t qb = cs[cl], qe = cs[cl + 1];
-  unsigned lt_mask;
-  asm("mov.u32 %0, %%lanemask_lt;" : "=r"(lt_mask));
-  // Each warp senses NQ queries of this cell at once: every candidate load, image shift
-  // and loop step is shared; each query has its own ballot, queue, sector row and
-  // accumulators.  A missing query gets a NaN position (never a neighbour).
-  constexpr int NQ = kSenseNQ;
-  // Pair-pass constants.  (ptxas sees through this empty asm and re-loads them from the
-  // parameter bank per pair batch; forcing them into registers with an opaque add costs 8
-  // registers and measured 4 % slower, DESIGN.md §6.)
-  float c_contact2 = P.contact2, c_mcollide = -P.c_collide, c_k_rise = P.k_rise,
-        c_b_rise = P.b_rise, c_nk_fall = P.nk_fall, c_b_fall = P.b_fall, c_inv_fov = P.inv_fov,
-        c_fv = P.fv, c_inv_dv = P.inv_dv;
-  asm volatile("" : "+f"(c_contact2), "+f"(c_mcollide), "+f"(c_k_rise), "+f"(c_b_rise),
-               "+f"(c_nk_fall), "+f"(c_b_fall), "+f"(c_inv_fov), "+f"(c_fv), "+f"(c_inv_dv));
-  const uint32_t qstride = NQ * kSenseWarps * gridDim.y;
-  for (uint32_t q0 = qb + NQ * (blockIdx.y * kSenseWarps + warp); q0 < qe; q0 += qstride) {
+    __syncthreads();
+    const int nseg = s_nseg;
+    const uint32_t qb = item.y, qe = min(cs[cl + 1], item.y + (uint32_t)chunk_q);
+    const uint32_t qstride = NQ * kSenseWarps;
+    for (uint32_t q0 = qb + NQ * warp; q0 < qe; q0 += qstride) {
     float4 me[NQ];
     bool live[NQ];
     // Ring queue of query t: kQueue float4 entries at byte address qbase[t] (aligned to the
@@ -1005,6 +1044,7 @@ __global__ void __launch_bounds__(kSenseWarps * 32, kSenseMinBlocks) k_sense(
       else emit(std::false_type{});
     }
     __syncwarp();
+    }
   }
 }
 
