@@ -251,6 +251,29 @@ vg_status launch_check(const char* what) {
   return VG_OK;
 }
 
+// K4 work items (WorkList, appended by K3b / the fused bin): queries per item, chosen so a world has ~4 items per
+// resident CTA when it is small (c1-c3) and whole cells (~54 queries at c5) when it is
+// large; dense cells (clusters) are split into many items.
+int sense_chunk_q(const vg_world* w) {
+  const long long queries = w->slab ? (long long)w->P.N / w->cfg.world_size : w->P.total;
+  const long long slots = (long long)w->n_sm * vg::kSenseMinBlocks * 4;
+  long long q = (queries / slots) / 8 * 8;
+#ifndef VG_SENSE_CHUNK_MAX
+#define VG_SENSE_CHUNK_MAX 128
+#endif
+  return (int)std::max(8LL, std::min(q, (long long)VG_SENSE_CHUNK_MAX));
+}
+
+vg::WorkList work_list(vg_world* w) {
+  vg::WorkList WL{};
+  WL.item = w->work;
+  WL.n = w->work_cnt;
+  WL.chunk_q = sense_chunk_q(w);
+  WL.lo = w->slab ? w->P.G : 0;                           // slab: owned local columns 1..W
+  WL.hi = w->slab ? (w->SL.W + 1) * w->P.G : w->n_cells;
+  return WL;
+}
+
 template <int ENV, bool INTEGRATE, bool BIN>
 vg_status launch_k1(vg_world* w, float4* io, const float4* in, const float2* act, cudaStream_t s) {
   const long long n = w->P.total;
@@ -277,9 +300,10 @@ vg_status scan_cells(vg_world* w, cudaStream_t s) {
 template <int ENV, bool INTEGRATE>
 vg_status launch_fused_bin(vg_world* w, float4* io, const float4* in, const float2* act,
                            cudaStream_t s) {
+  cudaMemsetAsync(w->work_cnt, 0, sizeof(uint32_t), s);   // the replica CTAs append items
   vg::k_replica_bin<ENV, INTEGRATE><<<w->P.R, vg::kRBThreads, 0, s>>>(
       w->P, io, in, act, w->cell_id, w->cell_start, w->sorted, w->perm, w->xo_rec, w->xo_perm,
-      w->xo_xy, w->sub_tab, w->err_dev, w->err_flag);
+      w->xo_xy, w->sub_tab, work_list(w), w->err_dev, w->err_flag);
   if (vg_status st = launch_check("k_replica_bin")) return st;
   w->binned = true;
   return VG_OK;
@@ -291,13 +315,13 @@ vg_status bin_rest(vg_world* w, const float4* state, cudaStream_t s, bool prof =
   if (vg_status st = scan_cells(w, s)) return st;
   if (prof) prof_mark(w, 2, s);
   vg::k_scatter<ENV><<<(unsigned)((n + 255) / 256), 256, 0, s>>>(
-      w->P, state, w->cell_id, w->slot, w->cell_start, w->tmp_rec, w->tmp_id);
+      w->P, state, w->cell_id, w->slot, w->cell_start, w->tmp_rec, w->tmp_id, w->work_cnt);
   if (vg_status st = launch_check("k_scatter")) return st;
   if (prof) prof_mark(w, 3, s);
   const long long threads = (long long)(w->n_cells + 1) * 32;   // + the sentinel row
   vg::k_cell_sort<<<(unsigned)((threads + 255) / 256), 256, 0, s>>>(
       w->P, w->n_cells, w->slab ? 1 : 0, w->cell_start, w->tmp_rec, w->tmp_id, w->sorted,
-      w->perm, w->xo_rec, w->xo_perm, w->xo_xy, w->sub_tab);
+      w->perm, w->xo_rec, w->xo_perm, w->xo_xy, w->sub_tab, work_list(w));
   if (vg_status st = launch_check("k_cell_sort")) return st;
   if (prof) prof_mark(w, 4, s);
   w->binned = true;
@@ -320,19 +344,6 @@ vg::Outs to_outs(const vg_world* w, const vg_outputs* o) {
   const long long rows = w->slab ? (long long)w->P.N : w->P.total;
   r.fast = (all && rows * (w->P.obs_dim + 1) < (1LL << 31)) ? 1 : 0;
   return r;
-}
-
-// K4 work items (k_sense_work): queries per item, chosen so a world has ~4 items per
-// resident CTA when it is small (c1-c3) and whole cells (~54 queries at c5) when it is
-// large; dense cells (clusters) are split into many items.
-int sense_chunk_q(const vg_world* w) {
-  const long long queries = w->slab ? (long long)w->P.N / w->cfg.world_size : w->P.total;
-  const long long slots = (long long)w->n_sm * vg::kSenseMinBlocks * 4;
-  long long q = (queries / slots) / 8 * 8;
-#ifndef VG_SENSE_CHUNK_MAX
-#define VG_SENSE_CHUNK_MAX 128
-#endif
-  return (int)std::max(8LL, std::min(q, (long long)VG_SENSE_CHUNK_MAX));
 }
 
 // K4's candidate reads hit L1: cap the shared-memory carve-out so the resident CTAs' shared
@@ -369,9 +380,6 @@ void set_kernel_attributes() {
 template <int ENV, bool VISION, bool SLAB>
 void sense_kernel(vg_world* w, int cells, const vg::Outs& O, cudaStream_t s) {
   const int cq = sense_chunk_q(w);
-  cudaMemsetAsync(w->work_cnt, 0, sizeof(uint32_t), s);
-  vg::k_sense_work<SLAB><<<(unsigned)((cells + 255) / 256), 256, 0, s>>>(
-      w->P, w->SL, w->cell_start, cells, cq, w->work, w->work_cnt);
   // items <= cells + queries / chunk_q (+1): an upper bound, surplus CTAs exit at once
   const long long queries = w->slab ? (long long)w->P.N : w->P.total;
   const unsigned grid = (unsigned)std::min<long long>(cells + queries / cq + 1, w->work_cap);
@@ -411,12 +419,12 @@ vg_status slab_bin(vg_world* w, cudaStream_t s) {
   if (vg_status st = launch_check("k_slab_keys")) return st;
   if (vg_status st = scan_cells(w, s)) return st;
   vg::k_slab_scatter<ENV><<<nb, 256, 0, s>>>(w->P, w->SB, w->cell_id, w->slot, w->cell_start,
-                                              w->tmp_rec, w->tmp_id);
+                                              w->tmp_rec, w->tmp_id, w->work_cnt);
   if (vg_status st = launch_check("k_slab_scatter")) return st;
   const long long threads = (long long)(w->n_cells + 1) * 32;   // + the sentinel row
   vg::k_cell_sort<<<(unsigned)((threads + 255) / 256), 256, 0, s>>>(
       w->P, w->n_cells, w->slab ? 1 : 0, w->cell_start, w->tmp_rec, w->tmp_id, w->sorted,
-      w->perm, w->xo_rec, w->xo_perm, w->xo_xy, w->sub_tab);
+      w->perm, w->xo_rec, w->xo_perm, w->xo_xy, w->sub_tab, work_list(w));
   if (vg_status st = launch_check("k_cell_sort")) return st;
   w->binned = true;
   return VG_OK;
@@ -599,8 +607,7 @@ vg_status vg_world_query(const vg_world* w, vg_world_info* info) {
   info->total_agents = w->P.total;
   info->scratch_bytes = (int64_t)w->scratch_bytes;
   const int scan_k = (w->n_cells > vg::kScanSmallMax) ? 2 : 1;
-  // (+1: the K4 work list; the memset of its counters is not a kernel)
-  info->kernels_per_step = w->slab ? 7 + scan_k : (w->fused_bin ? 3 : 5 + scan_k);
+  info->kernels_per_step = w->slab ? 6 + scan_k : (w->fused_bin ? 2 : 4 + scan_k);
   return VG_OK;
 }
 

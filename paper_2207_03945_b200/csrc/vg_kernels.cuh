@@ -289,8 +289,9 @@ template <int ENV>
 __global__ void __launch_bounds__(256) k_scatter(
     Params P, const float4* __restrict__ state, const uint32_t* __restrict__ cell_id,
     const uint32_t* __restrict__ slot, const uint32_t* __restrict__ cell_start,
-    float4* __restrict__ tmp_rec, uint32_t* __restrict__ tmp_id) {
+    float4* __restrict__ tmp_rec, uint32_t* __restrict__ tmp_id, uint32_t* __restrict__ work_n) {
   const long long gi = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (gi == 0) *work_n = 0u;                          // K3b appends the K4 work items next
   if (gi >= P.total) return;
   const int r = (int)(gi / P.N);
   const int i = (int)(gi - (long long)r * P.N);
@@ -299,6 +300,21 @@ __global__ void __launch_bounds__(256) k_scatter(
   if (ENV == kTag) s.w = (i >= P.first_chaser) ? 1.f : 0.f;   // type in the sorted record
   tmp_rec[pos] = s;
   tmp_id[pos] = (uint32_t)i;
+}
+
+// K4 work items: every sensed cell's queries in chunks of chunk_q as items
+// (sensed-cell index, first query), appended by the binning kernel that finishes the cell
+// (K3b, or pass 3 of the fused bin); K4 runs one CTA per item, so dense cells are split.
+struct WorkList {
+  uint2* item;
+  uint32_t* n;          // item count (zeroed by the kernel before the appending one)
+  int chunk_q;
+  int lo, hi;           // local cells [lo, hi) are sensed, as item cell index (cell - lo)
+};
+
+__device__ __forceinline__ uint32_t work_chunks(const WorkList& WL, int cell, uint32_t m) {
+  return (cell >= WL.lo && cell < WL.hi) ? (m + (uint32_t)WL.chunk_q - 1u) / (uint32_t)WL.chunk_q
+                                         : 0u;
 }
 
 // --------------------------------------------------------------------------------- K3b
@@ -382,9 +398,27 @@ __global__ void __launch_bounds__(256) k_cell_sort(
     Params P, int n_cells, int axis_y, const uint32_t* __restrict__ cell_start,
     const float4* __restrict__ tmp_rec, const uint32_t* __restrict__ tmp_id,
     float4* __restrict__ sorted, uint32_t* __restrict__ perm, float4* __restrict__ xo_rec,
-    uint32_t* __restrict__ xo_perm, float2* __restrict__ xo_xy, uint32_t* __restrict__ sub_tab) {
+    uint32_t* __restrict__ xo_perm, float2* __restrict__ xo_xy, uint32_t* __restrict__ sub_tab,
+    WorkList WL) {
   const int cell = (int)(((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5);
-  const int lane = threadIdx.x & 31;
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  // K4 work items of this block's 8 cells: one atomic per block.
+  __shared__ uint32_t s_nch[8], s_base;
+  const uint32_t b0 = (cell < n_cells) ? cell_start[cell] : 0u;
+  const uint32_t m0 = (cell < n_cells) ? cell_start[cell + 1] - b0 : 0u;
+  if (lane == 0) s_nch[wib] = (cell < n_cells) ? work_chunks(WL, cell, m0) : 0u;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    uint32_t t = 0;
+    for (int k = 0; k < 8; ++k) { const uint32_t c = s_nch[k]; s_nch[k] = t; t += c; }
+    s_base = t ? atomicAdd(WL.n, t) : 0u;
+  }
+  __syncthreads();
+  if (cell < n_cells) {
+    const uint32_t nch = work_chunks(WL, cell, m0), at = s_base + s_nch[wib];
+    for (uint32_t k = lane; k < nch; k += 32)
+      WL.item[at + k] = make_uint2((uint32_t)(cell - WL.lo), b0 + k * (uint32_t)WL.chunk_q);
+  }
   if (cell > n_cells) return;
   const uint32_t b = cell_start[cell];
   if (cell == n_cells) {
@@ -435,7 +469,7 @@ __global__ void __launch_bounds__(kRBThreads, 2) k_replica_bin(
     const float2* __restrict__ actions, uint32_t* __restrict__ cell_id,
     uint32_t* __restrict__ cell_start, float4* __restrict__ sorted,
     uint32_t* __restrict__ perm, float4* __restrict__ xo_rec, uint32_t* __restrict__ xo_perm,
-    float2* __restrict__ xo_xy, uint32_t* __restrict__ sub_tab,
+    float2* __restrict__ xo_xy, uint32_t* __restrict__ sub_tab, WorkList WL,
     unsigned long long* __restrict__ err, volatile uint32_t* flag) {
   constexpr int NW = kRBThreads / 32;
   __shared__ uint32_t s_wc[NW][kRBMaxCells + 1];     // per-warp counts, then offsets (+1: banks)
@@ -534,6 +568,32 @@ __global__ void __launch_bounds__(kRBThreads, 2) k_replica_bin(
       run += v[e];
     }
     if (r == (int)gridDim.x - 1 && lane == 0) cell_start[(size_t)P.R * C] = (uint32_t)P.total;
+    // K4 work items of this replica's cells: one atomic per replica
+    uint32_t nch[8], nsum = 0;
+#pragma unroll
+    for (int e = 0; e < 8; ++e) {
+      const int c = lane * 8 + e;
+      nch[e] = (c < C) ? work_chunks(WL, r * C + c, v[e]) : 0u;
+      nsum += nch[e];
+    }
+    uint32_t ninc = nsum;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t y = __shfl_up_sync(kFull, ninc, o);
+      if (lane >= o) ninc += y;
+    }
+    uint32_t wbase = 0u;
+    if (lane == 31 && ninc > 0u) wbase = atomicAdd(WL.n, ninc);
+    uint32_t at = __shfl_sync(kFull, wbase, 31) + ninc - nsum;
+    uint32_t qs = (uint32_t)base + inc - sum;             // this lane's first cell start
+#pragma unroll
+    for (int e = 0; e < 8; ++e) {
+      for (uint32_t k = 0; k < nch[e]; ++k)
+        WL.item[at + k] = make_uint2((uint32_t)(r * C + lane * 8 + e),
+                                     qs + k * (uint32_t)WL.chunk_q);
+      at += nch[e];
+      qs += v[e];
+    }
   }
   __syncthreads();
   // ---- pass 2: in-order walk of this warp's range, stable positions, scatter
@@ -639,38 +699,6 @@ struct __align__(16) Seg {
   float plo, phi;    // the run's extent across its axis (shifted frame, widened by the margin)
   int cbase, a0, a1;
 };
-
-// K4 work list: for every sensed cell (replica: all cells; slab: the owned W x G), items
-// (cell, first query) covering its queries in chunks of chunk_q; warp-aggregated append.
-template <bool SLAB>
-__global__ void __launch_bounds__(256) k_sense_work(Params P, Slab SL,
-                                                    const uint32_t* __restrict__ cell_start,
-                                                    int n_cells, int chunk_q,
-                                                    uint2* __restrict__ work,
-                                                    uint32_t* __restrict__ work_n) {
-  const int c = blockIdx.x * blockDim.x + threadIdx.x;
-  const int lane = threadIdx.x & 31;
-  uint32_t nch = 0u, qb = 0u;
-  if (c < n_cells) {
-    const int r = SLAB ? 0 : c / P.G2;
-    const int cl = SLAB ? (1 + c / P.G) * P.G + c % P.G : c - r * P.G2;
-    const uint32_t* cs = cell_start + (size_t)r * P.G2;
-    qb = cs[cl];
-    nch = (cs[cl + 1] - qb + (uint32_t)chunk_q - 1u) / (uint32_t)chunk_q;
-  }
-  uint32_t incl = nch;
-#pragma unroll
-  for (int o = 1; o < 32; o <<= 1) {
-    const uint32_t y = __shfl_up_sync(kFull, incl, o);
-    if (lane >= o) incl += y;
-  }
-  uint32_t base = 0u;
-  if (lane == 31 && incl > 0u) base = atomicAdd(work_n, incl);
-  base = __shfl_sync(kFull, base, 31) + incl - nch;
-  for (uint32_t k = 0; k < nch; ++k)
-    work[base + k] = make_uint2((uint32_t)c, qb + k * (uint32_t)chunk_q);
-  (void)SL;
-}
 
 template <int ENV, bool VISION, bool SLAB, bool RAY>
 __global__ void __launch_bounds__(kSenseWarps * 32, kSenseMinBlocks) k_sense(
@@ -1219,7 +1247,9 @@ __global__ void __launch_bounds__(256) k_slab_scatter(Params P, SlabBufs B,
                                                       const uint32_t* __restrict__ slot,
                                                       const uint32_t* __restrict__ cell_start,
                                                       float4* __restrict__ tmp_rec,
-                                                      uint32_t* __restrict__ tmp_id) {
+                                                      uint32_t* __restrict__ tmp_id,
+                                                      uint32_t* __restrict__ work_n) {
+  if (blockIdx.x == 0 && threadIdx.x == 0) *work_n = 0u;   // K3b appends the K4 items next
   const uint32_t n = min(*B.n_loc, B.cap_loc);
   for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n;
        i += gridDim.x * blockDim.x) {
