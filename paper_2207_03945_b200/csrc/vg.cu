@@ -695,10 +695,12 @@ bool same_outs(const vg_outputs& a, const vg_outputs& b) {
          a.agent_id == b.agent_id;
 }
 
-vg_status step_graph(vg_world* w, float4* io, const float2* a, const vg_outputs* outs,
-                     cudaStream_t s) {
+// Launch the kernel sequence `launch` as a cached CUDA graph keyed by (k1, k2, outs).
+extern "C++" template <typename F>
+vg_status cached_graph(vg_world* w, const void* k1, const void* k2, const vg_outputs* outs,
+                       cudaStream_t s, const char* what, F&& launch) {
   for (auto& g : w->graphs) {
-    if (g.state == io && g.actions == a && same_outs(g.outs, *outs)) {
+    if (g.state == k1 && g.actions == k2 && same_outs(g.outs, *outs)) {
       g.last_use = ++w->graph_clock;
       VG_CUDA(cudaGraphLaunch(g.exec, s));
       w->binned = true;
@@ -707,18 +709,18 @@ vg_status step_graph(vg_world* w, float4* io, const float2* a, const vg_outputs*
   }
   if (!w->cap_stream) VG_CUDA(cudaStreamCreateWithFlags(&w->cap_stream, cudaStreamNonBlocking));
   VG_CUDA(cudaStreamBeginCapture(w->cap_stream, cudaStreamCaptureModeThreadLocal));
-  vg_status st = launch_step(w, io, a, outs, w->cap_stream);
+  vg_status st = launch(w->cap_stream);
   cudaGraph_t graph = nullptr;
   cudaError_t e = cudaStreamEndCapture(w->cap_stream, &graph);
   if (st) {
     if (graph) cudaGraphDestroy(graph);
     return st;
   }
-  if (e != cudaSuccess) return fail(VG_ECUDA, "vg_step graph capture: %s", cudaGetErrorString(e));
+  if (e != cudaSuccess) return fail(VG_ECUDA, "%s graph capture: %s", what, cudaGetErrorString(e));
   cudaGraphExec_t exec = nullptr;
   e = cudaGraphInstantiate(&exec, graph, 0);
   cudaGraphDestroy(graph);
-  if (e != cudaSuccess) return fail(VG_ECUDA, "vg_step graph instantiate: %s", cudaGetErrorString(e));
+  if (e != cudaSuccess) return fail(VG_ECUDA, "%s graph instantiate: %s", what, cudaGetErrorString(e));
   if (w->graphs.size() >= 16) {                     // evict the least recently used
     size_t lru = 0;
     for (size_t i = 1; i < w->graphs.size(); ++i)
@@ -726,10 +728,26 @@ vg_status step_graph(vg_world* w, float4* io, const float2* a, const vg_outputs*
     cudaGraphExecDestroy(w->graphs[lru].exec);
     w->graphs.erase(w->graphs.begin() + lru);
   }
-  w->graphs.push_back({io, a, *outs, exec, ++w->graph_clock});
+  w->graphs.push_back({k1, k2, *outs, exec, ++w->graph_clock});
   VG_CUDA(cudaGraphLaunch(exec, s));
   w->binned = true;
   return VG_OK;
+}
+
+vg_status step_graph(vg_world* w, float4* io, const float2* a, const vg_outputs* outs,
+                     cudaStream_t s) {
+  return cached_graph(w, io, a, outs, s, "vg_step",
+                      [&](cudaStream_t cs) { return launch_step(w, io, a, outs, cs); });
+}
+
+// Graphs are used when enabled, not profiling, and the caller's stream is not capturing.
+bool graph_ok(vg_world* w, cudaStream_t s) {
+  cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+  if (cudaStreamIsCapturing(s, &cap) != cudaSuccess) {
+    cudaGetLastError();
+    cap = cudaStreamCaptureStatusActive;            // unknown: stay on the eager path
+  }
+  return w->graphs_enabled && w->prof_n >= w->prof_max && cap == cudaStreamCaptureStatusNone;
 }
 
 }  // namespace
@@ -743,13 +761,7 @@ vg_status vg_step(vg_world* w, float* state, const float* actions, const vg_outp
   cudaStream_t s = as_stream(stream);
   float4* io = reinterpret_cast<float4*>(state);
   const float2* a = reinterpret_cast<const float2*>(actions);
-  cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
-  if (cudaStreamIsCapturing(s, &cap) != cudaSuccess) {
-    cudaGetLastError();
-    cap = cudaStreamCaptureStatusActive;            // unknown: stay on the eager path
-  }
-  if (w->graphs_enabled && w->prof_n >= w->prof_max && cap == cudaStreamCaptureStatusNone)
-    return step_graph(w, io, a, outs, s);
+  if (graph_ok(w, s)) return step_graph(w, io, a, outs, s);
   vg_status st = launch_step(w, io, a, outs, s);
   if (w->prof_n < w->prof_max) ++w->prof_n;
   return st;
@@ -812,19 +824,13 @@ vg_status vg_slab_load(vg_world* w, const float* state_global, void* stream) {
   return slab_bin<vg::kTag>(w, s);
 }
 
-vg_status vg_slab_begin(vg_world* w, const float* actions, void* stream) {
-  if (vg_status st = need_slab(w, true, "vg_slab_begin")) return st;
-  if (!actions) return fail(VG_EINVAL, "actions: NULL");
-  if (!w->binned) return fail(VG_EINVAL, "vg_slab_begin: call vg_slab_load first");
-  DeviceGuard dg_(w->device);
-  if (vg_status st = check_pending(w)) return st;
-  cudaStream_t s = as_stream(stream);
+namespace {
+vg_status slab_begin_launch(vg_world* w, const float2* a, cudaStream_t s) {
   prof_mark(w, 0, s);
   VG_CUDA(cudaMemsetAsync(w->loc_n, 0, sizeof(uint32_t), s));
   VG_CUDA(cudaMemsetAsync(w->SB.send_l, 0, 16, s));
   VG_CUDA(cudaMemsetAsync(w->SB.send_r, 0, 16, s));
   const unsigned nb = stride_blocks((size_t)w->P.N / w->cfg.world_size + 1);
-  const float2* a = reinterpret_cast<const float2*>(actions);
   if (w->P.env == vg::kFlock)
     vg::k_slab_begin<vg::kFlock><<<nb, 256, 0, s>>>(w->P, w->SL, w->SB, w->cell_start, w->xo_rec,
                                                      w->xo_perm, a, w->err_dev, w->err_flag);
@@ -834,6 +840,24 @@ vg_status vg_slab_begin(vg_world* w, const float* actions, void* stream) {
   vg_status st = launch_check("k_slab_begin");
   prof_mark(w, 1, s);
   return st;
+}
+}  // namespace
+
+vg_status vg_slab_begin(vg_world* w, const float* actions, void* stream) {
+  if (vg_status st = need_slab(w, true, "vg_slab_begin")) return st;
+  if (!actions) return fail(VG_EINVAL, "actions: NULL");
+  if (!w->binned) return fail(VG_EINVAL, "vg_slab_begin: call vg_slab_load first");
+  DeviceGuard dg_(w->device);
+  if (vg_status st = check_pending(w)) return st;
+  cudaStream_t s = as_stream(stream);
+  const float2* a = reinterpret_cast<const float2*>(actions);
+  static const char kBeginKey = 0;                  // graph key: (actions, &kBeginKey, {})
+  if (graph_ok(w, s)) {
+    const vg_outputs none{};
+    return cached_graph(w, a, &kBeginKey, &none, s, "vg_slab_begin",
+                        [&](cudaStream_t cs) { return slab_begin_launch(w, a, cs); });
+  }
+  return slab_begin_launch(w, a, s);
 }
 
 vg_status vg_slab_get_io(vg_world* w, vg_slab_io* io) {
@@ -870,11 +894,8 @@ vg_status vg_slab_exchange_loopback(vg_world* const* ws, int32_t n, void* stream
   return VG_OK;
 }
 
-vg_status vg_slab_finish(vg_world* w, const vg_outputs* outs, void* stream) {
-  if (vg_status st = need_slab(w, true, "vg_slab_finish")) return st;
-  DeviceGuard dg_(w->device);
-  if (!outs) return fail(VG_EINVAL, "outs: NULL");
-  cudaStream_t s = as_stream(stream);
+namespace {
+vg_status slab_finish_launch(vg_world* w, const vg_outputs* outs, cudaStream_t s) {
   vg::k_slab_unpack<<<stride_blocks(2ull * w->SB.cap_msg), 256, 0, s>>>(w->SB);
   if (vg_status st = launch_check("k_slab_unpack")) return st;
   prof_mark(w, 2, s);
@@ -884,6 +905,20 @@ vg_status vg_slab_finish(vg_world* w, const vg_outputs* outs, void* stream) {
   prof_mark(w, 4, s);
   st = launch_sense<true>(w, outs, s);
   prof_mark(w, 5, s);
+  return st;
+}
+}  // namespace
+
+vg_status vg_slab_finish(vg_world* w, const vg_outputs* outs, void* stream) {
+  if (vg_status st = need_slab(w, true, "vg_slab_finish")) return st;
+  DeviceGuard dg_(w->device);
+  if (!outs) return fail(VG_EINVAL, "outs: NULL");
+  cudaStream_t s = as_stream(stream);
+  static const char kFinishKey = 0;                 // graph key: (nullptr, &kFinishKey, outs)
+  if (graph_ok(w, s))
+    return cached_graph(w, nullptr, &kFinishKey, outs, s, "vg_slab_finish",
+                        [&](cudaStream_t cs) { return slab_finish_launch(w, outs, cs); });
+  vg_status st = slab_finish_launch(w, outs, s);
   if (w->prof_n < w->prof_max) ++w->prof_n;
   return st;
 }
