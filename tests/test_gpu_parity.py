@@ -131,6 +131,30 @@ def test_sector_model_variants(cuda, fov, v):
     run_and_check(p, vi.init_state(p, seed=11), 2)
 
 
+def test_c5_clustered_sampled_rows(cuda):
+    # The stress state at full size: cells with ~2000 agents are split into many K4 work
+    # items (chunk_q = 128); rows sampled from the densest cells and at random.
+    torch = _torch()
+    p = vi.workload("c5")
+    w = make_world(p)
+    out = w.alloc_outputs()
+    st0 = vi.clustered_state(p, seed=2)
+    w.bin(dev(st0))
+    w.sense(out)
+    torch.cuda.synchronize()
+    bins = {k: host(v) for k, v in w.get_bins().items()}
+    parity.check_bins(p, bins, st0)
+    counts = np.diff(bins["cell_start"].astype(np.int64))
+    dense = np.argsort(counts)[-4:]                       # the four densest cells
+    rng = np.random.default_rng(3)
+    rows = [int(bins["perm"][0][bins["cell_start"][c] + rng.integers(0, counts[c])])
+            for c in dense for _ in range(6)]
+    rows += list(rng.choice(p.n_agents, 24, replace=False))
+    parity.check_sense(p, st0[0], outs_np(out, 0), rows=np.array(rows))
+    assert counts.max() > 8 * 128                         # really split over many items
+    w.close()
+
+
 @pytest.mark.parametrize("case", ["lone", "pair", "sparse", "g3", "many_replicas",
                                   "clustered", "tag_no_chasers", "tag_all_chasers"])
 def test_edge_cases(cuda, case):
