@@ -177,6 +177,31 @@ def test_dyadic_world_exact_thresholds():
     assert o["n_collide"][2] >= 1
 
 
+def test_periodic_translation_invariance():
+    # Torus (A9): translating every position by the same vector (mod L) changes nothing an
+    # agent senses.  On a 2^-8 lattice the translated coordinates are exact, so every output
+    # is identical, including pairs that now wrap across the seam and pairs exactly on
+    # the thresholds.
+    p = vi.flock_params(600, width=128.0, d_v=8.0)
+    rng = np.random.default_rng(12)
+    q = rng.integers(0, 128 * 256, size=(600, 2))
+    q[1] = q[0] + [8 * 256, 0]                            # on the radius
+    q[3] = q[2] + [0, 128]                                # on the contact distance
+    q %= 128 * 256
+    st = np.zeros((1, 600, 4))
+    st[0, :, 2] = rng.integers(0, 6 * 256, 600) / 256.0   # headings on the lattice too
+    st[0, :, 3] = 0.275
+    outs = []
+    for shift in ([0, 0], [64 * 256 + 17, 3 * 256 + 5], [127 * 256, 100 * 256 + 255]):
+        st[0, :, :2] = ((q + np.array(shift)) % (128 * 256)) / 256.0
+        outs.append(sense_all(p, st))
+    for o in outs[1:]:
+        for k in ("n_neigh", "n_collide", "sector_occ"):
+            assert np.array_equal(o[k], outs[0][k]), k
+        assert np.array_equal(o["obs"], outs[0]["obs"])
+        assert np.allclose(o["reward"], outs[0]["reward"], rtol=0, atol=1e-12)
+
+
 def _rot90(p, st):
     x, y, th = st[0, :, 0], st[0, :, 1], st[0, :, 2]
     out = st.copy()
