@@ -95,6 +95,14 @@ def test_c4_full_size_sampled_replicas(cuda):
     run_and_check(p, st0, 1, replicas=[0, 1, 511, 1023])
 
 
+def test_64bit_output_indexing(cuda):
+    # 3,500 replicas x 5,000 agents: rows x obs_dim > 2^31, so K4 takes its NULL-checked
+    # 64-bit-index path; first, middle and last replicas against the oracle.
+    p = vi.workload("c4").replace(n_replicas=3500)
+    assert p.total_agents * 130 > 2 ** 31
+    run_and_check(p, vi.init_state(p, seed=5), 1, replicas=[0, 1750, 3499], check_bins=False)
+
+
 def test_c5_full_size_sampled_rows(cuda):
     # configs[4]: 1M-agent world; bins bit-exact in full, sensing on sampled rows against
     # all N, plus size-independent properties (sum rule, closed-form expectations).
