@@ -300,7 +300,7 @@ vg_status scan_cells(vg_world* w, cudaStream_t s) {
 template <int ENV, bool INTEGRATE>
 vg_status launch_fused_bin(vg_world* w, float4* io, const float4* in, const float2* act,
                            cudaStream_t s) {
-  cudaMemsetAsync(w->work_cnt, 0, sizeof(uint32_t), s);   // the replica CTAs append items
+  VG_CUDA(cudaMemsetAsync(w->work_cnt, 0, sizeof(uint32_t), s));   // replica CTAs append items
   vg::k_replica_bin<ENV, INTEGRATE><<<w->P.R, vg::kRBThreads, 0, s>>>(
       w->P, io, in, act, w->cell_id, w->cell_start, w->sorted, w->perm, w->xo_rec, w->xo_perm,
       w->xo_xy, w->sub_tab, work_list(w), w->err_dev, w->err_flag);
