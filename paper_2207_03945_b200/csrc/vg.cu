@@ -380,17 +380,17 @@ void set_kernel_attributes() {
 template <int ENV, bool VISION, bool SLAB>
 void sense_kernel(vg_world* w, int cells, const vg::Outs& O, cudaStream_t s) {
   const int cq = sense_chunk_q(w);
-  // items <= cells + queries / chunk_q (+1): an upper bound, surplus CTAs exit at once
+  // one CTA per sensed cell + an upper bound on the overflow items (surplus CTAs exit)
   const long long queries = w->slab ? (long long)w->P.N : w->P.total;
-  const unsigned grid = (unsigned)std::min<long long>(cells + queries / cq + 1, w->work_cap);
+  const unsigned grid = (unsigned)(cells + std::min<long long>(queries / cq + 1, w->work_cap));
   if (w->cfg.vision == VG_VISION_RAY)
     vg::k_sense<ENV, VISION, SLAB, true><<<grid, vg::kSenseWarps * 32, 0, s>>>(
         w->P, w->cell_start, w->xo_rec, w->xo_xy, w->xo_perm, O, w->SL, w->ray_dir, w->sub_tab,
-        w->work, w->work_cnt, cq);
+        w->work, w->work_cnt, cq, cells);
   else
     vg::k_sense<ENV, VISION, SLAB, false><<<grid, vg::kSenseWarps * 32, 0, s>>>(
         w->P, w->cell_start, w->xo_rec, w->xo_xy, w->xo_perm, O, w->SL, w->ray_dir, w->sub_tab,
-        w->work, w->work_cnt, cq);
+        w->work, w->work_cnt, cq, cells);
 }
 
 template <bool VISION>

@@ -302,9 +302,11 @@ __global__ void __launch_bounds__(256) k_scatter(
   tmp_id[pos] = (uint32_t)i;
 }
 
-// K4 work items: every sensed cell's queries in chunks of chunk_q as items
-// (sensed-cell index, first query), appended by the binning kernel that finishes the cell
-// (K3b, or pass 3 of the fused bin); K4 runs one CTA per item, so dense cells are split.
+// K4 work items: K4 CTA c senses the first chunk_q queries of sensed cell c;
+// a denser cell's further chunks are appended here as items (sensed-cell index, first
+// query) by the binning kernel that finishes the cell (K3b, or the fused bin), and run by
+// the CTAs after the first n_cells — so dense cells are split over many CTAs while the
+// bulk keeps the spatial order of the cell grid.
 struct WorkList {
   uint2* item;
   uint32_t* n;          // item count (zeroed by the kernel before the appending one)
@@ -312,9 +314,10 @@ struct WorkList {
   int lo, hi;           // local cells [lo, hi) are sensed, as item cell index (cell - lo)
 };
 
+// Overflow chunks of a cell (its chunks after the first; K4 CTA c senses the first one).
 __device__ __forceinline__ uint32_t work_chunks(const WorkList& WL, int cell, uint32_t m) {
-  return (cell >= WL.lo && cell < WL.hi) ? (m + (uint32_t)WL.chunk_q - 1u) / (uint32_t)WL.chunk_q
-                                         : 0u;
+  return (cell >= WL.lo && cell < WL.hi && m > (uint32_t)WL.chunk_q)
+             ? (m - 1u) / (uint32_t)WL.chunk_q : 0u;
 }
 
 // --------------------------------------------------------------------------------- K3b
@@ -417,7 +420,7 @@ __global__ void __launch_bounds__(256) k_cell_sort(
   if (cell < n_cells) {
     const uint32_t nch = work_chunks(WL, cell, m0), at = s_base + s_nch[wib];
     for (uint32_t k = lane; k < nch; k += 32)
-      WL.item[at + k] = make_uint2((uint32_t)(cell - WL.lo), b0 + k * (uint32_t)WL.chunk_q);
+      WL.item[at + k] = make_uint2((uint32_t)(cell - WL.lo), b0 + (k + 1u) * (uint32_t)WL.chunk_q);
   }
   if (cell > n_cells) return;
   const uint32_t b = cell_start[cell];
@@ -590,7 +593,7 @@ __global__ void __launch_bounds__(kRBThreads, 2) k_replica_bin(
     for (int e = 0; e < 8; ++e) {
       for (uint32_t k = 0; k < nch[e]; ++k)
         WL.item[at + k] = make_uint2((uint32_t)(r * C + lane * 8 + e),
-                                     qs + k * (uint32_t)WL.chunk_q);
+                                     qs + (k + 1u) * (uint32_t)WL.chunk_q);
       at += nch[e];
       qs += v[e];
     }
@@ -705,7 +708,8 @@ __global__ void __launch_bounds__(kSenseWarps * 32, kSenseMinBlocks) k_sense(
     Params P, const uint32_t* __restrict__ cell_start, const float4* __restrict__ sorted,
     const float2* __restrict__ sorted_xy, const uint32_t* __restrict__ perm, Outs O, Slab SL,
     const float2* __restrict__ ray_dir, const uint32_t* __restrict__ sub_tab,
-    const uint2* __restrict__ work, const uint32_t* __restrict__ work_n, int chunk_q) {
+    const uint2* __restrict__ work, const uint32_t* __restrict__ work_n, int chunk_q,
+    int n_first) {
   // sorted / sorted_xy / perm are the sense-order arrays (xo_* of K3b): within a cell the
   // records ascend in x (replica grid, runs along rows) or y (slab grid, runs along columns).
   __shared__ uint32_t s_min[kSenseWarps][kSenseNQ][kMaxViewSlots];
@@ -734,12 +738,16 @@ __global__ void __launch_bounds__(kSenseWarps * 32, kSenseMinBlocks) k_sense(
         c_fv = P.fv, c_inv_dv = P.inv_dv;
   asm volatile("" : "+f"(c_contact2), "+f"(c_mcollide), "+f"(c_k_rise), "+f"(c_b_rise),
                "+f"(c_nk_fall), "+f"(c_b_fall), "+f"(c_inv_fov), "+f"(c_fv), "+f"(c_inv_dv));
-  // One CTA per work item of k_sense_work: item = (cell, first query), up to chunk_q
-  // queries of that cell — dense cells are split over many CTAs.  The grid is an upper
-  // bound on the item count (cells + queries / chunk_q); surplus CTAs exit at once.
+  // CTA c < n_first: the first chunk_q queries of sensed cell c; CTA n_first + k: overflow
+  // item k (a later chunk of a dense cell).  The grid bounds the item count; surplus CTAs
+  // exit at once.
   {
-    if (blockIdx.x >= *work_n) return;
-    const uint2 item = work[blockIdx.x];
+    uint2 item = make_uint2(blockIdx.x, 0xffffffffu);                 // y: first chunk
+    if ((int)blockIdx.x >= n_first) {
+      const uint32_t k = blockIdx.x - (uint32_t)n_first;
+      if (k >= *work_n) return;
+      item = work[k];
+    }
     const int c = (int)item.x;
   // Replica layout: cell = r G^2 + cy G + cx.  Slab layout: owned local column lcx = 1 + c/G.
   const int r = SLAB ? 0 : c / P.G2;
@@ -801,7 +809,8 @@ __global__ void __launch_bounds__(kSenseWarps * 32, kSenseMinBlocks) k_sense(
   }
     __syncthreads();
     const int nseg = s_nseg;
-    const uint32_t qb = item.y, qe = min(cs[cl + 1], item.y + (uint32_t)chunk_q);
+    const uint32_t qb = (item.y == 0xffffffffu) ? cs[cl] : item.y;
+    const uint32_t qe = min(cs[cl + 1], qb + (uint32_t)chunk_q);
     const uint32_t qstride = NQ * kSenseWarps;
     for (uint32_t q0 = qb + NQ * warp; q0 < qe; q0 += qstride) {
     float4 me[NQ];
