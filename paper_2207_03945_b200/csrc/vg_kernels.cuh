@@ -1,12 +1,16 @@
 // vg_kernels.cuh — sm_100a device kernels of the Vogue environment step.
 //
 // Citations: P:n = PAPER.md line n, S:n = SPEC.md line n, An = reading in DESIGN.md §3.
-// Pipeline of one step (P:190; DESIGN.md §4):
+// Pipeline of one step (P:190; DESIGN.md §6):
 //   K1 k_integrate_bin  integrate + cell id + per-cell histogram slot   (HBM-bound)
 //   K2 k_scan_cells     exclusive scan of the R*G*G cell counts          (latency)
+//      (k_scan_tiles + k_scan_apply above 12,288 cells)
 //   K3 k_scatter        place each agent at cell_start[cell] + slot      (HBM-bound)
-//   K3b k_cell_sort     order each cell by ascending agent id (stable)   (HBM-bound)
+//   K3b k_cell_sort     order each cell by ascending agent id (stable); the K4 sense order
+//                       (sub-bins), window table and overflow work items  (HBM/ALU)
+//   K1-K3b fused        k_replica_bin: one CTA per small replica world
 //   K4 k_sense          3x3-stencil neighbour pass: sector vision + reward (FP32/issue-bound)
+//   slab mode           k_slab_begin / load / unpack / keys / scatter
 // No library kernels: every step of the path runs here.
 #pragma once
 
