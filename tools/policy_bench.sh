@@ -1,3 +1,4 @@
+# Policy (K7) and rollout timing for the in-tree lib and a tanh variant (tools/build_variants.py tanh2:-DVG_TANH_NEWTON=0)
 for v in - tanh2; do
   if [ "$v" = "-" ]; then unset VG_LIB_VARIANT; else export VG_LIB_VARIANT=$v; fi
   timeout 300 python bench.py --steps 10 --warmup 3 --no-cpu-baseline --no-e2e > gpurun_out/pb_$v.json 2>gpurun_out/pb_$v.err

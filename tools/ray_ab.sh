@@ -1,3 +1,4 @@
+# Usage: bash tools/ray_ab.sh "variant ..." — ray-vision bench (2 runs) per build variant ("-" = in-tree lib)
 for v in $1; do
   if [ "$v" = "-" ]; then unset VG_LIB_VARIANT; else export VG_LIB_VARIANT=$v; fi
   for i in 1 2; do

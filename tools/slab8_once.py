@@ -1,3 +1,4 @@
+"""Run the c5 world split into 8 slabs (loopback exchange) for a few steps — the command profiled by ncu for the slab launch list."""
 import sys, os, torch
 sys.path[:0] = ["/root/repo"]
 import vg_inputs as vi
