@@ -130,13 +130,22 @@ def test_c5_full_size_sampled_rows(cuda):
     w.close()
 
 
-@pytest.mark.parametrize("fov,v", [(2 * math.pi, 128), (0.5, 128), (1.0, 7), (4.36, 64)])
+@pytest.mark.parametrize("fov,v", [(2 * math.pi, 128), (0.5, 128), (1.0, 7), (4.36, 64),
+                                   (4.36, 1), (2 * math.pi, 1)])
 def test_sector_model_variants(cuda, fov, v):
     # fov = 2 pi (the seam at phi = pi), narrow sectors (atan2 path: sector-table bins would
     # hold two boundaries), few wide sectors, tag-like v = 64: every sector decision agrees
     # with the oracle up to the bands.
     p = vi.flock_params(2500, width=70.0, d_v=7.0, fov=np.float32(fov), v=v)
     run_and_check(p, vi.init_state(p, seed=11), 2)
+
+
+@pytest.mark.parametrize("grid", [9, 0])
+def test_large_cells_small_radius(cuda, grid):
+    # d_v = 3 in cells of 11.1 (grid 9: a run is ~11 radii long, the windows cut most of it)
+    # and the auto grid (G = 33); sub-bin windows and chord narrowing at other ratios.
+    p = vi.flock_params(4000, width=100.0, d_v=3.0, grid=grid)
+    run_and_check(p, vi.init_state(p, seed=13), 2)
 
 
 def test_c5_clustered_sampled_rows(cuda):
