@@ -545,8 +545,10 @@ def run_ours(args):
         n = p.total_agents if not slab_mode else p.n_agents // world
         obs_b = 4 * w.obs_dim + 4 * w.occ_words + SENSE_BYTES_FIXED
         fused = getattr(w, "kernels_per_step", 5) == 2
-        stage_bytes = {"integrate_bin": (72 if fused else 48) * n, "scan_cells": 8 * w.n_cells,
-                       "scatter": 44 * n, "cell_sort": 40 * n, "sense": obs_b * n}
+        # algorithmic bytes per agent of each stage as designed (DESIGN.md §6 kernel table):
+        # the fused bin and K3b also write the K4 sense order (xo_rec, xo_perm, xo_xy)
+        stage_bytes = {"integrate_bin": (92 if fused else 48) * n, "scan_cells": 8 * w.n_cells,
+                       "scatter": 44 * n, "cell_sort": 68 * n, "sense": obs_b * n}
         stages = {}
         tot_ph = sum(phases.values()) or 1.0
         for k2, ms in phases.items():
