@@ -150,14 +150,17 @@ def measured_peaks():
 
 
 # ------------------------------------------------------------------------- oracle legs
-def oracle_rate(p, seconds: float, seed: int = 0, workers: int | None = None):
+def oracle_rate(p, seconds: float, seed: int = 0, workers: int | None = None,
+                state: str = "uniform"):
     """Oracle agent-steps/s on a bounded sample: integrate all agents of one replica (fp64),
-    then sense a sample of query rows against all N (rows are independent), extrapolated
-    linearly to the replica.  Returns (rate, sample description, cores used)."""
+    then sense a sample of query rows against all N (rows are independent; ray vision adds
+    the ray-disc views of those rows), extrapolated linearly to the replica.  Returns (rate,
+    sample description, cores used)."""
     import oracle
+    from oracle.ray import ray_views
     workers = workers or max(1, len(os.sched_getaffinity(0)))
     q = p.replace(n_replicas=1)
-    st = vi.init_state(q, seed=seed)
+    st = (vi.clustered_state if state == "clustered" else vi.init_state)(q, seed=seed)
     act = vi.actions(q, seed=seed, step=0)
     t0 = time.perf_counter()
     new = oracle.integrate(q, st, act)
@@ -171,6 +174,8 @@ def oracle_rate(p, seconds: float, seed: int = 0, workers: int | None = None):
     rows = rng.choice(q.n_agents, n_rows, replace=False)
     t0 = time.perf_counter()
     oracle.sense(q, new, rows=rows, workers=workers)
+    if q.vision == "ray":
+        ray_views(q, new[0], rows)
     t_sense = time.perf_counter() - t0
     per_agent = t_int / q.n_agents + t_sense / n_rows
     sample = (f"one replica of N={q.n_agents}: fp64 integrate of all N ({t_int:.2f} s) + "
@@ -180,14 +185,15 @@ def oracle_rate(p, seconds: float, seed: int = 0, workers: int | None = None):
 
 
 def run_reference(args):
+    import oracle
     rank, _, world = rank_info()
     if rank != 0:
         return 0
-    p = vi.workload(args.config)
+    p = vi.workload(args.config).replace(vision=args.vision)
     per_step = max(1.0, min(10.0, 150.0 / max(1, args.steps + args.warmup)))
     rates = []
     for k in range(args.warmup + args.steps):
-        rate, sample, cores = oracle_rate(p, per_step, seed=k)
+        rate, sample, cores = oracle_rate(p, per_step, seed=k, state=STATE)
         if k >= args.warmup:
             rates.append(rate)
     value = statistics.median(rates)
@@ -197,7 +203,10 @@ def run_reference(args):
         "ms_per_step": 1e3 * p.total_agents / value, "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": {"workload": args.config, "desc": vi.WORKLOAD_DESCRIPTIONS[args.config],
-                   "R": p.n_replicas, "N": p.n_agents},
+                   "R_per_gpu": p.n_replicas, "N": p.n_agents, "G": oracle.grid_size(p),
+                   "vision": args.vision, "state": STATE,
+                   "parallelism": f"host CPU: fp64 oracle, {cores} processes",
+                   "l2": "n/a (CPU)"},
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "oracle",
                          "sample": f"per step: {sample}"},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
