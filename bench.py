@@ -556,7 +556,11 @@ def run_ours(args):
         fused = getattr(w, "kernels_per_step", 5) == 2
         # algorithmic bytes per agent of each stage as designed (DESIGN.md §6 kernel table):
         # the fused bin and K3b also write the K4 sense order (xo_rec, xo_perm, xo_xy)
-        stage_bytes = {"integrate_bin": (92 if fused else 48) * n, "scan_cells": 8 * w.n_cells,
+        if slab_mode:                  # the exchange phase moves two fixed-size messages
+            scan_b = 2 * int(w.slab_io.message_bytes)
+        else:
+            scan_b = 8 * w.n_cells
+        stage_bytes = {"integrate_bin": (92 if fused else 48) * n, "scan_cells": scan_b,
                        "scatter": 44 * n, "cell_sort": 68 * n, "sense": obs_b * n}
         stages = {}
         tot_ph = sum(phases.values()) or 1.0
