@@ -148,6 +148,31 @@ def test_large_cells_small_radius(cuda, grid):
     run_and_check(p, vi.init_state(p, seed=13), 2)
 
 
+def test_long_run_stability(cuda):
+    # 300 steps of the 10^6-agent world through the cached graph with fresh random actions
+    # each step: no device error, state stays in its domain, and the last step still
+    # matches the oracle on sampled rows (no slow corruption, no rare race).
+    torch = _torch()
+    p = vi.workload("c5")
+    w = make_world(p)
+    out = w.alloc_outputs()
+    st = dev(vi.init_state(p, seed=4))
+    g = torch.Generator(device="cuda").manual_seed(7)
+    lo = torch.tensor([-0.1, -0.2], device="cuda")
+    for t in range(300):
+        a = (torch.rand((1, p.n_agents, 2), device="cuda", generator=g) * 2 - 1) * -lo
+        w.step(st, a, out)
+    torch.cuda.synchronize()
+    assert w.sync_errors() == -1
+    cur = host(st)
+    assert (cur[0, :, :2] >= 0).all() and (cur[0, :, :2] < p.width).all()
+    assert (cur[0, :, 2] >= 0).all() and (cur[0, :, 2] < 2 * math.pi).all()
+    assert (cur[0, :, 3] >= p.s_min).all() and (cur[0, :, 3] <= p.s_max).all()
+    rows = np.random.default_rng(9).choice(p.n_agents, 64, replace=False)
+    parity.check_sense(p, cur[0], outs_np(out, 0), rows=rows)
+    w.close()
+
+
 def test_c5_clustered_sampled_rows(cuda):
     # The stress state at full size: cells with ~2000 agents are split into many K4 work
     # items (chunk_q = 128); rows sampled from the densest cells and at random.
