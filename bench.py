@@ -585,7 +585,8 @@ def run_ours(args):
                         # committed) / (live mean k_sense time x 148 SM x 4 issue/clk x clk)
                         cap = 148 * 4 * sm_mhz * 1e6 * sense_s
                         issue = {"warp_instructions": wi, "frac": wi / cap,
-                                 "peak": "148 SM x 4 schedulers x 1 warp-instr/clk"}
+                                 "peak": "148 SM x 4 schedulers x 1 warp-instr/clk",
+                                 "ncu_pct_of_peak": tj.get("pct_of_peak")}
             except Exception:
                 pass
         parity_ev = None                 # committed GPU-vs-oracle statistics (tools/parity_stats.py)

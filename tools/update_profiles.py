@@ -24,9 +24,15 @@ num = lambda k: float(d[k].replace(",", ""))
 rd, wr = num("dram__bytes_read.sum"), num("dram__bytes_write.sum")
 unit = 1e6 if "Mbyte" in rows[1][h.index("dram__bytes_read.sum")] else 1.0
 inst = num("smsp__inst_executed.sum")
+pipes = {k.split("__")[1].split(".")[0]: num(k) for k in (
+    "sm__inst_executed_pipe_fma.avg.pct_of_peak_sustained_active",
+    "sm__inst_executed_pipe_alu.avg.pct_of_peak_sustained_active",
+    "sm__inst_executed_pipe_xu.avg.pct_of_peak_sustained_active",
+    "sm__inst_executed_pipe_lsu.avg.pct_of_peak_sustained_active",
+    "smsp__issue_active.avg.pct_of_peak_sustained_active") if k in d}
 json.dump({"config": "c5", "kernel": f"void k_sense<0, 1, 0, 0> ({tag})",
            "bytes_per_launch": (rd + wr) * unit, "dram_read_bytes": rd * unit,
-           "dram_write_bytes": wr * unit, "warp_instructions": inst,
+           "dram_write_bytes": wr * unit, "warp_instructions": inst, "pct_of_peak": pipes,
            "source": f"ncu --set full ({os.path.basename(rep)}), summary in r1_ncu_summary.md"},
           open(os.path.join(P, "sense_traffic.json"), "w"), indent=1)
 b = json.loads(open(bench).read().strip().splitlines()[-1])
