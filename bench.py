@@ -562,6 +562,15 @@ def run_ours(args):
             scan_b = 8 * w.n_cells
         stage_bytes = {"integrate_bin": (92 if fused else 48) * n, "scan_cells": scan_b,
                        "scatter": 44 * n, "cell_sort": 68 * n, "sense": obs_b * n}
+        # Model bound: every binning stage at the HBM roof + K4 at the larger of
+        # its HBM floor and its algorithmic ALU floor (45 ops per in-radius pair).
+        floor_s = sum(b for k2, b in stage_bytes.items() if k2 != "sense") / (hbm * 1e9)
+        floor_s += max(stage_bytes["sense"] / (hbm * 1e9),
+                       ALG_OPS_PER_PAIR * pairs_local / (alu_peak * 1e12))
+        bound = n / floor_s * world
+        model_bound = {"agent_steps_per_s": bound, "fraction": value / bound,
+                       "basis": "binning stages at the measured HBM peak + k_sense at "
+                                "max(HBM floor, 45 fp32 ops x in-radius pairs / FP32 peak)"}
         stages = {}
         tot_ph = sum(phases.values()) or 1.0
         for k2, ms in phases.items():
@@ -625,6 +634,7 @@ def run_ours(args):
                                   f"in-radius pairs per launch / mean k_sense time; peak = "
                                   f"148 SM x 128 lanes x {sm_mhz:.0f} MHz (1 op/lane/clk)"},
             "stages": stages,
+            "model_bound": model_bound,
             "sanity": san,
             "parity": parity_ev,
             "hbm_peak_gbs": hbm, "peak_source": peak_src,
