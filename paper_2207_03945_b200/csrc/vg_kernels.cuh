@@ -388,7 +388,9 @@ __device__ __forceinline__ void sense_order_cell(const Params& P, int ca, bool a
     if (valid) {
       xo_rec[b + pos] = rec;
       xo_perm[b + pos] = id;
-      xo_xy[b + pos] = make_float2(rec.x, rec.y);        // compact positions for K4
+      // compact positions for K4; tag: the type rides in the sign bit of x (x >= 0, so a
+      // chaser at x = 0 is -0.0)
+      xo_xy[b + pos] = make_float2((P.env == kTag && rec.w != 0.f) ? -rec.x : rec.x, rec.y);
     }
 #pragma unroll
     for (int s = 0; s < kSub; ++s) {
@@ -980,13 +982,15 @@ __global__ void __launch_bounds__(kSenseWarps * 32, kSenseMinBlocks) k_sense(
         const bool two = p0 + 32 < we;                               // warp-uniform
         float ax, ay, bx, by;
         uint32_t ta = 0u, tb = 0u;
-        if (ENV == kFlock) {                 // sorted_xy is padded by 64: no predicate
+        {                                    // sorted_xy is padded by 64: no predicate
           const float2 oa = __ldg(&sorted_xy[pa]), ob = __ldg(&sorted_xy[pb]);
           ax = oa.x; ay = oa.y; bx = ob.x; by = ob.y;
-        } else {
-          ax = ay = bx = by = 0.f;
-          if (va) { const float4 o = __ldg(&sorted[pa]); ax = o.x; ay = o.y; ta = (uint32_t)o.w << 31; }
-          if (vb) { const float4 o = __ldg(&sorted[pb]); bx = o.x; by = o.y; tb = (uint32_t)o.w << 31; }
+          if (ENV == kTag) {                 // type in the sign bit of x (K3b)
+            ta = __float_as_uint(ax) & 0x80000000u;
+            tb = __float_as_uint(bx) & 0x80000000u;
+            ax = fabsf(ax);
+            bx = fabsf(bx);
+          }
         }
         // Slots past the run end get a NaN position: never within d_v of anyone.
         ax = va ? ax + sg.csx : __int_as_float(0x7fc00000);          // exact (Sterbenz)
