@@ -321,7 +321,7 @@ vg_status bin_rest(vg_world* w, const float4* state, cudaStream_t s, bool prof =
   const long long threads = (long long)(w->n_cells + 1) * 32;   // + the sentinel row
   vg::k_cell_sort<<<(unsigned)((threads + 255) / 256), 256, 0, s>>>(
       w->P, w->n_cells, w->slab ? 1 : 0, w->cell_start, w->tmp_rec, w->tmp_id, w->sorted,
-      w->perm, w->xo_rec, w->xo_perm, w->xo_xy, w->sub_tab, work_list(w));
+      w->perm, w->xo_rec, w->xo_perm, w->xo_xy, w->sub_tab, work_list(w), w->slot);
   if (vg_status st = launch_check("k_cell_sort")) return st;
   if (prof) prof_mark(w, 4, s);
   w->binned = true;
@@ -424,7 +424,7 @@ vg_status slab_bin(vg_world* w, cudaStream_t s) {
   const long long threads = (long long)(w->n_cells + 1) * 32;   // + the sentinel row
   vg::k_cell_sort<<<(unsigned)((threads + 255) / 256), 256, 0, s>>>(
       w->P, w->n_cells, w->slab ? 1 : 0, w->cell_start, w->tmp_rec, w->tmp_id, w->sorted,
-      w->perm, w->xo_rec, w->xo_perm, w->xo_xy, w->sub_tab, work_list(w));
+      w->perm, w->xo_rec, w->xo_perm, w->xo_xy, w->sub_tab, work_list(w), w->slot);
   if (vg_status st = launch_check("k_cell_sort")) return st;
   w->binned = true;
   return VG_OK;

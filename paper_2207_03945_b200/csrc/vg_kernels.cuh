@@ -400,6 +400,56 @@ __device__ __forceinline__ void sense_order_cell(const Params& P, int ca, bool a
   }
 }
 
+// Dense cells (m > kRankMax): sort the cell's (id, arrival index) pairs by id with
+// 32-element bitonic blocks in registers and merge passes (merge path per output element),
+// O(m log m) instead of the O(m^2) rank.  Ping-pong scratch: (keys A, vals A) -> (keys B,
+// vals B) -> ...; returns the pair holding the result.  Ids are unique within a world.
+constexpr int kRankMax = 128;
+__device__ __forceinline__ void cell_merge_sort(uint32_t b, int m, uint32_t* ka, uint32_t* va,
+                                                uint32_t* kb, uint32_t* vb, int lane,
+                                                uint32_t*& kout, uint32_t*& vout) {
+  for (int base = 0; base < m; base += 32) {                // ka holds the arrival ids
+    uint32_t k = (base + lane < m) ? ka[b + base + lane] : 0xffffffffu;
+    uint32_t v = (uint32_t)(base + lane);
+#pragma unroll
+    for (int size = 2; size <= 32; size <<= 1) {
+#pragma unroll
+      for (int stride = size >> 1; stride > 0; stride >>= 1) {
+        const uint32_t ok = __shfl_xor_sync(kFull, k, stride), ov = __shfl_xor_sync(kFull, v, stride);
+        const bool take_min = ((lane & stride) == 0) == ((lane & size) == 0 || size == 32);
+        if (take_min ? (ok < k) : (ok > k)) { k = ok; v = ov; }
+      }
+    }
+    __syncwarp();
+    if (base + lane < m) { ka[b + base + lane] = k; va[b + base + lane] = v; }
+  }
+  __syncwarp();
+  uint32_t *sk = ka, *sv = va, *dk = kb, *dv = vb;
+  for (int run = 32; run < m; run <<= 1) {
+    for (int lo = 0; lo < m; lo += 2 * run) {
+      const int mid = min(lo + run, m), hi = min(lo + 2 * run, m);
+      const int nl = mid - lo, nr = hi - mid;
+      for (int o = lane; o < hi - lo; o += 32) {
+        int a = max(0, o - nr), z = min(o, nl);              // left elements among the first o
+        while (a < z) {
+          const int i = (a + z) >> 1;
+          if (sk[b + lo + i] < sk[b + mid + o - i - 1]) a = i + 1; else z = i;
+        }
+        const int j = o - a;
+        const bool left = j >= nr || (a < nl && sk[b + lo + a] < sk[b + mid + j]);
+        const uint32_t src = left ? b + lo + a : b + mid + j;
+        dk[b + lo + o] = sk[src];
+        dv[b + lo + o] = sv[src];
+      }
+    }
+    __syncwarp();
+    uint32_t* t = sk; sk = dk; dk = t;
+    t = sv; sv = dv; dv = t;
+  }
+  kout = sk;
+  vout = sv;
+}
+
 // One warp per cell: rank each member by agent id (ids are unique within a replica) and
 // write it to its stable slot ("ascending order (determinism anchor)"); then the
 // cell's sense order (above).  Warp n_cells writes the table sentinel.
@@ -408,7 +458,7 @@ __global__ void __launch_bounds__(256) k_cell_sort(
     const float4* __restrict__ tmp_rec, const uint32_t* __restrict__ tmp_id,
     float4* __restrict__ sorted, uint32_t* __restrict__ perm, float4* __restrict__ xo_rec,
     uint32_t* __restrict__ xo_perm, float2* __restrict__ xo_xy, uint32_t* __restrict__ sub_tab,
-    WorkList WL) {
+    WorkList WL, uint32_t* __restrict__ scratch) {
   const int cell = (int)(((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5);
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
   // K4 work items of this block's 8 cells: one atomic per block.
@@ -435,7 +485,16 @@ __global__ void __launch_bounds__(256) k_cell_sort(
     return;
   }
   const int m = (int)(cell_start[cell + 1] - b);
-  for (int base = 0; base < m; base += 32) {
+  if (m > kRankMax) {                                   // dense cell: merge sort
+    uint32_t *ks, *vs;
+    cell_merge_sort(b, m, const_cast<uint32_t*>(tmp_id), scratch, perm, xo_perm, lane, ks, vs);
+    for (int k = lane; k < m; k += 32) {
+      const uint32_t id = ks[b + k], src = vs[b + k];
+      sorted[b + k] = tmp_rec[b + src];
+      perm[b + k] = id;
+    }
+  }
+  for (int base = 0; base < (m > kRankMax ? 0 : m); base += 32) {
     const int idx = base + lane;
     const bool valid = idx < m;
     const uint32_t id = valid ? tmp_id[b + idx] : 0xffffffffu;
