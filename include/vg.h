@@ -187,7 +187,8 @@ vg_status vg_sync_errors(vg_world* w, void* stream, int64_t* bad_agent);
  *                   vg_slab_exchange_loopback for P worlds in one process);
  *   vg_slab_finish  append received records, bin owned + ghost agents (stable by global
  *                   id), sense + reward the owned cells.
- * Output rows are the owned agents in (local cell, y, global id) order; outs->agent_id
+ * Output rows are the owned agents in (local cell, y sub-bin of 8, global id) order (K4's
+ * sense order, a function of the state alone); outs->agent_id
  * gives each row's global id; the next vg_slab_begin takes actions[row] in that order.
  * Every per-agent result is bitwise identical to the single-world (replica) path.
  * Buffers: outputs need capacity N rows.  Messages: {u32 count, 3 x u32}, float4 rec[cap],
