@@ -210,6 +210,12 @@ vg::Params derive(const vg_config& c, int g) {
   P.b_rise = -P.k_rise * P.two_dr;
   P.nk_fall = -P.k_fall;
   P.b_fall = P.k_fall * c.d_v;
+  P.fx_k_rise = P.k_rise * 4294967296.0f;
+  P.fx_b_rise = P.b_rise * 4294967296.0f;
+  P.fx_nk_fall = P.nk_fall * 4294967296.0f;
+  P.fx_b_fall = P.b_fall * 4294967296.0f;
+  P.fx_mcollide = -P.c_collide * 4294967296.0f;
+  P.half_v = 0.5f * (float)c.v;
   P.touch_fix = (long long)std::llrint((double)c.r_touch * 4294967296.0);
   P.cell = L / (float)g;
   P.inv_smax = 1.0f / c.s_max;

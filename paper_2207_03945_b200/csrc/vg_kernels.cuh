@@ -41,6 +41,10 @@ struct Params {
   float half_fov, inv_fov, fv;  // fov/2, 1/fov, float(v)
   float c_collide, d_peak, k_rise, k_fall, w_prox;
   float b_rise, nk_fall, b_fall;   // f = min(k_rise d + b_rise, nk_fall d + b_fall) (A5)
+  // The same line pair and -c_collide times 2^32 (exact scalings): K4 evaluates f directly
+  // in fixed-point units, f * 2^32 (A16b), bit-identical to scaling afterwards.
+  float fx_k_rise, fx_b_rise, fx_nk_fall, fx_b_fall, fx_mcollide;
+  float half_v;                    // v / 2: sector coordinate phi v / fov + v / 2 (A3)
   float d_r, cand2, inv_w;         // ray vision: body radius, RN32((d_v + d_r)^2), v / fov
   float cell;                      // RN32(L / G) (K4 windows only)
   float inv_smax;                  // RN32(1 / s_max): obs[v] = s / s_max to <= 1.5 ulp (A24)
@@ -725,9 +729,9 @@ constexpr int kQueue = VG_SENSE_QUEUE;
 __device__ __forceinline__ float vg_atan2(float y, float x) {
   const float ax = fabsf(x), ay = fabsf(y);
   const float mx = fmaxf(ax, ay), mn = fminf(ax, ay);
-  float rc;
-  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(rc) : "f"(mx));       // <= 1 ulp
-  const float t = (mx > 0.f) ? mn * rc : 0.f;
+  float rc;                                 // <= 1 ulp; mx = 0 (then mn = 0) gives t = 0
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(rc) : "f"(fmaxf(mx, 1.17549435e-38f)));
+  const float t = mn * rc;
   const float s = t * t;
   float p = 0.006812420208007097f;
   p = fmaf(p, s, -0.03360610455274582f);
@@ -798,11 +802,11 @@ __global__ void __launch_bounds__(kSenseWarps * 32, kSenseMinBlocks) k_sense(
   // Pair-pass constants.  (ptxas sees through this empty asm and re-loads them from the
   // parameter bank per pair batch; forcing them into registers with an opaque add costs 8
   // registers and measured 4 % slower.)
-  float c_contact2 = P.contact2, c_mcollide = -P.c_collide, c_k_rise = P.k_rise,
-        c_b_rise = P.b_rise, c_nk_fall = P.nk_fall, c_b_fall = P.b_fall, c_inv_fov = P.inv_fov,
-        c_fv = P.fv, c_inv_dv = P.inv_dv;
+  float c_contact2 = P.contact2, c_mcollide = P.fx_mcollide, c_k_rise = P.fx_k_rise,
+        c_b_rise = P.fx_b_rise, c_nk_fall = P.fx_nk_fall, c_b_fall = P.fx_b_fall,
+        c_inv_w = P.inv_w, c_half_v = P.half_v, c_inv_dv = P.inv_dv;
   asm volatile("" : "+f"(c_contact2), "+f"(c_mcollide), "+f"(c_k_rise), "+f"(c_b_rise),
-               "+f"(c_nk_fall), "+f"(c_b_fall), "+f"(c_inv_fov), "+f"(c_fv), "+f"(c_inv_dv));
+               "+f"(c_nk_fall), "+f"(c_b_fall), "+f"(c_inv_w), "+f"(c_half_v), "+f"(c_inv_dv));
   // CTA c < n_first: the first chunk_q queries of sensed cell c; CTA n_first + k: overflow
   // item k (a later chunk of a dense cell).  The grid bounds the item count; surplus CTAs
   // exit at once.
@@ -913,22 +917,29 @@ __global__ void __launch_bounds__(kSenseWarps * 32, kSenseMinBlocks) k_sense(
       const uint32_t tj = (ENV == kTag) ? tagbits >> 31 : 0u;
       const float d2 = e.z;
       const bool contact = d2 <= c_contact2;                          // A6 (inclusive)
-      float rsq;                                   // MUFU.RSQ without the subnormal rescale:
-      asm("rsqrt.approx.ftz.f32 %0, %1;" : "=f"(rsq) : "f"(d2));
-      const float d = (d2 >= 1.17549435e-38f) ? d2 * rsq : 0.f;   // subnormal d^2 -> d = 0
-      // Eq. 1 / Fig. 4 (A5): contact -> -c_collide, else the tent min(rise, fall).
+      // d by the MUFU (~1 ulp; sqrt(0) = 0, subnormal d^2 -> 0).  Ray vision also needs
+      // 1 / d: MUFU.RSQ without the subnormal rescale, d = d^2 / sqrt(d^2).
+      float rsq = 0.f, d;
+      if (RAY) {
+        asm("rsqrt.approx.ftz.f32 %0, %1;" : "=f"(rsq) : "f"(d2));
+        d = (d2 >= 1.17549435e-38f) ? d2 * rsq : 0.f;
+      } else {
+        asm("sqrt.approx.ftz.f32 %0, %1;" : "=f"(d) : "f"(d2));
+      }
+      // Eq. 1 / Fig. 4 (A5): contact -> -c_collide, else the tent min(rise, fall); in
+      // fixed-point units (x 2^32, A16b).
       const float f = contact ? c_mcollide
                               : fminf(fmaf(c_k_rise, d, c_b_rise), fmaf(c_nk_fall, d, c_b_fall));
       if (!RAY || d2 < P.dv2) {                                       // Eq. 1: d < d_v
         if (RAY) ++nnb[t];
         if (ENV == kFlock) {
-          rs[t] += __float2ll_rn(f * kFix);
+          rs[t] += __float2ll_rn(f);
           ncol[t] += contact ? 1u : 0u;
         } else {
           if (contact) {
             if (tj == tq[t]) ++ncol[t]; else ++ntouch[t];
           }
-          if (tq[t] == 0u && tj == 0u) rs[t] += __float2ll_rn((P.w_prox * f) * kFix);
+          if (tq[t] == 0u && tj == 0u) rs[t] += __float2ll_rn(P.w_prox * f);
         }
       }
       if (VISION && RAY) {
@@ -976,9 +987,9 @@ __global__ void __launch_bounds__(kSenseWarps * 32, kSenseMinBlocks) k_sense(
         // Bearing in the agent frame (A3): phi = atan2(h x d, h . d), CCW-positive.
         const float fwd = fmaf(csn[t], e.x, sn[t] * e.y);
         const float left = fmaf(csn[t], e.y, -sn[t] * e.x);
-        const float u = fmaf(vg_atan2(left, fwd), c_inv_fov, 0.5f);   // fraction of the fov
-        if (u >= 0.f && u < 1.f) {
-          const int k = min((int)(u * c_fv), P.v - 1);
+        // Sector coordinate (phi + fov/2) v / fov; visible iff 0 <= k < v (A3).
+        const int k = __float2int_rd(fmaf(vg_atan2(left, fwd), c_inv_w, c_half_v));
+        if ((unsigned)k < (unsigned)P.v) {
           const float val = fminf(d * c_inv_dv, kBelowOne);
           atomicMin(&s_min[warp][t][tj * P.v + k], __float_as_uint(val));
         }
