@@ -562,6 +562,8 @@ def run_ours(args):
             scan_b = 8 * w.n_cells
         stage_bytes = {"integrate_bin": (92 if fused else 48) * n, "scan_cells": scan_b,
                        "scatter": 44 * n, "cell_sort": 68 * n, "sense": obs_b * n}
+        if fused:         # one kernel does K1-K3b: the other binning phases are empty
+            stage_bytes = {"integrate_bin": 92 * n, "sense": obs_b * n}
         # Model bound: every binning stage at the HBM roof + K4 at the larger of
         # its HBM floor and its algorithmic ALU floor (45 ops per in-radius pair).
         floor_s = sum(b for k2, b in stage_bytes.items() if k2 != "sense") / (hbm * 1e9)
@@ -574,6 +576,8 @@ def run_ours(args):
         stages = {}
         tot_ph = sum(phases.values()) or 1.0
         for k2, ms in phases.items():
+            if k2 not in stage_bytes:
+                continue
             avg = ms / nrec
             gbs = stage_bytes[k2] / (avg / 1e3) / 1e9 if avg > 0 else None
             stages[run.phase_names[k2]] = {
