@@ -315,6 +315,24 @@ vg_status launch_fused_bin(vg_world* w, float4* io, const float4* in, const floa
   return VG_OK;
 }
 
+// K3b: one warp per cell, or one CTA per cell when the world has few cells.
+#ifndef VG_CTA_SORT_CELLS_PER_SM
+#define VG_CTA_SORT_CELLS_PER_SM 8
+#endif
+vg_status launch_cell_sort(vg_world* w, cudaStream_t s) {
+  if (w->n_cells <= (long long)VG_CTA_SORT_CELLS_PER_SM * w->n_sm) {
+    vg::k_cell_sort_cta<<<(unsigned)(w->n_cells + 1), vg::kCtaSortThreads, 0, s>>>(
+        w->P, w->n_cells, w->slab ? 1 : 0, w->cell_start, w->tmp_rec, w->tmp_id, w->sorted,
+        w->perm, w->xo_rec, w->xo_perm, w->xo_xy, w->sub_tab, work_list(w), w->slot);
+    return launch_check("k_cell_sort_cta");
+  }
+  const long long threads = (long long)(w->n_cells + 1) * 32;   // + the sentinel row
+  vg::k_cell_sort<<<(unsigned)((threads + 255) / 256), 256, 0, s>>>(
+      w->P, w->n_cells, w->slab ? 1 : 0, w->cell_start, w->tmp_rec, w->tmp_id, w->sorted,
+      w->perm, w->xo_rec, w->xo_perm, w->xo_xy, w->sub_tab, work_list(w), w->slot);
+  return launch_check("k_cell_sort");
+}
+
 template <int ENV>
 vg_status bin_rest(vg_world* w, const float4* state, cudaStream_t s, bool prof = false) {
   const long long n = w->P.total;
@@ -324,11 +342,7 @@ vg_status bin_rest(vg_world* w, const float4* state, cudaStream_t s, bool prof =
       w->P, state, w->cell_id, w->slot, w->cell_start, w->tmp_rec, w->tmp_id, w->work_cnt);
   if (vg_status st = launch_check("k_scatter")) return st;
   if (prof) prof_mark(w, 3, s);
-  const long long threads = (long long)(w->n_cells + 1) * 32;   // + the sentinel row
-  vg::k_cell_sort<<<(unsigned)((threads + 255) / 256), 256, 0, s>>>(
-      w->P, w->n_cells, w->slab ? 1 : 0, w->cell_start, w->tmp_rec, w->tmp_id, w->sorted,
-      w->perm, w->xo_rec, w->xo_perm, w->xo_xy, w->sub_tab, work_list(w), w->slot);
-  if (vg_status st = launch_check("k_cell_sort")) return st;
+  if (vg_status st = launch_cell_sort(w, s)) return st;
   if (prof) prof_mark(w, 4, s);
   w->binned = true;
   return VG_OK;
@@ -427,11 +441,7 @@ vg_status slab_bin(vg_world* w, cudaStream_t s) {
   vg::k_slab_scatter<ENV><<<nb, 256, 0, s>>>(w->P, w->SB, w->cell_id, w->slot, w->cell_start,
                                               w->tmp_rec, w->tmp_id, w->work_cnt);
   if (vg_status st = launch_check("k_slab_scatter")) return st;
-  const long long threads = (long long)(w->n_cells + 1) * 32;   // + the sentinel row
-  vg::k_cell_sort<<<(unsigned)((threads + 255) / 256), 256, 0, s>>>(
-      w->P, w->n_cells, w->slab ? 1 : 0, w->cell_start, w->tmp_rec, w->tmp_id, w->sorted,
-      w->perm, w->xo_rec, w->xo_perm, w->xo_xy, w->sub_tab, work_list(w), w->slot);
-  if (vg_status st = launch_check("k_cell_sort")) return st;
+  if (vg_status st = launch_cell_sort(w, s)) return st;
   w->binned = true;
   return VG_OK;
 }

@@ -520,6 +520,86 @@ __global__ void __launch_bounds__(256) k_cell_sort(
                    sub_tab + (size_t)cell * kSub, lane, lt);
 }
 
+// K3b, one CTA per cell (worlds with few, populous cells: c2, c3 have 81 cells of 60-120
+// agents, where one warp per cell leaves most SMs idle).  The same outputs as k_cell_sort:
+// every member's stable slot is its rank by agent id, and its sense-order slot is its rank
+// by (sub-bin, id); both ranks are counted by comparison against the cell's keys staged in
+// shared memory, all threads of the CTA in parallel.  A cell above kCtaRankMax members
+// falls back to warp 0 running k_cell_sort's path.
+constexpr int kCtaSortThreads = 128;
+constexpr int kCtaRankMax = 1024;
+__global__ void __launch_bounds__(kCtaSortThreads) k_cell_sort_cta(
+    Params P, int n_cells, int axis_y, const uint32_t* __restrict__ cell_start,
+    const float4* __restrict__ tmp_rec, const uint32_t* __restrict__ tmp_id,
+    float4* __restrict__ sorted, uint32_t* __restrict__ perm, float4* __restrict__ xo_rec,
+    uint32_t* __restrict__ xo_perm, float2* __restrict__ xo_xy, uint32_t* __restrict__ sub_tab,
+    WorkList WL, uint32_t* __restrict__ scratch) {
+  __shared__ uint2 s_key[kCtaRankMax];        // (id, sub-bin << 29 | 0) per arrival slot
+  __shared__ uint32_t s_cnt[kSub];
+  const int cell = blockIdx.x, tid = threadIdx.x, lane = tid & 31;
+  const uint32_t b = cell_start[cell];
+  if (cell == n_cells) {                                 // sentinel
+    if (tid == 0) sub_tab[(size_t)n_cells * kSub] = b;
+    return;
+  }
+  const int m = (int)(cell_start[cell + 1] - b);
+  if (tid == 0) {                                        // K4 work items of this cell
+    const uint32_t nch = work_chunks(WL, cell, (uint32_t)m);
+    const uint32_t at = nch ? atomicAdd(WL.n, nch) : 0u;
+    for (uint32_t k = 0; k < nch; ++k)
+      WL.item[at + k] = make_uint2((uint32_t)(cell - WL.lo), b + (k + 1u) * (uint32_t)WL.chunk_q);
+  }
+  const int ca = cell % P.G;
+  if (m > kCtaRankMax) {                                 // rare: the warp path
+    if (tid >= 32) return;
+    uint32_t *ks, *vs;
+    cell_merge_sort(b, m, const_cast<uint32_t*>(tmp_id), scratch, perm, xo_perm, lane, ks, vs);
+    for (int k = lane; k < m; k += 32) {
+      const uint32_t id = ks[b + k], src = vs[b + k];
+      sorted[b + k] = tmp_rec[b + src];
+      perm[b + k] = id;
+    }
+    __syncwarp();
+    unsigned lt;
+    asm("mov.u32 %0, %%lanemask_lt;" : "=r"(lt));
+    sense_order_cell(P, ca, axis_y != 0, b, m, sorted, perm, xo_rec, xo_perm, xo_xy,
+                     sub_tab + (size_t)cell * kSub, lane, lt);
+    return;
+  }
+  if (tid < kSub) s_cnt[tid] = 0u;
+  __syncthreads();
+  for (int e = tid; e < m; e += kCtaSortThreads) {
+    const float4 rec = tmp_rec[b + e];
+    const int sb = sub_bin(P, ca, axis_y ? rec.y : rec.x);
+    s_key[e] = make_uint2(tmp_id[b + e], (uint32_t)sb);
+    atomicAdd(&s_cnt[sb], 1u);
+  }
+  __syncthreads();
+  if (tid < kSub) {                                      // sub-bin table: exclusive prefix
+    uint32_t before = 0;
+    for (int s = 0; s < tid; ++s) before += s_cnt[s];
+    sub_tab[(size_t)cell * kSub + tid] = b + before;
+  }
+  for (int e = tid; e < m; e += kCtaSortThreads) {
+    const uint2 me = s_key[e];
+    uint32_t rank = 0, pos = 0;                          // by id; by (sub-bin, id)
+#pragma unroll 4
+    for (int j = 0; j < m; ++j) {
+      const uint2 o = s_key[j];                          // broadcast
+      const bool lt_id = o.x < me.x;
+      rank += lt_id ? 1u : 0u;
+      pos += (o.y < me.y || (o.y == me.y && lt_id)) ? 1u : 0u;
+    }
+    float4 rec = tmp_rec[b + e];
+    sorted[b + rank] = rec;
+    perm[b + rank] = me.x;
+    xo_rec[b + pos] = rec;
+    xo_perm[b + pos] = me.x;
+    // compact positions for K4; tag: the type rides in the sign bit of x (as in K3b)
+    xo_xy[b + pos] = make_float2((P.env == kTag && rec.w != 0.f) ? -rec.x : rec.x, rec.y);
+  }
+}
+
 // ------------------------------------------------------------------------------ K1-K3 fused
 // Small replica worlds (G^2 <= 256 cells, N <= 32768, many replicas): one CTA of 1024
 // threads per replica integrates (optional), bins and stably scatters its agents — the same
