@@ -473,6 +473,9 @@ int32_t vg_abi_version(void) { return VG_ABI_VERSION; }
 
 const char* vg_last_error(void) { return g_err; }
 
+#ifndef VG_FUSED_SINGLE_MAX
+#define VG_FUSED_SINGLE_MAX 1024     // few replicas: the fused bin only for tiny worlds
+#endif
 vg_status vg_world_create(const vg_config* cfg, vg_world** out) {
   g_err[0] = 0;
   if (!out) return fail(VG_EINVAL, "out: NULL");
@@ -487,7 +490,7 @@ vg_status vg_world_create(const vg_config* cfg, vg_world** out) {
   // one CTA per replica: worth it when replicas fill the GPU or the world is tiny
   w->fused_bin = cfg->shard == VG_SHARD_REPLICA && g * g <= vg::kRBMaxCells &&
                  cfg->n_agents <= vg::kRBMaxAgents &&
-                 (cfg->n_replicas >= 64 || cfg->n_agents <= 1024);
+                 (cfg->n_replicas >= 64 || cfg->n_agents <= VG_FUSED_SINGLE_MAX);
   {
     const char* ng = std::getenv("VG_NO_GRAPH");
     w->graphs_enabled = !(ng && ng[0] && ng[0] != '0');

@@ -526,7 +526,11 @@ __global__ void __launch_bounds__(256) k_cell_sort(
 // by (sub-bin, id); both ranks are counted by comparison against the cell's keys staged in
 // shared memory, all threads of the CTA in parallel.  A cell above kCtaRankMax members
 // falls back to warp 0 running k_cell_sort's path.
-constexpr int kCtaSortThreads = 128;
+#ifndef VG_CTA_SORT_SPLIT
+#define VG_CTA_SORT_SPLIT 4
+#endif
+constexpr int kCtaSortSplit = VG_CTA_SORT_SPLIT;       // threads sharing one member's count
+constexpr int kCtaSortThreads = 128 * kCtaSortSplit;
 constexpr int kCtaRankMax = 1024;
 __global__ void __launch_bounds__(kCtaSortThreads) k_cell_sort_cta(
     Params P, int n_cells, int axis_y, const uint32_t* __restrict__ cell_start,
@@ -534,7 +538,8 @@ __global__ void __launch_bounds__(kCtaSortThreads) k_cell_sort_cta(
     float4* __restrict__ sorted, uint32_t* __restrict__ perm, float4* __restrict__ xo_rec,
     uint32_t* __restrict__ xo_perm, float2* __restrict__ xo_xy, uint32_t* __restrict__ sub_tab,
     WorkList WL, uint32_t* __restrict__ scratch) {
-  __shared__ uint2 s_key[kCtaRankMax];        // (id, sub-bin << 29 | 0) per arrival slot
+  __shared__ uint2 s_key[kCtaRankMax];        // (id, sub-bin) per arrival slot
+  __shared__ uint32_t s_rank[kCtaRankMax], s_pos[kCtaRankMax];
   __shared__ uint32_t s_cnt[kSub];
   const int cell = blockIdx.x, tid = threadIdx.x, lane = tid & 31;
   const uint32_t b = cell_start[cell];
@@ -572,6 +577,8 @@ __global__ void __launch_bounds__(kCtaSortThreads) k_cell_sort_cta(
     const float4 rec = tmp_rec[b + e];
     const int sb = sub_bin(P, ca, axis_y ? rec.y : rec.x);
     s_key[e] = make_uint2(tmp_id[b + e], (uint32_t)sb);
+    s_rank[e] = 0u;
+    s_pos[e] = 0u;
     atomicAdd(&s_cnt[sb], 1u);
   }
   __syncthreads();
@@ -580,21 +587,38 @@ __global__ void __launch_bounds__(kCtaSortThreads) k_cell_sort_cta(
     for (int s = 0; s < tid; ++s) before += s_cnt[s];
     sub_tab[(size_t)cell * kSub + tid] = b + before;
   }
-  for (int e = tid; e < m; e += kCtaSortThreads) {
-    const uint2 me = s_key[e];
-    uint32_t rank = 0, pos = 0;                          // by id; by (sub-bin, id)
+  // Member e's ranks by id and by (sub-bin, id), counted over kCtaSortSplit slices of the
+  // cell by as many threads (slice = tid / 128) and summed in shared memory.
+  {
+    const int slice = tid >> 7, per = (m + kCtaSortSplit - 1) / kCtaSortSplit;
+    const int j0 = slice * per, j1 = min(m, j0 + per);
+    for (int e = tid & 127; e < m; e += 128) {
+      const uint2 me = s_key[e];
+      uint32_t rank = 0, pos = 0;
 #pragma unroll 4
-    for (int j = 0; j < m; ++j) {
-      const uint2 o = s_key[j];                          // broadcast
-      const bool lt_id = o.x < me.x;
-      rank += lt_id ? 1u : 0u;
-      pos += (o.y < me.y || (o.y == me.y && lt_id)) ? 1u : 0u;
+      for (int j = j0; j < j1; ++j) {
+        const uint2 o = s_key[j];                        // broadcast
+        const bool lt_id = o.x < me.x;
+        rank += lt_id ? 1u : 0u;
+        pos += (o.y < me.y || (o.y == me.y && lt_id)) ? 1u : 0u;
+      }
+      if (kCtaSortSplit == 1) {
+        s_rank[e] = rank;
+        s_pos[e] = pos;
+      } else {
+        atomicAdd(&s_rank[e], rank);
+        atomicAdd(&s_pos[e], pos);
+      }
     }
-    float4 rec = tmp_rec[b + e];
+  }
+  __syncthreads();
+  for (int e = tid; e < m; e += kCtaSortThreads) {
+    const uint32_t id = s_key[e].x, rank = s_rank[e], pos = s_pos[e];
+    const float4 rec = tmp_rec[b + e];
     sorted[b + rank] = rec;
-    perm[b + rank] = me.x;
+    perm[b + rank] = id;
     xo_rec[b + pos] = rec;
-    xo_perm[b + pos] = me.x;
+    xo_perm[b + pos] = id;
     // compact positions for K4; tag: the type rides in the sign bit of x (as in K3b)
     xo_xy[b + pos] = make_float2((P.env == kTag && rec.w != 0.f) ? -rec.x : rec.x, rec.y);
   }
