@@ -47,6 +47,7 @@ struct vg_world {
   int n_cells = 0;
   bool binned = false;
   bool fused_bin = false;          // K1-K3 fused per replica (small worlds)
+  bool gather_bin = false;         // K2-K3b as one per-cell gather kernel (K3g)
   size_t scratch_bytes = 0;
   uint32_t* count = nullptr;       // [n_cells]     per-cell histogram (zero between uses)
   uint32_t* tile_sum = nullptr;    // [n_cells / 4096 + 1] multi-CTA scan partials
@@ -285,7 +286,8 @@ vg_status launch_k1(vg_world* w, float4* io, const float4* in, const float2* act
   const long long n = w->P.total;
   const unsigned blocks = (unsigned)((n + 255) / 256);
   vg::k_integrate_bin<ENV, INTEGRATE, BIN><<<blocks, 256, 0, s>>>(
-      w->P, io, in, act, w->cell_id, w->slot, w->count, w->err_dev, w->err_flag);
+      w->P, io, in, act, w->cell_id, w->slot, w->count, w->err_dev, w->err_flag,
+      (BIN && w->gather_bin) ? w->work_cnt : nullptr);
   return launch_check("k_integrate_bin");
 }
 
@@ -336,6 +338,15 @@ vg_status launch_cell_sort(vg_world* w, cudaStream_t s) {
 template <int ENV>
 vg_status bin_rest(vg_world* w, const float4* state, cudaStream_t s, bool prof = false) {
   const long long n = w->P.total;
+  if (w->gather_bin) {                 // K3g: K2 + K3 + K3b in one kernel (small worlds)
+    vg::k_cell_gather<ENV><<<(unsigned)(w->n_cells + 1), vg::kGatherThreads, 0, s>>>(
+        w->P, w->n_cells, state, w->cell_id, w->cell_start, w->sorted, w->perm, w->xo_rec,
+        w->xo_perm, w->xo_xy, w->sub_tab, work_list(w));
+    if (vg_status st = launch_check("k_cell_gather")) return st;
+    if (prof) for (int k = 2; k <= 4; ++k) prof_mark(w, k, s);
+    w->binned = true;
+    return VG_OK;
+  }
   if (vg_status st = scan_cells(w, s)) return st;
   if (prof) prof_mark(w, 2, s);
   vg::k_scatter<ENV><<<(unsigned)((n + 255) / 256), 256, 0, s>>>(
@@ -476,6 +487,9 @@ const char* vg_last_error(void) { return g_err; }
 #ifndef VG_FUSED_SINGLE_MAX
 #define VG_FUSED_SINGLE_MAX 1024     // few replicas: the fused bin only for tiny worlds
 #endif
+#ifndef VG_GATHER_BIN
+#define VG_GATHER_BIN 1
+#endif
 vg_status vg_world_create(const vg_config* cfg, vg_world** out) {
   g_err[0] = 0;
   if (!out) return fail(VG_EINVAL, "out: NULL");
@@ -499,6 +513,8 @@ vg_status vg_world_create(const vg_config* cfg, vg_world** out) {
   cudaGetDevice(&w->device);
   cudaDeviceGetAttribute(&w->n_sm, cudaDevAttrMultiProcessorCount, w->device);
   set_kernel_attributes();                         // per device (the current one)
+  w->gather_bin = VG_GATHER_BIN && cfg->shard == VG_SHARD_REPLICA && !w->fused_bin &&
+                  w->n_cells <= 8LL * w->n_sm && cfg->n_agents <= vg::kGatherMaxN;
   size_t n = (size_t)w->P.total;
   vg_status st = VG_OK;
   if (cfg->shard == VG_SHARD_SLAB) {
@@ -626,7 +642,8 @@ vg_status vg_world_query(const vg_world* w, vg_world_info* info) {
   info->total_agents = w->P.total;
   info->scratch_bytes = (int64_t)w->scratch_bytes;
   const int scan_k = (w->n_cells > vg::kScanSmallMax) ? 2 : 1;
-  info->kernels_per_step = w->slab ? 6 + scan_k : (w->fused_bin ? 2 : 4 + scan_k);
+  info->kernels_per_step = w->slab ? 6 + scan_k
+                                   : (w->fused_bin ? 2 : (w->gather_bin ? 3 : 4 + scan_k));
   return VG_OK;
 }
 

@@ -115,7 +115,8 @@ __global__ void __launch_bounds__(256) k_integrate_bin(
     Params P, float4* __restrict__ state_io, const float4* __restrict__ state_in,
     const float2* __restrict__ actions, uint32_t* __restrict__ cell_id,
     uint32_t* __restrict__ slot, uint32_t* __restrict__ count,
-    unsigned long long* __restrict__ err, volatile uint32_t* flag) {
+    unsigned long long* __restrict__ err, volatile uint32_t* flag,
+    uint32_t* __restrict__ gather_work_n) {
   const long long gi = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   if (gi >= P.total) return;
   const int r = (int)(gi / P.N);
@@ -158,7 +159,11 @@ __global__ void __launch_bounds__(256) k_integrate_bin(
     cy = min(max(cy, 0), P.G - 1);
     const uint32_t c = (uint32_t)(cy * P.G + cx);
     cell_id[gi] = c;
-    slot[gi] = atomicAdd(&count[(size_t)r * P.G2 + c], 1u);
+    if (gather_work_n) {                  // K3g follows: no histogram; zero its item count
+      if (gi == 0) *gather_work_n = 0u;
+    } else {
+      slot[gi] = atomicAdd(&count[(size_t)r * P.G2 + c], 1u);
+    }
   }
 }
 
@@ -621,6 +626,129 @@ __global__ void __launch_bounds__(kCtaSortThreads) k_cell_sort_cta(
     xo_perm[b + pos] = id;
     // compact positions for K4; tag: the type rides in the sign bit of x (as in K3b)
     xo_xy[b + pos] = make_float2((P.env == kTag && rec.w != 0.f) ? -rec.x : rec.x, rec.y);
+  }
+}
+
+// K3g — K2, K3 and K3b in one kernel for small single worlds (replica mode, few cells,
+// N <= kGatherMaxN: c2, c3).  One CTA per cell c of replica r gathers its members straight
+// from the cell ids K1 wrote, in agent-id order (so the stable order needs no rank): thread
+// t owns agents [t S, (t+1) S); pass A counts, per thread, agents in cells before c and in
+// c; one block scan gives cell_start and each thread's first slot; pass B writes the
+// members.  Then the sense order by (sub-bin, id) and the sub-bin table as in K3b'.  Two
+// fewer graph nodes than K1 + K2 + K3 + K3b (launch-bound worlds).
+constexpr int kGatherThreads = 512;
+constexpr int kGatherMaxN = kGatherThreads * 32;
+template <int ENV>
+__global__ void __launch_bounds__(kGatherThreads) k_cell_gather(
+    Params P, int n_cells, const float4* __restrict__ state, const uint32_t* __restrict__ cell_id,
+    uint32_t* __restrict__ cell_start, float4* __restrict__ sorted, uint32_t* __restrict__ perm,
+    float4* __restrict__ xo_rec, uint32_t* __restrict__ xo_perm, float2* __restrict__ xo_xy,
+    uint32_t* __restrict__ sub_tab, WorkList WL) {
+  constexpr int T = kGatherThreads, NW = T / 32;
+  __shared__ float4 s_rec[kCtaRankMax];
+  __shared__ uint32_t s_id[kCtaRankMax];
+  __shared__ uint8_t s_sb[kCtaRankMax];
+  __shared__ uint32_t s_wa[NW], s_wb[NW], s_cnt[kSub], s_start, s_m;
+  const int gc = blockIdx.x, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  if (gc == n_cells) {                                   // sentinels
+    if (tid == 0) {
+      cell_start[n_cells] = (uint32_t)P.total;
+      sub_tab[(size_t)n_cells * kSub] = (uint32_t)P.total;
+    }
+    return;
+  }
+  const int r = gc / P.G2;
+  const uint32_t c = (uint32_t)(gc - r * P.G2);
+  const size_t base = (size_t)r * P.N;
+  const int S = (P.N + T - 1) / T;
+  const int i0 = min(P.N, tid * S), i1 = min(P.N, i0 + S);
+  uint32_t before = 0, mine = 0;                         // pass A
+#pragma unroll 8
+  for (int i = i0; i < i1; ++i) {
+    const uint32_t cid = cell_id[base + i];
+    before += cid < c ? 1u : 0u;
+    mine += cid == c ? 1u : 0u;
+  }
+  if (tid < kSub) s_cnt[tid] = 0u;
+  uint32_t inc = mine;                                   // block exclusive scan of `mine`
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint32_t y = __shfl_up_sync(kFull, inc, o);
+    if (lane >= o) inc += y;
+  }
+  const uint32_t bsum = __reduce_add_sync(kFull, before);
+  if (lane == 31) s_wa[warp] = inc;
+  if (lane == 0) s_wb[warp] = bsum;
+  __syncthreads();
+  if (warp == 0) {
+    const uint32_t a = lane < NW ? s_wa[lane] : 0u, bb = lane < NW ? s_wb[lane] : 0u;
+    uint32_t ai = a;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t y = __shfl_up_sync(kFull, ai, o);
+      if (lane >= o) ai += y;
+    }
+    const uint32_t btot = __reduce_add_sync(kFull, bb);
+    if (lane < NW) s_wa[lane] = ai - a;
+    if (lane == 31) {
+      s_m = ai;
+      s_start = (uint32_t)base + btot;
+    }
+  }
+  __syncthreads();
+  const uint32_t start = s_start;
+  const int m = (int)s_m;
+  uint32_t k = s_wa[warp] + inc - mine;                  // pass B: this thread's first slot
+  const int ca = (int)(c % (uint32_t)P.G);
+#pragma unroll 4
+  for (int i = i0; i < i1; ++i) {
+    if (cell_id[base + i] != c) continue;
+    float4 rec = state[base + i];
+    if (ENV == kTag) rec.w = (i >= P.first_chaser) ? 1.f : 0.f;   // type in the record
+    sorted[start + k] = rec;
+    perm[start + k] = (uint32_t)i;
+    if (k < (uint32_t)kCtaRankMax) {
+      const int sb = sub_bin(P, ca, rec.x);
+      s_rec[k] = rec;
+      s_id[k] = (uint32_t)i;
+      s_sb[k] = (uint8_t)sb;
+      atomicAdd(&s_cnt[sb], 1u);
+    }
+    ++k;
+  }
+  if (tid == 0) {
+    cell_start[gc] = start;
+    const uint32_t nch = work_chunks(WL, gc, (uint32_t)m);   // K4 work items of this cell
+    const uint32_t at = nch ? atomicAdd(WL.n, nch) : 0u;
+    for (uint32_t q = 0; q < nch; ++q)
+      WL.item[at + q] = make_uint2((uint32_t)(gc - WL.lo), start + (q + 1u) * (uint32_t)WL.chunk_q);
+  }
+  __syncthreads();                                       // sorted / perm / s_* complete
+  if (m > kCtaRankMax) {                                 // rare: the warp path reads them back
+    if (warp == 0) {
+      unsigned lt;
+      asm("mov.u32 %0, %%lanemask_lt;" : "=r"(lt));
+      sense_order_cell(P, ca, false, start, m, sorted, perm, xo_rec, xo_perm, xo_xy,
+                       sub_tab + (size_t)gc * kSub, lane, lt);
+    }
+    return;
+  }
+  if (tid < kSub) {                                      // sub-bin table: exclusive prefix
+    uint32_t b4 = 0;
+    for (int q = 0; q < tid; ++q) b4 += s_cnt[q];
+    sub_tab[(size_t)gc * kSub + tid] = start + b4;
+    s_wa[tid] = b4;                                      // (s_wa is free again)
+  }
+  __syncthreads();
+  for (int e = tid; e < m; e += T) {                     // sense order: by (sub-bin, id)
+    const int sb = s_sb[e];
+    uint32_t pos = s_wa[sb];
+    for (int j = 0; j < e; ++j) pos += (s_sb[j] == sb) ? 1u : 0u;
+    const float4 rec = s_rec[e];
+    xo_rec[start + pos] = rec;
+    xo_perm[start + pos] = s_id[e];
+    // compact positions for K4; tag: the type rides in the sign bit of x (as in K3b)
+    xo_xy[start + pos] = make_float2((ENV == kTag && rec.w != 0.f) ? -rec.x : rec.x, rec.y);
   }
 }
 
