@@ -60,7 +60,7 @@ struct vg_world {
   float4* sorted = nullptr;        // [R*N]
   float4* xo_rec = nullptr;        // [R*N]         K4 sense order: within a cell by (axis key, id)
   uint32_t* xo_perm = nullptr;     // [R*N]         agent ids in sense order
-  float2* xo_xy = nullptr;         // [R*N + 64]    positions in sense order (K4 candidate reads)
+  float2* xo_xy = nullptr;         // [R*N + 32 H]  positions in sense order (K4 candidate reads)
   uint32_t* sub_tab = nullptr;     // [(n_cells + 1) * kSub] K4 window table (K3b)
   uint2* work = nullptr;           // [work_cap] K4 work items (cell, first query)
   uint32_t* work_cnt = nullptr;    // [1] item count
@@ -559,7 +559,7 @@ vg_status vg_world_create(const vg_config* cfg, vg_world** out) {
   if (!st) st = dalloc(w, &w->sorted, n);
   if (!st) st = dalloc(w, &w->xo_rec, n);
   if (!st) st = dalloc(w, &w->xo_perm, n);
-  if (!st) st = dalloc(w, &w->xo_xy, n + 64);       // padded: unpredicated K4 loads
+  if (!st) st = dalloc(w, &w->xo_xy, n + 32 * vg::kSenseHalves);   // padded: unpredicated K4 loads
   if (!st) st = dalloc(w, &w->sub_tab, ((size_t)w->n_cells + 1) * vg::kSub);
   if (!st) {
     w->work_cap = (long long)w->n_cells + (long long)n / 8 + 1;       // chunk_q >= 8

@@ -949,10 +949,15 @@ constexpr int kSenseMinBlocks = VG_SENSE_MINB;  // resident CTAs per SM
 // Ring (power of 2): >= 31 carried + 64 pushed, and large enough that one chunk's pushes
 // never reach the slots the previous drain read (carried + 64 + 2 x 32 <= kQueue), so one
 // warp sync per chunk (before the drain) orders all ring traffic.
+#ifndef VG_SENSE_HALVES
+#define VG_SENSE_HALVES 2          // 32-slot halves per candidate chunk
+#endif
+constexpr int kSenseHalves = VG_SENSE_HALVES;
 #ifndef VG_SENSE_QUEUE
-#define VG_SENSE_QUEUE 128
+#define VG_SENSE_QUEUE (VG_SENSE_HALVES > 2 ? 256 : 128)
 #endif
 constexpr int kQueue = VG_SENSE_QUEUE;
+static_assert(kQueue >= 31 + 32 * kSenseHalves, "ring: carried + one chunk of pushes");
 
 // atan2(y, x) in (-pi, pi] with |error| <~ 3.3e-7 rad (the sector band is
 // 1e-6 fov = 4.4e-6 rad): octant reduction, t = min/max by the hardware reciprocal, a
@@ -1278,26 +1283,7 @@ __global__ void __launch_bounds__(kSenseWarps * 32, kSenseMinBlocks) k_sense(
         qx[t] = me[t].x + sg.qsx;                                     // exact (Sterbenz)
         qy[t] = me[t].y + sg.qsy;
       }
-      for (uint32_t p0 = wb; p0 < we; p0 += 64) {
-        const uint32_t pa = p0 + lane, pb = p0 + 32 + lane;
-        const bool va = pa < we, vb = pb < we;
-        const bool two = p0 + 32 < we;                               // warp-uniform
-        float ax, ay, bx, by;
-        uint32_t ta = 0u, tb = 0u;
-        {                                    // sorted_xy is padded by 64: no predicate
-          const float2 oa = __ldg(&sorted_xy[pa]), ob = __ldg(&sorted_xy[pb]);
-          ax = oa.x; ay = oa.y; bx = ob.x; by = ob.y;
-          if (ENV == kTag) {                 // type in the sign bit of x (K3b)
-            ta = __float_as_uint(ax) & 0x80000000u;
-            tb = __float_as_uint(bx) & 0x80000000u;
-            ax = fabsf(ax);
-            bx = fabsf(bx);
-          }
-        }
-        // Slots past the run end get a NaN position: never within d_v of anyone.
-        ax = va ? ax + sg.csx : __int_as_float(0x7fc00000);          // exact (Sterbenz)
-        bx = vb ? bx + sg.csx : __int_as_float(0x7fc00000);
-        ay += sg.csy; by += sg.csy;
+      for (uint32_t p0 = wb; p0 < we; p0 += 32 * kSenseHalves) {
         // Ballot the in-radius candidates of one 32-slot half and append them to each
         // query's ring (dx, dy, d^2, index | type << 31).
         auto scan = [&](const float cx_, const float cy_, const uint32_t word) {
@@ -1313,8 +1299,28 @@ __global__ void __launch_bounds__(kSenseWarps * 32, kSenseMinBlocks) k_sense(
             tail[t] += __popc(bal) << 4;
           }
         };
-        scan(ax, ay, pa | ta);
-        if (two) scan(bx, by, pb | tb);
+        // kSenseHalves 32-slot halves per chunk, 1 candidate per lane each (sorted_xy is
+        // padded by 32 kSenseHalves: no load predicate); slots past the run end get a NaN
+        // position, never within d_v of anyone; halves wholly past it are skipped.
+        float cxh[kSenseHalves], cyh[kSenseHalves];
+        uint32_t wh[kSenseHalves];
+#pragma unroll
+        for (int h = 0; h < kSenseHalves; ++h) {
+          const uint32_t pj = p0 + 32u * h + lane;
+          const float2 o = __ldg(&sorted_xy[pj]);
+          float x = o.x;
+          uint32_t tj = 0u;
+          if (ENV == kTag) {                 // type in the sign bit of x (K3b)
+            tj = __float_as_uint(x) & 0x80000000u;
+            x = fabsf(x);
+          }
+          cxh[h] = (pj < we) ? x + sg.csx : __int_as_float(0x7fc00000);   // exact (Sterbenz)
+          cyh[h] = o.y + sg.csy;
+          wh[h] = pj | tj;
+        }
+#pragma unroll
+        for (int h = 0; h < kSenseHalves; ++h)
+          if (h == 0 || p0 + 32u * h < we) scan(cxh[h], cyh[h], wh[h]);   // warp-uniform
         __syncwarp();                       // ring pushes above are visible to the warp
 #pragma unroll
         for (int t = 0; t < NQ; ++t) {
@@ -1323,7 +1329,9 @@ __global__ void __launch_bounds__(kSenseWarps * 32, kSenseMinBlocks) k_sense(
             head[t] += 32u * 16u;
           }
         }
-        if (kQueue < 160) __syncwarp();     // small ring: drained slots may be rewritten next
+        // Drained slots may be rewritten by the next chunk's pushes unless the ring holds
+        // 31 carried + a chunk + 2 x 32 entries.
+        if (31 + 32 * kSenseHalves + 64 > kQueue) __syncwarp();
       }
     }
     __syncwarp();
