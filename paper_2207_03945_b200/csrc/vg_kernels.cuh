@@ -765,10 +765,13 @@ __global__ void __launch_bounds__(kGatherThreads) k_cell_gather(
 constexpr int kRBMaxCells = 256;
 constexpr int kRBMaxAgents = 32768;
 
-constexpr int kRBThreads = 1024;     // 32 warps per replica CTA, 2 CTAs per SM
+#ifndef VG_RB_THREADS
+#define VG_RB_THREADS 1024
+#endif
+constexpr int kRBThreads = VG_RB_THREADS;   // warps per replica CTA x 32; 2048 / it CTAs per SM
 
 template <int ENV, bool INTEGRATE>
-__global__ void __launch_bounds__(kRBThreads, 2) k_replica_bin(
+__global__ void __launch_bounds__(kRBThreads, 2048 / kRBThreads) k_replica_bin(
     Params P, float4* __restrict__ state_io, const float4* __restrict__ state_in,
     const float2* __restrict__ actions, uint32_t* __restrict__ cell_id,
     uint32_t* __restrict__ cell_start, float4* __restrict__ sorted,
