@@ -140,6 +140,29 @@ def test_sector_model_variants(cuda, fov, v):
     run_and_check(p, vi.init_state(p, seed=11), 2)
 
 
+@pytest.mark.parametrize("case", ["gather_replicas", "gather_tag_replicas", "cta_sort",
+                                  "warp_sort"])
+def test_binning_paths(cuda, case):
+    # Each K2-K3b variant against the oracle's bins (bit-exact) and sense outputs:
+    # K3g (per-cell gather, several replicas), K3b' (one CTA per cell: few cells, N above
+    # K3g's limit) and K3b (one warp per cell: many cells).  kernels_per_step names the path.
+    rows = None
+    if case == "gather_replicas":
+        p, kps = vi.flock_params(3000, n_replicas=4), 3
+    elif case == "gather_tag_replicas":
+        p, kps = vi.tag_params(2000, n_replicas=3), 3
+    elif case == "cta_sort":
+        p, kps = vi.flock_params(20000), 5
+        rows = np.arange(0, 20000, 41)
+    else:
+        p, kps = vi.flock_params(20000, width=400.0, d_v=10.0), 5
+        rows = np.arange(0, 20000, 41)
+    w = make_world(p)
+    assert w.kernels_per_step == kps
+    w.close()
+    run_and_check(p, vi.init_state(p, seed=17), 2, rows=rows)
+
+
 @pytest.mark.parametrize("grid", [9, 0])
 def test_large_cells_small_radius(cuda, grid):
     # d_v = 3 in cells of 11.1 (grid 9: a run is ~11 radii long, the windows cut most of it)
