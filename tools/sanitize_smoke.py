@@ -1,5 +1,6 @@
-"""Small workloads through every kernel, for compute-sanitizer (memcheck / racecheck /
-synccheck) — run one tool per process (B200_PROFILING.md)."""
+"""Small workloads through every kernel (every binning path included): a plain smoke run,
+and the input for compute-sanitizer (memcheck / racecheck / synccheck, one tool per
+process) where the pool allows it (it is closed on this round's pool)."""
 import os
 import sys
 
@@ -14,11 +15,21 @@ from paper_2207_03945_b200.policy import Policy, action_box  # noqa: E402
 from paper_2207_03945_b200.slab import SlabGroup  # noqa: E402
 
 os.environ.setdefault("VG_NO_GRAPH", "0")
-for p in (vi.flock_params(300, width=40.0), vi.tag_params(400, width=40.0),
-          vi.flock_params(7, n_replicas=5, width=40.0)):
+# fused replica bin (first three), K3g gather (one and two replicas), K3b' (few cells,
+# N > 16,384; and dense clustered cells: its merge-sort fallback), K3b (many cells)
+for p, clustered in ((vi.flock_params(300, width=40.0), False),
+                     (vi.tag_params(400, width=40.0), False),
+                     (vi.flock_params(7, n_replicas=5, width=40.0), False),
+                     (vi.flock_params(3000, width=40.0), False),
+                     (vi.tag_params(2000, n_replicas=2, width=40.0), False),
+                     (vi.flock_params(20000), False),
+                     (vi.flock_params(20000), True),        # 16 clusters of ~1250
+                     (vi.flock_params(4000, width=400.0, d_v=10.0), False)):
     w = vg.World(p)
     out = w.alloc_outputs()
-    st = torch.from_numpy(vi.init_state(p, seed=1)).cuda()
+    st0 = vi.clustered_state(p, seed=1, n_clusters=16, sigma=1.0) if clustered \
+        else vi.init_state(p, seed=1)
+    st = torch.from_numpy(st0).cuda()
     for t in range(2):
         w.step(st, torch.from_numpy(vi.actions(p, seed=1, step=t)).cuda(), out)
     w.reward(out)
