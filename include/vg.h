@@ -48,7 +48,7 @@
 extern "C" {
 #endif
 
-#define VG_ABI_VERSION 1
+#define VG_ABI_VERSION 2
 
 typedef enum {
   VG_OK = 0,
@@ -123,6 +123,9 @@ typedef struct {
   int64_t total_agents; /* R * N                                                           */
   int64_t scratch_bytes;/* device bytes owned by the world                                 */
   int32_t kernels_per_step; /* libvg kernels one vg_step (slab: begin + finish) launches   */
+  int32_t sense_defaults;   /* 1: K4's sector pass runs with the paper's default constants
+                               compiled in (the world's derived constants are bitwise those);
+                               0: constants read from the parameters (same results)         */
 } vg_world_info;
 
 typedef struct vg_world vg_world;

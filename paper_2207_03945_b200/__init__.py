@@ -100,6 +100,7 @@ class World:
         self.occ_words = info.occ_words
         self.scratch_bytes = info.scratch_bytes
         self.kernels_per_step = info.kernels_per_step
+        self.sense_defaults = bool(info.sense_defaults)
         self.R, self.N = int(params.n_replicas), int(params.n_agents)
         self.is_tag = params.env == "tag"
         if self.slab:

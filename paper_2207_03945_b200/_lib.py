@@ -72,6 +72,7 @@ class VgWorldInfo(ctypes.Structure):
         ("grid", c_int32), ("cell_size", c_float), ("n_cells", c_int32),
         ("obs_dim", c_int32), ("channels", c_int32), ("occ_words", c_int32),
         ("total_agents", c_int64), ("scratch_bytes", c_int64), ("kernels_per_step", c_int32),
+        ("sense_defaults", c_int32),
     ]
 
 

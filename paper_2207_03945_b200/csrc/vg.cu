@@ -390,8 +390,20 @@ void sense_carveout(K* k) {
 
 template <int ENV, bool VISION, bool SLAB>
 void sense_carveouts() {
-  sense_carveout(vg::k_sense<ENV, VISION, SLAB, true>);
-  sense_carveout(vg::k_sense<ENV, VISION, SLAB, false>);
+  sense_carveout(vg::k_sense<ENV, VISION, SLAB, true, false>);
+  sense_carveout(vg::k_sense<ENV, VISION, SLAB, false, false>);
+  if (VISION) sense_carveout(vg::k_sense<ENV, VISION, SLAB, false, VISION>);
+}
+
+// K4's sector pass with the paper's default constants as immediates (vg::sense_defaults):
+// only when the world's derived constants are bitwise those (A12: the same fp32 ops).
+#ifndef VG_SENSE_DEFAULTS
+#define VG_SENSE_DEFAULTS 1
+#endif
+template <int ENV>
+bool sense_defaults_match(const vg::Params& P) {
+  const vg::SenseConst a = vg::sense_const(P), b = vg::sense_defaults<ENV>();
+  return VG_SENSE_DEFAULTS && std::memcmp(&a, &b, sizeof(a)) == 0;
 }
 
 // Function attributes apply to the current device: set them for every world created.
@@ -415,11 +427,15 @@ void sense_kernel(vg_world* w, int cells, const vg::Outs& O, cudaStream_t s) {
   const long long queries = w->slab ? (long long)w->P.N : w->P.total;
   const unsigned grid = (unsigned)(cells + std::min<long long>(queries / cq + 1, w->work_cap));
   if (w->cfg.vision == VG_VISION_RAY)
-    vg::k_sense<ENV, VISION, SLAB, true><<<grid, vg::kSenseWarps * 32, 0, s>>>(
+    vg::k_sense<ENV, VISION, SLAB, true, false><<<grid, vg::kSenseWarps * 32, 0, s>>>(
+        w->P, w->cell_start, w->xo_rec, w->xo_xy, w->xo_perm, O, w->SL, w->ray_dir, w->sub_tab,
+        w->work, w->work_cnt, cq, cells);
+  else if (VISION && sense_defaults_match<ENV>(w->P))
+    vg::k_sense<ENV, VISION, SLAB, false, VISION><<<grid, vg::kSenseWarps * 32, 0, s>>>(
         w->P, w->cell_start, w->xo_rec, w->xo_xy, w->xo_perm, O, w->SL, w->ray_dir, w->sub_tab,
         w->work, w->work_cnt, cq, cells);
   else
-    vg::k_sense<ENV, VISION, SLAB, false><<<grid, vg::kSenseWarps * 32, 0, s>>>(
+    vg::k_sense<ENV, VISION, SLAB, false, false><<<grid, vg::kSenseWarps * 32, 0, s>>>(
         w->P, w->cell_start, w->xo_rec, w->xo_xy, w->xo_perm, O, w->SL, w->ray_dir, w->sub_tab,
         w->work, w->work_cnt, cq, cells);
 }
@@ -642,6 +658,9 @@ vg_status vg_world_query(const vg_world* w, vg_world_info* info) {
   info->total_agents = w->P.total;
   info->scratch_bytes = (int64_t)w->scratch_bytes;
   const int scan_k = (w->n_cells > vg::kScanSmallMax) ? 2 : 1;
+  info->sense_defaults = w->cfg.vision == VG_VISION_SECTOR &&
+                         (w->P.env == vg::kFlock ? sense_defaults_match<vg::kFlock>(w->P)
+                                                 : sense_defaults_match<vg::kTag>(w->P));
   info->kernels_per_step = w->slab ? 6 + scan_k
                                    : (w->fused_bin ? 2 : (w->gather_bin ? 3 : 4 + scan_k));
   return VG_OK;

@@ -1012,7 +1012,36 @@ struct __align__(16) Seg {
   int cbase, a0, a1;
 };
 
-template <int ENV, bool VISION, bool SLAB, bool RAY>
+// The constants of K4's sector pass.  DEF instances take them as compile-time immediates
+// for the paper's default parameters (d_v = 10, d_r = 0.25, fov = 250 deg,
+// v = 128 / 64, c_collide = 1, c_near = 0.5, d_peak = 5.25, w = 0.1, s_max = 0.5), computed
+// with derive()'s fp32 operations; the host uses them only when every field of the world's
+// Params is bitwise equal (sense_defaults_match), so results cannot differ.  Otherwise ptxas
+// re-loads these from the parameter bank in every 32-pair batch (~8 of 60 instructions).
+struct SenseConst {
+  float contact2, fx_mcollide, fx_k_rise, fx_b_rise, fx_nk_fall, fx_b_fall;
+  float inv_w, half_v, inv_dv, dv2, w_prox, inv_smax;
+  int v, view_slots, obs_dim, occ_words;
+};
+__host__ __device__ __forceinline__ SenseConst sense_const(const Params& P) {
+  return SenseConst{P.contact2, P.fx_mcollide, P.fx_k_rise, P.fx_b_rise, P.fx_nk_fall,
+                    P.fx_b_fall, P.inv_w, P.half_v, P.inv_dv, P.dv2, P.w_prox, P.inv_smax,
+                    P.v, P.view_slots, P.obs_dim, P.occ_words};
+}
+template <int ENV>
+__host__ __device__ constexpr SenseConst sense_defaults() {
+  constexpr float fov = (float)(250.0 * 3.14159265358979323846 / 180.0);
+  constexpr float d_v = 10.0f, two_dr = 2.0f * 0.25f, c_near = 0.5f, d_peak = 5.25f;
+  constexpr float k_rise = c_near / (d_peak - two_dr), k_fall = c_near / (d_v - d_peak);
+  constexpr float fx = 4294967296.0f;
+  constexpr int v = (ENV == kFlock) ? 128 : 64, ch = (ENV == kFlock) ? 1 : 2;
+  return SenseConst{two_dr * two_dr, -1.0f * fx, k_rise * fx, (-k_rise * two_dr) * fx,
+                    (-k_fall) * fx, (k_fall * d_v) * fx, (float)v / fov, 0.5f * (float)v,
+                    1.0f / d_v, d_v * d_v, 0.1f, 1.0f / 0.5f,
+                    v, ch * v, ch * v + ((ENV == kFlock) ? 1 : 0), (ch * v + 31) / 32};
+}
+
+template <int ENV, bool VISION, bool SLAB, bool RAY, bool DEF>
 __global__ void __launch_bounds__(kSenseWarps * 32, kSenseMinBlocks) k_sense(
     Params P, const uint32_t* __restrict__ cell_start, const float4* __restrict__ sorted,
     const float2* __restrict__ sorted_xy, const uint32_t* __restrict__ perm, Outs O, Slab SL,
@@ -1042,11 +1071,14 @@ __global__ void __launch_bounds__(kSenseWarps * 32, kSenseMinBlocks) k_sense(
   // Pair-pass constants.  (ptxas sees through this empty asm and re-loads them from the
   // parameter bank per pair batch; forcing them into registers with an opaque add costs 8
   // registers and measured 4 % slower.)
-  float c_contact2 = P.contact2, c_mcollide = P.fx_mcollide, c_k_rise = P.fx_k_rise,
-        c_b_rise = P.fx_b_rise, c_nk_fall = P.fx_nk_fall, c_b_fall = P.fx_b_fall,
-        c_inv_w = P.inv_w, c_half_v = P.half_v, c_inv_dv = P.inv_dv;
-  asm volatile("" : "+f"(c_contact2), "+f"(c_mcollide), "+f"(c_k_rise), "+f"(c_b_rise),
-               "+f"(c_nk_fall), "+f"(c_b_fall), "+f"(c_inv_w), "+f"(c_half_v), "+f"(c_inv_dv));
+  static_assert(!(DEF && (RAY || !VISION)), "DEF: sector vision only");
+  const SenseConst C = DEF ? sense_defaults<ENV>() : sense_const(P);
+  float c_contact2 = C.contact2, c_mcollide = C.fx_mcollide, c_k_rise = C.fx_k_rise,
+        c_b_rise = C.fx_b_rise, c_nk_fall = C.fx_nk_fall, c_b_fall = C.fx_b_fall,
+        c_inv_w = C.inv_w, c_half_v = C.half_v, c_inv_dv = C.inv_dv;
+  if (!DEF)
+    asm volatile("" : "+f"(c_contact2), "+f"(c_mcollide), "+f"(c_k_rise), "+f"(c_b_rise),
+                 "+f"(c_nk_fall), "+f"(c_b_fall), "+f"(c_inv_w), "+f"(c_half_v), "+f"(c_inv_dv));
   // CTA c < n_first: the first chunk_q queries of sensed cell c; CTA n_first + k: overflow
   // item k (a later chunk of a dense cell).  The grid bounds the item count; surplus CTAs
   // exit at once.
@@ -1179,7 +1211,7 @@ __global__ void __launch_bounds__(kSenseWarps * 32, kSenseMinBlocks) k_sense(
           if (contact) {
             if (tj == tq[t]) ++ncol[t]; else ++ntouch[t];
           }
-          if (tq[t] == 0u && tj == 0u) rs[t] += __float2ll_rn(P.w_prox * f);
+          if (tq[t] == 0u && tj == 0u) rs[t] += __float2ll_rn(C.w_prox * f);
         }
       }
       if (VISION && RAY) {
@@ -1229,9 +1261,9 @@ __global__ void __launch_bounds__(kSenseWarps * 32, kSenseMinBlocks) k_sense(
         const float left = fmaf(csn[t], e.y, -sn[t] * e.x);
         // Sector coordinate (phi + fov/2) v / fov; visible iff 0 <= k < v (A3).
         const int k = __float2int_rd(fmaf(vg_atan2(left, fwd), c_inv_w, c_half_v));
-        if ((unsigned)k < (unsigned)P.v) {
+        if ((unsigned)k < (unsigned)C.v) {
           const float val = fminf(d * c_inv_dv, kBelowOne);
-          atomicMin(&s_min[warp][t][tj * P.v + k], __float_as_uint(val));
+          atomicMin(&s_min[warp][t][tj * C.v + k], __float_as_uint(val));
         }
       }
     };
@@ -1294,7 +1326,7 @@ __global__ void __launch_bounds__(kSenseWarps * 32, kSenseMinBlocks) k_sense(
           for (int t = 0; t < NQ; ++t) {
             const float dx = cx_ - qx[t], dy = cy_ - qy[t];
             const float d2 = fmaf(dx, dx, dy * dy);
-            const bool in = d2 < (RAY ? P.cand2 : P.dv2);                // Eq. 1: d < d_v
+            const bool in = d2 < (RAY ? P.cand2 : C.dv2);                // Eq. 1: d < d_v
             const unsigned bal = __ballot_sync(kFull, in);
             if (in)
               sts128(qbase[t] | ((tail[t] + (__popc(bal & lt_mask) << 4)) & (kQueue * 16 - 16)),
@@ -1378,14 +1410,14 @@ __global__ void __launch_bounds__(kSenseWarps * 32, kSenseMinBlocks) k_sense(
 #pragma unroll
           for (int w = 0; w < kMaxViewSlots / 32; ++w) {
             const int k = 32 * w + lane;
-            vals[w] = (k < P.view_slots) ? s_min[warp][t][k] : kOneBits;
+            vals[w] = (k < C.view_slots) ? s_min[warp][t][k] : kOneBits;
           }
           if (FAST || O.obs) {
-            float* orow = O.obs + row * (idx_t)P.obs_dim;
+            float* orow = O.obs + row * (idx_t)C.obs_dim;
 #pragma unroll
             for (int w = 0; w < kMaxViewSlots / 32; ++w)
-              if (32 * w + lane < P.view_slots) orow[32 * w + lane] = __uint_as_float(vals[w]);
-            if (ENV == kFlock && lane == 0) orow[P.view_slots] = me[t].w * P.inv_smax;  // A24
+              if (32 * w + lane < C.view_slots) orow[32 * w + lane] = __uint_as_float(vals[w]);
+            if (ENV == kFlock && lane == 0) orow[C.view_slots] = me[t].w * C.inv_smax;  // A24
           }
           if (FAST || O.occ) {
             uint32_t mine = 0u;
@@ -1394,7 +1426,7 @@ __global__ void __launch_bounds__(kSenseWarps * 32, kSenseMinBlocks) k_sense(
               const unsigned bits = __ballot_sync(kFull, vals[w] < kOneBits);
               if (lane == w) mine = bits;
             }
-            if (lane < P.occ_words) O.occ[row * (idx_t)P.occ_words + lane] = mine;
+            if (lane < C.occ_words) O.occ[row * (idx_t)C.occ_words + lane] = mine;
           }
         }
       };

@@ -34,7 +34,7 @@ def test_library_exports_every_declared_symbol():
 
 def test_abi_version():
     from paper_2207_03945_b200 import _lib
-    assert _lib.lib.vg_abi_version() == 1
+    assert _lib.lib.vg_abi_version() == 2
 
 
 def test_struct_layout_matches_header():

@@ -140,6 +140,22 @@ def test_sector_model_variants(cuda, fov, v):
     run_and_check(p, vi.init_state(p, seed=11), 2)
 
 
+def test_default_constants_path(cuda):
+    # K4's sector pass has an instance with the paper's default constants compiled in; the
+    # benchmark worlds must take it (their derived fp32 constants are bitwise the compiled
+    # ones) and any other parameter set must not.  Parity of both instances is covered by
+    # the tests above (defaults: c1-c5, edge cases; generic: sector variants, d_v = 3, ...).
+    for name in ("c1", "c2", "c3", "c4", "c5"):
+        w = make_world(vi.workload(name))
+        assert w.sense_defaults, name
+        w.close()
+    for p in (vi.flock_params(2000, v=64), vi.flock_params(2000, d_v=12.0),
+              vi.tag_params(2000, w_prox=0.2), vi.workload("c2").replace(vision="ray")):
+        w = make_world(p)
+        assert not w.sense_defaults, p
+        w.close()
+
+
 @pytest.mark.parametrize("case", ["gather_replicas", "gather_tag_replicas", "cta_sort",
                                   "warp_sort"])
 def test_binning_paths(cuda, case):
