@@ -1072,10 +1072,14 @@ __global__ void __launch_bounds__(kSenseWarps * 32, kSenseMinBlocks) k_sense(
   // parameter bank per pair batch; forcing them into registers with an opaque add costs 8
   // registers and measured 4 % slower.)
   static_assert(!(DEF && (RAY || !VISION)), "DEF: sector vision only");
-  const SenseConst C = DEF ? sense_defaults<ENV>() : sense_const(P);
-  float c_contact2 = C.contact2, c_mcollide = C.fx_mcollide, c_k_rise = C.fx_k_rise,
-        c_b_rise = C.fx_b_rise, c_nk_fall = C.fx_nk_fall, c_b_fall = C.fx_b_fall,
-        c_inv_w = C.inv_w, c_half_v = C.half_v, c_inv_dv = C.inv_dv;
+  // DEF: compile-time constants; otherwise each use reads the parameter bank (a copy of
+  // the whole set held in registers costs the generic instances their occupancy).
+  constexpr SenseConst D = sense_defaults<ENV>();
+#define VG_SC(f) (DEF ? D.f : P.f)
+  float c_contact2 = VG_SC(contact2), c_mcollide = VG_SC(fx_mcollide),
+        c_k_rise = VG_SC(fx_k_rise), c_b_rise = VG_SC(fx_b_rise), c_nk_fall = VG_SC(fx_nk_fall),
+        c_b_fall = VG_SC(fx_b_fall), c_inv_w = VG_SC(inv_w), c_half_v = VG_SC(half_v),
+        c_inv_dv = VG_SC(inv_dv);
   if (!DEF)
     asm volatile("" : "+f"(c_contact2), "+f"(c_mcollide), "+f"(c_k_rise), "+f"(c_b_rise),
                  "+f"(c_nk_fall), "+f"(c_b_fall), "+f"(c_inv_w), "+f"(c_half_v), "+f"(c_inv_dv));
@@ -1211,7 +1215,7 @@ __global__ void __launch_bounds__(kSenseWarps * 32, kSenseMinBlocks) k_sense(
           if (contact) {
             if (tj == tq[t]) ++ncol[t]; else ++ntouch[t];
           }
-          if (tq[t] == 0u && tj == 0u) rs[t] += __float2ll_rn(C.w_prox * f);
+          if (tq[t] == 0u && tj == 0u) rs[t] += __float2ll_rn(VG_SC(w_prox) * f);
         }
       }
       if (VISION && RAY) {
@@ -1261,9 +1265,9 @@ __global__ void __launch_bounds__(kSenseWarps * 32, kSenseMinBlocks) k_sense(
         const float left = fmaf(csn[t], e.y, -sn[t] * e.x);
         // Sector coordinate (phi + fov/2) v / fov; visible iff 0 <= k < v (A3).
         const int k = __float2int_rd(fmaf(vg_atan2(left, fwd), c_inv_w, c_half_v));
-        if ((unsigned)k < (unsigned)C.v) {
+        if ((unsigned)k < (unsigned)VG_SC(v)) {
           const float val = fminf(d * c_inv_dv, kBelowOne);
-          atomicMin(&s_min[warp][t][tj * C.v + k], __float_as_uint(val));
+          atomicMin(&s_min[warp][t][tj * VG_SC(v) + k], __float_as_uint(val));
         }
       }
     };
@@ -1326,7 +1330,7 @@ __global__ void __launch_bounds__(kSenseWarps * 32, kSenseMinBlocks) k_sense(
           for (int t = 0; t < NQ; ++t) {
             const float dx = cx_ - qx[t], dy = cy_ - qy[t];
             const float d2 = fmaf(dx, dx, dy * dy);
-            const bool in = d2 < (RAY ? P.cand2 : C.dv2);                // Eq. 1: d < d_v
+            const bool in = d2 < (RAY ? P.cand2 : VG_SC(dv2));                // Eq. 1: d < d_v
             const unsigned bal = __ballot_sync(kFull, in);
             if (in)
               sts128(qbase[t] | ((tail[t] + (__popc(bal & lt_mask) << 4)) & (kQueue * 16 - 16)),
@@ -1410,14 +1414,14 @@ __global__ void __launch_bounds__(kSenseWarps * 32, kSenseMinBlocks) k_sense(
 #pragma unroll
           for (int w = 0; w < kMaxViewSlots / 32; ++w) {
             const int k = 32 * w + lane;
-            vals[w] = (k < C.view_slots) ? s_min[warp][t][k] : kOneBits;
+            vals[w] = (k < VG_SC(view_slots)) ? s_min[warp][t][k] : kOneBits;
           }
           if (FAST || O.obs) {
-            float* orow = O.obs + row * (idx_t)C.obs_dim;
+            float* orow = O.obs + row * (idx_t)VG_SC(obs_dim);
 #pragma unroll
             for (int w = 0; w < kMaxViewSlots / 32; ++w)
-              if (32 * w + lane < C.view_slots) orow[32 * w + lane] = __uint_as_float(vals[w]);
-            if (ENV == kFlock && lane == 0) orow[C.view_slots] = me[t].w * C.inv_smax;  // A24
+              if (32 * w + lane < VG_SC(view_slots)) orow[32 * w + lane] = __uint_as_float(vals[w]);
+            if (ENV == kFlock && lane == 0) orow[VG_SC(view_slots)] = me[t].w * VG_SC(inv_smax);  // A24
           }
           if (FAST || O.occ) {
             uint32_t mine = 0u;
@@ -1426,7 +1430,7 @@ __global__ void __launch_bounds__(kSenseWarps * 32, kSenseMinBlocks) k_sense(
               const unsigned bits = __ballot_sync(kFull, vals[w] < kOneBits);
               if (lane == w) mine = bits;
             }
-            if (lane < C.occ_words) O.occ[row * (idx_t)C.occ_words + lane] = mine;
+            if (lane < VG_SC(occ_words)) O.occ[row * (idx_t)VG_SC(occ_words) + lane] = mine;
           }
         }
       };
@@ -1438,6 +1442,8 @@ __global__ void __launch_bounds__(kSenseWarps * 32, kSenseMinBlocks) k_sense(
   }
 }
 
+
+#undef VG_SC
 
 // ------------------------------------------------------------------------- slab mode
 // One world split over P ranks by x-slabs of cell columns.
