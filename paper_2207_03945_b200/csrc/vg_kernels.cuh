@@ -952,6 +952,9 @@ constexpr int kSenseMinBlocks = VG_SENSE_MINB;  // resident CTAs per SM
 // Ring (power of 2): >= 31 carried + 64 pushed, and large enough that one chunk's pushes
 // never reach the slots the previous drain read (carried + 64 + 2 x 32 <= kQueue), so one
 // warp sync per chunk (before the drain) orders all ring traffic.
+#ifndef VG_SENSE_TAG_DEF_MINB
+#define VG_SENSE_TAG_DEF_MINB 8     // the tag default-constant instance: <= 64 registers, 8 CTAs/SM
+#endif
 #ifndef VG_SENSE_HALVES
 #define VG_SENSE_HALVES 2          // 32-slot halves per candidate chunk
 #endif
@@ -1042,7 +1045,7 @@ __host__ __device__ constexpr SenseConst sense_defaults() {
 }
 
 template <int ENV, bool VISION, bool SLAB, bool RAY, bool DEF>
-__global__ void __launch_bounds__(kSenseWarps * 32, kSenseMinBlocks) k_sense(
+__global__ void __launch_bounds__(kSenseWarps * 32, (DEF && ENV == kTag) ? VG_SENSE_TAG_DEF_MINB : kSenseMinBlocks) k_sense(
     Params P, const uint32_t* __restrict__ cell_start, const float4* __restrict__ sorted,
     const float2* __restrict__ sorted_xy, const uint32_t* __restrict__ perm, Outs O, Slab SL,
     const float2* __restrict__ ray_dir, const uint32_t* __restrict__ sub_tab,
