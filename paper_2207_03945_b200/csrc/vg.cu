@@ -48,6 +48,7 @@ struct vg_world {
   bool binned = false;
   bool fused_bin = false;          // K1-K3 fused per replica (small worlds)
   bool gather_bin = false;         // K2-K3b as one per-cell gather kernel (K3g)
+  bool sense_def = false;          // K4 sector pass: the default-constant instance
   size_t scratch_bytes = 0;
   uint32_t* count = nullptr;       // [n_cells]     per-cell histogram (zero between uses)
   uint32_t* tile_sum = nullptr;    // [n_cells / 4096 + 1] multi-CTA scan partials
@@ -430,7 +431,7 @@ void sense_kernel(vg_world* w, int cells, const vg::Outs& O, cudaStream_t s) {
     vg::k_sense<ENV, VISION, SLAB, true, false><<<grid, vg::kSenseWarps * 32, 0, s>>>(
         w->P, w->cell_start, w->xo_rec, w->xo_xy, w->xo_perm, O, w->SL, w->ray_dir, w->sub_tab,
         w->work, w->work_cnt, cq, cells);
-  else if (VISION && sense_defaults_match<ENV>(w->P))
+  else if (VISION && w->sense_def)
     vg::k_sense<ENV, VISION, SLAB, false, VISION><<<grid, vg::kSenseWarps * 32, 0, s>>>(
         w->P, w->cell_start, w->xo_rec, w->xo_xy, w->xo_perm, O, w->SL, w->ray_dir, w->sub_tab,
         w->work, w->work_cnt, cq, cells);
@@ -529,6 +530,12 @@ vg_status vg_world_create(const vg_config* cfg, vg_world** out) {
   cudaGetDevice(&w->device);
   cudaDeviceGetAttribute(&w->n_sm, cudaDevAttrMultiProcessorCount, w->device);
   set_kernel_attributes();                         // per device (the current one)
+  {                                // VG_SENSE_GENERIC=1: always the generic instance (tests)
+    const char* gen = std::getenv("VG_SENSE_GENERIC");
+    w->sense_def = !(gen && gen[0] && gen[0] != '0') && cfg->vision == VG_VISION_SECTOR &&
+                   (w->P.env == vg::kFlock ? sense_defaults_match<vg::kFlock>(w->P)
+                                           : sense_defaults_match<vg::kTag>(w->P));
+  }
   w->gather_bin = VG_GATHER_BIN && cfg->shard == VG_SHARD_REPLICA && !w->fused_bin &&
                   w->n_cells <= 8LL * w->n_sm && cfg->n_agents <= vg::kGatherMaxN;
   size_t n = (size_t)w->P.total;
@@ -658,9 +665,7 @@ vg_status vg_world_query(const vg_world* w, vg_world_info* info) {
   info->total_agents = w->P.total;
   info->scratch_bytes = (int64_t)w->scratch_bytes;
   const int scan_k = (w->n_cells > vg::kScanSmallMax) ? 2 : 1;
-  info->sense_defaults = w->cfg.vision == VG_VISION_SECTOR &&
-                         (w->P.env == vg::kFlock ? sense_defaults_match<vg::kFlock>(w->P)
-                                                 : sense_defaults_match<vg::kTag>(w->P));
+  info->sense_defaults = w->sense_def;
   info->kernels_per_step = w->slab ? 6 + scan_k
                                    : (w->fused_bin ? 2 : (w->gather_bin ? 3 : 4 + scan_k));
   return VG_OK;

@@ -156,6 +156,30 @@ def test_default_constants_path(cuda):
         w.close()
 
 
+@pytest.mark.parametrize("name", ["c2", "c3"])
+def test_default_constants_bitwise_generic(cuda, name, monkeypatch):
+    # The default-constant instance and the generic one (VG_SENSE_GENERIC=1) must give
+    # bitwise-identical outputs on the same state: the constants are the same fp32 values.
+    torch = _torch()
+    p = vi.workload(name)
+    st = dev(vi.init_state(p, seed=23))
+    res = []
+    for gen in ("0", "1"):
+        monkeypatch.setenv("VG_SENSE_GENERIC", gen)
+        w = make_world(p)
+        assert w.sense_defaults == (gen == "0")
+        out = w.alloc_outputs()
+        w.bin(st)
+        w.sense(out)
+        torch.cuda.synchronize()
+        res.append({k: host(getattr(out, k)).copy() for k in
+                    ("obs", "reward", "n_neigh", "n_collide", "n_touch", "sector_occ")
+                    if getattr(out, k) is not None})
+        w.close()
+    for k in res[0]:
+        assert np.array_equal(res[0][k].view(np.uint8), res[1][k].view(np.uint8)), k
+
+
 @pytest.mark.parametrize("case", ["gather_replicas", "gather_tag_replicas", "cta_sort",
                                   "warp_sort"])
 def test_binning_paths(cuda, case):
