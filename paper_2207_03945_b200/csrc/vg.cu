@@ -393,7 +393,10 @@ template <int ENV, bool VISION, bool SLAB>
 void sense_carveouts() {
   sense_carveout(vg::k_sense<ENV, VISION, SLAB, true, false>);
   sense_carveout(vg::k_sense<ENV, VISION, SLAB, false, false>);
-  if (VISION) sense_carveout(vg::k_sense<ENV, VISION, SLAB, false, VISION>);
+  if (VISION) {
+    sense_carveout(vg::k_sense<ENV, VISION, SLAB, false, VISION>);
+    sense_carveout(vg::k_sense<ENV, VISION, SLAB, true, VISION>);
+  }
 }
 
 // K4's sector pass with the paper's default constants as immediates (vg::sense_defaults):
@@ -427,7 +430,11 @@ void sense_kernel(vg_world* w, int cells, const vg::Outs& O, cudaStream_t s) {
   // one CTA per sensed cell + an upper bound on the overflow items (surplus CTAs exit)
   const long long queries = w->slab ? (long long)w->P.N : w->P.total;
   const unsigned grid = (unsigned)(cells + std::min<long long>(queries / cq + 1, w->work_cap));
-  if (w->cfg.vision == VG_VISION_RAY)
+  if (w->cfg.vision == VG_VISION_RAY && VISION && w->sense_def)
+    vg::k_sense<ENV, VISION, SLAB, true, VISION><<<grid, vg::kSenseWarps * 32, 0, s>>>(
+        w->P, w->cell_start, w->xo_rec, w->xo_xy, w->xo_perm, O, w->SL, w->ray_dir, w->sub_tab,
+        w->work, w->work_cnt, cq, cells);
+  else if (w->cfg.vision == VG_VISION_RAY)
     vg::k_sense<ENV, VISION, SLAB, true, false><<<grid, vg::kSenseWarps * 32, 0, s>>>(
         w->P, w->cell_start, w->xo_rec, w->xo_xy, w->xo_perm, O, w->SL, w->ray_dir, w->sub_tab,
         w->work, w->work_cnt, cq, cells);
@@ -532,7 +539,7 @@ vg_status vg_world_create(const vg_config* cfg, vg_world** out) {
   set_kernel_attributes();                         // per device (the current one)
   {                                // VG_SENSE_GENERIC=1: always the generic instance (tests)
     const char* gen = std::getenv("VG_SENSE_GENERIC");
-    w->sense_def = !(gen && gen[0] && gen[0] != '0') && cfg->vision == VG_VISION_SECTOR &&
+    w->sense_def = !(gen && gen[0] && gen[0] != '0') &&
                    (w->P.env == vg::kFlock ? sense_defaults_match<vg::kFlock>(w->P)
                                            : sense_defaults_match<vg::kTag>(w->P));
   }

@@ -1024,11 +1024,13 @@ struct __align__(16) Seg {
 struct SenseConst {
   float contact2, fx_mcollide, fx_k_rise, fx_b_rise, fx_nk_fall, fx_b_fall;
   float inv_w, half_v, inv_dv, dv2, w_prox, inv_smax;
+  float d_r, cand2, half_fov, two_pi, d_v;         // ray vision
   int v, view_slots, obs_dim, occ_words;
 };
 __host__ __device__ __forceinline__ SenseConst sense_const(const Params& P) {
   return SenseConst{P.contact2, P.fx_mcollide, P.fx_k_rise, P.fx_b_rise, P.fx_nk_fall,
                     P.fx_b_fall, P.inv_w, P.half_v, P.inv_dv, P.dv2, P.w_prox, P.inv_smax,
+                    P.d_r, P.cand2, P.half_fov, P.two_pi, P.d_v,
                     P.v, P.view_slots, P.obs_dim, P.occ_words};
 }
 template <int ENV>
@@ -1041,6 +1043,8 @@ __host__ __device__ constexpr SenseConst sense_defaults() {
   return SenseConst{two_dr * two_dr, -1.0f * fx, k_rise * fx, (-k_rise * two_dr) * fx,
                     (-k_fall) * fx, (k_fall * d_v) * fx, (float)v / fov, 0.5f * (float)v,
                     1.0f / d_v, d_v * d_v, 0.1f, 1.0f / 0.5f,
+                    0.25f, (d_v + 0.25f) * (d_v + 0.25f), 0.5f * fov,
+                    (float)(2.0 * 3.14159265358979323846), d_v,
                     v, ch * v, ch * v + ((ENV == kFlock) ? 1 : 0), (ch * v + 31) / 32};
 }
 
@@ -1074,7 +1078,7 @@ __global__ void __launch_bounds__(kSenseWarps * 32, (DEF && ENV == kTag) ? VG_SE
   // Pair-pass constants.  (ptxas sees through this empty asm and re-loads them from the
   // parameter bank per pair batch; forcing them into registers with an opaque add costs 8
   // registers and measured 4 % slower.)
-  static_assert(!(DEF && (RAY || !VISION)), "DEF: sector vision only");
+  static_assert(!(DEF && !VISION), "DEF: vision passes only");
   // DEF: compile-time constants; otherwise each use reads the parameter bank (a copy of
   // the whole set held in registers costs the generic instances their occupancy).
   constexpr SenseConst D = sense_defaults<ENV>();
@@ -1209,7 +1213,7 @@ __global__ void __launch_bounds__(kSenseWarps * 32, (DEF && ENV == kTag) ? VG_SE
       // fixed-point units (x 2^32, A16b).
       const float f = contact ? c_mcollide
                               : fminf(fmaf(c_k_rise, d, c_b_rise), fmaf(c_nk_fall, d, c_b_fall));
-      if (!RAY || d2 < P.dv2) {                                       // Eq. 1: d < d_v
+      if (!RAY || d2 < VG_SC(dv2)) {                                       // Eq. 1: d < d_v
         if (RAY) ++nnb[t];
         if (ENV == kFlock) {
           rs[t] += __float2ll_rn(f);
@@ -1224,16 +1228,16 @@ __global__ void __launch_bounds__(kSenseWarps * 32, (DEF && ENV == kTag) ? VG_SE
       if (VISION && RAY) {
         const float fwd = fmaf(csn[t], e.x, sn[t] * e.y);
         const float left = fmaf(csn[t], e.y, -sn[t] * e.x);
-        uint32_t* row = &s_min[warp][t][tj * P.v];
-        if (d <= P.d_r) {                          // origin inside the disc: every ray hits at 0
-          for (int k = 0; k < P.v; ++k) atomicMin(&row[k], 0u);
+        uint32_t* row = &s_min[warp][t][tj * VG_SC(v)];
+        if (d <= VG_SC(d_r)) {                          // origin inside the disc: every ray hits at 0
+          for (int k = 0; k < VG_SC(v); ++k) atomicMin(&row[k], 0u);
           return;
         }
         const float phi = vg_atan2(left, fwd);
         // Angular half-width of the disc, asin(d_r / d), bounded from above (the per-ray test
         // below is exact, so the range only has to be conservative): for s = d_r/d <= 1/2,
         // asin(s) <= s (1 + s^2 (1/6 + s^2/10)); nearer discs take asinf.
-        const float sr = fminf(P.d_r * rsq, 1.f);
+        const float sr = fminf(VG_SC(d_r) * rsq, 1.f);
         const float alpha = (sr <= 0.5f)
             ? fmaf(sr * sr * sr, fmaf(sr * sr, 0.1f, 0.16666667f), sr) + 1e-6f
             : asinf(sr);
@@ -1242,21 +1246,21 @@ __global__ void __launch_bounds__(kSenseWarps * 32, (DEF && ENV == kTag) ? VG_SE
         // the fp32 error of phi and alpha; every ray in the range is then tested exactly.
 #pragma unroll 1
         for (int wrap = -1; wrap <= 1; ++wrap) {
-          const float lo = phi - alpha + wrap * P.two_pi, hi = phi + alpha + wrap * P.two_pi;
-          if (hi < -P.half_fov - 0.1f || lo > P.half_fov + 0.1f) continue;
-          const int k0 = max(0, (int)ceilf((lo + P.half_fov) * P.inv_w - 0.5f - 1e-4f));
-          const int k1 = min(P.v - 1, (int)floorf((hi + P.half_fov) * P.inv_w - 0.5f + 1e-4f));
+          const float lo = phi - alpha + wrap * VG_SC(two_pi), hi = phi + alpha + wrap * VG_SC(two_pi);
+          if (hi < -VG_SC(half_fov) - 0.1f || lo > VG_SC(half_fov) + 0.1f) continue;
+          const int k0 = max(0, (int)ceilf((lo + VG_SC(half_fov)) * VG_SC(inv_w) - 0.5f - 1e-4f));
+          const int k1 = min(VG_SC(v) - 1, (int)floorf((hi + VG_SC(half_fov)) * VG_SC(inv_w) - 0.5f + 1e-4f));
           for (int k = k0; k <= k1; ++k) {
             const float2 ud = s_ray[k];
             const float bb = fmaf(ud.x, fwd, ud.y * left);       // along the ray
             const float pp = fmaf(ud.x, left, -ud.y * fwd);      // perpendicular offset
-            const float h = (P.d_r - pp) * (P.d_r + pp);         // r^2 - p^2, well conditioned
+            const float h = (VG_SC(d_r) - pp) * (VG_SC(d_r) + pp);         // r^2 - p^2, well conditioned
             if (h >= 0.f && bb > 0.f) {
               float sh;                                          // MUFU sqrt (~1 ulp): the
               asm("sqrt.approx.ftz.f32 %0, %1;" : "=f"(sh) : "f"(h));   // IEEE sqrtf's slow path
               const float tt = fmaxf(bb - sh, 0.f);              // entry distance
-              if (tt < P.d_v)
-                atomicMin(&row[k], __float_as_uint(fminf(tt * P.inv_dv, kBelowOne)));
+              if (tt < VG_SC(d_v))
+                atomicMin(&row[k], __float_as_uint(fminf(tt * VG_SC(inv_dv), kBelowOne)));
             }
           }
         }
@@ -1333,7 +1337,7 @@ __global__ void __launch_bounds__(kSenseWarps * 32, (DEF && ENV == kTag) ? VG_SE
           for (int t = 0; t < NQ; ++t) {
             const float dx = cx_ - qx[t], dy = cy_ - qy[t];
             const float d2 = fmaf(dx, dx, dy * dy);
-            const bool in = d2 < (RAY ? P.cand2 : VG_SC(dv2));                // Eq. 1: d < d_v
+            const bool in = d2 < (RAY ? VG_SC(cand2) : VG_SC(dv2));                // Eq. 1: d < d_v
             const unsigned bal = __ballot_sync(kFull, in);
             if (in)
               sts128(qbase[t] | ((tail[t] + (__popc(bal & lt_mask) << 4)) & (kQueue * 16 - 16)),

@@ -145,23 +145,26 @@ def test_default_constants_path(cuda):
     # benchmark worlds must take it (their derived fp32 constants are bitwise the compiled
     # ones) and any other parameter set must not.  Parity of both instances is covered by
     # the tests above (defaults: c1-c5, edge cases; generic: sector variants, d_v = 3, ...).
-    for name in ("c1", "c2", "c3", "c4", "c5"):
-        w = make_world(vi.workload(name))
-        assert w.sense_defaults, name
+    for p in [vi.workload(n) for n in ("c1", "c2", "c3", "c4", "c5")] + \
+            [vi.workload("c2").replace(vision="ray"), vi.workload("c3").replace(vision="ray")]:
+        w = make_world(p)
+        assert w.sense_defaults, p
         w.close()
     for p in (vi.flock_params(2000, v=64), vi.flock_params(2000, d_v=12.0),
-              vi.tag_params(2000, w_prox=0.2), vi.workload("c2").replace(vision="ray")):
+              vi.tag_params(2000, w_prox=0.2),
+              vi.flock_params(2000, d_r=0.3).replace(vision="ray")):
         w = make_world(p)
         assert not w.sense_defaults, p
         w.close()
 
 
-@pytest.mark.parametrize("name", ["c2", "c3"])
-def test_default_constants_bitwise_generic(cuda, name, monkeypatch):
+@pytest.mark.parametrize("name,vision", [("c2", "sector"), ("c3", "sector"), ("c2", "ray"),
+                                         ("c3", "ray")])
+def test_default_constants_bitwise_generic(cuda, name, vision, monkeypatch):
     # The default-constant instance and the generic one (VG_SENSE_GENERIC=1) must give
     # bitwise-identical outputs on the same state: the constants are the same fp32 values.
     torch = _torch()
-    p = vi.workload(name)
+    p = vi.workload(name).replace(vision=vision)
     st = dev(vi.init_state(p, seed=23))
     res = []
     for gen in ("0", "1"):
