@@ -765,6 +765,9 @@ __global__ void __launch_bounds__(kGatherThreads) k_cell_gather(
 constexpr int kRBMaxCells = 256;
 constexpr int kRBMaxAgents = 32768;
 
+#ifndef VG_RB_PREFETCH
+#define VG_RB_PREFETCH 1
+#endif
 #ifndef VG_RB_THREADS
 #define VG_RB_THREADS 1024
 #endif
@@ -790,6 +793,17 @@ __global__ void __launch_bounds__(kRBThreads, 2048 / kRBThreads) k_replica_bin(
   unsigned lt;
   asm("mov.u32 %0, %%lanemask_lt;" : "=r"(lt));
   for (int c = lane; c < C; c += 32) s_wc[warp][c] = 0u;
+  if (VG_RB_PREFETCH && i1 > i0) {
+    // The warp walks its range serially, one 32-agent load round at a time: ask L2 for the
+    // whole range (state, actions) up front, so later rounds wait on L2, not HBM.
+    auto pf = [&](const void* lo, size_t bytes) {
+      const uintptr_t a0 = (uintptr_t)lo & ~(uintptr_t)127, a1 = (uintptr_t)lo + bytes;
+      for (uintptr_t a = a0 + 128u * lane; a < a1; a += 32u * 128u)
+        asm volatile("prefetch.global.L2 [%0];" ::"l"(a));
+    };
+    pf(src + base + i0, (size_t)(i1 - i0) * sizeof(float4));
+    if (INTEGRATE) pf(actions + base + i0, (size_t)(i1 - i0) * sizeof(float2));
+  }
   __syncwarp();
   // ---- pass 1: integrate + cell id + warp-private histogram
   for (int b = i0; b < i1; b += 32) {
