@@ -184,7 +184,7 @@ def test_default_constants_bitwise_generic(cuda, name, vision, monkeypatch):
 
 
 @pytest.mark.parametrize("case", ["gather_replicas", "gather_tag_replicas", "cta_sort",
-                                  "warp_sort"])
+                                  "warp_sort", "gather_tag_dense", "cta_sort_dense"])
 def test_binning_paths(cuda, case):
     # Each K2-K3b variant against the oracle's bins (bit-exact) and sense outputs:
     # K3g (per-cell gather, several replicas), K3b' (one CTA per cell: few cells, N above
@@ -197,13 +197,25 @@ def test_binning_paths(cuda, case):
     elif case == "cta_sort":
         p, kps = vi.flock_params(20000), 5
         rows = np.arange(0, 20000, 41)
-    else:
+    elif case == "warp_sort":
         p, kps = vi.flock_params(20000, width=400.0, d_v=10.0), 5
         rows = np.arange(0, 20000, 41)
+    elif case == "gather_tag_dense":         # cells above 1,024 members: K3g's fallback
+        p, kps = vi.tag_params(4000), 3
+        rows = np.arange(0, 4000, 7)
+    else:                                    # N > 16,384 with dense cells: K3b''s fallback
+        p, kps = vi.flock_params(17000), 5
+        rows = np.arange(0, 17000, 53)
+    st0 = vi.clustered_state(p, seed=5, n_clusters=3, sigma=1.5) if case.endswith("dense") \
+        else vi.init_state(p, seed=17)
     w = make_world(p)
     assert w.kernels_per_step == kps
+    if case.endswith("dense"):
+        w.bin(dev(st0))
+        cs = host(w.get_bins()["cell_start"]).astype(np.int64)
+        assert np.diff(cs).max() > 1024                  # the fallback path really runs
     w.close()
-    run_and_check(p, vi.init_state(p, seed=17), 2, rows=rows)
+    run_and_check(p, st0, 2, rows=rows)
 
 
 @pytest.mark.parametrize("grid", [9, 0])
