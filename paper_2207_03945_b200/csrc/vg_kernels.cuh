@@ -503,19 +503,29 @@ __global__ void __launch_bounds__(256) k_cell_sort(
       perm[b + k] = id;
     }
   }
-  for (int base = 0; base < (m > kRankMax ? 0 : m); base += 32) {
-    const int idx = base + lane;
-    const bool valid = idx < m;
-    const uint32_t id = valid ? tmp_id[b + idx] : 0xffffffffu;
-    int rank = 0;
-    for (int jb = 0; jb < m; jb += 32) {
-      const uint32_t other = (jb + lane < m) ? tmp_id[b + jb + lane] : 0xffffffffu;
-#pragma unroll 8
-      for (int t = 0; t < 32; ++t) rank += (__shfl_sync(kFull, other, t) < id) ? 1 : 0;
-    }
-    if (valid) {
-      sorted[b + rank] = tmp_rec[b + idx];
-      perm[b + rank] = id;
+  if (m <= kRankMax) {
+    // Rank by id against the cell's ids staged in this warp's shared slice (4 per 16-byte
+    // broadcast load; padding ids 0xffffffff never count).
+    __shared__ __align__(16) uint32_t s_ids[8][kRankMax];
+    for (int k = lane; k < ((m + 3) & ~3); k += 32)
+      s_ids[wib][k] = (k < m) ? tmp_id[b + k] : 0xffffffffu;
+    __syncwarp();
+    const uint4* ids4 = reinterpret_cast<const uint4*>(s_ids[wib]);
+    for (int base = 0; base < m; base += 32) {
+      const int idx = base + lane;
+      const bool valid = idx < m;
+      const uint32_t id = valid ? s_ids[wib][idx] : 0xffffffffu;
+      uint32_t rank = 0;
+#pragma unroll 4
+      for (int j4 = 0; j4 < (m + 3) >> 2; ++j4) {
+        const uint4 o = ids4[j4];
+        rank += (o.x < id ? 1u : 0u) + (o.y < id ? 1u : 0u) + (o.z < id ? 1u : 0u) +
+                (o.w < id ? 1u : 0u);
+      }
+      if (valid) {
+        sorted[b + rank] = tmp_rec[b + idx];
+        perm[b + rank] = id;
+      }
     }
   }
   __syncwarp();                                         // this warp's writes are visible
