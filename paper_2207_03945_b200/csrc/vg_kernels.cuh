@@ -172,7 +172,10 @@ __global__ void __launch_bounds__(256) k_integrate_bin(
 // for the next binning.  One CTA of 1024 threads: the counts are staged in shared memory
 // with coalesced loads, each thread scans a contiguous chunk there, and the results go
 // back out coalesced (n <= kScanSmallMax; larger grids use K2').
-constexpr int kScanSmallMax = 12288;   // 48 KB; above it the 2-kernel K2' is faster (c5: 18,496)
+#ifndef VG_SCAN_SMALL_MAX
+#define VG_SCAN_SMALL_MAX 12288
+#endif
+constexpr int kScanSmallMax = VG_SCAN_SMALL_MAX;   // 48 KB; above it the 2-kernel K2' is faster (c5: 18,496)
 __global__ void __launch_bounds__(1024) k_scan_cells(uint32_t* __restrict__ count,
                                                       uint32_t* __restrict__ start, int n) {
   extern __shared__ uint32_t s_c[];                     // [n]
