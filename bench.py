@@ -273,7 +273,9 @@ class ReplicaRunner:
         self.state = torch.from_numpy(init(p, seed=1000 * rank)).to(device)
         self.launches = self.w.kernels_per_step
         self.phase_names = {"integrate_bin": ("integrate+bin (fused K1-K3)" if self.launches == 2
-                                              else "integrate_bin"), "scan_cells": "scan_cells",
+                                              else "integrate_bin"),
+                            "scan_cells": ("gather bin (K3g: K2-K3b)" if self.launches == 3
+                                           else "scan_cells"),
                             "scatter": "scatter", "cell_sort": "cell_sort", "sense": "sense"}
 
     def step(self, acts):
@@ -568,6 +570,9 @@ def run_ours(args):
                        "scatter": 44 * n, "cell_sort": 68 * n, "sense": obs_b * n}
         if fused:         # one kernel does K1-K3b: the other binning phases are empty
             stage_bytes = {"integrate_bin": 92 * n, "sense": obs_b * n}
+        elif not slab_mode and getattr(w, "kernels_per_step", 5) == 3:   # K1 + K3g + K4
+            stage_bytes = {"integrate_bin": 48 * n, "scan_cells": (44 + 68) * n + scan_b,
+                           "sense": obs_b * n}
         # Model bound: every binning stage at the HBM roof + K4 at the larger of
         # its HBM floor and its algorithmic ALU floor (45 ops per in-radius pair).
         floor_s = sum(b for k2, b in stage_bytes.items() if k2 != "sense") / (hbm * 1e9)

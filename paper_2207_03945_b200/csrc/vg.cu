@@ -525,10 +525,6 @@ vg_status vg_world_create(const vg_config* cfg, vg_world** out) {
   if (!w) return fail(VG_ENOMEM, "host allocation failed");
   w->cfg = *cfg;
   w->P = derive(*cfg, g);
-  // one CTA per replica: worth it when replicas fill the GPU or the world is tiny
-  w->fused_bin = cfg->shard == VG_SHARD_REPLICA && g * g <= vg::kRBMaxCells &&
-                 cfg->n_agents <= vg::kRBMaxAgents &&
-                 (cfg->n_replicas >= 64 || cfg->n_agents <= VG_FUSED_SINGLE_MAX);
   {
     const char* ng = std::getenv("VG_NO_GRAPH");
     w->graphs_enabled = !(ng && ng[0] && ng[0] != '0');
@@ -537,14 +533,23 @@ vg_status vg_world_create(const vg_config* cfg, vg_world** out) {
   cudaGetDevice(&w->device);
   cudaDeviceGetAttribute(&w->n_sm, cudaDevAttrMultiProcessorCount, w->device);
   set_kernel_attributes();                         // per device (the current one)
+  // Binning path.  K3g (per-cell gather) for worlds with few cells and N <= 16,384 unless
+  // they are many replicas, which take the one-CTA-per-replica fused bin; the fused bin
+  // also for tiny worlds K3g cannot take; the 4-kernel path otherwise.
+  const bool gather_ok = VG_GATHER_BIN && cfg->shard == VG_SHARD_REPLICA &&
+                         (long long)g * g * cfg->n_replicas <= 8LL * w->n_sm &&
+                         cfg->n_agents <= vg::kGatherMaxN;
+  w->fused_bin = cfg->shard == VG_SHARD_REPLICA && g * g <= vg::kRBMaxCells &&
+                 cfg->n_agents <= vg::kRBMaxAgents &&
+                 (cfg->n_replicas >= 64 ||
+                  (cfg->n_agents <= VG_FUSED_SINGLE_MAX && !gather_ok));
   {                                // VG_SENSE_GENERIC=1: always the generic instance (tests)
     const char* gen = std::getenv("VG_SENSE_GENERIC");
     w->sense_def = !(gen && gen[0] && gen[0] != '0') &&
                    (w->P.env == vg::kFlock ? sense_defaults_match<vg::kFlock>(w->P)
                                            : sense_defaults_match<vg::kTag>(w->P));
   }
-  w->gather_bin = VG_GATHER_BIN && cfg->shard == VG_SHARD_REPLICA && !w->fused_bin &&
-                  w->n_cells <= 8LL * w->n_sm && cfg->n_agents <= vg::kGatherMaxN;
+  w->gather_bin = gather_ok && !w->fused_bin;
   size_t n = (size_t)w->P.total;
   vg_status st = VG_OK;
   if (cfg->shard == VG_SHARD_SLAB) {
