@@ -975,7 +975,7 @@ __global__ void __launch_bounds__(kRBThreads, 2048 / kRBThreads) k_replica_bin(
 #endif
 constexpr int kSenseWarps = VG_SENSE_WARPS;
 constexpr int kSenseNQ = VG_SENSE_NQ;         // queries sensed together by one warp
-constexpr int kSenseMinBlocks = VG_SENSE_MINB;  // resident CTAs per SM
+constexpr int kSenseMinBlocks = VG_SENSE_MINB;  // launch-bounds minimum; 64 registers give 8 CTAs/SM
 // Ring (power of 2): >= 31 carried + 64 pushed, and large enough that one chunk's pushes
 // never reach the slots the previous drain read (carried + 64 + 2 x 32 <= kQueue), so one
 // warp sync per chunk (before the drain) orders all ring traffic.
