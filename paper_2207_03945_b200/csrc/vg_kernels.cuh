@@ -348,7 +348,10 @@ __device__ __forceinline__ uint32_t work_chunks(const WorkList& WL, int cell, ui
 // missed.  Outputs never depend on this order (fixed-point sums, min, counts).
 // With u = RN32(a G/L) (the A16 product, so ca = min(G-1, floor(u))), the sub-bin is
 // floor(kSub u) - kSub ca clamped to [0, kSub) (kSub u is exact): a monotone function of a.
-constexpr int kSub = 8;
+#ifndef VG_SUB_BINS
+#define VG_SUB_BINS 16
+#endif
+constexpr int kSub = VG_SUB_BINS;           // power of 2, <= 16 (K3g keeps the table prefix in s_wa[16])
 __device__ __forceinline__ int sub_bin(const Params& P, int ca, float a) {
   const int sb = __float2int_rd(__fmul_rn(a, P.gs) * (float)kSub) - kSub * ca;
   return min(max(sb, 0), kSub - 1);
