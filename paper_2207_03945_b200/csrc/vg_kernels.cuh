@@ -357,6 +357,18 @@ __device__ __forceinline__ int sub_bin(const Params& P, int ca, float a) {
   return min(max(sb, 0), kSub - 1);
 }
 
+// Lanes of a 32-record batch whose sub-bin is `bin`: from the log2(kSub) bit ballots of the
+// lanes' sub-bins (a radix-style multi-split: log2(kSub) ballots instead of kSub).
+constexpr int kSubBits = (kSub >= 32) ? 5 : (kSub >= 16) ? 4 : (kSub >= 8) ? 3 : (kSub >= 4) ? 2 : 1;
+static_assert((1 << kSubBits) == kSub, "kSub: a power of 2, 2..32");
+__device__ __forceinline__ unsigned bin_lanes(const unsigned (&bits)[kSubBits], unsigned valid,
+                                              int bin) {
+  unsigned m = valid;
+#pragma unroll
+  for (int k = 0; k < kSubBits; ++k) m &= ((bin >> k) & 1) ? bits[k] : ~bits[k];
+  return m;
+}
+
 // Sense order of one cell from its stable (id-ordered) records [b, b + m): a stable counting
 // sort by sub-bin, one warp.  Writes xo_* and the cell's kSub table entries.
 __device__ __forceinline__ void sense_order_cell(const Params& P, int ca, bool axis_y,
@@ -369,18 +381,17 @@ __device__ __forceinline__ void sense_order_cell(const Params& P, int ca, bool a
   uint32_t cnt = 0;                                       // lane s < kSub: records in sub-bin s
   for (int ib = 0; ib < m; ib += 32) {
     const bool valid = ib + lane < m;
-    int sb = kSub;
+    int sb = 0;
     if (valid) {
       const float4 rec = sorted[b + ib + lane];
       sb = sub_bin(P, ca, axis_y ? rec.y : rec.x);
     }
+    unsigned bits[kSubBits];
 #pragma unroll
-    for (int s = 0; s < kSub; ++s) {
-      const uint32_t n = __popc(__ballot_sync(kFull, sb == s));
-      if (lane == s) cnt += n;
-    }
+    for (int k = 0; k < kSubBits; ++k) bits[k] = __ballot_sync(kFull, (sb >> k) & 1);
+    cnt += __popc(bin_lanes(bits, __ballot_sync(kFull, valid), lane));   // (lane < kSub used)
   }
-  uint32_t inc = cnt;                                     // exclusive scan over lanes 0..7
+  uint32_t inc = cnt;                                     // exclusive scan over lanes < kSub
 #pragma unroll
   for (int o = 1; o < kSub; o <<= 1) {
     const uint32_t y = __shfl_up_sync(kFull, inc, o);
@@ -392,14 +403,17 @@ __device__ __forceinline__ void sense_order_cell(const Params& P, int ca, bool a
     const bool valid = ib + lane < m;
     float4 rec = make_float4(0.f, 0.f, 0.f, 0.f);
     uint32_t id = 0u;
-    int sb = kSub;
+    int sb = 0;
     if (valid) {
       rec = sorted[b + ib + lane];
       id = perm[b + ib + lane];
       sb = sub_bin(P, ca, axis_y ? rec.y : rec.x);
     }
-    const unsigned grp = __match_any_sync(kFull, sb);
-    const uint32_t pos = __shfl_sync(kFull, run, sb & (kSub - 1)) + __popc(grp & lt);
+    unsigned bits[kSubBits];
+#pragma unroll
+    for (int k = 0; k < kSubBits; ++k) bits[k] = __ballot_sync(kFull, (sb >> k) & 1);
+    const unsigned vmask = __ballot_sync(kFull, valid);
+    const uint32_t pos = __shfl_sync(kFull, run, sb) + __popc(bin_lanes(bits, vmask, sb) & lt);
     if (valid) {
       xo_rec[b + pos] = rec;
       xo_perm[b + pos] = id;
@@ -407,11 +421,7 @@ __device__ __forceinline__ void sense_order_cell(const Params& P, int ca, bool a
       // chaser at x = 0 is -0.0)
       xo_xy[b + pos] = make_float2((P.env == kTag && rec.w != 0.f) ? -rec.x : rec.x, rec.y);
     }
-#pragma unroll
-    for (int s = 0; s < kSub; ++s) {
-      const uint32_t n = __popc(__ballot_sync(kFull, sb == s));
-      if (lane == s) run += n;
-    }
+    run += __popc(bin_lanes(bits, vmask, lane));          // (lane < kSub used)
   }
 }
 
