@@ -349,9 +349,9 @@ __device__ __forceinline__ uint32_t work_chunks(const WorkList& WL, int cell, ui
 // With u = RN32(a G/L) (the A16 product, so ca = min(G-1, floor(u))), the sub-bin is
 // floor(kSub u) - kSub ca clamped to [0, kSub) (kSub u is exact): a monotone function of a.
 #ifndef VG_SUB_BINS
-#define VG_SUB_BINS 16
+#define VG_SUB_BINS 32
 #endif
-constexpr int kSub = VG_SUB_BINS;           // power of 2, <= 16 (K3g keeps the table prefix in s_wa[16])
+constexpr int kSub = VG_SUB_BINS;           // power of 2, 2..32
 __device__ __forceinline__ int sub_bin(const Params& P, int ca, float a) {
   const int sb = __float2int_rd(__fmul_rn(a, P.gs) * (float)kSub) - kSub * ca;
   return min(max(sb, 0), kSub - 1);
@@ -674,7 +674,7 @@ __global__ void __launch_bounds__(kGatherThreads) k_cell_gather(
   __shared__ float4 s_rec[kCtaRankMax];
   __shared__ uint32_t s_id[kCtaRankMax];
   __shared__ uint8_t s_sb[kCtaRankMax];
-  __shared__ uint32_t s_wa[NW], s_wb[NW], s_cnt[kSub], s_start, s_m;
+  __shared__ uint32_t s_wa[NW > kSub ? NW : kSub], s_wb[NW], s_cnt[kSub], s_start, s_m;
   const int gc = blockIdx.x, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   if (gc == n_cells) {                                   // sentinels
     if (tid == 0) {
