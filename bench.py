@@ -37,6 +37,7 @@ UNIT = "agent-steps/s"
 PAPER_CONTEXT = ("paper Fig. 1 (P:45): 5,000 agents, 500 training steps in ~16 min on a "
                  "laptop GTX 1650 (whole PPO training, not env-only)")
 ALG_OPS_PER_PAIR = 45          # fp32 ops of the definition per in-radius pair
+HBM_SPEC_GBS = 8000.0           # B200 HBM3e spec (SURVEY §8d reports both peaks)
 SENSE_BYTES_FIXED = 16 + 4 + 4 + 4 + 4   # query record, perm, reward, n_neigh, n_collide
 
 
@@ -584,6 +585,17 @@ def run_ours(args):
                                 "max(HBM floor, 45 fp32 ops x in-radius pairs / FP32 peak)"}
         stages = {}
         tot_ph = sum(phases.values()) or 1.0
+        # DRAM bytes of each stage's kernels from the committed ncu capture of this config
+        # (profiles/stage_traffic.json; cold caches, so they bound the live traffic above)
+        st_ncu = {}
+        sp = os.path.join(ROOT, "profiles", "stage_traffic.json")
+        if os.path.exists(sp) and world == 1 and args.vision == "sector" and STATE == "uniform":
+            try:
+                sj = json.load(open(sp))
+                if sj.get("config") == args.config:
+                    st_ncu = sj.get("stages", {})
+            except Exception:
+                st_ncu = {}
         for k2, ms in phases.items():
             if k2 not in stage_bytes:
                 continue
@@ -593,7 +605,14 @@ def run_ours(args):
                 "ms": round(avg, 5), "alg_bytes": stage_bytes[k2],
                 "GBps": round(gbs, 1) if gbs else None,
                 "hbm_frac": round(gbs / hbm, 4) if gbs else None,
+                "hbm_frac_spec": round(gbs / HBM_SPEC_GBS, 4) if gbs else None,
                 "share": round(ms / tot_ph, 4)}
+            if k2 in st_ncu:
+                n_ = st_ncu[k2]
+                stages[run.phase_names[k2]]["ncu"] = {
+                    "dram_read_B": n_["dram_read_B"], "dram_write_B": n_["dram_write_B"],
+                    "us": n_["ncu_us"], "kernels": n_["kernels"],
+                    "source": "profiles/stage_traffic.json"}
         traffic, issue = None, None
         tpath = os.path.join(ROOT, "profiles", "sense_traffic.json")
         if os.path.exists(tpath) and world == 1:
