@@ -613,13 +613,14 @@ def run_ours(args):
                     "dram_read_B": n_["dram_read_B"], "dram_write_B": n_["dram_write_B"],
                     "us": n_["ncu_us"], "kernels": n_["kernels"],
                     "source": "profiles/stage_traffic.json"}
-        traffic, issue = None, None
+        traffic, issue, cand_tests = None, None, None
         tpath = os.path.join(ROOT, "profiles", "sense_traffic.json")
         if os.path.exists(tpath) and world == 1:
             try:
                 tj = json.load(open(tpath))
                 if tj.get("config") == args.config and args.vision == "sector":
                     traffic = tj.get("bytes_per_launch")
+                    cand_tests = tj.get("candidate_tests")
                     wi = tj.get("warp_instructions")
                     if wi:
                         # issue-slot roofline of the same launch: warp instructions (ncu,
@@ -662,6 +663,7 @@ def run_ours(args):
             "roofline": {"kernel": "k_sense (sector vision + reward)", "bound": "alu",
                          "achieved": achieved, "peak": alu_peak, "unit": "TFLOP/s",
                          "frac": achieved / alu_peak, "traffic": traffic, "issue": issue,
+                         "pairs_in_radius": pairs_local, "candidate_tests": cand_tests,
                          "basis": f"{ALG_OPS_PER_PAIR} fp32 ops x {pairs_local:.4g} "
                                   f"in-radius pairs per launch / mean k_sense time; peak = "
                                   f"148 SM x 128 lanes x {sm_mhz:.0f} MHz (1 op/lane/clk)"},
