@@ -551,8 +551,8 @@ __global__ void __launch_bounds__(256) k_cell_sort(
                    sub_tab + (size_t)cell * kSub, lane, lt);
 }
 
-// K3b, one CTA per cell (worlds with few, populous cells: c2, c3 have 81 cells of 60-120
-// agents, where one warp per cell leaves most SMs idle).  The same outputs as k_cell_sort:
+// K3b, one CTA per cell (worlds with few, populous cells that K3g does not take — N above
+// 16,384, or slab mode — where one warp per cell leaves most SMs idle).  The same outputs as k_cell_sort:
 // every member's stable slot is its rank by agent id, and its sense-order slot is its rank
 // by (sub-bin, id); both ranks are counted by comparison against the cell's keys staged in
 // shared memory, all threads of the CTA in parallel.  A cell above kCtaRankMax members
@@ -655,8 +655,8 @@ __global__ void __launch_bounds__(kCtaSortThreads) k_cell_sort_cta(
   }
 }
 
-// K3g — K2, K3 and K3b in one kernel for small single worlds (replica mode, few cells,
-// N <= kGatherMaxN: c2, c3).  One CTA per cell c of replica r gathers its members straight
+// K3g — K2, K3 and K3b in one kernel for small worlds (replica mode, <= 8 cells per SM,
+// N <= kGatherMaxN, < 64 replicas: c1, c2, c3).  One CTA per cell c of replica r gathers its members straight
 // from the cell ids K1 wrote, in agent-id order (so the stable order needs no rank): thread
 // t owns agents [t S, (t+1) S); pass A counts, per thread, agents in cells before c and in
 // c; one block scan gives cell_start and each thread's first slot; pass B writes the
