@@ -381,7 +381,7 @@ vg::Outs to_outs(const vg_world* w, const vg_outputs* o) {
 // K4's candidate reads hit L1: cap the shared-memory carve-out so the resident CTAs' shared
 // memory leaves L1 room.  Set once per kernel instance.
 #ifndef VG_SENSE_CARVEOUT
-#define VG_SENSE_CARVEOUT 86
+#define VG_SENSE_CARVEOUT 80     // 75-83: same; 86 (8 CTAs/SM, less L1) 1 % slower; 70 11 % slower
 #endif
 template <typename K>
 void sense_carveout(K* k) {
