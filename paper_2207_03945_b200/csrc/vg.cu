@@ -383,19 +383,21 @@ vg::Outs to_outs(const vg_world* w, const vg_outputs* o) {
 #ifndef VG_SENSE_CARVEOUT
 #define VG_SENSE_CARVEOUT 80     // 75-83: same; 86 (8 CTAs/SM, less L1) 1 % slower; 70 11 % slower
 #endif
+#ifndef VG_SENSE_CARVEOUT_RAY
+#define VG_SENSE_CARVEOUT_RAY 86 // the ray instances keep a 1 KB ray table too: 80 gives 7 CTAs
+#endif
 template <typename K>
-void sense_carveout(K* k) {
-  if (VG_SENSE_CARVEOUT >= 0)
-    cudaFuncSetAttribute(k, cudaFuncAttributePreferredSharedMemoryCarveout, VG_SENSE_CARVEOUT);
+void sense_carveout(K* k, int pct) {
+  if (pct >= 0) cudaFuncSetAttribute(k, cudaFuncAttributePreferredSharedMemoryCarveout, pct);
 }
 
 template <int ENV, bool VISION, bool SLAB>
 void sense_carveouts() {
-  sense_carveout(vg::k_sense<ENV, VISION, SLAB, true, false>);
-  sense_carveout(vg::k_sense<ENV, VISION, SLAB, false, false>);
+  sense_carveout(vg::k_sense<ENV, VISION, SLAB, true, false>, VG_SENSE_CARVEOUT_RAY);
+  sense_carveout(vg::k_sense<ENV, VISION, SLAB, false, false>, VG_SENSE_CARVEOUT);
   if (VISION) {
-    sense_carveout(vg::k_sense<ENV, VISION, SLAB, false, VISION>);
-    sense_carveout(vg::k_sense<ENV, VISION, SLAB, true, VISION>);
+    sense_carveout(vg::k_sense<ENV, VISION, SLAB, false, VISION>, VG_SENSE_CARVEOUT);
+    sense_carveout(vg::k_sense<ENV, VISION, SLAB, true, VISION>, VG_SENSE_CARVEOUT_RAY);
   }
 }
 
