@@ -264,7 +264,10 @@ vg_status launch_check(const char* what) {
 // large; dense cells (clusters) are split into many items.
 int sense_chunk_q(const vg_world* w) {
   const long long queries = w->slab ? (long long)w->P.N / w->cfg.world_size : w->P.total;
-  const long long slots = (long long)w->n_sm * vg::kSenseMinBlocks * 4;
+#ifndef VG_SENSE_ITEMS_PER_SLOT
+#define VG_SENSE_ITEMS_PER_SLOT 4   // slab P = 2/4/8: 2 and 8 measured worse at one of them
+#endif
+  const long long slots = (long long)w->n_sm * vg::kSenseMinBlocks * VG_SENSE_ITEMS_PER_SLOT;
   long long q = (queries / slots) / 8 * 8;
 #ifndef VG_SENSE_CHUNK_MAX
 #define VG_SENSE_CHUNK_MAX 128
