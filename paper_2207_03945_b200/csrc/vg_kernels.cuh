@@ -1029,6 +1029,19 @@ __device__ __forceinline__ float vg_atan2(float y, float x) {
   return copysignf(r, y);
 }
 
+// K4's outputs (~0.5 KB per agent) are written once and not re-read by the step: with
+// VG_SENSE_STREAM_OUT they go out as streaming stores (st.global.cs, evict-first), so the
+// output stream does not push the candidate arrays out of L2.
+#ifndef VG_SENSE_STREAM_OUT
+#define VG_SENSE_STREAM_OUT 1
+#endif
+__device__ __forceinline__ void vg_st_out(float* p, float v) {
+  if (VG_SENSE_STREAM_OUT) __stcs(p, v); else *p = v;
+}
+__device__ __forceinline__ void vg_st_out(uint32_t* p, uint32_t v) {
+  if (VG_SENSE_STREAM_OUT) __stcs(reinterpret_cast<unsigned int*>(p), (unsigned int)v); else *p = v;
+}
+
 __device__ __forceinline__ uint32_t sh_addr(const void* p) {
   return (uint32_t)__cvta_generic_to_shared(p);
 }
@@ -1467,8 +1480,8 @@ __global__ void __launch_bounds__(kSenseWarps * 32, (DEF && ENV == kTag) ? VG_SE
             float* orow = O.obs + row * (idx_t)VG_SC(obs_dim);
 #pragma unroll
             for (int w = 0; w < kMaxViewSlots / 32; ++w)
-              if (32 * w + lane < VG_SC(view_slots)) orow[32 * w + lane] = __uint_as_float(vals[w]);
-            if (ENV == kFlock && lane == 0) orow[VG_SC(view_slots)] = me[t].w * VG_SC(inv_smax);  // A24
+              if (32 * w + lane < VG_SC(view_slots)) vg_st_out(&orow[32 * w + lane], __uint_as_float(vals[w]));
+            if (ENV == kFlock && lane == 0) vg_st_out(&orow[VG_SC(view_slots)], me[t].w * VG_SC(inv_smax));  // A24
           }
           if (FAST || O.occ) {
             uint32_t mine = 0u;
@@ -1477,7 +1490,7 @@ __global__ void __launch_bounds__(kSenseWarps * 32, (DEF && ENV == kTag) ? VG_SE
               const unsigned bits = __ballot_sync(kFull, vals[w] < kOneBits);
               if (lane == w) mine = bits;
             }
-            if (lane < VG_SC(occ_words)) O.occ[row * (idx_t)VG_SC(occ_words) + lane] = mine;
+            if (lane < VG_SC(occ_words)) vg_st_out(&O.occ[row * (idx_t)VG_SC(occ_words) + lane], mine);
           }
         }
       };
