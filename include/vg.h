@@ -48,7 +48,7 @@
 extern "C" {
 #endif
 
-#define VG_ABI_VERSION 2
+#define VG_ABI_VERSION 3
 
 typedef enum {
   VG_OK = 0,
@@ -148,7 +148,14 @@ vg_status vg_bin(vg_world* w, const float* state, void* stream);
 vg_status vg_sense(vg_world* w, const vg_outputs* outs, void* stream);
 
 /* Reward and neighbour/contact counts only (no bearings, no observation), for the state
- * last binned.  Writes reward, n_neigh, n_collide, n_touch of *outs (others ignored). */
+ * last binned: flock r_i = sum over j != i with d_ij < d_v of f(d_ij) (Eq. 1, P:174-175;
+ * f = the Fig. 4 shape, reading A5: -c_collide for d <= 2 d_r, else rising
+ * linearly to c_near at d_peak and falling to 0 at d_v); tag: the P:194 touch rules plus
+ * w_prox x the runner-runner f (A15).  n_neigh = #{j: d < d_v}, n_collide (and tag n_touch)
+ * = same-type (opposite-type) contacts d <= 2 d_r (A6).  Same values as vg_sense's fused
+ * reward (an unfused pass, for tests).  Writes reward, n_neigh, n_collide, n_touch of *outs
+ * (others ignored).  Errors: VG_EINVAL (NULL world / outs, or no prior vg_bin / vg_step),
+ * VG_ECUDA. */
 vg_status vg_reward(vg_world* w, const vg_outputs* outs, void* stream);
 
 /* Integrate actions into state in place (A7, A8, A10): rotate, then
@@ -225,7 +232,8 @@ vg_status vg_slab_own_count(vg_world* w, void* stream, int64_t* n_own);
  * The actor-critic MLP of P:212 ("two hidden layers with 64 nodes each", tanh)
  * over all agents, on the tcgen05 tensor cores (fp16 operands, fp32 accumulation in TMEM),
  * followed by the Gaussian action sample of P:198 / S:355-372: a = clip(mean +
- * exp(log_std) eps, box), log-prob of the unclipped sample, eps from Philox4x32-10
+ * exp(log_std) eps, box) with log_std clamped to [-5, 2], log-prob of the
+ * unclipped sample, eps from Philox4x32-10
  * (key = seed, counter = (row, step)) + Box-Muller. */
 typedef struct vg_policy vg_policy;
 typedef struct {
@@ -285,10 +293,20 @@ vg_status vg_rollout(vg_world* w, vg_policy* pol, float* state, const vg_rollout
  * (me), over its out-edges in CSR order (sorted by (src, dst), row_ptr [n+1], col [E] =
  * dst, weight [E] >= 0): if |op[me] - op[you]| < threshold then w = strength weight,
  * new = (1 - w) new + w op[you]; new starts at op[me]; op_out[me] = new.  op_in and
- * op_out are distinct device arrays [n] (simultaneous update). */
+ * op_out are distinct device arrays [n] (simultaneous update).  n_edges = E (the
+ * length of col and weight).
+ * Errors: NULL row_ptr/op_in/op_out (or col/weight with E > 0), n < 0, E outside
+ * [0, 2^31), op_in == op_out, negative threshold/strength -> VG_EINVAL (synchronous).  A
+ * row with row_ptr[i] < 0, row_ptr[i+1] < row_ptr[i] or row_ptr[i+1] > E, or an edge whose
+ * col is outside [0, n) (a dangling index) is never read: the node keeps its opinion
+ * / skips the edge, and the first such node is recorded for vg_opinion_sync_errors. */
 vg_status vg_opinion_step(const int32_t* row_ptr, const int32_t* col, const float* weight,
-                          int32_t n, const float* op_in, float* op_out, float threshold,
-                          float strength, void* stream);
+                          int32_t n, int64_t n_edges, const float* op_in, float* op_out,
+                          float threshold, float strength, void* stream);
+/* Synchronizes `stream`; if any vg_opinion_step on this device since the last call met an
+ * invalid row or dangling edge, writes the lowest such node to *bad_node (else -1), clears
+ * the record and returns VG_ESTATE. */
+vg_status vg_opinion_sync_errors(void* stream, int64_t* bad_node);
 
 /* Phase timing for measurement.  After vg_profile_begin(w, max_steps), each of the next
  * max_steps vg_step calls records CUDA events on its stream between its phases

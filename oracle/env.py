@@ -240,6 +240,18 @@ def sense_rows(p, state_r: np.ndarray, rows, overrides: dict | None = None) -> d
     contact = contact & in_r
     ksec = np.where(in_r, ksec, -1)
 
+    # ---- conditioning of the reward terms (for the comparator's derived fp32 bound,
+    # DESIGN.md §5): per row, over the in-radius non-contact terms (weight w_prox for
+    # tag runner pairs), sum_j |f'(d_j)| d_j (sensitivity to a relative distance error)
+    # and sum_j (|k| d_j + |b|) over both lines of f = min(rise, fall) (A5; magnitudes
+    # of the line evaluation, i.e. sensitivity to relative coefficient errors).
+    two_dr = 2.0 * float(p.d_r)
+    k_rise = p.c_near / (p.d_peak - two_dr)
+    k_fall = p.c_near / (p.d_v - p.d_peak)
+    slope = np.where(d <= p.d_peak, k_rise, k_fall)
+    lines = k_rise * d + k_rise * two_dr + k_fall * d + k_fall * p.d_v
+    f_term = in_r & ~contact
+
     # ---- counts
     n_neigh = np.bincount(b[in_r], minlength=nr).astype(np.uint32)
     n_touch = np.zeros(nr, np.uint32)
@@ -248,6 +260,7 @@ def sense_rows(p, state_r: np.ndarray, rows, overrides: dict | None = None) -> d
         terms = np.where(in_r, reward_f(p, d, contact), 0.0)
         reward = np.bincount(b, weights=terms, minlength=nr)
         sum_abs = np.bincount(b, weights=np.abs(terms), minlength=nr)
+        wt = f_term.astype(np.float64)
         chan = np.zeros_like(j)
     else:
         first_chaser = n - p.n_chasers
@@ -263,7 +276,11 @@ def sense_rows(p, state_r: np.ndarray, rows, overrides: dict | None = None) -> d
         reward = np.where(row_is_chaser, touch,
                           -touch + np.bincount(b, weights=prox, minlength=nr))
         sum_abs = touch + np.bincount(b, weights=np.abs(prox), minlength=nr)
+        wt = np.where(f_term & (tq == 0) & (tj == 0), float(p.w_prox), 0.0)
         chan = tj
+    n_terms = np.bincount(b, weights=(wt > 0).astype(np.float64), minlength=nr)
+    slope_d = np.bincount(b, weights=wt * slope * d, minlength=nr)
+    line_abs = np.bincount(b, weights=wt * lines, minlength=nr)
 
     # ---- observation (per-sector nearest distance)
     view = np.ones((nr, ch * v), dtype=np.float64)
@@ -282,7 +299,8 @@ def sense_rows(p, state_r: np.ndarray, rows, overrides: dict | None = None) -> d
         seg = occ[:, 32 * w:32 * (w + 1)]
         occ_bits[:, w] = (seg.astype(np.uint64) << np.arange(seg.shape[1], dtype=np.uint64)).sum(1)
     return {
-        "obs": obs, "reward": reward, "sum_abs": sum_abs, "n_neigh": n_neigh,
+        "obs": obs, "reward": reward, "sum_abs": sum_abs, "n_terms": n_terms,
+        "slope_d": slope_d, "line_abs": line_abs, "n_neigh": n_neigh,
         "n_collide": n_collide, "n_touch": n_touch,
         "sector_occ": occ_bits.astype(np.uint32), "bands": bands,
     }

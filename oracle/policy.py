@@ -79,9 +79,10 @@ def forward(w: dict, obs: np.ndarray) -> dict:
 def sample(w: dict, mean: np.ndarray, rows: np.ndarray, seed: int, step: int,
            lo: np.ndarray, hi: np.ndarray) -> dict:
     """a_raw = mean + exp(log_std) eps; action = clip(a_raw, box); log-prob of
-    the unclipped Gaussian: sum_d -eps_d^2/2 - log_std_d - log(2 pi)/2."""
+    the unclipped Gaussian: sum_d -eps_d^2/2 - log_std_d - log(2 pi)/2; log_std
+    clamped to [-5, 2] first."""
     eps = normals(rows, seed, step)
-    ls = np.asarray(w["log_std"], dtype=np.float64)
+    ls = np.clip(np.asarray(w["log_std"], dtype=np.float64), -5.0, 2.0)
     raw = np.asarray(mean, np.float64) + np.exp(ls) * eps
     act = np.clip(raw, np.asarray(lo, np.float64), np.asarray(hi, np.float64))
     logp = (-0.5 * eps ** 2 - ls - 0.5 * math.log(2 * math.pi)).sum(-1)

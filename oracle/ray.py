@@ -35,10 +35,14 @@ def ray_disc(ux, uy, cx, cy, r):
     return np.where(inside, 0.0, t), h
 
 
-def ray_views(p, state_r, rows, dh_rel=5e-5):
+def ray_views(p, state_r, rows, dh_rel=5e-5, return_cond=False):
     """View [len(rows), channels * v] under the ray-disc reading, plus per-sector bounds
     [lo, hi] that the fp32 kernel must fall in (interval comparator):
-    a near-grazing ray (|h| <= dh_rel r^2) may hit or miss and its t is ill-conditioned."""
+    a near-grazing ray (|h| <= dh_rel r^2) may hit or miss and its t is ill-conditioned.
+
+    ``return_cond`` also returns a mask of the *well-conditioned* sectors: every disc that
+    may be hit is surely hit (no grazing disc) and the nearest one's sqrt sensitivity
+    dh / (2 sqrt h) is <= 1e-6 d_v, or nothing can be hit at all."""
     st = np.asarray(state_r, np.float64)
     n = st.shape[0]
     rows = np.asarray(rows)
@@ -51,6 +55,7 @@ def ray_views(p, state_r, rows, dh_rel=5e-5):
     psi = -fov / 2 + (np.arange(v) + 0.5) * w
     dh = dh_rel * r * r
     view = np.ones((len(rows), ch * v))
+    cond = np.ones((len(rows), ch * v), dtype=bool)
     lo = np.ones((len(rows), ch * v))
     hi = np.ones((len(rows), ch * v))
     first_chaser = n - getattr(p, "n_chasers", 0) if p.env == "tag" else n
@@ -84,4 +89,10 @@ def ray_views(p, state_r, rows, dh_rel=5e-5):
             view[b, c * v:(c + 1) * v] = tc[sel].min(0)
             lo[b, c * v:(c + 1) * v] = np.minimum(np.where(maybe[sel], tmay[sel] - err[sel] - 1e-6, 1.0).min(0), 1.0)
             hi[b, c * v:(c + 1) * v] = np.minimum(np.where(sure[sel], tc[sel] + err[sel], 1.0).min(0), 1.0)
+            sens = np.minimum(dh / (2 * np.maximum(sq[sel], 1e-300)), math.sqrt(dh)) / dv
+            arg = np.where(sure[sel], tc[sel], np.inf).argmin(0)
+            near_ok = np.take_along_axis(np.where(sure[sel], sens, 0.0), arg[None, :], 0)[0] <= 1e-6
+            cond[b, c * v:(c + 1) * v] = ~np.any(maybe[sel] & ~sure[sel], axis=0) & near_ok
+    if return_cond:
+        return view, np.clip(lo, 0.0, 1.0), hi, cond
     return view, np.clip(lo, 0.0, 1.0), hi

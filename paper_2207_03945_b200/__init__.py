@@ -205,8 +205,12 @@ class World:
                 tuple(actions_host.shape) != (self.R, self.N, 2) or not actions_host.is_contiguous():
             raise ValueError("actions_host: contiguous float32 CPU tensor [R, N, 2] required")
         if reward_host is not None and (reward_host.device.type != "cpu" or
-                                        tuple(reward_host.shape) != (self.R, self.N)):
-            raise ValueError("reward_host: float32 CPU tensor [R, N] required")
+                                        reward_host.dtype != torch.float32 or
+                                        tuple(reward_host.shape) != (self.R, self.N) or
+                                        not reward_host.is_contiguous()):
+            # vg_step_host writes exactly 4 R N bytes at data_ptr(): anything else would be
+            # a host heap overrun or land on the wrong elements
+            raise ValueError("reward_host: contiguous float32 CPU tensor [R, N] required")
         o = self._outs(out)
         check(_lib.lib.vg_step_host(self._h, state.data_ptr(), actions_host.data_ptr(),
                                     byref(o), _ptr(reward_host), self._stream()))

@@ -110,8 +110,9 @@ SIGNATURES = {
                              ctypes.c_uint64, ctypes.c_uint64, c_float, c_float, c_void_p]),
     "vg_gae": (c_int32, [c_void_p, c_void_p, c_int64, c_int32, c_float, c_float, c_void_p,
                          c_void_p, c_void_p]),
-    "vg_opinion_step": (c_int32, [c_void_p, c_void_p, c_void_p, c_int32, c_void_p, c_void_p,
-                                  c_float, c_float, c_void_p]),
+    "vg_opinion_step": (c_int32, [c_void_p, c_void_p, c_void_p, c_int32, c_int64, c_void_p,
+                                  c_void_p, c_float, c_float, c_void_p]),
+    "vg_opinion_sync_errors": (c_int32, [c_void_p, POINTER(c_int64)]),
     "vg_profile_begin": (c_int32, [c_void_p, c_int32]),
     "vg_profile_end": (c_int32, [c_void_p, c_void_p, POINTER(ctypes.c_double),
                                  POINTER(c_int32)]),

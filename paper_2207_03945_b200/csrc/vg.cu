@@ -139,6 +139,14 @@ vg_status validate(const vg_config& c, int* grid_out) {
   if (!(c.c_collide > 0.f) || !std::isfinite(c.c_collide) || c.c_collide > 1e6f) return fail(VG_EINVAL, "c_collide: must be in (0, 1e6]");
   if (!(c.c_near > 0.f) || !std::isfinite(c.c_near) || c.c_near > 1e6f) return fail(VG_EINVAL, "c_near: must be in (0, 1e6]");
   if (!(c.d_peak > 2.f * c.d_r) || !(c.d_peak < c.d_v)) return fail(VG_EINVAL, "d_peak: must satisfy 2 d_r < d_peak < d_v (A5)");
+  {
+    // The reward is an int64 sum in 2^-32 units (A16b): every row's |reward| <= (N - 1) x
+    // the largest per-pair magnitude must stay below 2^31 reward units.
+    double mag = std::max((double)c.c_collide, (double)c.c_near);
+    if (c.env == VG_ENV_TAG) mag = std::max((double)c.r_touch, (double)c.r_touch + (double)c.w_prox * std::max((double)c.c_collide, (double)c.c_near));
+    if (mag * (double)(c.n_agents - 1) >= 2147483647.0)
+      return fail(VG_EINVAL, "c_collide/c_near/r_touch/w_prox: (n_agents - 1) x max per-pair reward %g must be < 2^31 (fixed-point reward sum, A16b)", mag);
+  }
   int g = c.grid;
   const double need = (double)c.d_v * (1.0 + std::ldexp(1.0, -12));
   if (g == 0) g = auto_grid(c.width, c.d_v);
@@ -1115,16 +1123,31 @@ vg_status vg_gae(const float* reward, const float* value, int64_t n, int32_t t, 
 }
 
 vg_status vg_opinion_step(const int32_t* row_ptr, const int32_t* col, const float* weight,
-                          int32_t n, const float* op_in, float* op_out, float threshold,
-                          float strength, void* stream) {
+                          int32_t n, int64_t n_edges, const float* op_in, float* op_out,
+                          float threshold, float strength, void* stream) {
   if (!row_ptr || !op_in || !op_out) return fail(VG_EINVAL, "vg_opinion_step: NULL pointer");
   if (n < 0) return fail(VG_EINVAL, "vg_opinion_step: n must be >= 0");
+  if (n_edges < 0 || n_edges > INT32_MAX) return fail(VG_EINVAL, "vg_opinion_step: n_edges must be in [0, 2^31)");
+  if (n_edges > 0 && (!col || !weight)) return fail(VG_EINVAL, "vg_opinion_step: col / weight NULL with n_edges > 0");
   if (op_in == op_out) return fail(VG_EINVAL, "vg_opinion_step: op_in and op_out must differ (simultaneous update)");
   if (!(threshold >= 0.f) || !(strength >= 0.f)) return fail(VG_EINVAL, "vg_opinion_step: threshold, strength must be >= 0");
   if (n == 0) return VG_OK;
   vg::k_opinion<<<(unsigned)((n + 255) / 256), 256, 0, as_stream(stream)>>>(
-      row_ptr, col, weight, n, op_in, op_out, threshold, strength);
+      row_ptr, col, weight, n, (long long)n_edges, op_in, op_out, threshold, strength);
   return launch_check("k_opinion");
+}
+
+vg_status vg_opinion_sync_errors(void* stream, int64_t* bad_node) {
+  if (bad_node) *bad_node = -1;
+  if (cudaError_t e = cudaStreamSynchronize(as_stream(stream)))
+    return fail(VG_ECUDA, "vg_opinion_sync_errors: %s", cudaGetErrorString(e));
+  unsigned long long bad = 0, none = ~0ull;
+  if (cudaError_t e = cudaMemcpyFromSymbol(&bad, vg::g_opinion_bad, sizeof(bad)))
+    return fail(VG_ECUDA, "vg_opinion_sync_errors: %s", cudaGetErrorString(e));
+  if (bad == none) return VG_OK;
+  cudaMemcpyToSymbol(vg::g_opinion_bad, &none, sizeof(none));
+  if (bad_node) *bad_node = (int64_t)bad;
+  return fail(VG_ESTATE, "vg_opinion_step: node %llu has an invalid row (row_ptr) or a dangling edge (col outside [0, n))", bad);
 }
 
 vg_status vg_rollout(vg_world* w, vg_policy* pol, float* state, const vg_rollout_buffers* b,

@@ -1446,14 +1446,18 @@ __global__ void __launch_bounds__(kSenseWarps * 32, (DEF && ENV == kTag) ? VG_SE
       const uint32_t q = q0 + t;
       const uint32_t nn = RAY ? __reduce_add_sync(kFull, nnb[t])
                               : (tail[t] >> 4) - 1u;            // minus the self pair
-      // Warp reductions (REDUX): the int64 reward sum as exact 32-bit partial sums.
+      // Warp reductions (REDUX): the int64 reward sum as four exact 16-bit-limb partial sums
+      // (no 32-bit wrap for any reward validate() admits).
       const uint32_t nc = __reduce_add_sync(kFull, ncol[t]);
       const uint32_t nt = (ENV == kTag) ? __reduce_add_sync(kFull, ntouch[t]) : 0u;
       const unsigned long long ur = (unsigned long long)rs[t];
       const uint32_t s_lo = __reduce_add_sync(kFull, (uint32_t)(ur & 0xffffu));
       const uint32_t s_mid = __reduce_add_sync(kFull, (uint32_t)((ur >> 16) & 0xffffu));
-      const int s_hi = __reduce_add_sync(kFull, (int)(uint32_t)(ur >> 32));
-      long long rsum = ((long long)s_hi << 32) + ((long long)s_mid << 16) + (long long)s_lo;
+      const uint32_t s_hi = __reduce_add_sync(kFull, (uint32_t)((ur >> 32) & 0xffffu));
+      const int s_top = __reduce_add_sync(kFull, (int)((long long)ur >> 48));
+      long long rsum = (long long)(((unsigned long long)(long long)s_top << 48) +
+                                   ((unsigned long long)s_hi << 32) +
+                                   ((unsigned long long)s_mid << 16) + (unsigned long long)s_lo);
       if (ENV == kTag) {
         const long long tt = (long long)nt * P.touch_fix;
         rsum += (tq[t] == 1u) ? tt : -tt;                             // P:194 touch rule

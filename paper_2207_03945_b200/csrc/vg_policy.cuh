@@ -224,7 +224,9 @@ __global__ void k_policy_pack(int obs_dim, const float* __restrict__ W1, const f
   }
   if (t == 0) {
     pk.consts[256] = b3[0]; pk.consts[257] = b3[1]; pk.consts[258] = c3[0]; pk.consts[259] = 0.f;
-    pk.consts[260] = log_std[0]; pk.consts[261] = log_std[1];
+    // log_std clamped to [-5, 2] (both the sample scale and the log-prob use it)
+    pk.consts[260] = fminf(fmaxf(log_std[0], -5.f), 2.f);
+    pk.consts[261] = fminf(fmaxf(log_std[1], -5.f), 2.f);
     pk.consts[262] = lo0; pk.consts[263] = lo1; pk.consts[264] = hi0; pk.consts[265] = hi1;
   }
 }

@@ -55,18 +55,34 @@ __global__ void __launch_bounds__(256) k_gae(const float* __restrict__ r,
 //      me.new_opinion = (1 - w) me.new_opinion + w you.opinion
 // with new_opinion starting at the current opinion and every read of `opinion`
 // from the previous step (simultaneous update); then opinion <- new_opinion.
+// First node whose row or edges are invalid (row_ptr not non-decreasing within [0, E], or
+// col outside [0, n)): reported by vg_opinion_sync_errors ("a dangling index is an
+// invariant violation").  Invalid edges are never read.
+__device__ unsigned long long g_opinion_bad = ~0ull;
+
 __global__ void __launch_bounds__(256) k_opinion(const int32_t* __restrict__ row_ptr,
                                                  const int32_t* __restrict__ col,
                                                  const float* __restrict__ weight, int n,
+                                                 long long n_edges,
                                                  const float* __restrict__ op,
                                                  float* __restrict__ op_new, float threshold,
                                                  float strength) {
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
     const float x = op[i];
     float acc = x;
-    const int e1 = row_ptr[i + 1];
-    for (int e = row_ptr[i]; e < e1; ++e) {
-      const float y = __ldg(op + __ldg(col + e));
+    const int e0 = row_ptr[i], e1 = row_ptr[i + 1];
+    if (e0 < 0 || e1 < e0 || (long long)e1 > n_edges) {
+      atomicMin(&g_opinion_bad, (unsigned long long)i);
+      op_new[i] = x;
+      continue;
+    }
+    for (int e = e0; e < e1; ++e) {
+      const int c = __ldg(col + e);
+      if ((unsigned)c >= (unsigned)n) {
+        atomicMin(&g_opinion_bad, (unsigned long long)i);
+        continue;
+      }
+      const float y = __ldg(op + c);
       if (fabsf(x - y) < threshold) {
         const float w = strength * __ldg(weight + e);
         acc = fmaf(w, y, (1.f - w) * acc);

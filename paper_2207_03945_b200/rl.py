@@ -52,7 +52,10 @@ def gae(reward, value, adv, ret, gamma: float = 0.99, lam: float = 0.95) -> None
                           adv.data_ptr(), ret.data_ptr(), _stream(reward)))
 
 
-def opinion_step(row_ptr, col, weight, op_in, op_out, threshold: float, strength: float) -> None:
+def opinion_step(row_ptr, col, weight, op_in, op_out, threshold: float, strength: float,
+                 check_errors: bool = True) -> None:
+    """vg_opinion_step; with ``check_errors`` (default) also vg_opinion_sync_errors, which
+    synchronizes the stream and raises VG_ESTATE on an invalid row or dangling edge."""
     n = op_in.numel()
     for x, nm in ((row_ptr, "row_ptr"), (col, "col")):
         if not (x.is_cuda and x.dtype == torch.int32 and x.is_contiguous()):
@@ -62,9 +65,17 @@ def opinion_step(row_ptr, col, weight, op_in, op_out, threshold: float, strength
     _f32(op_out, "op_out", (n,))
     if row_ptr.numel() != n + 1:
         raise ValueError("row_ptr: n + 1 entries required")
+    if weight.numel() != col.numel():
+        raise ValueError(f"weight: {weight.numel()} entries, col has {col.numel()}")
+    if not (row_ptr.device == col.device == weight.device == op_in.device == op_out.device):
+        raise ValueError("opinion_step: all tensors must be on one device")
     check(_lib.lib.vg_opinion_step(row_ptr.data_ptr(), col.data_ptr(), weight.data_ptr(), n,
-                                   op_in.data_ptr(), op_out.data_ptr(), threshold, strength,
-                                   _stream(op_in)))
+                                   col.numel(), op_in.data_ptr(), op_out.data_ptr(), threshold,
+                                   strength, _stream(op_in)))
+    if check_errors:
+        import ctypes
+        bad = ctypes.c_int64(-1)
+        check(_lib.lib.vg_opinion_sync_errors(_stream(op_in), ctypes.byref(bad)))
 
 
 def rollout(world, policy, state: torch.Tensor, buf: TrajectoryBuffer, seed: int = 0,
@@ -72,6 +83,11 @@ def rollout(world, policy, state: torch.Tensor, buf: TrajectoryBuffer, seed: int
     """vg_rollout: t steps of the paper's experience-collection loop (Fig. 5) on device.
     buf.obs[0] must hold the current observation (e.g. from world.bin + world.sense)."""
     import ctypes
+    world._check_tensor(state, "state", (world.R, world.N, 4))
+    if buf.obs.device != state.device:
+        raise ValueError(f"trajectory buffer on {buf.obs.device}, state on {state.device}")
+    if getattr(policy, "device", state.device) != state.device:
+        raise ValueError(f"policy on {policy.device}, state on {state.device}")
     b = _lib.VgRolloutBuffers(buf.obs.data_ptr(), buf.action.data_ptr(), buf.logp.data_ptr(),
                               buf.reward.data_ptr(), buf.value.data_ptr(), buf.adv.data_ptr(),
                               buf.ret.data_ptr())

@@ -34,7 +34,7 @@ def test_library_exports_every_declared_symbol():
 
 def test_abi_version():
     from paper_2207_03945_b200 import _lib
-    assert _lib.lib.vg_abi_version() == 2
+    assert _lib.lib.vg_abi_version() == 3
 
 
 def test_struct_layout_matches_header():
@@ -70,6 +70,8 @@ def test_struct_layout_matches_header():
     ("fov", 7.0, "fov"), ("v", 129, "v:"), ("theta_max", 4.0, "theta_max"),
     ("s_min", 0.6, "s_min"), ("a_max", 0.0, "a_max"), ("grid", 10, "grid"),
     ("grid", 2, "grid"), ("d_peak", 0.4, "d_peak"), ("c_collide", -1.0, "c_collide"),
+    # (N - 1) x max per-pair reward must fit the 2^-32 fixed-point sum (< 2^31, A16b)
+    ("c_collide", 5e5, "fixed-point"), ("c_near", 5e5, "fixed-point"),
 ])
 def test_config_validation_names_field(field, value, needle):
     import paper_2207_03945_b200 as vg
@@ -113,6 +115,8 @@ def test_unbuilt_modes_rejected():
 
 def test_null_arguments():
     from paper_2207_03945_b200 import _lib
+    assert _lib.lib.vg_opinion_step(None, None, None, 4, 0, None, None, 0.1, 0.1,
+                                    None) == _lib.VG_EINVAL
     assert _lib.lib.vg_world_create(None, None) == _lib.VG_EINVAL
     assert _lib.lib.vg_bin(None, None, None) == _lib.VG_EINVAL
     assert _lib.lib.vg_step(None, None, None, None, None) == _lib.VG_EINVAL

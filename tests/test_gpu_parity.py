@@ -43,7 +43,13 @@ def make_world(p):
     return vg.World(p)
 
 
-def run_and_check(p, state0, n_steps, replicas=None, rows=None, seed=0, check_bins=True):
+def _workers():
+    import os
+    return max(1, min(32, len(os.sched_getaffinity(0))))
+
+
+def run_and_check(p, state0, n_steps, replicas=None, rows=None, seed=0, check_bins=True,
+                  workers=1):
     """Step the GPU world n_steps with seeded actions; check every step against the oracle."""
     torch = _torch()
     w = make_world(p)
@@ -64,7 +70,8 @@ def run_and_check(p, state0, n_steps, replicas=None, rows=None, seed=0, check_bi
             bins = {k: host(v) for k, v in w.get_bins().items()}
             parity.check_bins(p, bins, cur)
         for r in reps:
-            stats.append(parity.check_sense(p, cur[r], outs_np(out, r), rows=rows))
+            stats.append(parity.check_sense(p, cur[r], outs_np(out, r), rows=rows,
+                                            workers=workers))
     w.close()
     return stats
 
@@ -77,22 +84,27 @@ def test_c1_100_steps(cuda):
 
 
 def test_c2_flock_5000(cuda):
+    # configs[1], every row, 10 steps (SURVEY.md §8c parity depth)
     p = vi.workload("c2")
-    stats = run_and_check(p, vi.init_state(p, seed=0), 3)
-    print(stats)
+    stats = run_and_check(p, vi.init_state(p, seed=0), 10, workers=_workers())
+    assert sum(s["rows"] for s in stats) == 10 * p.n_agents
+    print(stats[-1])
 
 
 def test_c3_tag_10000(cuda):
+    # configs[2] (tag, 9,000 runners + 1,000 chasers), every row, 10 steps
     p = vi.workload("c3")
-    stats = run_and_check(p, vi.init_state(p, seed=0), 2)
-    print(stats)
+    stats = run_and_check(p, vi.init_state(p, seed=0), 10, workers=_workers())
+    assert sum(s["rows"] for s in stats) == 10 * p.n_agents
+    print(stats[-1])
 
 
 def test_c4_full_size_sampled_replicas(cuda):
-    # configs[3] at its full size (the bench launch configuration), replicas {0,1,511,1023}.
+    # configs[3] at its full size (the bench launch configuration), replicas {0,1,511,1023},
+    # every row of each, 3 steps.
     p = vi.workload("c4")
     st0 = vi.init_state(p, seed=0)
-    run_and_check(p, st0, 1, replicas=[0, 1, 511, 1023])
+    run_and_check(p, st0, 3, replicas=[0, 1, 511, 1023], workers=_workers())
 
 
 def test_64bit_output_indexing(cuda):
@@ -104,22 +116,26 @@ def test_64bit_output_indexing(cuda):
 
 
 def test_c5_full_size_sampled_rows(cuda):
-    # configs[4]: 1M-agent world; bins bit-exact in full, sensing on sampled rows against
-    # all N, plus size-independent properties (sum rule, closed-form expectations).
+    # configs[4]: 1M-agent world in the bench's launch configuration, 3 steps; each step:
+    # integrate and bins bit-exact in full, sensing on 4,096 sampled rows against all N
+    # (SURVEY.md §8c), plus size-independent properties (sum rule, closed-form expectations).
     torch = _torch()
     p = vi.workload("c5")
     w = make_world(p)
     out = w.alloc_outputs()
     st = dev(vi.init_state(p, seed=0))
-    prev = host(st)
-    act = vi.actions(p, seed=0, step=0)
-    w.step(st, dev(act), out)
-    torch.cuda.synchronize()
-    cur = host(st)
-    parity.check_integrate(p, cur, oracle.integrate(p, prev, act))
-    parity.check_bins(p, {k: host(v) for k, v in w.get_bins().items()}, cur)
-    rows = np.random.default_rng(1).choice(p.n_agents, 96, replace=False)
-    parity.check_sense(p, cur[0], outs_np(out, 0), rows=rows)
+    for t in range(3):
+        prev = host(st)
+        act = vi.actions(p, seed=0, step=t)
+        w.step(st, dev(act), out)
+        torch.cuda.synchronize()
+        assert w.sync_errors() == -1
+        cur = host(st)
+        parity.check_integrate(p, cur, oracle.integrate(p, prev, act))
+        parity.check_bins(p, {k: host(v) for k, v in w.get_bins().items()}, cur)
+        rows = np.random.default_rng(1 + t).choice(p.n_agents, 4096, replace=False)
+        s = parity.check_sense(p, cur[0], outs_np(out, 0), rows=rows, workers=_workers())
+        print(t, s)
     nn = host(out.n_neigh).astype(np.int64)
     assert nn.sum() % 2 == 0
     e = (p.n_agents - 1) * math.pi * p.d_v ** 2 / p.width ** 2

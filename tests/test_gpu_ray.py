@@ -42,10 +42,18 @@ def _check(p, g, state_r, rows):
     gg = {k: (v.view(np.uint32) if v.dtype == np.int32 else v) for k, v in g.items()
           if k in ("reward", "n_neigh", "n_collide", "n_touch")}
     parity.check_sense(p.replace(vision="sector"), state_r, gg, rows=rows)
-    view, lo, hi = ray_views(p, state_r, rows)
+    view, lo, hi, cond = ray_views(p, state_r, rows, return_cond=True)
     gv = g["obs"][rows, :nv].astype(np.float64)
     assert np.all(gv >= lo - 1e-7) and np.all(gv <= hi + 1e-7), \
         (np.max(lo - gv), np.max(gv - hi))
+    # The interval is not loose where the geometry is well conditioned (no grazing disc,
+    # nearest hit's sqrt sensitivity <= 1e-6 d_v): width <= 2 (1e-5 view + 1e-6) + 1e-6,
+    # and the kernel matches the fp64 view there within 1e-5 relative + 1e-6.
+    hit = view < 1.0
+    assert np.all((hi - lo)[cond] <= 2e-5 * view[cond] + 3e-6 + 1e-12), np.max((hi - lo)[cond])
+    assert np.all(np.abs(gv - view)[cond] <= 1e-5 * view[cond] + 1e-6), \
+        np.max((np.abs(gv - view) - 1e-5 * view)[cond])
+    assert (cond & hit).sum() >= 0.5 * hit.sum(), ((cond & hit).sum(), hit.sum())
     occ = np.unpackbits(g["sector_occ"][rows].view(np.uint8), axis=1, bitorder="little")[:, :nv]
     assert np.array_equal(occ.astype(bool), gv < 1.0)
     if p.env == "flock":

@@ -117,3 +117,33 @@ def test_opinion_consensus_dynamics(cuda):
         assert s <= spread
         spread = s
     assert spread < 1e-5
+
+
+@pytest.mark.parametrize("bad", ["dangling_col", "negative_col", "row_ptr_decreasing",
+                                 "row_ptr_past_end"])
+def test_opinion_invalid_graph_raises(cuda, bad):
+    # a dangling index is an invariant violation -> VG_ESTATE naming the node; the
+    # invalid edge is never read (no out-of-bounds access), valid nodes are still updated.
+    import torch
+    from paper_2207_03945_b200 import rl
+    from paper_2207_03945_b200._lib import VgError
+    g = vi.opinion_graph(64, 4, seed=2)
+    rp, col = g["row_ptr"].copy(), g["col"].copy()
+    if bad == "dangling_col":
+        col[int(rp[10])] = 64
+    elif bad == "negative_col":
+        col[int(rp[10])] = -5
+    elif bad == "row_ptr_decreasing":
+        rp[11] = rp[10] - 1
+    else:
+        rp[11] = len(col) + 7
+        rp[12:] = len(col) + 7
+    d = {k: torch.from_numpy(v).cuda() for k, v in
+         (("rp", rp), ("col", col), ("w", g["weight"]), ("op", g["op"]))}
+    nxt = torch.empty_like(d["op"])
+    with pytest.raises(VgError, match="VG_ESTATE.*node 10"):
+        rl.opinion_step(d["rp"], d["col"], d["w"], d["op"], nxt, 0.3, 0.5)
+    # the record is cleared: a valid graph afterwards passes
+    v = {k: torch.from_numpy(x).cuda() for k, x in
+         (("rp", g["row_ptr"]), ("col", g["col"]), ("w", g["weight"]))}
+    rl.opinion_step(v["rp"], v["col"], v["w"], d["op"], nxt, 0.3, 0.5)

@@ -69,12 +69,17 @@ def test_matches_torch_float64():
 
 
 def test_sample_rules():
-    # near-deterministic limit, log-prob at the mode, clipping
+    # log-prob of the unclipped sample, clipping to the box; S:332:
+    # log_std clamped to [-5, 2] (-30 acts as -5, 10 as 2)
     w = vi.policy_weights(129)
-    w["log_std"] = np.array([-30.0, 0.0], np.float32)
+    w["log_std"] = np.array([-30.0, 10.0], np.float32)
     mean = np.array([[0.3, 0.0], [10.0, -10.0]])
     s = pol.sample(w, mean, np.array([0, 1]), seed=1, step=0, lo=[-0.1, -0.2], hi=[0.1, 0.2])
-    assert s["raw"][0, 0] == pytest.approx(0.3, abs=1e-9)
-    assert s["action"][0, 0] == 0.1 and s["action"][1, 0] == 0.1 and s["action"][1, 1] == -0.2
     eps = s["eps"]
-    assert s["logp"][0] == pytest.approx(-0.5 * (eps[0] ** 2).sum() + 30.0 - math.log(2 * math.pi))
+    assert s["raw"][0, 0] == pytest.approx(0.3 + math.exp(-5.0) * eps[0, 0], abs=1e-12)
+    assert s["raw"][0, 1] == pytest.approx(math.exp(2.0) * eps[0, 1], abs=1e-12)
+    assert s["action"][1, 0] == 0.1 and s["action"][1, 1] == -0.2
+    assert s["logp"][0] == pytest.approx(-0.5 * (eps[0] ** 2).sum() + 5.0 - 2.0 - math.log(2 * math.pi))
+    w["log_std"] = np.array([-1.0, 0.5], np.float32)        # inside the clamp: unchanged
+    s = pol.sample(w, mean, np.array([0]), seed=1, step=0, lo=[-9, -9], hi=[9, 9])
+    assert s["raw"][0, 0] == pytest.approx(0.3 + math.exp(-1.0) * s["eps"][0, 0], abs=1e-12)

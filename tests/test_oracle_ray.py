@@ -92,3 +92,18 @@ def test_bounds_bracket_the_value():
     st = vi.init_state(p, seed=3)[0].astype(np.float64)
     view, lo, hi = ray_views(p, st, np.arange(100))
     assert np.all(lo <= view + 1e-15) and np.all(view <= hi + 1e-15)
+
+
+def test_interval_narrow_where_well_conditioned():
+    # The comparator's [lo, hi] must not be loose: on sectors with no grazing
+    # disc and a well-conditioned nearest hit, hi - lo <= 2 (1e-5 view + 1e-6) + 1e-6; those
+    # sectors are the bulk of the hits.
+    import vg_inputs as vi
+    from oracle.ray import ray_views
+    p = vi.flock_params(3000).replace(vision="ray")
+    st = vi.init_state(p, seed=4)[0].astype(np.float64)
+    view, lo, hi, cond = ray_views(p, st, np.arange(200), return_cond=True)
+    assert np.all((lo <= view + 1e-12) & (view <= hi + 1e-12))
+    assert np.all((hi - lo)[cond] <= 2e-5 * view[cond] + 3e-6 + 1e-12)
+    hit = view < 1.0
+    assert (cond & hit).sum() >= 0.7 * hit.sum()

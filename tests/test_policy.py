@@ -90,7 +90,7 @@ def _check(obs_np, w, box, seed=5, step=3):
     assert np.abs(g["value"] - evv).max() <= EMU_TOL, np.abs(g["value"] - evv).max()
     s = pol.sample(w, g["mean"].astype(np.float64), np.arange(obs_np.shape[0]), seed, step,
                    np.array(box[0]), np.array(box[1]))      # noise on the GPU's own mean
-    sig = np.exp(np.asarray(w["log_std"], np.float64))
+    sig = np.exp(np.clip(np.asarray(w["log_std"], np.float64), -5.0, 2.0))
     tol_a = 1e-5 * (np.abs(s["eps"]) + 1) * sig + 1e-6
     assert np.all(np.abs(g["action"] - s["action"]) <= tol_a)
     assert np.all(np.abs(g["logp"] - s["logp"]) <= 1e-5 * (1 + (s["eps"] ** 2).sum(-1)))
@@ -109,6 +109,20 @@ def test_policy_random_obs(cuda, rows):
     obs = rng.random((rows, p.obs_dim)).astype(np.float32)
     obs[rng.random(obs.shape) < 0.4] = 1.0                  # empty sectors read 1.0
     print(_check(obs, w, ((-p.a_max, -p.theta_max), (p.a_max, p.theta_max))))
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("log_std", [(-30.0, 10.0), (3.0, -6.0)])
+def test_policy_log_std_clamped(cuda, log_std):
+    # log_std clamped to [-5, 2] in the sample scale and the log-prob (the oracle
+    # clamps too, pinned by test_oracle_policy.test_sample_rules)
+    p = vi.workload("c2")
+    w = vi.policy_weights(p.obs_dim, seed=1)
+    w["log_std"] = np.array(log_std, np.float32)
+    obs = np.random.default_rng(0).random((300, p.obs_dim)).astype(np.float32)
+    _check(obs, w, ((-50.0, -50.0), (50.0, 50.0)))
+    g = _run(obs, w, ((-50.0, -50.0), (50.0, 50.0)))
+    assert np.all(np.isfinite(g["action"])) and np.all(np.isfinite(g["logp"]))
 
 
 @pytest.mark.gpu
