@@ -290,13 +290,27 @@ class ReplicaRunner:
 
 
 class SlabRunner:
-    """c5 at N > 1: one world split into x-slabs (vg_slab_*), halo exchanged with
-    torch.distributed P2P over NCCL every step."""
+    """c5 at N > 1: one world split into x-slabs (vg_slab_*), halo exchanged every step
+    (DESIGN.md §7): by the world's own NCCL communicator inside vg_slab_step (overlapped
+    with the interior phase), or — if libvg cannot create it — by torch.distributed P2P
+    around vg_slab_interior (also overlapped)."""
 
     def __init__(self, p, device, rank, world, torch, vg):
+        import torch.distributed as dist
         from paper_2207_03945_b200 import slab
         self.p, self.torch, self.slab = p, torch, slab
-        self.w = vg.World(p, device=device, slab={"rank": rank, "world_size": world})
+        nid = [vg.nccl_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(nid, src=0)
+        cfg = {"rank": rank, "world_size": world, "nccl_unique_id": nid[0]}
+        try:
+            self.w = vg.World(p, device=device, slab=cfg)
+            self.exchange = "libvg vg_slab_step (world-owned NCCL comm, grouped send/recv on its comm stream)"
+        except vg.VgError as e:                    # same decision on every rank
+            print(f"[rank {rank}] libvg NCCL unavailable ({e}); torch.distributed P2P", file=sys.stderr)
+            del cfg["nccl_unique_id"]
+            self.w = vg.World(p, device=device, slab=cfg)
+            self.exchange = "torch.distributed P2P (NCCL) around vg_slab_interior"
+        self.owned_comm = "nccl_unique_id" in cfg
         self.out = self.w.alloc_outputs()
         init = vi.clustered_state if STATE == "clustered" else vi.init_state
         full = torch.from_numpy(init(p, seed=0)).to(device)   # same world everywhere
@@ -304,17 +318,23 @@ class SlabRunner:
         self.w.slab_sense(self.out)
         del full
         self.act_dev = torch.zeros((1, p.n_agents, 2), dtype=torch.float32, device=device)
-        self.launches = 7   # begin, unpack, keys, scan, scatter, cell_sort, sense
+        # begin; interior: keys, scan, scatter, cell sort, sense; finish: unpack, keys,
+        # scan, scatter, cell sort, sense
+        self.launches = 12
         self.phase_names = {"integrate_bin": "begin (integrate+route)",
-                            "scan_cells": "exchange+unpack", "scatter": "bin local set",
-                            "cell_sort": "-", "sense": "sense"}
+                            "scan_cells": "interior (bin+sense, halo in flight)",
+                            "scatter": "halo wait+unpack", "cell_sort": "bin boundary",
+                            "sense": "sense boundary"}
 
     def step(self, acts):
-        self.slab.slab_step_dist(self.w, acts, self.out)
+        if self.owned_comm:
+            self.w.slab_step(acts, self.out)
+        else:
+            self.slab.slab_step_dist(self.w, acts, self.out)
 
     def step_host(self, acts_h, rew_h):
         self.act_dev.copy_(acts_h, non_blocking=True)
-        self.slab.slab_step_dist(self.w, self.act_dev, self.out)
+        self.step(self.act_dev)
         rew_h.copy_(self.out.reward, non_blocking=True)
 
     def pairs_local(self):
@@ -557,20 +577,25 @@ def run_ours(args):
         hbm = float(peaks.get("hbm_gbs", 6441.6))
         sm_mhz = float(peaks.get("sm_max_mhz", 1965.0))
         alu_peak = 148 * 128 * sm_mhz * 1e6 / 1e12      # fp32 lane-ops/s, TFLOP/s-equivalent
-        sense_s = phases["sense"] / 1e3 / nrec
+        # K4 time: slab mode senses in two launches (the interior phase, which also bins
+        # the interior columns, and the boundary phase)
+        sense_ms = phases["sense"] + (phases["scan_cells"] if slab_mode else 0.0)
+        sense_s = sense_ms / 1e3 / nrec
         achieved = ALG_OPS_PER_PAIR * pairs_local / sense_s / 1e12
         n = p.total_agents if not slab_mode else p.n_agents // world
         obs_b = 4 * w.obs_dim + 4 * w.occ_words + SENSE_BYTES_FIXED
         fused = getattr(w, "kernels_per_step", 5) == 2
         # algorithmic bytes per agent of each stage as designed (DESIGN.md §6 kernel table):
         # the fused bin and K3b also write the K4 sense order (xo_rec, xo_perm, xo_xy)
-        if slab_mode:                  # the exchange phase moves two fixed-size messages
-            scan_b = 2 * int(w.slab_io.message_bytes)
-        else:
-            scan_b = 8 * w.n_cells
+        scan_b = 8 * w.n_cells
         stage_bytes = {"integrate_bin": (92 if fused else 48) * n, "scan_cells": scan_b,
                        "scatter": 44 * n, "cell_sort": 68 * n, "sense": obs_b * n}
-        if fused:         # one kernel does K1-K3b: the other binning phases are empty
+        if slab_mode:     # begin | interior bin + sense | halo wait + unpack | boundary bin | sense
+            msg = 2 * int(w.slab_io.message_bytes)
+            stage_bytes = {"integrate_bin": 48 * n, "scan_cells": (44 + 68) * n + obs_b * n,
+                           "scatter": msg, "cell_sort": (44 + 68) * 4 * n // (w.grid // world),
+                           "sense": obs_b * 4 * n // (w.grid // world)}
+        elif fused:         # one kernel does K1-K3b: the other binning phases are empty
             stage_bytes = {"integrate_bin": 92 * n, "sense": obs_b * n}
         elif not slab_mode and getattr(w, "kernels_per_step", 5) == 3:   # K1 + K3g + K4
             stage_bytes = {"integrate_bin": 48 * n, "scan_cells": (44 + 68) * n + scan_b,
@@ -647,7 +672,7 @@ def run_ours(args):
             cpu = {"value": rate, "unit": UNIT, "cores": cores, "kind": "oracle",
                    "sample": sample}
         if slab_mode:
-            par = f"slab{world}: x-slabs of {w.grid // world} cell columns + halo over NCCL"
+            par = f"slab{world}: x-slabs of {w.grid // world} cell columns + halo: {run.exchange}"
         elif world > 1:
             par = f"replicas over {world} ranks (no collective)"
         else:

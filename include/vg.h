@@ -94,7 +94,7 @@ typedef struct {
   float w_prox;         /* tag runner proximity weight                         [0.1]       */
   float s_max_chaser;   /* tag chaser move bound (runners use s_max)           [0.375]     */
   int32_t rank, world_size, halo_capacity; /* slab mode: this rank, P, records/message   */
-  const void* nccl_unique_id;              /* reserved (the exchange is the caller's)     */
+  const void* nccl_unique_id;              /* slab mode: NULL, or 128 bytes from vg_nccl_unique_id: the world creates and owns an NCCL communicator (collective over the P ranks) for vg_slab_step */
 } vg_config;
 
 /* Caller-owned device output buffers; a NULL pointer means "do not write".  Rows are in
@@ -189,21 +189,36 @@ vg_status vg_sync_errors(vg_world* w, void* stream, int64_t* bad_agent);
  * One world (n_replicas = 1, N = n_agents global) split over world_size = P ranks by
  * x-slabs of whole cell columns: rank g owns global columns [g G/P, (g+1) G/P) (P | G,
  * >= 2 columns per rank, and the largest move per step < cell size so an agent crosses
- * at most one column).  Each step:
- *   vg_slab_begin   integrate the owned rows and route them: stay, migrate (<= 1 slab), or
- *                   copy as a ghost (boundary column) into two messages (left, right);
- *   exchange        the caller moves send_left -> left rank's recv_right and send_right ->
- *                   right rank's recv_left (torch.distributed P2P over NCCL, or
- *                   vg_slab_exchange_loopback for P worlds in one process);
- *   vg_slab_finish  append received records, bin owned + ghost agents (stable by global
- *                   id), sense + reward the owned cells.
- * Output rows are the owned agents in (local cell, y sub-bin of 8, global id) order (K4's
- * sense order, a function of the state alone); outs->agent_id
- * gives each row's global id; the next vg_slab_begin takes actions[row] in that order.
- * Every per-agent result is bitwise identical to the single-world (replica) path.
+ * at most one column).  All agents are updated simultaneously from one snapshot:
+ * the slab decomposition changes nothing but where the work runs.  Each step:
+ *   vg_slab_begin     integrate the owned rows and route them: stay, migrate (<= 1 slab),
+ *                     or copy as a ghost (boundary column) into two messages (left, right);
+ *   exchange          send_left -> left rank's recv_right, send_right -> right rank's
+ *                     recv_left (the world's own NCCL communicator in vg_slab_step; or
+ *                     the caller: torch.distributed P2P, host staging, or
+ *                     vg_slab_exchange_loopback for P worlds in one process);
+ *   vg_slab_interior  while the messages are in flight: bin the interior owned columns
+ *                     (local 2..W-1, which no neighbour can send records into) and sense
+ *                     + reward the owned cells whose 3x3 stencil lies inside them (local
+ *                     columns 3..W-2);
+ *   vg_slab_finish    after the exchange: append the received records, bin the boundary
+ *                     and ghost columns, sense + reward the remaining owned cells (it runs
+ *                     vg_slab_interior first if the caller skipped it).
+ *   vg_slab_step      all of the above in one call: begin on `stream`, the halo exchange
+ *                     (grouped ncclSend/ncclRecv) on the world's comm stream, the interior
+ *                     phase on `stream` meanwhile, then the boundary phase after a stream
+ *                     wait on the exchange (no host synchronization).  Needs a world
+ *                     created with cfg.nccl_unique_id (VG_EINVAL otherwise); NCCL errors
+ *                     (synchronous, or asynchronous via vg_sync_errors) are VG_ENCCL.
+ * Output rows are the owned agents in (memory cell, y sub-bin, global id) order (K4's
+ * sense order, a function of the state alone); outs->agent_id gives each row's global id;
+ * the next vg_slab_begin takes actions[row] in that order.  vg_slab_interior and
+ * vg_slab_finish of one step must get the same outs.  Every per-agent result is bitwise
+ * identical to the single-world (replica) path.
  * Buffers: outputs need capacity N rows.  Messages: {u32 count, 3 x u32}, float4 rec[cap],
  * u32 id[cap], cap = halo_capacity (0 = auto: 4 N/G + 256, >= 1024).  A message or local
- * overflow is reported as VG_EOVERFLOW by vg_sync_errors. */
+ * overflow is reported as VG_EOVERFLOW by vg_sync_errors.  Calls out of order (interior or
+ * finish without begin, step without a communicator) are VG_EINVAL. */
 typedef struct {
   void* send_left;
   void* send_right;
@@ -224,9 +239,15 @@ vg_status vg_slab_sense(vg_world* w, const vg_outputs* outs, void* stream);
 vg_status vg_slab_begin(vg_world* w, const float* actions, void* stream);
 vg_status vg_slab_get_io(vg_world* w, vg_slab_io* io);
 vg_status vg_slab_exchange_loopback(vg_world* const* worlds, int32_t n, void* stream);
+vg_status vg_slab_interior(vg_world* w, const vg_outputs* outs, void* stream);
 vg_status vg_slab_finish(vg_world* w, const vg_outputs* outs, void* stream);
+vg_status vg_slab_step(vg_world* w, const float* actions, const vg_outputs* outs, void* stream);
 /* Synchronizes `stream`; *n_own = number of owned agents (valid output rows). */
 vg_status vg_slab_own_count(vg_world* w, void* stream, int64_t* n_own);
+/* Host-only: a new NCCL unique id (128 bytes into out[nbytes >= 128]) for the slab group's
+ * communicator; rank 0 makes it, every rank passes the same bytes in cfg.nccl_unique_id.
+ * libnccl is loaded at run time ($VG_NCCL_LIB, else libnccl.so.2): VG_ENCCL if missing. */
+vg_status vg_nccl_unique_id(void* out, int32_t nbytes);
 
 /* ------------------------------------------- shared policy forward
  * The actor-critic MLP of P:212 ("two hidden layers with 64 nodes each", tanh)
@@ -257,6 +278,16 @@ vg_status vg_policy_set_weights(vg_policy* p, const float* const* weights, void*
 vg_status vg_policy_forward(vg_policy* p, const float* obs, int64_t rows,
                             const vg_policy_outputs* outs, uint64_t seed, uint64_t step,
                             void* stream);
+/* The same, writing only the rows of one class (per-type policies, "the runner and
+ * chaser types share independent policies"): row r is of class ((r mod period) >= split),
+ * i.e. for a tag world period = N, split = N - n_chasers (chasers are the last indices of
+ * every replica, A14); period = 0 means every row (= vg_policy_forward).  Rows of the
+ * other class are left untouched; the noise of row r is the same as in vg_policy_forward.
+ * Errors: VG_EINVAL for period < 0, split outside [0, period], cls not 0/1. */
+vg_status vg_policy_forward_class(vg_policy* p, const float* obs, int64_t rows,
+                                  int64_t period, int64_t split, int32_t cls,
+                                  const vg_policy_outputs* outs, uint64_t seed, uint64_t step,
+                                  void* stream);
 
 /* ------------------------------------------------- GAE over the trajectory buffer (§8f #3)
  * Generalized advantage estimation for n agents x t steps, continuing task
@@ -271,6 +302,10 @@ vg_status vg_gae(const float* reward, const float* value, int64_t n, int32_t t, 
  * the shared policy samples actions from obs[k] (value[k], action[k], logp[k]; noise
  * counter step0 + k), then vg_step integrates them and writes obs[k+1] and reward[k];
  * finally value[t] = V(obs[t]) (bootstrap) and GAE (vg_gae) fills adv / ret.
+ * Tag worlds may pass pol_chaser != NULL: runners (agents [0, N - n_chasers) of each
+ * replica) then act with `pol` and chasers with `pol_chaser` — the two independent
+ * policies of P:198 (vg_policy_forward_class per type); NULL = one shared policy.
+ * pol_chaser on a flock world is VG_EINVAL.
  * Time-major device buffers for M = R*N agents: obs [t+1][M][obs_dim] (obs[0] from a prior
  * vg_bin + vg_sense or the previous rollout's obs[t]), action [t][M][2], logp [t][M],
  * reward [t][M], value [t+1][M], adv [t][M], ret [t][M].  Replica mode only.  No host
@@ -284,9 +319,9 @@ typedef struct {
   float* adv;
   float* ret;
 } vg_rollout_buffers;
-vg_status vg_rollout(vg_world* w, vg_policy* pol, float* state, const vg_rollout_buffers* buf,
-                     int32_t t, uint64_t seed, uint64_t step0, float gamma, float lambda,
-                     void* stream);
+vg_status vg_rollout(vg_world* w, vg_policy* pol, vg_policy* pol_chaser, float* state,
+                     const vg_rollout_buffers* buf, int32_t t, uint64_t seed, uint64_t step0,
+                     float gamma, float lambda, void* stream);
 
 /* --------------------------------------- opinion dynamics, Listing 1 (§8f #4)
  * One step of the bounded-confidence graph interaction + self interaction: for each node

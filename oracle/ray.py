@@ -42,7 +42,8 @@ def ray_views(p, state_r, rows, dh_rel=5e-5, return_cond=False):
 
     ``return_cond`` also returns a mask of the *well-conditioned* sectors: every disc that
     may be hit is surely hit (no grazing disc) and the nearest one's sqrt sensitivity
-    dh / (2 sqrt h) is <= 1e-6 d_v, or nothing can be hit at all."""
+    dh / (2 sqrt h) is <= 1e-6 d_v for every disc whose interval reaches the sector's upper
+    bound, or nothing can be hit at all."""
     st = np.asarray(state_r, np.float64)
     n = st.shape[0]
     rows = np.asarray(rows)
@@ -89,9 +90,12 @@ def ray_views(p, state_r, rows, dh_rel=5e-5, return_cond=False):
             view[b, c * v:(c + 1) * v] = tc[sel].min(0)
             lo[b, c * v:(c + 1) * v] = np.minimum(np.where(maybe[sel], tmay[sel] - err[sel] - 1e-6, 1.0).min(0), 1.0)
             hi[b, c * v:(c + 1) * v] = np.minimum(np.where(sure[sel], tc[sel] + err[sel], 1.0).min(0), 1.0)
+            # well conditioned: no grazing disc, and every disc whose interval reaches down
+            # to the sector's hi has a small sqrt sensitivity
             sens = np.minimum(dh / (2 * np.maximum(sq[sel], 1e-300)), math.sqrt(dh)) / dv
-            arg = np.where(sure[sel], tc[sel], np.inf).argmin(0)
-            near_ok = np.take_along_axis(np.where(sure[sel], sens, 0.0), arg[None, :], 0)[0] <= 1e-6
+            hic = hi[b, c * v:(c + 1) * v][None, :]
+            relevant = sure[sel] & (tc[sel] - err[sel] - 1e-6 <= hic)
+            near_ok = ~np.any(relevant & (sens > 1e-6), axis=0)
             cond[b, c * v:(c + 1) * v] = ~np.any(maybe[sel] & ~sure[sel], axis=0) & near_ok
     if return_cond:
         return view, np.clip(lo, 0.0, 1.0), hi, cond

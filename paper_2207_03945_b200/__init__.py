@@ -39,6 +39,12 @@ def config_from_params(p, slab: dict | None = None) -> _lib.VgConfig:
         c.rank = int(slab["rank"])
         c.world_size = int(slab["world_size"])
         c.halo_capacity = int(slab.get("halo_capacity", 0))
+        nid = slab.get("nccl_unique_id")       # bytes (vg_nccl_unique_id): world owns a comm
+        if nid is not None:
+            if len(nid) != 128:
+                raise ValueError("nccl_unique_id: 128 bytes required")
+            c._nccl_id_buf = ctypes.create_string_buffer(bytes(nid), 128)   # kept alive
+            c.nccl_unique_id = ctypes.cast(c._nccl_id_buf, ctypes.c_void_p)
     c.n_agents = int(p.n_agents)
     c.n_replicas = int(p.n_replicas)
     for f in ("width", "d_v", "d_r", "fov", "s_min", "s_max", "a_max", "theta_max",
@@ -73,6 +79,14 @@ class _CudaArray:
         self.__cuda_array_interface__ = {"data": (ptr, False), "shape": tuple(shape),
                                          "typestr": typestr, "version": 3, "strides": None}
         self._owner = owner
+
+
+def nccl_unique_id() -> bytes:
+    """vg_nccl_unique_id: 128 bytes naming a new NCCL communicator (make on one rank,
+    broadcast, pass to every rank's World(slab={..., "nccl_unique_id": id}))."""
+    buf = ctypes.create_string_buffer(128)
+    check(_lib.lib.vg_nccl_unique_id(buf, 128))
+    return buf.raw
 
 
 class World:
@@ -245,17 +259,29 @@ class World:
         self._check_tensor(actions, "actions", (1, self.N, 2))
         check(_lib.lib.vg_slab_begin(self._h, actions.data_ptr(), self._stream()))
 
+    def slab_interior(self, out: Outputs) -> None:
+        """vg_slab_interior: bin + sense the interior columns (no halo needed)."""
+        o = self._outs(out)
+        check(_lib.lib.vg_slab_interior(self._h, byref(o), self._stream()))
+
     def slab_finish(self, out: Outputs) -> None:
         o = self._outs(out)
         check(_lib.lib.vg_slab_finish(self._h, byref(o), self._stream()))
 
+    def slab_step(self, actions: torch.Tensor, out: Outputs) -> None:
+        """vg_slab_step: one step with the world's own NCCL halo exchange, overlapped with
+        the interior phase (needs slab={"nccl_unique_id": ...} at creation)."""
+        self._check_tensor(actions, "actions", (1, self.N, 2))
+        o = self._outs(out)
+        check(_lib.lib.vg_slab_step(self._h, actions.data_ptr(), byref(o), self._stream()))
+
     def slab_owned(self) -> tuple:
         """(global ids [n_own], state records [n_own, 4]) of the owned agents in (cell, id)
-        order (vg_get_bins); output rows use the sense order — map them by outs.agent_id."""
+        order (vg_get_bins; owned = the first n_own records, memory columns 0..W-1); output
+        rows use the sense order — map them by outs.agent_id."""
         n = self.slab_own_count()
         b = self.get_bins()
-        own_b = int(b["cell_start"][self.grid].item())
-        return b["perm"][0, own_b:own_b + n].clone(), b["sorted"][0, own_b:own_b + n].clone()
+        return b["perm"][0, :n].clone(), b["sorted"][0, :n].clone()
 
     def slab_own_count(self) -> int:
         n = c_int64(0)

@@ -99,15 +99,22 @@ SIGNATURES = {
     "vg_slab_begin": (c_int32, [c_void_p, c_void_p, c_void_p]),
     "vg_slab_get_io": (c_int32, [c_void_p, POINTER(VgSlabIo)]),
     "vg_slab_exchange_loopback": (c_int32, [POINTER(c_void_p), c_int32, c_void_p]),
+    "vg_slab_interior": (c_int32, [c_void_p, POINTER(VgOutputs), c_void_p]),
     "vg_slab_finish": (c_int32, [c_void_p, POINTER(VgOutputs), c_void_p]),
+    "vg_slab_step": (c_int32, [c_void_p, c_void_p, POINTER(VgOutputs), c_void_p]),
+    "vg_nccl_unique_id": (c_int32, [c_void_p, c_int32]),
     "vg_slab_own_count": (c_int32, [c_void_p, c_void_p, POINTER(c_int64)]),
     "vg_policy_create": (c_int32, [POINTER(VgPolicyConfig), POINTER(c_void_p)]),
     "vg_policy_destroy": (None, [c_void_p]),
     "vg_policy_set_weights": (c_int32, [c_void_p, POINTER(c_void_p), c_void_p]),
     "vg_policy_forward": (c_int32, [c_void_p, c_void_p, c_int64, POINTER(VgPolicyOutputs),
                                     ctypes.c_uint64, ctypes.c_uint64, c_void_p]),
-    "vg_rollout": (c_int32, [c_void_p, c_void_p, c_void_p, POINTER(VgRolloutBuffers), c_int32,
-                             ctypes.c_uint64, ctypes.c_uint64, c_float, c_float, c_void_p]),
+    "vg_rollout": (c_int32, [c_void_p, c_void_p, c_void_p, c_void_p, POINTER(VgRolloutBuffers),
+                             c_int32, ctypes.c_uint64, ctypes.c_uint64, c_float, c_float,
+                             c_void_p]),
+    "vg_policy_forward_class": (c_int32, [c_void_p, c_void_p, c_int64, c_int64, c_int64, c_int32,
+                                          POINTER(VgPolicyOutputs), ctypes.c_uint64,
+                                          ctypes.c_uint64, c_void_p]),
     "vg_gae": (c_int32, [c_void_p, c_void_p, c_int64, c_int32, c_float, c_float, c_void_p,
                          c_void_p, c_void_p]),
     "vg_opinion_step": (c_int32, [c_void_p, c_void_p, c_void_p, c_int32, c_int64, c_void_p,

@@ -13,6 +13,11 @@
 #include <new>
 #include <vector>
 
+#include <dlfcn.h>
+#include <mutex>
+
+#include <nccl.h>          // types only: libnccl is loaded at run time (NcclApi below)
+
 #include "vg.h"
 #include "vg_kernels.cuh"
 #include "vg_policy.cuh"
@@ -36,6 +41,68 @@ vg_status fail(vg_status st, const char* fmt, ...) {
     if (e_ != cudaSuccess)                                                             \
       return fail(VG_ECUDA, "%s: %s (%s:%d)", #call, cudaGetErrorString(e_), __FILE__, \
                   __LINE__);                                                           \
+  } while (0)
+
+// NCCL, loaded with dlopen on first use (the library itself has no link-time NCCL
+// dependency, so it loads on CPU-only machines): $VG_NCCL_LIB, else the libnccl.so.2
+// already in the process (torch's), else the system one.
+struct NcclApi {
+  void* h = nullptr;
+  ncclResult_t (*GetUniqueId)(ncclUniqueId*) = nullptr;
+  ncclResult_t (*CommInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+  ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
+  ncclResult_t (*CommGetAsyncError)(ncclComm_t, ncclResult_t*) = nullptr;
+  ncclResult_t (*Send)(const void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*Recv)(void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*GroupStart)() = nullptr;
+  ncclResult_t (*GroupEnd)() = nullptr;
+  const char* (*GetErrorString)(ncclResult_t) = nullptr;
+  char err[256] = "";
+};
+
+NcclApi& nccl_state() {
+  static NcclApi api;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    const char* env = std::getenv("VG_NCCL_LIB");
+    const char* names[] = {env, "libnccl.so.2", "libnccl.so"};
+    for (const char* n : names) {
+      if (!n || !n[0]) continue;
+      api.h = dlopen(n, RTLD_NOW | RTLD_LOCAL);
+      if (api.h) break;
+    }
+    if (!api.h) {
+      snprintf(api.err, sizeof(api.err), "cannot load libnccl (set VG_NCCL_LIB): %s", dlerror());
+      return;
+    }
+#define VG_NCCL_SYM(f) api.f = reinterpret_cast<decltype(api.f)>(dlsym(api.h, "nccl" #f))
+    VG_NCCL_SYM(GetUniqueId);
+    VG_NCCL_SYM(CommInitRank);
+    VG_NCCL_SYM(CommDestroy);
+    VG_NCCL_SYM(CommGetAsyncError);
+    VG_NCCL_SYM(Send);
+    VG_NCCL_SYM(Recv);
+    VG_NCCL_SYM(GroupStart);
+    VG_NCCL_SYM(GroupEnd);
+    VG_NCCL_SYM(GetErrorString);
+#undef VG_NCCL_SYM
+    if (!api.GetUniqueId || !api.CommInitRank || !api.CommDestroy || !api.CommGetAsyncError ||
+        !api.Send || !api.Recv || !api.GroupStart || !api.GroupEnd || !api.GetErrorString) {
+      snprintf(api.err, sizeof(api.err), "libnccl lacks a needed symbol (ncclSend/ncclRecv need NCCL >= 2.7)");
+      dlclose(api.h);
+      api.h = nullptr;
+    }
+  });
+  return api;
+}
+const NcclApi* nccl_api() { return nccl_state().h ? &nccl_state() : nullptr; }
+const char* nccl_err() { return nccl_state().err; }
+
+#define VG_NCCL(call)                                                                  \
+  do {                                                                                 \
+    ncclResult_t r_ = (call);                                                          \
+    if (r_ != ncclSuccess)                                                             \
+      return fail(VG_ENCCL, "%s: %s", #call, nccl_api()->GetErrorString(r_));        \
   } while (0)
 
 }  // namespace
@@ -79,6 +146,10 @@ struct vg_world {
   unsigned char* msg = nullptr;    // 4 messages: send_l, send_r, recv_l, recv_r
   size_t msg_bytes = 0;
   int left = -1, right = -1;
+  int slab_stage = 0;              // 0 binned / 1 begun (vg_slab_begin) / 2 interior done
+  ncclComm_t comm = nullptr;       // the world's communicator (cfg.nccl_unique_id)
+  cudaStream_t comm_stream = nullptr;
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   // phase timing (vg_profile_begin/end): VG_N_PHASES + 1 events per recorded step
   std::vector<cudaEvent_t> prof_ev;
   int prof_max = 0, prof_n = 0;
@@ -288,8 +359,8 @@ vg::WorkList work_list(vg_world* w) {
   WL.item = w->work;
   WL.n = w->work_cnt;
   WL.chunk_q = sense_chunk_q(w);
-  WL.lo = w->slab ? w->P.G : 0;                           // slab: owned local columns 1..W
-  WL.hi = w->slab ? (w->SL.W + 1) * w->P.G : w->n_cells;
+  WL.lo = 0;                                              // slab: owned memory columns 0..W-1
+  WL.hi = w->slab ? w->SL.W * w->P.G : w->n_cells;
   return WL;
 }
 
@@ -303,17 +374,22 @@ vg_status launch_k1(vg_world* w, float4* io, const float4* in, const float2* act
   return launch_check("k_integrate_bin");
 }
 
-// Exclusive scan of the cell counts into cell_start (re-zeroing the counts).
-vg_status scan_cells(vg_world* w, cudaStream_t s) {
-  const int n = w->n_cells;
+// Exclusive scan of the counts of cells [c0, c1) into cell_start[c0 .. c1] (re-zeroing the
+// counts); `cont`: continue from cell_start[c0] (written by an earlier phase) instead of 0.
+vg_status scan_cells(vg_world* w, cudaStream_t s, int c0 = 0, int c1 = -1, bool cont = false) {
+  if (c1 < 0) c1 = w->n_cells;
+  const int n = c1 - c0;
+  uint32_t* cnt = w->count + c0;
+  uint32_t* start = w->cell_start + c0;
+  const uint32_t* base = cont ? start : nullptr;
   if (n <= vg::kScanSmallMax) {                 // (dynamic smem limit set at world creation)
-    vg::k_scan_cells<<<1, 1024, (size_t)n * 4, s>>>(w->count, w->cell_start, n);
+    vg::k_scan_cells<<<1, 1024, (size_t)n * 4, s>>>(cnt, start, n, base);
     return launch_check("k_scan_cells");
   }
   const unsigned tiles = (unsigned)((n + vg::kScanTile - 1) / vg::kScanTile);
-  vg::k_scan_tiles<<<tiles, 1024, 0, s>>>(w->count, n, w->tile_sum);
+  vg::k_scan_tiles<<<tiles, 1024, 0, s>>>(cnt, n, w->tile_sum);
   if (vg_status st = launch_check("k_scan_tiles")) return st;
-  vg::k_scan_apply<<<tiles, 1024, 0, s>>>(w->count, w->cell_start, n, w->tile_sum);
+  vg::k_scan_apply<<<tiles, 1024, 0, s>>>(cnt, start, n, w->tile_sum, base);
   return launch_check("k_scan_apply");
 }
 
@@ -333,17 +409,19 @@ vg_status launch_fused_bin(vg_world* w, float4* io, const float4* in, const floa
 #ifndef VG_CTA_SORT_CELLS_PER_SM
 #define VG_CTA_SORT_CELLS_PER_SM 8
 #endif
-vg_status launch_cell_sort(vg_world* w, cudaStream_t s) {
+// Cells [c0, c1) (default: all), + the sentinel row at c1.
+vg_status launch_cell_sort(vg_world* w, cudaStream_t s, int c0 = 0, int c1 = -1) {
+  if (c1 < 0) c1 = w->n_cells;
   if (w->n_cells <= (long long)VG_CTA_SORT_CELLS_PER_SM * w->n_sm) {
-    vg::k_cell_sort_cta<<<(unsigned)(w->n_cells + 1), vg::kCtaSortThreads, 0, s>>>(
-        w->P, w->n_cells, w->slab ? 1 : 0, w->cell_start, w->tmp_rec, w->tmp_id, w->sorted,
-        w->perm, w->xo_rec, w->xo_perm, w->xo_xy, w->sub_tab, work_list(w), w->slot);
+    vg::k_cell_sort_cta<<<(unsigned)(c1 - c0 + 1), vg::kCtaSortThreads, 0, s>>>(
+        w->P, c1, w->slab ? 1 : 0, w->cell_start, w->tmp_rec, w->tmp_id, w->sorted,
+        w->perm, w->xo_rec, w->xo_perm, w->xo_xy, w->sub_tab, work_list(w), w->slot, c0);
     return launch_check("k_cell_sort_cta");
   }
-  const long long threads = (long long)(w->n_cells + 1) * 32;   // + the sentinel row
+  const long long threads = (long long)(c1 - c0 + 1) * 32;   // + the sentinel row
   vg::k_cell_sort<<<(unsigned)((threads + 255) / 256), 256, 0, s>>>(
-      w->P, w->n_cells, w->slab ? 1 : 0, w->cell_start, w->tmp_rec, w->tmp_id, w->sorted,
-      w->perm, w->xo_rec, w->xo_perm, w->xo_xy, w->sub_tab, work_list(w), w->slot);
+      w->P, c1, w->slab ? 1 : 0, w->cell_start, w->tmp_rec, w->tmp_id, w->sorted,
+      w->perm, w->xo_rec, w->xo_perm, w->xo_xy, w->sub_tab, work_list(w), w->slot, c0);
   return launch_check("k_cell_sort");
 }
 
@@ -461,13 +539,35 @@ void sense_kernel(vg_world* w, int cells, const vg::Outs& O, cudaStream_t s) {
         w->work, w->work_cnt, cq, cells);
 }
 
+enum { kSlabInterior = 0, kSlabBoundary = 1, kSlabAll = 2 };   // slab binning / sensing phases
+
+// Slab mode: the owned cells K4 senses in one phase (memory columns, vg::Slab): all
+// owned columns [0, W); the inner interior l = 3..W-2 = memory [1, W-3) while the halo is in
+// flight; the rest (memory 0, W-3, W-2, W-1; all of [0, W) when W <= 4) after it.
+vg::Slab slab_sense_set(const vg_world* w, int phase) {
+  vg::Slab SL = w->SL;
+  const int W = SL.W;
+  SL.snl = 0;
+  if (phase == kSlabAll) { SL.sc0 = 0; SL.snc = W; }
+  else if (phase == kSlabInterior) { SL.sc0 = 1; SL.snc = std::max(0, W - 4); }
+  else if (W <= 4) { SL.sc0 = 0; SL.snc = W; }
+  else { SL.snl = 4; SL.scol[0] = 0; SL.scol[1] = W - 3; SL.scol[2] = W - 2; SL.scol[3] = W - 1; }
+  return SL;
+}
+
 template <bool VISION>
-vg_status launch_sense(vg_world* w, const vg_outputs* outs, cudaStream_t s) {
+vg_status launch_sense(vg_world* w, const vg_outputs* outs, cudaStream_t s,
+                       int slab_phase = kSlabAll) {
   const vg::Outs O = to_outs(w, outs);
-  if (w->slab) {                      // owned cells only: local columns 1..W
-    const int cells = w->SL.W * w->P.G;
-    if (w->P.env == vg::kFlock) sense_kernel<vg::kFlock, VISION, true>(w, cells, O, s);
-    else sense_kernel<vg::kTag, VISION, true>(w, cells, O, s);
+  if (w->slab) {                      // owned cells only (this phase's memory columns)
+    const vg::Slab saved = w->SL;
+    w->SL = slab_sense_set(w, slab_phase);
+    const int cells = (w->SL.snl ? w->SL.snl : w->SL.snc) * w->P.G;
+    if (cells > 0) {
+      if (w->P.env == vg::kFlock) sense_kernel<vg::kFlock, VISION, true>(w, cells, O, s);
+      else sense_kernel<vg::kTag, VISION, true>(w, cells, O, s);
+    }
+    w->SL = saved;
     return launch_check("k_sense(slab)");
   }
   if (w->P.env == vg::kFlock) sense_kernel<vg::kFlock, VISION, false>(w, w->n_cells, O, s);
@@ -479,18 +579,31 @@ unsigned stride_blocks(size_t n) {
   return (unsigned)std::max<size_t>(1, std::min<size_t>((n + 255) / 256, 148 * 8));   // grid-stride
 }
 
-// Bin the slab's local set (owned + ghosts) on the column-major local grid.
+// Bin the slab's local set (owned + ghosts) on the column-major local grid (memory column
+// order, vg::Slab), one phase at a time: kSlabInterior = memory columns [0, W-2) (nothing
+// there can arrive from a neighbour), kSlabBoundary = [W-2, W+2) after the halo arrived
+// (continuing the interior's cell_start and work items), kSlabAll = both at once.
 template <int ENV>
-vg_status slab_bin(vg_world* w, cudaStream_t s) {
+vg_status slab_bin(vg_world* w, cudaStream_t s, int phase = kSlabAll) {
+  const int nA = (w->SL.W - 2) * w->P.G;
+  if (phase == kSlabInterior && nA == 0) {         // W = 2: no interior columns
+    VG_CUDA(cudaMemsetAsync(w->work_cnt, 0, sizeof(uint32_t), s));
+    VG_CUDA(cudaMemsetAsync(w->cell_start, 0, sizeof(uint32_t), s));
+    VG_CUDA(cudaMemsetAsync(w->sub_tab, 0, sizeof(uint32_t), s));
+    return VG_OK;
+  }
   const unsigned nb = stride_blocks(w->SB.cap_loc);
-  vg::k_slab_keys<<<nb, 256, 0, s>>>(w->P, w->SL, w->SB, w->cell_id, w->slot, w->count);
+  vg::k_slab_keys<<<nb, 256, 0, s>>>(w->P, w->SL, w->SB, w->cell_id, w->slot, w->count, phase);
   if (vg_status st = launch_check("k_slab_keys")) return st;
-  if (vg_status st = scan_cells(w, s)) return st;
+  const int c0 = (phase == kSlabBoundary) ? nA : 0;
+  const int c1 = (phase == kSlabInterior) ? nA : w->n_cells;
+  if (vg_status st = scan_cells(w, s, c0, c1, phase == kSlabBoundary)) return st;
   vg::k_slab_scatter<ENV><<<nb, 256, 0, s>>>(w->P, w->SB, w->cell_id, w->slot, w->cell_start,
-                                              w->tmp_rec, w->tmp_id, w->work_cnt);
+                                              w->tmp_rec, w->tmp_id, w->work_cnt,
+                                              phase != kSlabBoundary);
   if (vg_status st = launch_check("k_slab_scatter")) return st;
-  if (vg_status st = launch_cell_sort(w, s)) return st;
-  w->binned = true;
+  if (vg_status st = launch_cell_sort(w, s, c0, c1)) return st;
+  if (phase != kSlabInterior) w->binned = true;
   return VG_OK;
 }
 
@@ -593,7 +706,27 @@ vg_status vg_world_create(const vg_config* cfg, vg_world** out) {
       w->SB.recv_r = w->msg + 3 * w->msg_bytes;
       cudaError_t e = cudaMemset(w->msg, 0, 4 * w->msg_bytes);
       if (e == cudaSuccess) e = cudaMemset(w->slab_ovf, 0, sizeof(uint32_t));
+      if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&w->comm_stream, cudaStreamNonBlocking);
+      if (e == cudaSuccess) e = cudaEventCreateWithFlags(&w->ev_fork, cudaEventDisableTiming);
+      if (e == cudaSuccess) e = cudaEventCreateWithFlags(&w->ev_join, cudaEventDisableTiming);
       if (e != cudaSuccess) st = fail(VG_ECUDA, "slab init: %s", cudaGetErrorString(e));
+    }
+    if (!st && cfg->nccl_unique_id) {
+      // The world owns its communicator: a collective call, every rank of
+      // the slab group creates its world at the same time.
+      const NcclApi* nc = nccl_api();
+      if (!nc) {
+        st = fail(VG_ENCCL, "vg_world_create: %s", nccl_err());
+      } else {
+        ncclUniqueId id;
+        std::memcpy(&id, cfg->nccl_unique_id, sizeof(id));
+        ncclResult_t r = nc->CommInitRank(&w->comm, cfg->world_size, id, cfg->rank);
+        if (r != ncclSuccess) {
+          w->comm = nullptr;
+          st = fail(VG_ENCCL, "ncclCommInitRank(%d of %d): %s", cfg->rank, cfg->world_size,
+                    nc->GetErrorString(r));
+        }
+      }
     }
   }
   if (!st) st = dalloc(w, &w->count, w->n_cells);
@@ -675,6 +808,10 @@ void vg_world_destroy(vg_world* w) {
   cudaFree(w->SB.loc_rec);
   cudaFree(w->SB.loc_id);
   cudaFree(w->msg);
+  if (w->comm) nccl_api()->CommDestroy(w->comm);
+  if (w->comm_stream) cudaStreamDestroy(w->comm_stream);
+  if (w->ev_fork) cudaEventDestroy(w->ev_fork);
+  if (w->ev_join) cudaEventDestroy(w->ev_join);
   if (w->err_flag) cudaFreeHost(w->err_flag);
   delete w;
 }
@@ -937,12 +1074,16 @@ vg_status vg_slab_begin(vg_world* w, const float* actions, void* stream) {
   cudaStream_t s = as_stream(stream);
   const float2* a = reinterpret_cast<const float2*>(actions);
   static const char kBeginKey = 0;                  // graph key: (actions, &kBeginKey, {})
+  vg_status st;
   if (graph_ok(w, s)) {
     const vg_outputs none{};
-    return cached_graph(w, a, &kBeginKey, &none, s, "vg_slab_begin",
-                        [&](cudaStream_t cs) { return slab_begin_launch(w, a, cs); });
+    st = cached_graph(w, a, &kBeginKey, &none, s, "vg_slab_begin",
+                      [&](cudaStream_t cs) { return slab_begin_launch(w, a, cs); });
+  } else {
+    st = slab_begin_launch(w, a, s);
   }
-  return slab_begin_launch(w, a, s);
+  if (!st) w->slab_stage = 1;
+  return st;
 }
 
 vg_status vg_slab_get_io(vg_world* w, vg_slab_io* io) {
@@ -980,32 +1121,120 @@ vg_status vg_slab_exchange_loopback(vg_world* const* ws, int32_t n, void* stream
 }
 
 namespace {
+// The interior phase: bin memory columns [0, W-2) of the local set and sense their inner
+// cells — nothing here waits for the halo.
+vg_status slab_interior_launch(vg_world* w, const vg_outputs* outs, cudaStream_t s) {
+  vg_status st = (w->P.env == vg::kFlock) ? slab_bin<vg::kFlock>(w, s, kSlabInterior)
+                                          : slab_bin<vg::kTag>(w, s, kSlabInterior);
+  if (st) return st;
+  st = launch_sense<true>(w, outs, s, kSlabInterior);
+  prof_mark(w, 2, s);
+  return st;
+}
+// The boundary phase, once the halo arrived: append the received records, bin the boundary
+// and ghost columns, sense the owned cells whose stencil reaches them.
 vg_status slab_finish_launch(vg_world* w, const vg_outputs* outs, cudaStream_t s) {
   vg::k_slab_unpack<<<stride_blocks(2ull * w->SB.cap_msg), 256, 0, s>>>(w->SB);
   if (vg_status st = launch_check("k_slab_unpack")) return st;
-  prof_mark(w, 2, s);
-  vg_status st = (w->P.env == vg::kFlock) ? slab_bin<vg::kFlock>(w, s) : slab_bin<vg::kTag>(w, s);
-  if (st) return st;
   prof_mark(w, 3, s);
+  vg_status st = (w->P.env == vg::kFlock) ? slab_bin<vg::kFlock>(w, s, kSlabBoundary)
+                                          : slab_bin<vg::kTag>(w, s, kSlabBoundary);
+  if (st) return st;
   prof_mark(w, 4, s);
-  st = launch_sense<true>(w, outs, s);
+  st = launch_sense<true>(w, outs, s, kSlabBoundary);
   prof_mark(w, 5, s);
   return st;
 }
+
+vg_status slab_interior(vg_world* w, const vg_outputs* outs, cudaStream_t s) {
+  static const char kInteriorKey = 0;               // graph key: (nullptr, &kInteriorKey, outs)
+  vg_status st;
+  if (graph_ok(w, s))
+    st = cached_graph(w, nullptr, &kInteriorKey, outs, s, "vg_slab_interior",
+                      [&](cudaStream_t cs) { return slab_interior_launch(w, outs, cs); });
+  else
+    st = slab_interior_launch(w, outs, s);
+  w->binned = false;                                // until the boundary phase
+  if (!st) w->slab_stage = 2;
+  return st;
+}
+
+vg_status slab_finish(vg_world* w, const vg_outputs* outs, cudaStream_t s) {
+  static const char kFinishKey = 0;                 // graph key: (nullptr, &kFinishKey, outs)
+  vg_status st;
+  if (graph_ok(w, s)) {
+    st = cached_graph(w, nullptr, &kFinishKey, outs, s, "vg_slab_finish",
+                      [&](cudaStream_t cs) { return slab_finish_launch(w, outs, cs); });
+  } else {
+    st = slab_finish_launch(w, outs, s);
+    if (w->prof_n < w->prof_max) ++w->prof_n;
+  }
+  if (!st) {
+    w->slab_stage = 0;
+    w->binned = true;
+  }
+  return st;
+}
 }  // namespace
+
+vg_status vg_slab_interior(vg_world* w, const vg_outputs* outs, void* stream) {
+  if (vg_status st = need_slab(w, true, "vg_slab_interior")) return st;
+  DeviceGuard dg_(w->device);
+  if (!outs) return fail(VG_EINVAL, "outs: NULL");
+  if (w->slab_stage != 1) return fail(VG_EINVAL, "vg_slab_interior: call vg_slab_begin first (once per step)");
+  return slab_interior(w, outs, as_stream(stream));
+}
 
 vg_status vg_slab_finish(vg_world* w, const vg_outputs* outs, void* stream) {
   if (vg_status st = need_slab(w, true, "vg_slab_finish")) return st;
   DeviceGuard dg_(w->device);
   if (!outs) return fail(VG_EINVAL, "outs: NULL");
+  if (w->slab_stage == 0) return fail(VG_EINVAL, "vg_slab_finish: call vg_slab_begin first");
   cudaStream_t s = as_stream(stream);
-  static const char kFinishKey = 0;                 // graph key: (nullptr, &kFinishKey, outs)
-  if (graph_ok(w, s))
-    return cached_graph(w, nullptr, &kFinishKey, outs, s, "vg_slab_finish",
-                        [&](cudaStream_t cs) { return slab_finish_launch(w, outs, cs); });
-  vg_status st = slab_finish_launch(w, outs, s);
-  if (w->prof_n < w->prof_max) ++w->prof_n;
-  return st;
+  if (w->slab_stage == 1)                           // no vg_slab_interior this step
+    if (vg_status st = slab_interior(w, outs, s)) return st;
+  return slab_finish(w, outs, s);
+}
+
+vg_status vg_slab_step(vg_world* w, const float* actions, const vg_outputs* outs, void* stream) {
+  if (vg_status st = need_slab(w, true, "vg_slab_step")) return st;
+  if (!actions || !outs) return fail(VG_EINVAL, "actions/outs: NULL");
+  if (!w->comm)
+    return fail(VG_EINVAL, "vg_slab_step: the world has no communicator (create it with "
+                           "cfg.nccl_unique_id), or use vg_slab_begin / exchange / vg_slab_finish");
+  DeviceGuard dg_(w->device);
+  cudaStream_t s = as_stream(stream);
+  if (vg_status st = vg_slab_begin(w, actions, stream)) return st;
+  // Halo exchange on the world's comm stream, overlapped with the interior phase on `s`:
+  // send_left -> left's recv_right, send_right -> right's recv_left.  Per peer pair NCCL
+  // matches sends and receives in issue order, so the same order on every rank pairs them
+  // for P = 2 too (both neighbours the same rank).
+  const NcclApi* nc = nccl_api();
+  VG_CUDA(cudaEventRecord(w->ev_fork, s));
+  VG_CUDA(cudaStreamWaitEvent(w->comm_stream, w->ev_fork, 0));
+  VG_NCCL(nc->GroupStart());
+  VG_NCCL(nc->Send(w->SB.send_l, w->msg_bytes, ncclUint8, w->left, w->comm, w->comm_stream));
+  VG_NCCL(nc->Send(w->SB.send_r, w->msg_bytes, ncclUint8, w->right, w->comm, w->comm_stream));
+  VG_NCCL(nc->Recv(const_cast<unsigned char*>(w->SB.recv_r), w->msg_bytes, ncclUint8, w->right,
+                   w->comm, w->comm_stream));
+  VG_NCCL(nc->Recv(const_cast<unsigned char*>(w->SB.recv_l), w->msg_bytes, ncclUint8, w->left,
+                   w->comm, w->comm_stream));
+  VG_NCCL(nc->GroupEnd());
+  VG_CUDA(cudaEventRecord(w->ev_join, w->comm_stream));
+  if (vg_status st = slab_interior(w, outs, s)) return st;
+  VG_CUDA(cudaStreamWaitEvent(s, w->ev_join, 0));
+  return slab_finish(w, outs, s);
+}
+
+vg_status vg_nccl_unique_id(void* out, int32_t nbytes) {
+  if (!out || nbytes < (int32_t)sizeof(ncclUniqueId))
+    return fail(VG_EINVAL, "vg_nccl_unique_id: need a %d-byte buffer", (int)sizeof(ncclUniqueId));
+  const NcclApi* nc = nccl_api();
+  if (!nc) return fail(VG_ENCCL, "vg_nccl_unique_id: %s", nccl_err());
+  ncclUniqueId id;
+  VG_NCCL(nc->GetUniqueId(&id));
+  std::memcpy(out, &id, sizeof(id));
+  return VG_OK;
 }
 
 vg_status vg_slab_sense(vg_world* w, const vg_outputs* outs, void* stream) {
@@ -1021,10 +1250,9 @@ vg_status vg_slab_own_count(vg_world* w, void* stream, int64_t* n_own) {
   DeviceGuard dg_(w->device);
   if (!n_own) return fail(VG_EINVAL, "n_own: NULL");
   VG_CUDA(cudaStreamSynchronize(as_stream(stream)));
-  uint32_t a = 0, b = 0;
-  VG_CUDA(cudaMemcpy(&a, w->cell_start + w->P.G, 4, cudaMemcpyDeviceToHost));
-  VG_CUDA(cudaMemcpy(&b, w->cell_start + (size_t)(w->SL.W + 1) * w->P.G, 4, cudaMemcpyDeviceToHost));
-  *n_own = (int64_t)b - (int64_t)a;
+  uint32_t b = 0;                                  // owned: memory columns [0, W)
+  VG_CUDA(cudaMemcpy(&b, w->cell_start + (size_t)w->SL.W * w->P.G, 4, cudaMemcpyDeviceToHost));
+  *n_own = (int64_t)b;
   return VG_OK;
 }
 
@@ -1092,12 +1320,15 @@ vg_status vg_policy_set_weights(vg_policy* p, const float* const* w, void* strea
   return VG_OK;
 }
 
-vg_status vg_policy_forward(vg_policy* p, const float* obs, int64_t rows,
-                            const vg_policy_outputs* outs, uint64_t seed, uint64_t step,
-                            void* stream) {
+vg_status vg_policy_forward_class(vg_policy* p, const float* obs, int64_t rows,
+                                  int64_t period, int64_t split, int32_t cls,
+                                  const vg_policy_outputs* outs, uint64_t seed, uint64_t step,
+                                  void* stream) {
   if (!p || !obs || !outs) return fail(VG_EINVAL, "policy/obs/outs: NULL");
   if (!p->have_weights) return fail(VG_EINVAL, "vg_policy_forward: call vg_policy_set_weights first");
   if (rows < 0) return fail(VG_EINVAL, "rows: must be >= 0");
+  if (period < 0 || (period > 0 && (split < 0 || split > period || (cls != 0 && cls != 1))))
+    return fail(VG_EINVAL, "vg_policy_forward_class: need period >= 0, 0 <= split <= period, cls in {0, 1}");
   if (rows == 0) return VG_OK;
   DeviceGuard dg_(p->device);
   vg::PolicyOut o{outs->mean, outs->value, outs->action, outs->logp};
@@ -1105,8 +1336,14 @@ vg_status vg_policy_forward(vg_policy* p, const float* obs, int64_t rows,
   const unsigned grid = (unsigned)std::min<int64_t>(tiles, p->n_sm);
   vg::k_policy<<<grid, vg::kPolThreads, vg::kPolSmem, as_stream(stream)>>>(
       obs, rows, p->cfg.obs_dim, p->pk, o, (uint32_t)seed, (uint32_t)(seed >> 32),
-      (uint32_t)step, (uint32_t)(step >> 32));
+      (uint32_t)step, (uint32_t)(step >> 32), period, split, cls);
   return launch_check("k_policy");
+}
+
+vg_status vg_policy_forward(vg_policy* p, const float* obs, int64_t rows,
+                            const vg_policy_outputs* outs, uint64_t seed, uint64_t step,
+                            void* stream) {
+  return vg_policy_forward_class(p, obs, rows, 0, 0, 0, outs, seed, step, stream);
 }
 
 vg_status vg_gae(const float* reward, const float* value, int64_t n, int32_t t, float gamma,
@@ -1150,10 +1387,13 @@ vg_status vg_opinion_sync_errors(void* stream, int64_t* bad_node) {
   return fail(VG_ESTATE, "vg_opinion_step: node %llu has an invalid row (row_ptr) or a dangling edge (col outside [0, n))", bad);
 }
 
-vg_status vg_rollout(vg_world* w, vg_policy* pol, float* state, const vg_rollout_buffers* b,
-                     int32_t t, uint64_t seed, uint64_t step0, float gamma, float lambda,
-                     void* stream) {
+vg_status vg_rollout(vg_world* w, vg_policy* pol, vg_policy* pol_chaser, float* state,
+                     const vg_rollout_buffers* b, int32_t t, uint64_t seed, uint64_t step0,
+                     float gamma, float lambda, void* stream) {
   if (!w || !pol || !state || !b) return fail(VG_EINVAL, "vg_rollout: NULL argument");
+  if (pol_chaser && w->P.env != vg::kTag) return fail(VG_EINVAL, "vg_rollout: pol_chaser needs a tag world");
+  if (pol_chaser && pol_chaser->cfg.obs_dim != w->P.obs_dim)
+    return fail(VG_EINVAL, "vg_rollout: chaser policy obs_dim %d != world obs_dim %d", pol_chaser->cfg.obs_dim, w->P.obs_dim);
   if (vg_status st = need_slab(w, false, "vg_rollout")) return st;
   DeviceGuard dg_(w->device);
   if (!b->obs || !b->action || !b->reward || !b->value) return fail(VG_EINVAL, "vg_rollout: obs/action/reward/value buffers required");
@@ -1163,19 +1403,28 @@ vg_status vg_rollout(vg_world* w, vg_policy* pol, float* state, const vg_rollout
   cudaStream_t s = as_stream(stream);
   const size_t M = (size_t)w->P.total;
   float4* io = reinterpret_cast<float4*>(state);
+  // per-type policies: runners = class 0, chasers = class 1 of period N
+  const int64_t per = pol_chaser ? (int64_t)w->P.N : 0;
+  const int64_t split = pol_chaser ? (int64_t)(w->P.N - w->cfg.n_chasers) : 0;
+  auto forward = [&](const float* obs, const vg_policy_outputs* po, uint64_t step) -> vg_status {
+    if (vg_status st = vg_policy_forward_class(pol, obs, (int64_t)M, per, split, 0, po, seed,
+                                               step, stream)) return st;
+    if (pol_chaser)
+      return vg_policy_forward_class(pol_chaser, obs, (int64_t)M, per, split, 1, po, seed,
+                                     step, stream);
+    return VG_OK;
+  };
   for (int k = 0; k < t; ++k) {
     const vg_policy_outputs po{nullptr, b->value + k * M, b->action + k * M * 2,
                                b->logp ? b->logp + k * M : nullptr};
-    if (vg_status st = vg_policy_forward(pol, b->obs + k * M * w->P.obs_dim, (int64_t)M, &po,
-                                         seed, step0 + (uint64_t)k, stream)) return st;
+    if (vg_status st = forward(b->obs + k * M * w->P.obs_dim, &po, step0 + (uint64_t)k)) return st;
     vg_outputs o{};
     o.obs = b->obs + (k + 1) * M * w->P.obs_dim;
     o.reward = b->reward + k * M;
     if (vg_status st = launch_step(w, io, reinterpret_cast<const float2*>(b->action + k * M * 2), &o, s)) return st;
   }
   const vg_policy_outputs pv{nullptr, b->value + (size_t)t * M, nullptr, nullptr};
-  if (vg_status st = vg_policy_forward(pol, b->obs + (size_t)t * M * w->P.obs_dim, (int64_t)M, &pv,
-                                       seed, step0 + (uint64_t)t, stream)) return st;
+  if (vg_status st = forward(b->obs + (size_t)t * M * w->P.obs_dim, &pv, step0 + (uint64_t)t)) return st;
   if (b->adv && b->ret)
     return vg_gae(b->reward, b->value, (int64_t)M, t, gamma, lambda, b->adv, b->ret, stream);
   return VG_OK;
@@ -1220,6 +1469,12 @@ vg_status vg_sync_errors(vg_world* w, void* stream, int64_t* bad_agent) {
   unsigned long long v = 0;
   VG_CUDA(cudaMemcpy(&v, w->err_dev, sizeof(v), cudaMemcpyDeviceToHost));
   if (bad_agent) *bad_agent = (v == ~0ull) ? -1 : (int64_t)v;
+  if (w->comm) {
+    ncclResult_t ar = ncclSuccess;
+    VG_NCCL(nccl_api()->CommGetAsyncError(w->comm, &ar));
+    if (ar != ncclSuccess && ar != ncclInProgress)
+      return fail(VG_ENCCL, "slab halo exchange: %s", nccl_api()->GetErrorString(ar));
+  }
   if (w->slab) {
     uint32_t ovf = 0;
     VG_CUDA(cudaMemcpy(&ovf, w->slab_ovf, 4, cudaMemcpyDeviceToHost));

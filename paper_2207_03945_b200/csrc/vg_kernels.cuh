@@ -65,12 +65,33 @@ struct Outs {
 };
 
 // Slab mode: this rank owns global cell columns [lo, hi), W = hi - lo >= 2.
-// The local grid has W + 2 columns (ghost columns 0 and W+1) x G rows, column-major:
-// local cell = lcx * G + cy, so the owned agents are the contiguous sorted range
-// [cell_start[G], cell_start[(W+1) G]).
+// The local grid has W + 2 columns l = 0..W+1 (l = 1..W owned, ghost columns 0 and W+1)
+// x G rows, column-major, stored in the MEMORY column order m = slab_mcol(l): the interior
+// owned columns l = 2..W-1 first (m = 0..W-3), then the owned boundary columns l = 1, W
+// (m = W-2, W-1), then the ghosts l = 0, W+1 (m = W, W+1).  Memory cell = m G + cy.  The
+// owned agents are the contiguous sorted range [0, cell_start[W G]); the interior columns
+// [0, cell_start[(W-2) G]) hold no record a neighbour can send, so they are binned and
+// their inner cells (l = 3..W-2) sensed while the halo is in flight (vg_slab_interior),
+// and only the boundary columns are binned after it arrives (vg_slab_finish).
 struct Slab {
   int lo, hi, W, n_lcells;
+  // cells sensed by this K4 launch: memory columns [sc0, sc0 + snc), or, if snl > 0, the
+  // memory columns scol[0..snl)
+  int sc0, snc, snl, scol[4];
 };
+__host__ __device__ __forceinline__ int slab_mcol(int l, int W) {
+  return (l >= 2 && l <= W - 1) ? l - 2 : (l == 1) ? W - 2 : (l == W) ? W - 1 : (l == 0) ? W : W + 1;
+}
+__host__ __device__ __forceinline__ int slab_lcol(int m, int W) {
+  return (m < W - 2) ? m + 2 : (m == W - 2) ? 1 : (m == W - 1) ? W : (m == W) ? 0 : W + 1;
+}
+// Does this K4 launch sense memory column m?
+__host__ __device__ __forceinline__ bool slab_senses(const Slab& SL, int m) {
+  if (SL.snl == 0) return m >= SL.sc0 && m < SL.sc0 + SL.snc;
+  bool in = false;
+  for (int k = 0; k < 4; ++k) in |= (k < SL.snl && SL.scol[k] == m);
+  return in;
+}
 
 // Record the smallest offending global agent index (S:59 error convention) and raise the
 // host-visible flag (mapped pinned memory, plain store).
@@ -176,12 +197,17 @@ __global__ void __launch_bounds__(256) k_integrate_bin(
 #define VG_SCAN_SMALL_MAX 12288
 #endif
 constexpr int kScanSmallMax = VG_SCAN_SMALL_MAX;   // 48 KB; above it the 2-kernel K2' is faster (c5: 18,496)
+// `base` (nullable): the scan starts from *base instead of 0 (a slab binning phase that
+// continues an earlier one: base = start, whose [0] the earlier phase wrote as its total).
 __global__ void __launch_bounds__(1024) k_scan_cells(uint32_t* __restrict__ count,
-                                                      uint32_t* __restrict__ start, int n) {
+                                                      uint32_t* start, int n,
+                                                      const uint32_t* base) {
   extern __shared__ uint32_t s_c[];                     // [n]
   __shared__ uint32_t warp_sums[32];
   __shared__ uint32_t total_s;
   const int t = threadIdx.x, lane = t & 31, w = t >> 5;
+  const uint32_t b0 = base ? *base : 0u;                // read before any thread writes start[]
+  __syncthreads();
   for (int k = t; k < n; k += blockDim.x) s_c[k] = count[k];
   __syncthreads();
   const int per = (n + blockDim.x - 1) / blockDim.x;
@@ -208,7 +234,7 @@ __global__ void __launch_bounds__(1024) k_scan_cells(uint32_t* __restrict__ coun
     if (lane == 31) total_s = wi;
   }
   __syncthreads();
-  uint32_t run = warp_sums[w] + inc - sum;
+  uint32_t run = b0 + warp_sums[w] + inc - sum;
   for (int k = b; k < e; ++k) {
     const uint32_t c = s_c[k];
     s_c[k] = run;
@@ -219,7 +245,7 @@ __global__ void __launch_bounds__(1024) k_scan_cells(uint32_t* __restrict__ coun
     start[k] = s_c[k];
     count[k] = 0u;
   }
-  if (t == 0) start[n] = total_s;
+  if (t == 0) start[n] = b0 + total_s;
 }
 
 // K2' (multi-CTA): tiles of 4096 counts.  k_scan_tiles sums each tile; k_scan_apply lets
@@ -247,14 +273,16 @@ __global__ void __launch_bounds__(1024) k_scan_tiles(const uint32_t* __restrict_
 }
 
 __global__ void __launch_bounds__(1024) k_scan_apply(uint32_t* __restrict__ count,
-                                                      uint32_t* __restrict__ start, int n,
-                                                      const uint32_t* __restrict__ tile_sum) {
+                                                      uint32_t* start, int n,
+                                                      const uint32_t* __restrict__ tile_sum,
+                                                      const uint32_t* base0) {
   __shared__ uint32_t ws[32];
   __shared__ uint32_t s_off;
   const int t = threadIdx.x, lane = t & 31, w = t >> 5;
   const int base = blockIdx.x * kScanTile;
   if (w == 0) {                                           // offset = sum of earlier tiles
-    uint32_t o = 0;
+    uint32_t o = base0 ? *base0 : 0u;                     // (+ an earlier phase's total:
+    if (lane != 0) o = 0u;                                //  every CTA reads the same value)
     for (int k = lane; k < (int)blockIdx.x; k += 32) o += tile_sum[k];
     o = __reduce_add_sync(kFull, o);
     if (lane == 0) s_off = o;
@@ -483,8 +511,9 @@ __global__ void __launch_bounds__(256) k_cell_sort(
     const float4* __restrict__ tmp_rec, const uint32_t* __restrict__ tmp_id,
     float4* __restrict__ sorted, uint32_t* __restrict__ perm, float4* __restrict__ xo_rec,
     uint32_t* __restrict__ xo_perm, float2* __restrict__ xo_xy, uint32_t* __restrict__ sub_tab,
-    WorkList WL, uint32_t* __restrict__ scratch) {
-  const int cell = (int)(((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5);
+    WorkList WL, uint32_t* __restrict__ scratch, int cell0) {
+  // cells [cell0, n_cells) (slab binning phases: a range of memory columns)
+  const int cell = cell0 + (int)(((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5);
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
   // K4 work items of this block's 8 cells: one atomic per block.
   __shared__ uint32_t s_nch[8], s_base;
@@ -568,11 +597,12 @@ __global__ void __launch_bounds__(kCtaSortThreads) k_cell_sort_cta(
     const float4* __restrict__ tmp_rec, const uint32_t* __restrict__ tmp_id,
     float4* __restrict__ sorted, uint32_t* __restrict__ perm, float4* __restrict__ xo_rec,
     uint32_t* __restrict__ xo_perm, float2* __restrict__ xo_xy, uint32_t* __restrict__ sub_tab,
-    WorkList WL, uint32_t* __restrict__ scratch) {
+    WorkList WL, uint32_t* __restrict__ scratch, int cell0) {
   __shared__ uint2 s_key[kCtaRankMax];        // (id, sub-bin) per arrival slot
   __shared__ uint32_t s_rank[kCtaRankMax], s_pos[kCtaRankMax];
   __shared__ uint32_t s_cnt[kSub];
-  const int cell = blockIdx.x, tid = threadIdx.x, lane = tid & 31;
+  // cells [cell0, n_cells) (slab binning phases: a range of memory columns)
+  const int cell = cell0 + (int)blockIdx.x, tid = threadIdx.x, lane = tid & 31;
   const uint32_t b = cell_start[cell];
   if (cell == n_cells) {                                 // sentinel
     if (tid == 0) sub_tab[(size_t)n_cells * kSub] = b;
@@ -797,6 +827,9 @@ constexpr int kRBMaxAgents = 32768;
 #ifndef VG_RB_THREADS
 #define VG_RB_THREADS 1024
 #endif
+#ifndef VG_RB_TIMING_SKIP
+#define VG_RB_TIMING_SKIP 0        // tuning builds only: 1 skips pass 3, 2 passes 2 + 3
+#endif
 constexpr int kRBThreads = VG_RB_THREADS;   // warps per replica CTA x 32; 2048 / it CTAs per SM
 
 template <int ENV, bool INTEGRATE>
@@ -943,6 +976,7 @@ __global__ void __launch_bounds__(kRBThreads, 2048 / kRBThreads) k_replica_bin(
     }
   }
   __syncthreads();
+  if (VG_RB_TIMING_SKIP & 2) return;   // timing experiments only (wrong results)
   // ---- pass 2: in-order walk of this warp's range, stable positions, scatter
   for (int b = i0; b < i1; b += 32) {
     const int i = b + lane;
@@ -962,6 +996,7 @@ __global__ void __launch_bounds__(kRBThreads, 2048 / kRBThreads) k_replica_bin(
   }
   __syncthreads();                   // the block's sorted / perm writes are now visible
   // ---- pass 3: K4 sense order of each cell (see K3b)
+  if (VG_RB_TIMING_SKIP & 1) return;   // timing experiments only (wrong results)
   for (int c = warp; c < C; c += NW) {
     const int m = ((c + 1 < C) ? (int)s_tot[c + 1] : N) - (int)s_tot[c];
     sense_order_cell(P, c % P.G, false, (uint32_t)base + s_tot[c], m, sorted, perm, xo_rec,
@@ -992,6 +1027,15 @@ constexpr int kSenseMinBlocks = VG_SENSE_MINB;  // launch-bounds minimum; 64 reg
 // Ring (power of 2): >= 31 carried + 64 pushed, and large enough that one chunk's pushes
 // never reach the slots the previous drain read (carried + 64 + 2 x 32 <= kQueue), so one
 // warp sync per chunk (before the drain) orders all ring traffic.
+#ifndef VG_SENSE_PAIRED
+#define VG_SENSE_PAIRED 0           // sector pass: both queries' pair batches in packed pairs
+#endif
+#ifndef VG_SENSE_PACKED_SCAN
+#define VG_SENSE_PACKED_SCAN 0      // candidate test of both queries in packed pairs
+#endif
+#ifndef VG_SENSE_DEF_MINB
+#define VG_SENSE_DEF_MINB 8         // the flock default-constant instance: <= 64 registers, 8 CTAs/SM
+#endif
 #ifndef VG_SENSE_TAG_DEF_MINB
 #define VG_SENSE_TAG_DEF_MINB 8     // the tag default-constant instance: <= 64 registers, 8 CTAs/SM
 #endif
@@ -1009,6 +1053,9 @@ static_assert(kQueue >= 31 + 32 * kSenseHalves, "ring: carried + one chunk of pu
 // 1e-6 fov = 4.4e-6 rad): octant reduction, t = min/max by the hardware reciprocal, a
 // degree-6 minimax polynomial in t^2 for atan(t)/t on [0, 1] (fit error 2.5e-7), then the
 // quadrant fix-ups; atan2(+-0, +-0) = +-0.
+#ifndef VG_ATAN_DEG
+#define VG_ATAN_DEG 6
+#endif
 __device__ __forceinline__ float vg_atan2(float y, float x) {
   const float ax = fabsf(x), ay = fabsf(y);
   const float mx = fmaxf(ax, ay), mn = fminf(ax, ay);
@@ -1016,6 +1063,16 @@ __device__ __forceinline__ float vg_atan2(float y, float x) {
   asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(rc) : "f"(fmaxf(mx, 1.17549435e-38f)));
   const float t = mn * rc;
   const float s = t * t;
+#if VG_ATAN_DEG == 5
+  // degree 5 in t^2: fit error 1.7e-6 rad; with the heading (4e-7), fwd/left (2e-7) and
+  // sector-coordinate (2.6e-7) errors 2.5e-6 rad, inside the 4.36e-6 rad band (A17)
+  float p = -0.011721630f;
+  p = fmaf(p, s, 0.052653560f);
+  p = fmaf(p, s, -0.11643203f);
+  p = fmaf(p, s, 0.19354250f);
+  p = fmaf(p, s, -0.33262315f);
+  p = fmaf(p, s, 0.99997723f);
+#else
   float p = 0.006812420208007097f;
   p = fmaf(p, s, -0.03360610455274582f);
   p = fmaf(p, s, 0.07962583005428314f);
@@ -1023,10 +1080,73 @@ __device__ __forceinline__ float vg_atan2(float y, float x) {
   p = fmaf(p, s, 0.198078453540802f);
   p = fmaf(p, s, -0.3331737220287323f);
   p = fmaf(p, s, 0.9999961256980896f);
+#endif
   float r = p * t;
   r = (ay > ax) ? (1.5707963705062866f - r) : r;
   r = (x < 0.f) ? (3.1415927410125732f - r) : r;
   return copysignf(r, y);
+}
+
+// Packed fp32 pairs (PTX 8.6 .f32x2, sm_100+: FADD2 / FMUL2 / FFMA2, one issue slot for two
+// IEEE-rounded lane operations, bitwise equal to the scalar ops).  K4 evaluates the two
+// queries of a warp in the two halves of a pair (v19).
+typedef unsigned long long f32x2;
+__device__ __forceinline__ f32x2 pk2(float lo, float hi) {
+  f32x2 r;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(lo), "f"(hi));
+  return r;
+}
+__device__ __forceinline__ float lo2(f32x2 r) {
+  float a, b;
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(a), "=f"(b) : "l"(r));
+  (void)b;
+  return a;
+}
+__device__ __forceinline__ float hi2(f32x2 r) {
+  float a, b;
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(a), "=f"(b) : "l"(r));
+  (void)a;
+  return b;
+}
+__device__ __forceinline__ f32x2 sub2(f32x2 a, f32x2 b) {
+  f32x2 r;
+  asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+  return r;
+}
+__device__ __forceinline__ f32x2 mul2(f32x2 a, f32x2 b) {
+  f32x2 r;
+  asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+  return r;
+}
+__device__ __forceinline__ f32x2 fma2(f32x2 a, f32x2 b, f32x2 c) {
+  f32x2 r;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(a), "l"(b), "l"(c));
+  return r;
+}
+__device__ __forceinline__ f32x2 bc2(float a) { return pk2(a, a); }
+
+// vg_atan2 on both halves of a pair: the same operations in the same order (the polynomial,
+// the products and the pi/2, pi reflections as packed ops), so each half is bitwise
+// vg_atan2 of its inputs.
+__device__ __forceinline__ f32x2 vg_atan2x2(f32x2 y, f32x2 x) {
+  const float x0 = lo2(x), x1 = hi2(x), y0 = lo2(y), y1 = hi2(y);
+  const float ax0 = fabsf(x0), ay0 = fabsf(y0), ax1 = fabsf(x1), ay1 = fabsf(y1);
+  float rc0, rc1;
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(rc0) : "f"(fmaxf(fmaxf(ax0, ay0), 1.17549435e-38f)));
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(rc1) : "f"(fmaxf(fmaxf(ax1, ay1), 1.17549435e-38f)));
+  const f32x2 t = mul2(pk2(fminf(ax0, ay0), fminf(ax1, ay1)), pk2(rc0, rc1));
+  const f32x2 s = mul2(t, t);
+  f32x2 p = fma2(bc2(0.006812420208007097f), s, bc2(-0.03360610455274582f));
+  p = fma2(p, s, bc2(0.07962583005428314f));
+  p = fma2(p, s, bc2(-0.13233458995819092f));
+  p = fma2(p, s, bc2(0.198078453540802f));
+  p = fma2(p, s, bc2(-0.3331737220287323f));
+  p = fma2(p, s, bc2(0.9999961256980896f));
+  const f32x2 r = mul2(p, t);
+  const f32x2 rf = sub2(bc2(1.5707963705062866f), r);
+  const float r0 = (ay0 > ax0) ? lo2(rf) : lo2(r), r1 = (ay1 > ax1) ? hi2(rf) : hi2(r);
+  const f32x2 rp = sub2(bc2(3.1415927410125732f), pk2(r0, r1));
+  return pk2(copysignf((x0 < 0.f) ? lo2(rp) : r0, y0), copysignf((x1 < 0.f) ? hi2(rp) : r1, y1));
 }
 
 // K4's outputs (~0.5 KB per agent) are written once and not re-read by the step: with
@@ -1044,6 +1164,15 @@ __device__ __forceinline__ void vg_st_out(uint32_t* p, uint32_t v) {
 
 __device__ __forceinline__ uint32_t sh_addr(const void* p) {
   return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void red_min(uint32_t addr, uint32_t v) {
+  asm volatile("red.shared.min.u32 [%0], %1;" :: "r"(addr), "r"(v) : "memory");
+}
+// Predicated shared-memory min (no return value): one RED instruction under a predicate,
+// no branch around it (the compiler's atomicMin in an `if` costs a BSSY/BRA/BSYNC).
+__device__ __forceinline__ void red_min_if(bool p, uint32_t addr, uint32_t v) {
+  asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.u32 q, %2, 0;\n\t@q red.shared.min.u32 [%0], %1;\n\t}"
+               :: "r"(addr), "r"(v), "r"((uint32_t)p) : "memory");
 }
 __device__ __forceinline__ void sts128(uint32_t a, float4 v) {
   asm volatile("st.shared.v4.f32 [%0], {%1, %2, %3, %4};" ::"r"(a), "f"(v.x), "f"(v.y), "f"(v.z),
@@ -1102,7 +1231,7 @@ __host__ __device__ constexpr SenseConst sense_defaults() {
 }
 
 template <int ENV, bool VISION, bool SLAB, bool RAY, bool DEF>
-__global__ void __launch_bounds__(kSenseWarps * 32, (DEF && ENV == kTag) ? VG_SENSE_TAG_DEF_MINB : kSenseMinBlocks) k_sense(
+__global__ void __launch_bounds__(kSenseWarps * 32, (DEF && ENV == kTag) ? VG_SENSE_TAG_DEF_MINB : DEF ? VG_SENSE_DEF_MINB : kSenseMinBlocks) k_sense(
     Params P, const uint32_t* __restrict__ cell_start, const float4* __restrict__ sorted,
     const float2* __restrict__ sorted_xy, const uint32_t* __restrict__ perm, Outs O, Slab SL,
     const float2* __restrict__ ray_dir, const uint32_t* __restrict__ sub_tab,
@@ -1128,6 +1257,10 @@ __global__ void __launch_bounds__(kSenseWarps * 32, (DEF && ENV == kTag) ? VG_SE
   // and loop step is shared; each query has its own ballot, queue, sector row and
   // accumulators.  A missing query gets a NaN position (never a neighbour).
   constexpr int NQ = kSenseNQ;
+  // Sector vision / reward with two queries per warp: packed candidate tests and the
+  // paired pair pass (process2).  Ray vision keeps the per-query pass.
+  constexpr bool PAIRED = VG_SENSE_PAIRED && !RAY && NQ == 2;
+  constexpr bool PACKED_SCAN = VG_SENSE_PACKED_SCAN && NQ == 2;
   // Pair-pass constants.  (ptxas sees through this empty asm and re-loads them from the
   // parameter bank per pair batch; forcing them into registers with an opaque add costs 8
   // registers and measured 4 % slower.)
@@ -1152,13 +1285,18 @@ __global__ void __launch_bounds__(kSenseWarps * 32, (DEF && ENV == kTag) ? VG_SE
       const uint32_t k = blockIdx.x - (uint32_t)n_first;
       if (k >= *work_n) return;
       item = work[k];
+      if (SLAB && !slab_senses(SL, (int)item.x / P.G)) return;       // another launch's cell
+    } else if (SLAB) {                                                // this launch's k-th cell
+      const int kc = (int)blockIdx.x / P.G;
+      item.x = (uint32_t)(((SL.snl ? SL.scol[kc] : SL.sc0 + kc)) * P.G + (int)blockIdx.x % P.G);
     }
     const int c = (int)item.x;
-  // Replica layout: cell = r G^2 + cy G + cx.  Slab layout: owned local column lcx = 1 + c/G.
+  // Replica layout: cell = r G^2 + cy G + cx.  Slab layout: memory cell c = m G + cy of
+  // local column lcx = slab_lcol(m).
   const int r = SLAB ? 0 : c / P.G2;
-  const int cl = SLAB ? (1 + c / P.G) * P.G + c % P.G : c - r * P.G2;
+  const int cl = SLAB ? c : c - r * P.G2;
   const int cy = SLAB ? c % P.G : cl / P.G;
-  const int cx = SLAB ? 1 + c / P.G : cl - cy * P.G;
+  const int cx = SLAB ? slab_lcol(c / P.G, SL.W) : cl - cy * P.G;
   const uint32_t* cs = cell_start + (size_t)r * P.G2;
 
   if (threadIdx.x == 0 && SLAB) {
@@ -1174,7 +1312,7 @@ __global__ void __launch_bounds__(kSenseWarps * 32, (DEF && ENV == kTag) ? VG_SE
       const int gcol = (SL.lo + col - 1 + P.G) % P.G;
       const float plo = (float)gcol * P.cell + csx - P.win_margin;
       const float phi = (float)(gcol + 1) * P.cell + csx + P.win_margin;
-      const int base = col * P.G;
+      const int base = slab_mcol(col, SL.W) * P.G;
       const int g1 = P.G - 1;
       if (cy >= 1 && cy <= P.G - 2) {
         s_seg[ns++] = Seg{csx, 0.f, qsx, 0.f, plo, phi, base, cy - 1, cy + 1};
@@ -1246,10 +1384,15 @@ __global__ void __launch_bounds__(kSenseWarps * 32, (DEF && ENV == kTag) ? VG_SE
     }
     __syncwarp();
 
+    const uint32_t srow = sh_addr(&s_min[warp][0][0]);         // this warp's sector rows
     // Pair pass over one queue entry (dx, dy, d^2, index | type << 31) of query t.
     auto process = [&](const int t, const float4 e) {
       const uint32_t tagbits = __float_as_uint(e.w);
-      if (ENV == kFlock ? tagbits == q0 + t : (tagbits & 0x7fffffffu) == q0 + t) return;  // j != i
+      // j != i.  The sector pass takes no branch for it: the self pair (always in
+      // the queue exactly once, at d = 0: a contact with f = -c_collide) is counted and
+      // removed exactly at the emit; it only has to be kept out of the sector minima.
+      const bool self = ENV == kFlock ? tagbits == q0 + t : (tagbits & 0x7fffffffu) == q0 + t;
+      if ((RAY || PAIRED) && self) return;
       const uint32_t tj = (ENV == kTag) ? tagbits >> 31 : 0u;
       const float d2 = e.z;
       const bool contact = d2 <= c_contact2;                          // A6 (inclusive)
@@ -1325,10 +1468,59 @@ __global__ void __launch_bounds__(kSenseWarps * 32, (DEF && ENV == kTag) ? VG_SE
         const float left = fmaf(csn[t], e.y, -sn[t] * e.x);
         // Sector coordinate (phi + fov/2) v / fov; visible iff 0 <= k < v (A3).
         const int k = __float2int_rd(fmaf(vg_atan2(left, fwd), c_inv_w, c_half_v));
-        if ((unsigned)k < (unsigned)VG_SC(v)) {
-          const float val = fminf(d * c_inv_dv, kBelowOne);
-          atomicMin(&s_min[warp][t][tj * VG_SC(v) + k], __float_as_uint(val));
-        }
+        const bool vis = (unsigned)k < (unsigned)VG_SC(v) && !self;
+        // Branch-free update: an invisible pair applies the no-op min(x, ~0) to slot 0.
+        const uint32_t val = vis ? __float_as_uint(fminf(d * c_inv_dv, kBelowOne)) : 0xffffffffu;
+        red_min(srow + (uint32_t)(t * kMaxViewSlots * 4) +
+                             (uint32_t)(tj * VG_SC(v) + (vis ? k : 0)) * 4u, val);
+      }
+    };
+
+    // Pair pass over one queue entry of EACH query (sector vision / reward only, NQ = 2):
+    // entry e0 of query 0 and e1 of query 1 in the two halves of packed fp32 pairs, so the
+    // line pair of f, the bearing, the atan2 polynomial, the sector coordinate and d / d_v
+    // take one FFMA2 / FMUL2 / FADD2 for both (v19).  Every half is the
+    // same IEEE operation as `process` on that entry, so the outputs are bitwise those of
+    // the scalar pass.  v0 / v1: the lane holds an entry of that query.
+    auto process2 = [&](const float4 e0, const float4 e1, const bool v0, const bool v1) {
+      const uint32_t w0 = __float_as_uint(e0.w), w1 = __float_as_uint(e1.w);
+      const uint32_t id0 = (ENV == kTag) ? (w0 & 0x7fffffffu) : w0;
+      const uint32_t id1 = (ENV == kTag) ? (w1 & 0x7fffffffu) : w1;
+      const bool ok0 = v0 && id0 != q0, ok1 = v1 && id1 != q0 + 1u;          // j != i
+      const uint32_t tj0 = (ENV == kTag) ? w0 >> 31 : 0u, tj1 = (ENV == kTag) ? w1 >> 31 : 0u;
+      const bool c0 = e0.z <= c_contact2, c1 = e1.z <= c_contact2;            // A6
+      float d0, d1;
+      asm("sqrt.approx.ftz.f32 %0, %1;" : "=f"(d0) : "f"(e0.z));
+      asm("sqrt.approx.ftz.f32 %0, %1;" : "=f"(d1) : "f"(e1.z));
+      const f32x2 dd = pk2(d0, d1);
+      // Eq. 1 / Fig. 4 (A5) in fixed-point units (A16b): contact -> -c_collide, else the tent.
+      const f32x2 rise = fma2(bc2(c_k_rise), dd, bc2(c_b_rise));
+      const f32x2 fall = fma2(bc2(c_nk_fall), dd, bc2(c_b_fall));
+      const float f0 = c0 ? c_mcollide : fminf(lo2(rise), lo2(fall));
+      const float f1 = c1 ? c_mcollide : fminf(hi2(rise), hi2(fall));
+      if (ENV == kFlock) {
+        if (ok0) { rs[0] += __float2ll_rn(f0); ncol[0] += c0 ? 1u : 0u; }
+        if (ok1) { rs[1] += __float2ll_rn(f1); ncol[1] += c1 ? 1u : 0u; }
+      } else {
+        if (ok0 && c0) { if (tj0 == tq[0]) ++ncol[0]; else ++ntouch[0]; }
+        if (ok1 && c1) { if (tj1 == tq[1]) ++ncol[1]; else ++ntouch[1]; }
+        const f32x2 wf = mul2(bc2(VG_SC(w_prox)), pk2(f0, f1));
+        if (ok0 && tq[0] == 0u && tj0 == 0u) rs[0] += __float2ll_rn(lo2(wf));
+        if (ok1 && tq[1] == 0u && tj1 == 0u) rs[1] += __float2ll_rn(hi2(wf));
+      }
+      if (VISION) {
+        // Bearing in the agent frame (A3), CCW-positive; sector k = floor(phi v/fov + v/2).
+        const f32x2 dx = pk2(e0.x, e1.x), dy = pk2(e0.y, e1.y);
+        const f32x2 fwd = fma2(pk2(csn[0], csn[1]), dx, mul2(pk2(sn[0], sn[1]), dy));
+        const f32x2 left = fma2(pk2(csn[0], csn[1]), dy, mul2(pk2(-sn[0], -sn[1]), dx));
+        const f32x2 kk = fma2(vg_atan2x2(left, fwd), bc2(c_inv_w), bc2(c_half_v));
+        const f32x2 val = mul2(dd, bc2(c_inv_dv));
+        const int k0 = __float2int_rd(lo2(kk)), k1 = __float2int_rd(hi2(kk));
+        red_min_if(ok0 && (unsigned)k0 < (unsigned)VG_SC(v), srow + (uint32_t)(tj0 * VG_SC(v) + k0) * 4u,
+                   __float_as_uint(fminf(lo2(val), kBelowOne)));
+        red_min_if(ok1 && (unsigned)k1 < (unsigned)VG_SC(v),
+                   srow + (uint32_t)(kMaxViewSlots * 4) + (uint32_t)(tj1 * VG_SC(v) + k1) * 4u,
+                   __float_as_uint(fminf(hi2(val), kBelowOne)));
       }
     };
 
@@ -1337,10 +1529,8 @@ __global__ void __launch_bounds__(kSenseWarps * 32, (DEF && ENV == kTag) ? VG_SE
     // run axis bounds the reach along it to sqrt(r^2 - dperp^2); keys in the candidates' raw
     // frame.  A dead query (NaN) drops out of fminf / fmaxf (dperp -> 0: only ever wider).
     uint32_t my_wb = 0u, my_we = 0u;
-    float my_csx = 0.f, my_csy = 0.f, my_qsx = 0.f, my_qsy = 0.f;
     if (lane < nseg) {
       const Seg sg = s_seg[lane];
-      my_csx = sg.csx; my_csy = sg.csy; my_qsx = sg.qsx; my_qsy = sg.qsy;
       float amin = 3.0e38f, amax = -3.0e38f, dperp = 3.0e38f;
 #pragma unroll
       for (int t = 0; t < NQ; ++t) {
@@ -1372,10 +1562,13 @@ __global__ void __launch_bounds__(kSenseWarps * 32, (DEF && ENV == kTag) ? VG_SE
       const uint32_t wb = __shfl_sync(kFull, my_wb, sgi), we = __shfl_sync(kFull, my_we, sgi);
       if (wb >= we) continue;                                        // warp-uniform
       Seg sg;
-      sg.csx = __shfl_sync(kFull, my_csx, sgi);
-      sg.csy = __shfl_sync(kFull, my_csy, sgi);
-      sg.qsx = __shfl_sync(kFull, my_qsx, sgi);
-      sg.qsy = __shfl_sync(kFull, my_qsy, sgi);
+      {                                     // the run's image shifts: one broadcast load
+        const float4 sh = *reinterpret_cast<const float4*>(&s_seg[sgi]);
+        sg.csx = sh.x;
+        sg.csy = sh.y;
+        sg.qsx = sh.z;
+        sg.qsy = sh.w;
+      }
       float qx[NQ], qy[NQ];
 #pragma unroll
       for (int t = 0; t < NQ; ++t) {
@@ -1386,10 +1579,26 @@ __global__ void __launch_bounds__(kSenseWarps * 32, (DEF && ENV == kTag) ? VG_SE
         // Ballot the in-radius candidates of one 32-slot half and append them to each
         // query's ring (dx, dy, d^2, index | type << 31).
         auto scan = [&](const float cx_, const float cy_, const uint32_t word) {
+          // PAIRED: dx, dy, d^2 of both queries as packed pairs (FADD2 with the candidate
+          // broadcast, FMUL2, FFMA2), bitwise the scalar fmaf(dx, dx, dy * dy).
+          f32x2 dx2 = 0ull, dy2 = 0ull, dd2 = 0ull;
+          if (PACKED_SCAN) {
+            dx2 = sub2(bc2(cx_), pk2(qx[0], qx[NQ - 1]));
+            dy2 = sub2(bc2(cy_), pk2(qy[0], qy[NQ - 1]));
+            dd2 = fma2(dx2, dx2, mul2(dy2, dy2));
+          }
 #pragma unroll
           for (int t = 0; t < NQ; ++t) {
-            const float dx = cx_ - qx[t], dy = cy_ - qy[t];
-            const float d2 = fmaf(dx, dx, dy * dy);
+            float dx, dy, d2;
+            if (PACKED_SCAN) {
+              dx = t ? hi2(dx2) : lo2(dx2);
+              dy = t ? hi2(dy2) : lo2(dy2);
+              d2 = t ? hi2(dd2) : lo2(dd2);
+            } else {
+              dx = cx_ - qx[t];
+              dy = cy_ - qy[t];
+              d2 = fmaf(dx, dx, dy * dy);
+            }
             const bool in = d2 < (RAY ? VG_SC(cand2) : VG_SC(dv2));                // Eq. 1: d < d_v
             const unsigned bal = __ballot_sync(kFull, in);
             if (in)
@@ -1421,23 +1630,57 @@ __global__ void __launch_bounds__(kSenseWarps * 32, (DEF && ENV == kTag) ? VG_SE
         for (int h = 0; h < kSenseHalves; ++h)
           if (h == 0 || p0 + 32u * h < we) scan(cxh[h], cyh[h], wh[h]);   // warp-uniform
         __syncwarp();                       // ring pushes above are visible to the warp
+        if (PAIRED) {
+          // Full batches of both queries together (process2); a query's ring is drained
+          // alone only when it holds >= 64 entries, so each ring carries <= 63 into the
+          // next chunk (63 + 32 kSenseHalves <= kQueue - 1).
+          while (tail[0] - head[0] >= 32u * 16u && tail[1] - head[1] >= 32u * 16u) {
+            process2(lds128(qbase[0] | ((head[0] + lane * 16u) & (kQueue * 16 - 16))),
+                     lds128(qbase[1] | ((head[1] + lane * 16u) & (kQueue * 16 - 16))), true, true);
+            head[0] += 32u * 16u;
+            head[1] += 32u * 16u;
+          }
 #pragma unroll
-        for (int t = 0; t < NQ; ++t) {
-          while (tail[t] - head[t] >= 32u * 16u) {
-            process(t, lds128(qbase[t] | ((head[t] + lane * 16u) & (kQueue * 16 - 16))));
-            head[t] += 32u * 16u;
+          for (int t = 0; t < NQ; ++t) {
+            while (tail[t] - head[t] >= 64u * 16u) {
+              process(t, lds128(qbase[t] | ((head[t] + lane * 16u) & (kQueue * 16 - 16))));
+              head[t] += 32u * 16u;
+            }
+          }
+        } else {
+#pragma unroll
+          for (int t = 0; t < NQ; ++t) {
+            while (tail[t] - head[t] >= 32u * 16u) {
+              process(t, lds128(qbase[t] | ((head[t] + lane * 16u) & (kQueue * 16 - 16))));
+              head[t] += 32u * 16u;
+            }
           }
         }
         // Drained slots may be rewritten by the next chunk's pushes unless the ring holds
-        // 31 carried + a chunk + 2 x 32 entries.
-        if (31 + 32 * kSenseHalves + 64 > kQueue) __syncwarp();
+        // the carried entries + a chunk + 2 x 32 entries.
+        if ((PAIRED ? 63 : 31) + 32 * kSenseHalves + 64 > kQueue) __syncwarp();
       }
     }
     __syncwarp();
+    if (PAIRED) {
+      // The last (partial) batches of both queries together; lanes past a ring's end hold
+      // no entry of that query (v0 / v1 false: nothing is accumulated or stored).
+      int n0 = (int)(tail[0] - head[0]) >> 4, n1 = (int)(tail[1] - head[1]) >> 4;
+      while (n0 > 0 || n1 > 0) {                                     // warp-uniform
+        process2(lds128(qbase[0] | ((head[0] + lane * 16u) & (kQueue * 16 - 16))),
+                 lds128(qbase[1] | ((head[1] + lane * 16u) & (kQueue * 16 - 16))),
+                 lane < n0, lane < n1);
+        head[0] += 32u * 16u;
+        head[1] += 32u * 16u;
+        n0 -= 32;
+        n1 -= 32;
+      }
+    } else {
 #pragma unroll
-    for (int t = 0; t < NQ; ++t)
-      if (lane * 16u < tail[t] - head[t])
-        process(t, lds128(qbase[t] | ((head[t] + lane * 16u) & (kQueue * 16 - 16))));
+      for (int t = 0; t < NQ; ++t)
+        if (lane * 16u < tail[t] - head[t])
+          process(t, lds128(qbase[t] | ((head[t] + lane * 16u) & (kQueue * 16 - 16))));
+    }
     __syncwarp();
 
 #pragma unroll
@@ -1448,7 +1691,8 @@ __global__ void __launch_bounds__(kSenseWarps * 32, (DEF && ENV == kTag) ? VG_SE
                               : (tail[t] >> 4) - 1u;            // minus the self pair
       // Warp reductions (REDUX): the int64 reward sum as four exact 16-bit-limb partial sums
       // (no 32-bit wrap for any reward validate() admits).
-      const uint32_t nc = __reduce_add_sync(kFull, ncol[t]);
+      // the self pair's contact and -c_collide term (sector pass, see `process`), removed
+      const uint32_t nc = __reduce_add_sync(kFull, ncol[t]) - ((RAY || PAIRED) ? 0u : 1u);
       const uint32_t nt = (ENV == kTag) ? __reduce_add_sync(kFull, ntouch[t]) : 0u;
       const unsigned long long ur = (unsigned long long)rs[t];
       const uint32_t s_lo = __reduce_add_sync(kFull, (uint32_t)(ur & 0xffffu));
@@ -1458,6 +1702,10 @@ __global__ void __launch_bounds__(kSenseWarps * 32, (DEF && ENV == kTag) ? VG_SE
       long long rsum = (long long)(((unsigned long long)(long long)s_top << 48) +
                                    ((unsigned long long)s_hi << 32) +
                                    ((unsigned long long)s_mid << 16) + (unsigned long long)s_lo);
+      if (!RAY && !PAIRED) {
+        if (ENV == kFlock) rsum -= __float2ll_rn(c_mcollide);
+        else if (tq[t] == 0u) rsum -= __float2ll_rn(VG_SC(w_prox) * c_mcollide);
+      }
       if (ENV == kTag) {
         const long long tt = (long long)nt * P.touch_fix;
         rsum += (tq[t] == 1u) ? tt : -tt;                             // P:194 touch rule
@@ -1465,7 +1713,7 @@ __global__ void __launch_bounds__(kSenseWarps * 32, (DEF && ENV == kTag) ? VG_SE
       auto emit = [&](auto fast_c) {
         constexpr bool FAST = decltype(fast_c)::value;
         using idx_t = typename std::conditional<FAST, uint32_t, size_t>::type;
-        const idx_t row = SLAB ? (idx_t)(q - cs[P.G]) : (idx_t)r * (idx_t)P.N + (idx_t)perm[q];
+        const idx_t row = SLAB ? (idx_t)q : (idx_t)r * (idx_t)P.N + (idx_t)perm[q];
         if (lane == 0) {
           if (SLAB && (FAST || O.agent_id)) O.agent_id[row] = perm[q];
           if (FAST || O.reward) O.reward[row] = __ll2float_rn(rsum) * kFixInv;
@@ -1583,8 +1831,8 @@ __global__ void __launch_bounds__(256) k_slab_begin(
     Params P, Slab SL, SlabBufs B, const uint32_t* __restrict__ cell_start,
     const float4* __restrict__ sorted, const uint32_t* __restrict__ perm,
     const float2* __restrict__ actions, unsigned long long* err, volatile uint32_t* flag) {
-  const uint32_t own_b = cell_start[P.G];
-  const uint32_t n_own = cell_start[(SL.W + 1) * P.G] - own_b;
+  const uint32_t own_b = 0u;                              // owned: memory columns 0..W-1
+  const uint32_t n_own = cell_start[SL.W * P.G];
   for (uint32_t row = blockIdx.x * blockDim.x + threadIdx.x; row < n_own;
        row += gridDim.x * blockDim.x) {
     float4 s = sorted[own_b + row];
@@ -1649,18 +1897,26 @@ __global__ void __launch_bounds__(256) k_slab_unpack(SlabBufs B) {
   }
 }
 
-// Local cell ids (column-major, A16 global formula) + histogram slot of the local set.
+// Local cell ids (memory column order, A16 global formula) + histogram slot of the local
+// set, for the columns of one binning phase: 0 = interior (memory columns < W-2), 1 =
+// boundary + ghosts (>= W-2), 2 = all.  Records of the other phase get kNoCell.
+constexpr uint32_t kNoCell = 0xffffffffu;
 __global__ void __launch_bounds__(256) k_slab_keys(Params P, Slab SL, SlabBufs B,
                                                    uint32_t* __restrict__ cell_id,
                                                    uint32_t* __restrict__ slot,
-                                                   uint32_t* __restrict__ count) {
+                                                   uint32_t* __restrict__ count, int phase) {
   const uint32_t n = min(*B.n_loc, B.cap_loc);
   for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n;
        i += gridDim.x * blockDim.x) {
     const float4 s = B.loc_rec[i];
     const int gx = global_col(P, s.x), gy = global_col(P, s.y);
     const int lcx = min((gx - SL.lo + 1 + P.G) % P.G, SL.W + 1);
-    const uint32_t c = (uint32_t)(lcx * P.G + gy);
+    const int m = slab_mcol(lcx, SL.W);
+    if (phase != 2 && (m < SL.W - 2) != (phase == 0)) {
+      cell_id[i] = kNoCell;
+      continue;
+    }
+    const uint32_t c = (uint32_t)(m * P.G + gy);
     cell_id[i] = c;
     // The local set is in the previous sense order (cell-major), so a warp's agents share
     // few cells: one atomic per cell group (match_any), slots by lane rank within it.
@@ -1680,12 +1936,16 @@ __global__ void __launch_bounds__(256) k_slab_scatter(Params P, SlabBufs B,
                                                       const uint32_t* __restrict__ cell_start,
                                                       float4* __restrict__ tmp_rec,
                                                       uint32_t* __restrict__ tmp_id,
-                                                      uint32_t* __restrict__ work_n) {
-  if (blockIdx.x == 0 && threadIdx.x == 0) *work_n = 0u;   // K3b appends the K4 items next
+                                                      uint32_t* __restrict__ work_n,
+                                                      int reset_work) {
+  // K3b appends the K4 items next (the boundary phase keeps the interior phase's items)
+  if (reset_work && blockIdx.x == 0 && threadIdx.x == 0) *work_n = 0u;
   const uint32_t n = min(*B.n_loc, B.cap_loc);
   for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n;
        i += gridDim.x * blockDim.x) {
-    const uint32_t pos = cell_start[cell_id[i]] + slot[i];
+    const uint32_t c = cell_id[i];
+    if (c == kNoCell) continue;                              // the other binning phase's
+    const uint32_t pos = cell_start[c] + slot[i];
     float4 s = B.loc_rec[i];
     const uint32_t id = B.loc_id[i];
     if (ENV == kTag) s.w = (id >= (uint32_t)P.first_chaser) ? 1.f : 0.f;

@@ -128,6 +128,12 @@ __device__ __forceinline__ void tma_load_1d(uint32_t dst, const void* src, uint3
 #ifndef VG_TANH_NEWTON
 #define VG_TANH_NEWTON 1
 #endif
+// Hidden-layer tanh: 0 = tanh_fast (fp32, ~2e-7, then rounded to the fp16 operand),
+// 1 = tanh.approx.f32 (one MUFU), 2 = tanh.approx.f16x2 on the fp16-rounded pre-activation
+// (one MUFU per two units; the result is the fp16 operand itself).
+#ifndef VG_TANH_MODE
+#define VG_TANH_MODE 0
+#endif
 __device__ __forceinline__ float tanh_fast(float x) {
 #if VG_TANH_NEWTON
   // One MUFU op: e = 2^(-2|x| log2 e) in (0, 1], y = 1 + e in (1, 2], 1/y from a linear
@@ -235,9 +241,13 @@ __device__ __forceinline__ void group_sync(int g) {      // named barrier of one
   asm volatile("bar.sync %0, %1;" ::"r"(1 + g), "r"(kPolGroup) : "memory");
 }
 
+// Row classes (per-type policies): with cls_period > 0, row r is of class
+// ((r mod cls_period) >= cls_split) and only rows of class `cls` are written (the tiles are
+// all computed: a tag world's runner and chaser rows share tiles at every replica edge).
 __global__ void __launch_bounds__(kPolThreads, 1) k_policy(
     const float* __restrict__ obs, int64_t M, int obs_dim, PolicyPacked pk, PolicyOut out,
-    uint32_t seed_lo, uint32_t seed_hi, uint32_t step_lo, uint32_t step_hi) {
+    uint32_t seed_lo, uint32_t seed_hi, uint32_t step_lo, uint32_t step_hi,
+    int64_t cls_period, int64_t cls_split, int cls) {
   extern __shared__ __align__(1024) unsigned char smem[];
   __half* sB1 = reinterpret_cast<__half*>(smem + kOffB1);
   __half* sB2 = reinterpret_cast<__half*>(smem + kOffB2);
@@ -327,14 +337,33 @@ __global__ void __launch_bounds__(kPolThreads, 1) k_policy(
 #pragma unroll
       for (int q = 0; q < 4; ++q) {
         const int c0 = cb + 8 * q;
+        uint4 pkd;
+#if VG_TANH_MODE == 2
+        // The activation feeds an fp16 operand: z + b rounded to fp16 pairs, then one
+        // packed MUFU tanh.approx.f16x2 per two units (test_policy bound).
+        uint32_t hz[4];
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          const uint32_t zz = h2_bits(__floats2half2_rn(v[8 * q + 2 * e] + bias[c0 + 2 * e],
+                                                        v[8 * q + 2 * e + 1] + bias[c0 + 2 * e + 1]));
+          asm("tanh.approx.f16x2 %0, %1;" : "=r"(hz[e]) : "r"(zz));
+        }
+        pkd.x = hz[0]; pkd.y = hz[1]; pkd.z = hz[2]; pkd.w = hz[3];
+#else
         float t[8];
 #pragma unroll
-        for (int e = 0; e < 8; ++e) t[e] = tanh_fast(v[8 * q + e] + bias[c0 + e]);
-        uint4 pkd;
+        for (int e = 0; e < 8; ++e) {
+#if VG_TANH_MODE == 1
+          asm("tanh.approx.f32 %0, %1;" : "=f"(t[e]) : "f"(v[8 * q + e] + bias[c0 + e]));
+#else
+          t[e] = tanh_fast(v[8 * q + e] + bias[c0 + e]);
+#endif
+        }
         pkd.x = h2_bits(__floats2half2_rn(t[0], t[1]));
         pkd.y = h2_bits(__floats2half2_rn(t[2], t[3]));
         pkd.z = h2_bits(__floats2half2_rn(t[4], t[5]));
         pkd.w = h2_bits(__floats2half2_rn(t[6], t[7]));
+#endif
         *reinterpret_cast<uint4*>(sA + cm_offset(erow, c0, kPolTile)) = pkd;
       }
     }
@@ -403,7 +432,8 @@ __global__ void __launch_bounds__(kPolThreads, 1) k_policy(
       float o[4];
       tmem_ld4(tmem + tlane + 128u, o);
       const int64_t gr = m0 + erow;
-      if (gr < M) {
+      const bool mine = cls_period <= 0 || ((gr % cls_period) >= cls_split) == (cls == 1);
+      if (gr < M && mine) {
         const float mu0 = o[0] + sC[256], mu1 = o[1] + sC[257];
         if (out.value) out.value[gr] = o[2] + sC[258];
         if (out.mean) { out.mean[2 * gr] = mu0; out.mean[2 * gr + 1] = mu1; }

@@ -51,7 +51,10 @@ class Policy:
         return {"mean": z(rows, 2), "value": z(rows), "action": z(rows, 2) if sample else None,
                 "logp": z(rows) if sample else None}
 
-    def forward(self, obs: torch.Tensor, out: dict, seed: int = 0, step: int = 0) -> None:
+    def forward(self, obs: torch.Tensor, out: dict, seed: int = 0, step: int = 0,
+                row_class: tuple | None = None) -> None:
+        """vg_policy_forward; ``row_class`` = (period, split, cls) writes only the rows r
+        with ((r mod period) >= split) == cls (vg_policy_forward_class: per-type policies)."""
         rows = obs.numel() // self.obs_dim
         if obs.dtype != torch.float32 or obs.device != self.device or not obs.is_contiguous() \
                 or obs.numel() != rows * self.obs_dim:
@@ -63,9 +66,11 @@ class Policy:
                                   t.numel() < rows * (2 if k in ("mean", "action") else 1)):
                 raise ValueError(f"{k}: float32 CUDA tensor with enough rows required")
             setattr(o, k, None if t is None else t.data_ptr())
-        check(_lib.lib.vg_policy_forward(self._h, obs.data_ptr(), rows, byref(o),
-                                         ctypes.c_uint64(seed), ctypes.c_uint64(step),
-                                         torch.cuda.current_stream(self.device).cuda_stream))
+        period, split, cls = row_class if row_class is not None else (0, 0, 0)
+        check(_lib.lib.vg_policy_forward_class(self._h, obs.data_ptr(), rows, int(period),
+                                               int(split), int(cls), byref(o),
+                                               ctypes.c_uint64(seed), ctypes.c_uint64(step),
+                                               torch.cuda.current_stream(self.device).cuda_stream))
 
     def close(self) -> None:
         if self._h:

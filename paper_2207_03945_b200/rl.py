@@ -79,20 +79,26 @@ def opinion_step(row_ptr, col, weight, op_in, op_out, threshold: float, strength
 
 
 def rollout(world, policy, state: torch.Tensor, buf: TrajectoryBuffer, seed: int = 0,
-            step0: int = 0, gamma: float = 0.99, lam: float = 0.95) -> None:
+            step0: int = 0, gamma: float = 0.99, lam: float = 0.95,
+            policy_chaser=None) -> None:
     """vg_rollout: t steps of the paper's experience-collection loop (Fig. 5) on device.
-    buf.obs[0] must hold the current observation (e.g. from world.bin + world.sense)."""
+    buf.obs[0] must hold the current observation (e.g. from world.bin + world.sense).
+    Tag worlds: ``policy_chaser`` gives the chasers their own policy, ``policy``
+    then drives the runners."""
     import ctypes
     world._check_tensor(state, "state", (world.R, world.N, 4))
     if buf.obs.device != state.device:
         raise ValueError(f"trajectory buffer on {buf.obs.device}, state on {state.device}")
-    if getattr(policy, "device", state.device) != state.device:
-        raise ValueError(f"policy on {policy.device}, state on {state.device}")
+    for pl in (policy, policy_chaser):
+        if pl is not None and getattr(pl, "device", state.device) != state.device:
+            raise ValueError(f"policy on {pl.device}, state on {state.device}")
     b = _lib.VgRolloutBuffers(buf.obs.data_ptr(), buf.action.data_ptr(), buf.logp.data_ptr(),
                               buf.reward.data_ptr(), buf.value.data_ptr(), buf.adv.data_ptr(),
                               buf.ret.data_ptr())
     if buf.n != world.R * world.N or buf.obs.shape[2] != world.obs_dim:
         raise ValueError("trajectory buffer does not match the world")
-    check(_lib.lib.vg_rollout(world._h, policy._h, state.data_ptr(), ctypes.byref(b), buf.t,
+    check(_lib.lib.vg_rollout(world._h, policy._h,
+                              policy_chaser._h if policy_chaser is not None else None,
+                              state.data_ptr(), ctypes.byref(b), buf.t,
                               ctypes.c_uint64(seed), ctypes.c_uint64(step0), gamma, lam,
                               _stream(state)))

@@ -90,3 +90,53 @@ def test_rollout_graph_capture(cuda):
     for k, v in eager.items():
         assert torch.equal(getattr(buf, k), v), k
     w.close(); pol.close()
+
+
+def test_rollout_tag_per_type_policies(cuda):
+    # "In the tag environment, the runner and chaser types share independent
+    # policies" — runners act with one weight set, chasers with another; each row's value,
+    # action and log-prob equal the single-policy forward of its own type's weights (the
+    # same calls one by one, bit for bit), and differ from the other type's.
+    import torch
+    from paper_2207_03945_b200 import rl
+    from paper_2207_03945_b200.policy import Policy, action_box
+    p = vi.tag_params(3000, n_replicas=2)
+    t = 3
+    w, pol, buf, st = _setup(p, t)
+    pc = Policy(w.obs_dim, *action_box(p))
+    pc.set_weights(vi.policy_weights(w.obs_dim, seed=5, log_std=-1.3))
+    st_manual, obs0 = st.clone(), buf.obs[0].clone()
+    rl.rollout(w, pol, st, buf, seed=4, step0=7, policy_chaser=pc)
+    torch.cuda.synchronize()
+    M, N, nc = p.total_agents, p.n_agents, p.n_chasers
+    chaser = (torch.arange(M, device="cuda") % N) >= N - nc
+    obs = obs0
+    for k in range(t):
+        outs = []
+        for pl in (pol, pc):
+            po = {"mean": None, "value": torch.empty(M, device="cuda"),
+                  "action": torch.empty(M, 2, device="cuda"), "logp": torch.empty(M, device="cuda")}
+            pl.forward(obs.contiguous(), po, seed=4, step=7 + k)
+            outs.append(po)
+        for key, dst in (("value", buf.value[k]), ("action", buf.action[k]), ("logp", buf.logp[k])):
+            ref = torch.where(chaser.view(-1, *([1] * (outs[0][key].dim() - 1))),
+                              outs[1][key], outs[0][key])
+            assert torch.equal(dst, ref), (k, key)
+            assert not torch.equal(outs[0][key][chaser], outs[1][key][chaser])
+        act = buf.action[k].view(p.n_replicas, N, 2)
+        o = w.alloc_outputs(counts=False, sector_occ=False)
+        w.step(st_manual, act.contiguous(), o)
+        obs = o.obs.view(M, -1)
+    torch.cuda.synchronize()
+    assert torch.equal(st, st_manual)
+    w.close(); pol.close(); pc.close()
+
+
+def test_rollout_chaser_policy_needs_tag(cuda):
+    import paper_2207_03945_b200 as vg
+    from paper_2207_03945_b200 import rl
+    p = vi.flock_params(500)
+    w, pol, buf, st = _setup(p, 2)
+    with pytest.raises(vg.VgError, match="VG_EINVAL.*tag"):
+        rl.rollout(w, pol, st, buf, policy_chaser=pol)
+    w.close(); pol.close()

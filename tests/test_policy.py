@@ -178,3 +178,27 @@ def test_policy_config_validation():
     h = ctypes.c_void_p()
     assert _lib.lib.vg_policy_create(ctypes.byref(cfg), ctypes.byref(h)) == _lib.VG_EINVAL
     assert "obs_dim" in _lib.lib.vg_last_error().decode()
+
+
+@pytest.mark.gpu
+def test_policy_row_class_writes_only_its_rows(cuda):
+    # vg_policy_forward_class: period 700, split 500 -> rows with (r mod 700) >= 500 are
+    # class 1; a class-1 call writes exactly those rows, with the values of the full call.
+    import torch
+    from paper_2207_03945_b200.policy import Policy
+    p = vi.workload("c3")
+    w = vi.policy_weights(p.obs_dim, seed=3)
+    rows = 2100
+    obs = torch.rand((rows, p.obs_dim), device="cuda")
+    pl = Policy(p.obs_dim, (-1.0, 0.0), (1.0, 1.0))
+    pl.set_weights(w)
+    full = pl.alloc(rows)
+    pl.forward(obs, full, seed=2, step=5)
+    part = {k: (torch.full_like(v, 7.0) if v is not None else None) for k, v in pl.alloc(rows).items()}
+    pl.forward(obs, part, seed=2, step=5, row_class=(700, 500, 1))
+    torch.cuda.synchronize()
+    cls1 = (torch.arange(rows, device="cuda") % 700) >= 500
+    for k in ("mean", "value", "action", "logp"):
+        assert torch.equal(part[k][cls1], full[k][cls1]), k
+        assert bool((part[k][~cls1] == 7.0).all()), k
+    pl.close()

@@ -98,7 +98,7 @@ def test_slab_config_validation():
 
 
 # ------------------------------------------------------------------------------ GPU
-def _compare_group(p, P, steps, state0, seed=0, halo=0):
+def _compare_group(p, P, steps, state0, seed=0, halo=0, interior=True):
     import torch
     import paper_2207_03945_b200 as vg
     from paper_2207_03945_b200.slab import SlabGroup
@@ -142,7 +142,7 @@ def _compare_group(p, P, steps, state0, seed=0, halo=0):
             a[0, :n] = act[0][o.agent_id[0, :n].long()]
             rows.append(a)
         rep.step(st, act, out_r)
-        grp.step(rows, outs)
+        grp.step(rows, outs, interior=interior)
         check(f"step {t}")
     grp.close()
     rep.close()
@@ -153,6 +153,33 @@ def _compare_group(p, P, steps, state0, seed=0, halo=0):
 def test_slab_bit_identical_flock(cuda, P):
     p = vi.flock_params(20000, width=200.0, d_v=10.0, grid=16)
     _compare_group(p, P, 4, vi.init_state(p, seed=3))
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("P", [2, 4])
+def test_slab_finish_runs_interior_phase(cuda, P):
+    # vg_slab_finish without a vg_slab_interior call runs the interior phase itself
+    p = vi.flock_params(20000, width=200.0, d_v=10.0, grid=16)
+    _compare_group(p, P, 2, vi.init_state(p, seed=9), interior=False)
+
+
+@pytest.mark.gpu
+def test_slab_call_order_and_step_without_comm(cuda):
+    import torch
+    import paper_2207_03945_b200 as vg
+    p = vi.flock_params(4000, width=170.0, d_v=10.0, grid=16)
+    w = vg.World(p, slab={"rank": 0, "world_size": 2})
+    out = w.alloc_outputs()
+    w.slab_load(torch.from_numpy(vi.init_state(p, seed=1)).cuda())
+    w.slab_sense(out)
+    with pytest.raises(vg.VgError, match="VG_EINVAL.*slab_begin first"):
+        w.slab_interior(out)
+    with pytest.raises(vg.VgError, match="VG_EINVAL.*slab_begin first"):
+        w.slab_finish(out)
+    a = torch.zeros((1, p.n_agents, 2), device="cuda")
+    with pytest.raises(vg.VgError, match="VG_EINVAL.*communicator"):
+        w.slab_step(a, out)
+    w.close()
 
 
 @pytest.mark.gpu
@@ -208,3 +235,80 @@ def test_slab_c5_full_size(cuda):
     # configs[4] (10^6 agents, G = 136) at P = 8 slabs: bit-identical to one world.
     p = vi.workload("c5")
     _compare_group(p, 8, 2, vi.init_state(p, seed=0))
+
+
+# ------------------------------------------------- multi-process slab step (one GPU)
+def _mp_slab_worker(rank, world, port, params, steps, seed, q):
+    """One slab rank in its own process: gloo process group, messages staged through
+    pinned host tensors (slab.HostStaging), begin -> interior -> exchange -> finish."""
+    import torch
+    import torch.distributed as dist
+    import paper_2207_03945_b200 as vg
+    from paper_2207_03945_b200 import slab
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        dev = torch.device("cuda", 0)
+        torch.cuda.set_device(dev)
+        p = params
+        w = vg.World(p, device=dev, slab={"rank": rank, "world_size": world})
+        out = w.alloc_outputs()
+        stg = slab.HostStaging(w)
+        w.slab_load(torch.from_numpy(vi.init_state(p, seed=seed)).to(dev))
+        w.slab_sense(out)
+        res = []
+        for t in range(steps):
+            act = torch.from_numpy(vi.actions(p, seed=seed, step=t)).to(dev)
+            n = w.slab_own_count()
+            a = torch.zeros((1, p.n_agents, 2), dtype=torch.float32, device=dev)
+            a[0, :n] = act[0][out.agent_id[0, :n].long()]
+            slab.slab_step_dist(w, a, out, staging=stg)
+            torch.cuda.synchronize()
+            assert w.sync_errors() == -1
+            n = w.slab_own_count()
+            keys = ["obs", "reward", "n_neigh", "n_collide", "sector_occ", "agent_id"]
+            res.append({k: getattr(out, k)[0, :n].cpu().numpy().copy() for k in keys})
+        q.put((rank, res))
+        w.close()
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("P", [2, 4])
+def test_slab_multiprocess_host_staging(cuda, P):
+    # P ranks as P processes on the one GPU, exchanging the halo through host memory (gloo;
+    # no kernel waits on another process): every agent's outputs bitwise equal to one world.
+    import torch
+    import torch.multiprocessing as mp
+    import paper_2207_03945_b200 as vg
+    p = vi.flock_params(12000, width=170.0, d_v=10.0, grid=16)
+    steps, seed = 3, 6
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_mp_slab_worker, args=(r, P, port, p, steps, seed, q))
+             for r in range(P)]
+    for pr in procs:
+        pr.start()
+    got = dict(q.get(timeout=300) for _ in range(P))
+    for pr in procs:
+        pr.join(timeout=120)
+        assert pr.exitcode == 0
+    rep = vg.World(p)
+    out = rep.alloc_outputs()
+    st = torch.from_numpy(vi.init_state(p, seed=seed)).cuda()
+    for t in range(steps):
+        rep.step(st, torch.from_numpy(vi.actions(p, seed=seed, step=t)).cuda(), out)
+        torch.cuda.synchronize()
+        seen = np.zeros(p.n_agents, np.int64)
+        for r in range(P):
+            g = got[r][t]
+            ids = g["agent_id"].astype(np.int64)
+            seen[ids] += 1
+            for k in ("obs", "reward", "n_neigh", "n_collide", "sector_occ"):
+                ref = getattr(out, k)[0].cpu().numpy()[ids]
+                assert np.array_equal(g[k].view(np.uint32), ref.view(np.uint32)), (t, r, k)
+        assert np.all(seen == 1)
+    rep.close()

@@ -1,0 +1,5 @@
+# K4 v19 (paired pair pass): GPU parity + A/B of launch-bound variants
+timeout 1200 python -m pytest tests -m gpu -x -q -p no:cacheprovider > gpurun_out/gpu_tests_r2b.log 2>&1; echo "tests rc $?"
+tail -3 gpurun_out/gpu_tests_r2b.log
+VARS="- new7 tag7" CFGS="c5 c4 c3" timeout 1200 bash tools/ab.sh > gpurun_out/ab_r2b.txt 2>&1
+cat gpurun_out/ab_r2b.txt

@@ -1,7 +1,7 @@
 """Single-GPU estimate of the slab-mode (c5 split over P ranks) per-rank step: P slab
 worlds stepped with the loopback exchange on one device (kernels of all P ranks serialised,
 so GPU time / P ~ one rank's kernels), plus the host enqueue time of one rank's
-begin + finish calls.  NCCL transfer time is not included (one GPU)."""
+begin + interior + finish calls.  NCCL transfer time is not included (one GPU)."""
 import json
 import os
 import sys
@@ -41,6 +41,7 @@ for P in (2, 4, 8):
     t0 = time.perf_counter()
     for _ in range(K):
         w.slab_begin(acts[0])
+        w.slab_interior(outs[0])
         w.slab_finish(outs[0])
     host_ms = (time.perf_counter() - t0) * 1e3 / K
     torch.cuda.synchronize()
