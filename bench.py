@@ -57,6 +57,8 @@ def parse():
                     help="bounded oracle sample for cpu_baseline (seconds of CPU work)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-c4-binning", action="store_true",
+                    help="skip the c4 binning sub-measurement of the default c5 line")
     ap.add_argument("--no-policy", action="store_true",
                     help="skip the NEXT-row measurements (policy, GAE, opinion dynamics)")
     return ap.parse_args()
@@ -482,7 +484,7 @@ def run_ours(args):
         policy = {"kernel": "k_policy (tcgen05 kind::f16, TMEM accumulators)", "rows": rows,
                   "ms": pms, "agents_per_s": rows / (pms / 1e3),
                   "tensor_TFLOPs": tfs, "tensor_frac": tfs / tf_peak,
-                  "hbm_GBps": gbs, "hbm_frac": gbs / float(pk.get("hbm_gbs", 6441.6)),
+                  "hbm_GBps": gbs, "hbm_frac": gbs / float(pk["hbm_gbs"]),
                   "limiter": "issue / SFU of the fp32-accurate tanh epilogue (ncu, DESIGN.md "
                              "6b); HBM floor = 4 obs_dim B per row"}
         pl.close()
@@ -572,9 +574,56 @@ def run_ours(args):
                   "bound": "hbm/L2 gather", "alg_bytes": obytes}
         del od, onext
 
+    # ---- north_star's HBM rule is judged on binning + integration where it is HBM-bound:
+    # c4 (1,024 replicas x 5,000; 92 algorithmic bytes per agent through the fused bin,
+    # DESIGN.md §6), measured here beside the c5 line (c5's binning is L2-resident).
+    c4_bin = None
+    if rank == 0 and world == 1 and args.config == "c5" and not args.no_c4_binning \
+            and args.vision == "sector" and STATE == "uniform":
+        q4 = vi.workload("c4")
+        w4 = vg.World(q4, device=device)
+        out4 = w4.alloc_outputs()
+        st4 = torch.from_numpy(vi.init_state(q4, seed=7)).to(device)
+        acts4 = action_pool(q4, torch, device, count=2, seed=7)
+        for k in range(max(3, args.warmup)):
+            w4.step(st4, acts4[k % 2], out4)
+        torch.cuda.synchronize()
+        K4 = max(3, min(K, 10))
+        w4.profile_begin(K4)
+        for k in range(K4):
+            flush.fill_(k & 0xFF)
+            w4.step(st4, acts4[k % 2], out4)
+        torch.cuda.synchronize()
+        ph4, n4 = w4.profile_end()
+        w4.sync_errors()
+        ms4 = ph4["integrate_bin"] / max(1, n4)
+        alg4 = 92 * q4.total_agents
+        pk4 = measured_peaks()[0]
+        c4_bin = {"workload": "c4", "kernel": ("k_replica_bin (persistent, shared-memory staged)"
+                                               if w4.kernels_per_step == 2 else "K1-K3b"),
+                  "what": "integrate + cell id + histogram + scan + stable scatter + sense order",
+                  "ms": ms4, "alg_bytes": alg4, "bytes_per_agent": 92,
+                  "GBps": alg4 / (ms4 / 1e3) / 1e9,
+                  "hbm_frac": alg4 / (ms4 / 1e3) / 1e9 / float(pk4["hbm_gbs"]),
+                  "steps": n4}
+        cp = os.path.join(ROOT, "profiles", "stage_traffic_c4.json")
+        if os.path.exists(cp):
+            try:
+                cj = json.load(open(cp))
+                c4_bin["ncu"] = {k2: cj[k2] for k2 in ("kernel", "dram_read_B", "dram_write_B",
+                                                       "ncu_us") if k2 in cj}
+                c4_bin["ncu"]["dram_over_alg"] = round(
+                    (cj["dram_read_B"] + cj["dram_write_B"]) / alg4, 3)
+                c4_bin["ncu"]["source"] = "profiles/stage_traffic_c4.json"
+            except Exception:
+                pass
+        w4.close()
+        del out4, st4, acts4
+        torch.cuda.empty_cache()
+
     if rank == 0:
         peaks, peak_src = measured_peaks()
-        hbm = float(peaks.get("hbm_gbs", 6441.6))
+        hbm = float(peaks["hbm_gbs"])
         sm_mhz = float(peaks.get("sm_max_mhz", 1965.0))
         alu_peak = 148 * 128 * sm_mhz * 1e6 / 1e12      # fp32 lane-ops/s, TFLOP/s-equivalent
         # K4 time: slab mode senses in two launches (the interior phase, which also bins
@@ -627,16 +676,21 @@ def run_ours(args):
                 continue
             avg = ms / nrec
             gbs = stage_bytes[k2] / (avg / 1e3) / 1e9 if avg > 0 else None
+            # algorithmic bytes / time against the HBM peak: an upper-bound view of the
+            # stage; where the committed ncu capture shows most of those bytes never
+            # reached DRAM (L2-resident at this size), it is not an HBM fraction
             stages[run.phase_names[k2]] = {
                 "ms": round(avg, 5), "alg_bytes": stage_bytes[k2],
-                "GBps": round(gbs, 1) if gbs else None,
-                "hbm_frac": round(gbs / hbm, 4) if gbs else None,
-                "hbm_frac_spec": round(gbs / HBM_SPEC_GBS, 4) if gbs else None,
+                "GBps_alg": round(gbs, 1) if gbs else None,
+                "alg_GBps_over_hbm_peak": round(gbs / hbm, 4) if gbs else None,
                 "share": round(ms / tot_ph, 4)}
             if k2 in st_ncu:
                 n_ = st_ncu[k2]
+                dram = n_["dram_read_B"] + n_["dram_write_B"]
                 stages[run.phase_names[k2]]["ncu"] = {
                     "dram_read_B": n_["dram_read_B"], "dram_write_B": n_["dram_write_B"],
+                    "dram_over_alg": round(dram / max(1, stage_bytes[k2]), 3),
+                    "served_from": "L2" if dram < 0.5 * stage_bytes[k2] else "HBM",
                     "us": n_["ncu_us"], "kernels": n_["kernels"],
                     "source": "profiles/stage_traffic.json"}
         traffic, issue, cand_tests = None, None, None
@@ -694,6 +748,7 @@ def run_ours(args):
                                   f"in-radius pairs per launch / mean k_sense time; peak = "
                                   f"148 SM x 128 lanes x {sm_mhz:.0f} MHz (1 op/lane/clk)"},
             "stages": stages,
+            "c4_binning": c4_bin,
             "model_bound": model_bound,
             "sanity": san,
             "parity": parity_ev,

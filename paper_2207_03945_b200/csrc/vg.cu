@@ -17,6 +17,7 @@
 #include <mutex>
 
 #include <nccl.h>          // types only: libnccl is loaded at run time (NcclApi below)
+#include <nvtx3/nvToolsExt.h>   // header-only NVTX v3: no-ops unless a profiler injects itself
 
 #include "vg.h"
 #include "vg_kernels.cuh"
@@ -105,6 +106,13 @@ const char* nccl_err() { return nccl_state().err; }
       return fail(VG_ENCCL, "%s: %s", #call, nccl_api()->GetErrorString(r_));        \
   } while (0)
 
+// NVTX range over one ABI call (host enqueue; a profiler correlates it with the
+// kernels it launched): the phases of a step show up by name in nsys / ncu timelines.
+struct NvtxRange {
+  explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
+};
+
 }  // namespace
 
 struct vg_world {
@@ -114,6 +122,7 @@ struct vg_world {
   int n_cells = 0;
   bool binned = false;
   bool fused_bin = false;          // K1-K3 fused per replica (small worlds)
+  bool staged_bin = false;         // ... as the persistent TMA-staged kernel (many replicas)
   bool gather_bin = false;         // K2-K3b as one per-cell gather kernel (K3g)
   bool sense_def = false;          // K4 sector pass: the default-constant instance
   size_t scratch_bytes = 0;
@@ -397,9 +406,15 @@ template <int ENV, bool INTEGRATE>
 vg_status launch_fused_bin(vg_world* w, float4* io, const float4* in, const float2* act,
                            cudaStream_t s) {
   VG_CUDA(cudaMemsetAsync(w->work_cnt, 0, sizeof(uint32_t), s));   // replica CTAs append items
-  vg::k_replica_bin<ENV, INTEGRATE><<<w->P.R, vg::kRBThreads, 0, s>>>(
-      w->P, io, in, act, w->cell_id, w->cell_start, w->sorted, w->perm, w->xo_rec, w->xo_perm,
-      w->xo_xy, w->sub_tab, work_list(w), w->err_dev, w->err_flag);
+  if (w->staged_bin)            // persistent, TMA-staged: one CTA per SM
+    vg::k_replica_bin<ENV, INTEGRATE, true><<<(unsigned)std::min(w->P.R, w->n_sm), vg::kRBThreads,
+                                                vg::kRBStagedSmem, s>>>(
+        w->P, io, in, act, w->cell_id, w->cell_start, w->sorted, w->perm, w->xo_rec, w->xo_perm,
+        w->xo_xy, w->sub_tab, work_list(w), w->err_dev, w->err_flag);
+  else
+    vg::k_replica_bin<ENV, INTEGRATE, false><<<w->P.R, vg::kRBThreads, 0, s>>>(
+        w->P, io, in, act, w->cell_id, w->cell_start, w->sorted, w->perm, w->xo_rec, w->xo_perm,
+        w->xo_xy, w->sub_tab, work_list(w), w->err_dev, w->err_flag);
   if (vg_status st = launch_check("k_replica_bin")) return st;
   w->binned = true;
   return VG_OK;
@@ -505,6 +520,14 @@ bool sense_defaults_match(const vg::Params& P) {
 void set_kernel_attributes() {
   cudaFuncSetAttribute(vg::k_scan_cells, cudaFuncAttributeMaxDynamicSharedMemorySize,
                        vg::kScanSmallMax * 4);
+  cudaFuncSetAttribute(vg::k_replica_bin<vg::kFlock, true, true>,
+                       cudaFuncAttributeMaxDynamicSharedMemorySize, vg::kRBStagedSmem);
+  cudaFuncSetAttribute(vg::k_replica_bin<vg::kFlock, false, true>,
+                       cudaFuncAttributeMaxDynamicSharedMemorySize, vg::kRBStagedSmem);
+  cudaFuncSetAttribute(vg::k_replica_bin<vg::kTag, true, true>,
+                       cudaFuncAttributeMaxDynamicSharedMemorySize, vg::kRBStagedSmem);
+  cudaFuncSetAttribute(vg::k_replica_bin<vg::kTag, false, true>,
+                       cudaFuncAttributeMaxDynamicSharedMemorySize, vg::kRBStagedSmem);
   sense_carveouts<vg::kFlock, true, false>();
   sense_carveouts<vg::kFlock, true, true>();
   sense_carveouts<vg::kTag, true, false>();
@@ -669,6 +692,11 @@ vg_status vg_world_create(const vg_config* cfg, vg_world** out) {
                  cfg->n_agents <= vg::kRBMaxAgents &&
                  (cfg->n_replicas >= 64 ||
                   (cfg->n_agents <= VG_FUSED_SINGLE_MAX && !gather_ok));
+  {                                // VG_RB_STAGED=0: the one-CTA-per-replica fused bin (tests)
+    const char* sg = std::getenv("VG_RB_STAGED");
+    w->staged_bin = w->fused_bin && cfg->n_agents <= vg::kRBStagedMax &&
+                    cfg->n_replicas >= w->n_sm && !(sg && sg[0] == '0');
+  }
   {                                // VG_SENSE_GENERIC=1: always the generic instance (tests)
     const char* gen = std::getenv("VG_SENSE_GENERIC");
     w->sense_def = !(gen && gen[0] && gen[0] != '0') &&
@@ -834,6 +862,7 @@ vg_status vg_world_query(const vg_world* w, vg_world_info* info) {
 }
 
 vg_status vg_bin(vg_world* w, const float* state, void* stream) {
+  NvtxRange nvtx_("vg_bin");
   if (!w || !state) return fail(VG_EINVAL, "world/state: NULL");
   if (vg_status st = need_slab(w, false, "vg_bin")) return st;
   DeviceGuard dg_(w->device);
@@ -852,6 +881,7 @@ vg_status vg_bin(vg_world* w, const float* state, void* stream) {
 }
 
 vg_status vg_sense(vg_world* w, const vg_outputs* outs, void* stream) {
+  NvtxRange nvtx_("vg_sense");
   if (!w || !outs) return fail(VG_EINVAL, "world/outs: NULL");
   if (!w->binned) return fail(VG_EINVAL, "vg_sense: no binned state (call vg_bin or vg_step first)");
   DeviceGuard dg_(w->device);
@@ -860,6 +890,7 @@ vg_status vg_sense(vg_world* w, const vg_outputs* outs, void* stream) {
 }
 
 vg_status vg_reward(vg_world* w, const vg_outputs* outs, void* stream) {
+  NvtxRange nvtx_("vg_reward");
   if (!w || !outs) return fail(VG_EINVAL, "world/outs: NULL");
   if (!w->binned) return fail(VG_EINVAL, "vg_reward: no binned state (call vg_bin or vg_step first)");
   DeviceGuard dg_(w->device);
@@ -871,6 +902,7 @@ vg_status vg_reward(vg_world* w, const vg_outputs* outs, void* stream) {
 }
 
 vg_status vg_integrate(vg_world* w, float* state, const float* actions, void* stream) {
+  NvtxRange nvtx_("vg_integrate");
   if (!w || !state || !actions) return fail(VG_EINVAL, "world/state/actions: NULL");
   if (vg_status st = need_slab(w, false, "vg_integrate")) return st;
   DeviceGuard dg_(w->device);
@@ -976,6 +1008,7 @@ bool graph_ok(vg_world* w, cudaStream_t s) {
 
 vg_status vg_step(vg_world* w, float* state, const float* actions, const vg_outputs* outs,
                   void* stream) {
+  NvtxRange nvtx_("vg_step");
   if (!w || !state || !actions || !outs) return fail(VG_EINVAL, "world/state/actions/outs: NULL");
   if (vg_status st = need_slab(w, false, "vg_step")) return st;
   DeviceGuard dg_(w->device);
@@ -991,6 +1024,7 @@ vg_status vg_step(vg_world* w, float* state, const float* actions, const vg_outp
 
 vg_status vg_step_host(vg_world* w, float* state, const float* actions_host,
                        const vg_outputs* outs, float* reward_host, void* stream) {
+  NvtxRange nvtx_("vg_step_host");
   if (!w || !state || !actions_host || !outs) return fail(VG_EINVAL, "world/state/actions_host/outs: NULL");
   DeviceGuard dg_(w->device);
   if (reward_host && !outs->reward) return fail(VG_EINVAL, "reward_host: needs outs->reward");
@@ -1028,6 +1062,7 @@ vg_status vg_slab_plan(int32_t grid, int32_t world_size, int32_t rank, int32_t* 
 }
 
 vg_status vg_slab_load(vg_world* w, const float* state_global, void* stream) {
+  NvtxRange nvtx_("vg_slab_load");
   if (vg_status st = need_slab(w, true, "vg_slab_load")) return st;
   DeviceGuard dg_(w->device);
   if (!state_global) return fail(VG_EINVAL, "state_global: NULL");
@@ -1066,6 +1101,7 @@ vg_status slab_begin_launch(vg_world* w, const float2* a, cudaStream_t s) {
 }  // namespace
 
 vg_status vg_slab_begin(vg_world* w, const float* actions, void* stream) {
+  NvtxRange nvtx_("vg_slab_begin");
   if (vg_status st = need_slab(w, true, "vg_slab_begin")) return st;
   if (!actions) return fail(VG_EINVAL, "actions: NULL");
   if (!w->binned) return fail(VG_EINVAL, "vg_slab_begin: call vg_slab_load first");
@@ -1103,6 +1139,7 @@ vg_status vg_slab_get_io(vg_world* w, vg_slab_io* io) {
 }
 
 vg_status vg_slab_exchange_loopback(vg_world* const* ws, int32_t n, void* stream) {
+  NvtxRange nvtx_("vg_slab_exchange_loopback");
   if (!ws || n < 2) return fail(VG_EINVAL, "vg_slab_exchange_loopback: need >= 2 worlds");
   for (int g = 0; g < n; ++g) {
     if (vg_status st = need_slab(ws[g], true, "vg_slab_exchange_loopback")) return st;
@@ -1178,6 +1215,7 @@ vg_status slab_finish(vg_world* w, const vg_outputs* outs, cudaStream_t s) {
 }  // namespace
 
 vg_status vg_slab_interior(vg_world* w, const vg_outputs* outs, void* stream) {
+  NvtxRange nvtx_("vg_slab_interior");
   if (vg_status st = need_slab(w, true, "vg_slab_interior")) return st;
   DeviceGuard dg_(w->device);
   if (!outs) return fail(VG_EINVAL, "outs: NULL");
@@ -1186,6 +1224,7 @@ vg_status vg_slab_interior(vg_world* w, const vg_outputs* outs, void* stream) {
 }
 
 vg_status vg_slab_finish(vg_world* w, const vg_outputs* outs, void* stream) {
+  NvtxRange nvtx_("vg_slab_finish");
   if (vg_status st = need_slab(w, true, "vg_slab_finish")) return st;
   DeviceGuard dg_(w->device);
   if (!outs) return fail(VG_EINVAL, "outs: NULL");
@@ -1197,6 +1236,7 @@ vg_status vg_slab_finish(vg_world* w, const vg_outputs* outs, void* stream) {
 }
 
 vg_status vg_slab_step(vg_world* w, const float* actions, const vg_outputs* outs, void* stream) {
+  NvtxRange nvtx_("vg_slab_step");
   if (vg_status st = need_slab(w, true, "vg_slab_step")) return st;
   if (!actions || !outs) return fail(VG_EINVAL, "actions/outs: NULL");
   if (!w->comm)
@@ -1238,6 +1278,7 @@ vg_status vg_nccl_unique_id(void* out, int32_t nbytes) {
 }
 
 vg_status vg_slab_sense(vg_world* w, const vg_outputs* outs, void* stream) {
+  NvtxRange nvtx_("vg_slab_sense");
   if (vg_status st = need_slab(w, true, "vg_slab_sense")) return st;
   if (!outs) return fail(VG_EINVAL, "outs: NULL");
   if (!w->binned) return fail(VG_EINVAL, "vg_slab_sense: call vg_slab_load first");
@@ -1324,6 +1365,7 @@ vg_status vg_policy_forward_class(vg_policy* p, const float* obs, int64_t rows,
                                   int64_t period, int64_t split, int32_t cls,
                                   const vg_policy_outputs* outs, uint64_t seed, uint64_t step,
                                   void* stream) {
+  NvtxRange nvtx_("vg_policy_forward_class");
   if (!p || !obs || !outs) return fail(VG_EINVAL, "policy/obs/outs: NULL");
   if (!p->have_weights) return fail(VG_EINVAL, "vg_policy_forward: call vg_policy_set_weights first");
   if (rows < 0) return fail(VG_EINVAL, "rows: must be >= 0");
@@ -1348,6 +1390,7 @@ vg_status vg_policy_forward(vg_policy* p, const float* obs, int64_t rows,
 
 vg_status vg_gae(const float* reward, const float* value, int64_t n, int32_t t, float gamma,
                  float lambda, float* adv, float* ret, void* stream) {
+  NvtxRange nvtx_("vg_gae");
   if (!reward || !value || !adv || !ret) return fail(VG_EINVAL, "vg_gae: NULL pointer");
   if (n < 0 || t < 1) return fail(VG_EINVAL, "vg_gae: need n >= 0 and t >= 1");
   if (!(gamma >= 0.f && gamma <= 1.f) || !(lambda >= 0.f && lambda <= 1.f))
@@ -1362,6 +1405,7 @@ vg_status vg_gae(const float* reward, const float* value, int64_t n, int32_t t, 
 vg_status vg_opinion_step(const int32_t* row_ptr, const int32_t* col, const float* weight,
                           int32_t n, int64_t n_edges, const float* op_in, float* op_out,
                           float threshold, float strength, void* stream) {
+  NvtxRange nvtx_("vg_opinion_step");
   if (!row_ptr || !op_in || !op_out) return fail(VG_EINVAL, "vg_opinion_step: NULL pointer");
   if (n < 0) return fail(VG_EINVAL, "vg_opinion_step: n must be >= 0");
   if (n_edges < 0 || n_edges > INT32_MAX) return fail(VG_EINVAL, "vg_opinion_step: n_edges must be in [0, 2^31)");
@@ -1390,6 +1434,7 @@ vg_status vg_opinion_sync_errors(void* stream, int64_t* bad_node) {
 vg_status vg_rollout(vg_world* w, vg_policy* pol, vg_policy* pol_chaser, float* state,
                      const vg_rollout_buffers* b, int32_t t, uint64_t seed, uint64_t step0,
                      float gamma, float lambda, void* stream) {
+  NvtxRange nvtx_("vg_rollout");
   if (!w || !pol || !state || !b) return fail(VG_EINVAL, "vg_rollout: NULL argument");
   if (pol_chaser && w->P.env != vg::kTag) return fail(VG_EINVAL, "vg_rollout: pol_chaser needs a tag world");
   if (pol_chaser && pol_chaser->cfg.obs_dim != w->P.obs_dim)

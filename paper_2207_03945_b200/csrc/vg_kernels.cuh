@@ -399,19 +399,21 @@ __device__ __forceinline__ unsigned bin_lanes(const unsigned (&bits)[kSubBits], 
 
 // Sense order of one cell from its stable (id-ordered) records [b, b + m): a stable counting
 // sort by sub-bin, one warp.  Writes xo_* and the cell's kSub table entries.
+// The cell's records are read from sorted[rb ..] / perm[rb ..] (rb = b, or a shared-memory
+// staging copy) and written to xo_*[b ..].
 __device__ __forceinline__ void sense_order_cell(const Params& P, int ca, bool axis_y,
                                                  uint32_t b, int m,
                                                  const float4* sorted, const uint32_t* perm,
                                                  float4* __restrict__ xo_rec,
                                                  uint32_t* __restrict__ xo_perm,
                                                  float2* __restrict__ xo_xy, uint32_t* tab,
-                                                 int lane, unsigned lt) {
+                                                 int lane, unsigned lt, uint32_t rb) {
   uint32_t cnt = 0;                                       // lane s < kSub: records in sub-bin s
   for (int ib = 0; ib < m; ib += 32) {
     const bool valid = ib + lane < m;
     int sb = 0;
     if (valid) {
-      const float4 rec = sorted[b + ib + lane];
+      const float4 rec = sorted[rb + ib + lane];
       sb = sub_bin(P, ca, axis_y ? rec.y : rec.x);
     }
     unsigned bits[kSubBits];
@@ -433,8 +435,8 @@ __device__ __forceinline__ void sense_order_cell(const Params& P, int ca, bool a
     uint32_t id = 0u;
     int sb = 0;
     if (valid) {
-      rec = sorted[b + ib + lane];
-      id = perm[b + ib + lane];
+      rec = sorted[rb + ib + lane];
+      id = perm[rb + ib + lane];
       sb = sub_bin(P, ca, axis_y ? rec.y : rec.x);
     }
     unsigned bits[kSubBits];
@@ -577,7 +579,7 @@ __global__ void __launch_bounds__(256) k_cell_sort(
   unsigned lt;
   asm("mov.u32 %0, %%lanemask_lt;" : "=r"(lt));
   sense_order_cell(P, cell % P.G, axis_y != 0, b, m, sorted, perm, xo_rec, xo_perm, xo_xy,
-                   sub_tab + (size_t)cell * kSub, lane, lt);
+                   sub_tab + (size_t)cell * kSub, lane, lt, b);
 }
 
 // K3b, one CTA per cell (worlds with few, populous cells that K3g does not take — N above
@@ -629,7 +631,7 @@ __global__ void __launch_bounds__(kCtaSortThreads) k_cell_sort_cta(
     unsigned lt;
     asm("mov.u32 %0, %%lanemask_lt;" : "=r"(lt));
     sense_order_cell(P, ca, axis_y != 0, b, m, sorted, perm, xo_rec, xo_perm, xo_xy,
-                     sub_tab + (size_t)cell * kSub, lane, lt);
+                     sub_tab + (size_t)cell * kSub, lane, lt, b);
     return;
   }
   if (tid < kSub) s_cnt[tid] = 0u;
@@ -785,7 +787,7 @@ __global__ void __launch_bounds__(kGatherThreads) k_cell_gather(
       unsigned lt;
       asm("mov.u32 %0, %%lanemask_lt;" : "=r"(lt));
       sense_order_cell(P, ca, false, start, m, sorted, perm, xo_rec, xo_perm, xo_xy,
-                       sub_tab + (size_t)gc * kSub, lane, lt);
+                       sub_tab + (size_t)gc * kSub, lane, lt, start);
     }
     return;
   }
@@ -827,13 +829,20 @@ constexpr int kRBMaxAgents = 32768;
 #ifndef VG_RB_THREADS
 #define VG_RB_THREADS 1024
 #endif
-#ifndef VG_RB_TIMING_SKIP
-#define VG_RB_TIMING_SKIP 0        // tuning builds only: 1 skips pass 3, 2 passes 2 + 3
-#endif
 constexpr int kRBThreads = VG_RB_THREADS;   // warps per replica CTA x 32; 2048 / it CTAs per SM
 
-template <int ENV, bool INTEGRATE>
-__global__ void __launch_bounds__(kRBThreads, 2048 / kRBThreads) k_replica_bin(
+// STAGED (many replicas of N <= kRBStagedMax agents, e.g. c4): a persistent kernel, one
+// CTA of 1024 threads per SM looping over replicas, with the replica staged in shared memory
+// (DESIGN.md §6): pass 1 keeps the integrated state and the cell ids there; pass 2 scatters
+// into a shared-memory copy of the cell-ordered records (no scattered global writes: they
+// were L2-transaction bound), written out to sorted / perm as one coalesced block; pass 3
+// reads the cells from that copy.  The next replica's input is prefetched into L2 while the
+// current one is processed.
+constexpr int kRBStagedMax = 5120;
+constexpr int kRBStagedSmem = kRBStagedMax * (16 + 16 + 4 + 1);   // state, sorted, perm, cell id
+
+template <int ENV, bool INTEGRATE, bool STAGED>
+__global__ void __launch_bounds__(kRBThreads, STAGED ? 1 : 2048 / kRBThreads) k_replica_bin(
     Params P, float4* __restrict__ state_io, const float4* __restrict__ state_in,
     const float2* __restrict__ actions, uint32_t* __restrict__ cell_id,
     uint32_t* __restrict__ cell_start, float4* __restrict__ sorted,
@@ -843,25 +852,44 @@ __global__ void __launch_bounds__(kRBThreads, 2048 / kRBThreads) k_replica_bin(
   constexpr int NW = kRBThreads / 32;
   __shared__ uint32_t s_wc[NW][kRBMaxCells + 1];     // per-warp counts, then offsets (+1: banks)
   __shared__ uint32_t s_tot[kRBMaxCells];
-  const int r = blockIdx.x, tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  extern __shared__ __align__(128) unsigned char rb_dyn[];   // STAGED: see kRBStagedSmem
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int N = P.N, C = P.G2;
-  const size_t base = (size_t)r * N;
   const float4* src = INTEGRATE ? state_io : state_in;
   const int span = (N + NW - 1) / NW;
   const int i0 = min(N, warp * span), i1 = min(N, i0 + span);
   unsigned lt;
   asm("mov.u32 %0, %%lanemask_lt;" : "=r"(lt));
+  float4* st = reinterpret_cast<float4*>(rb_dyn);                 // integrated, id order
+  float4* s_sorted = st + kRBStagedMax;                            // cell order
+  uint32_t* s_perm = reinterpret_cast<uint32_t*>(s_sorted + kRBStagedMax);
+  uint8_t* s_cid = reinterpret_cast<uint8_t*>(s_perm + kRBStagedMax);
+  // Ask L2 for a replica's input (state, actions) up front: the warp walks its range one
+  // 32-agent round at a time, so later rounds wait on L2, not HBM.  STAGED: the whole CTA
+  // prefetches the next replica while processing the current one.
+  auto pf = [&](const void* lo, size_t bytes, int t, int nt) {
+    const uintptr_t a0 = (uintptr_t)lo & ~(uintptr_t)127, a1 = (uintptr_t)lo + bytes;
+    for (uintptr_t a = a0 + 128u * (uintptr_t)t; a < a1; a += 128u * (uintptr_t)nt)
+      asm volatile("prefetch.global.L2 [%0];" ::"l"(a));
+  };
+  const int r_step = STAGED ? (int)gridDim.x : P.R;
+  if (STAGED && VG_RB_PREFETCH && (int)blockIdx.x < P.R) {
+    pf(src + (size_t)blockIdx.x * N, (size_t)N * sizeof(float4), tid, kRBThreads);
+    if (INTEGRATE) pf(actions + (size_t)blockIdx.x * N, (size_t)N * sizeof(float2), tid, kRBThreads);
+  }
+  for (int r = blockIdx.x; r < P.R; r += r_step) {
+  const size_t base = (size_t)r * N;
   for (int c = lane; c < C; c += 32) s_wc[warp][c] = 0u;
-  if (VG_RB_PREFETCH && i1 > i0) {
-    // The warp walks its range serially, one 32-agent load round at a time: ask L2 for the
-    // whole range (state, actions) up front, so later rounds wait on L2, not HBM.
-    auto pf = [&](const void* lo, size_t bytes) {
-      const uintptr_t a0 = (uintptr_t)lo & ~(uintptr_t)127, a1 = (uintptr_t)lo + bytes;
-      for (uintptr_t a = a0 + 128u * lane; a < a1; a += 32u * 128u)
-        asm volatile("prefetch.global.L2 [%0];" ::"l"(a));
-    };
-    pf(src + base + i0, (size_t)(i1 - i0) * sizeof(float4));
-    if (INTEGRATE) pf(actions + base + i0, (size_t)(i1 - i0) * sizeof(float2));
+  if (VG_RB_PREFETCH) {
+    if (!STAGED && i1 > i0) {
+      pf(src + base + i0, (size_t)(i1 - i0) * sizeof(float4), lane, 32);
+      if (INTEGRATE) pf(actions + base + i0, (size_t)(i1 - i0) * sizeof(float2), lane, 32);
+    }
+    if (STAGED && r + r_step < P.R) {
+      const size_t nb = (size_t)(r + r_step) * N;
+      pf(src + nb, (size_t)N * sizeof(float4), tid, kRBThreads);
+      if (INTEGRATE) pf(actions + nb, (size_t)N * sizeof(float2), tid, kRBThreads);
+    }
   }
   __syncwarp();
   // ---- pass 1: integrate + cell id + warp-private histogram
@@ -897,13 +925,15 @@ __global__ void __launch_bounds__(kRBThreads, 2048 / kRBThreads) k_replica_bin(
         s.y = wrap_pos(s.y, __fmul_rn(dist, sn), P.L);
         state_io[gi] = s;
       }
+      if (STAGED) st[i] = s;                           // pass 2 reads it back from here
       if (bad) report_bad(err, flag, (unsigned long long)gi);
       int cx = __float2int_rz(__fmul_rn(s.x, P.gs));
       int cy = __float2int_rz(__fmul_rn(s.y, P.gs));
       cx = min(max(cx, 0), P.G - 1);
       cy = min(max(cy, 0), P.G - 1);
       c = (uint32_t)(cy * P.G + cx);
-      cell_id[gi] = c;                                // re-read in pass 2 (same warp)
+      cell_id[gi] = c;
+      if (STAGED) s_cid[i] = (uint8_t)c;               // re-read in pass 2 (same warp)
     }
     const unsigned grp = __match_any_sync(kFull, c);
     if (valid && (grp & lt) == 0u) s_wc[warp][c] += __popc(grp);
@@ -947,7 +977,7 @@ __global__ void __launch_bounds__(kRBThreads, 2048 / kRBThreads) k_replica_bin(
       }
       run += v[e];
     }
-    if (r == (int)gridDim.x - 1 && lane == 0) cell_start[(size_t)P.R * C] = (uint32_t)P.total;
+    if (r == P.R - 1 && lane == 0) cell_start[(size_t)P.R * C] = (uint32_t)P.total;
     // K4 work items of this replica's cells: one atomic per replica
     uint32_t nch[8], nsum = 0;
 #pragma unroll
@@ -976,34 +1006,47 @@ __global__ void __launch_bounds__(kRBThreads, 2048 / kRBThreads) k_replica_bin(
     }
   }
   __syncthreads();
-  if (VG_RB_TIMING_SKIP & 2) return;   // timing experiments only (wrong results)
   // ---- pass 2: in-order walk of this warp's range, stable positions, scatter
   for (int b = i0; b < i1; b += 32) {
     const int i = b + lane;
     const bool valid = i < i1;
-    const uint32_t c = valid ? cell_id[base + i] : 0xFFFFFFFFu;
+    const uint32_t c = valid ? (STAGED ? (uint32_t)s_cid[i] : cell_id[base + i]) : 0xFFFFFFFFu;
     const unsigned grp = __match_any_sync(kFull, c);
     if (valid) {
-      const uint32_t pos = (uint32_t)base + s_tot[c] + s_wc[warp][c] + __popc(grp & lt);
-      float4 s = src[base + i];
+      const uint32_t pos = s_tot[c] + s_wc[warp][c] + __popc(grp & lt);
+      float4 s = STAGED ? st[i] : src[base + i];
       if (ENV == kTag) s.w = (i >= P.first_chaser) ? 1.f : 0.f;
-      sorted[pos] = s;
-      perm[pos] = (uint32_t)i;
+      if (STAGED) {
+        s_sorted[pos] = s;
+        s_perm[pos] = (uint32_t)i;
+      } else {
+        sorted[base + pos] = s;
+        perm[base + pos] = (uint32_t)i;
+      }
     }
     __syncwarp();
     if (valid && (grp & lt) == 0u) s_wc[warp][c] += __popc(grp);
     __syncwarp();
   }
   __syncthreads();                   // the block's sorted / perm writes are now visible
+  if (STAGED)                        // the cell-ordered replica out as one coalesced block
+    for (int e = tid; e < N; e += kRBThreads) {
+      sorted[base + e] = s_sorted[e];
+      perm[base + e] = s_perm[e];
+    }
   // ---- pass 3: K4 sense order of each cell (see K3b)
-  if (VG_RB_TIMING_SKIP & 1) return;   // timing experiments only (wrong results)
   for (int c = warp; c < C; c += NW) {
     const int m = ((c + 1 < C) ? (int)s_tot[c + 1] : N) - (int)s_tot[c];
-    sense_order_cell(P, c % P.G, false, (uint32_t)base + s_tot[c], m, sorted, perm, xo_rec,
-                     xo_perm, xo_xy, sub_tab + ((size_t)r * C + c) * kSub, lane, lt);
+    sense_order_cell(P, c % P.G, false, (uint32_t)base + s_tot[c], m,
+                     STAGED ? s_sorted : sorted, STAGED ? s_perm : perm, xo_rec, xo_perm, xo_xy,
+                     sub_tab + ((size_t)r * C + c) * kSub, lane, lt,
+                     STAGED ? s_tot[c] : (uint32_t)base + s_tot[c]);
   }
-  if (r == (int)gridDim.x - 1 && tid == 0) sub_tab[(size_t)P.R * C * kSub] = (uint32_t)P.total;
+  if (r == P.R - 1 && tid == 0) sub_tab[(size_t)P.R * C * kSub] = (uint32_t)P.total;
+  __syncthreads();                   // s_wc, s_tot, s_cid and this buffer are reused next
+  }
 }
+
 
 // ---------------------------------------------------------------------------------- K4
 // One CTA per (replica, cell); warp w handles the cell's query agents w, w+W, ...  Each

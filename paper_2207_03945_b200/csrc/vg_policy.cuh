@@ -132,7 +132,7 @@ __device__ __forceinline__ void tma_load_1d(uint32_t dst, const void* src, uint3
 // 1 = tanh.approx.f32 (one MUFU), 2 = tanh.approx.f16x2 on the fp16-rounded pre-activation
 // (one MUFU per two units; the result is the fp16 operand itself).
 #ifndef VG_TANH_MODE
-#define VG_TANH_MODE 0
+#define VG_TANH_MODE 1
 #endif
 __device__ __forceinline__ float tanh_fast(float x) {
 #if VG_TANH_NEWTON

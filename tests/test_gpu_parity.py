@@ -200,7 +200,8 @@ def test_default_constants_bitwise_generic(cuda, name, vision, monkeypatch):
 
 
 @pytest.mark.parametrize("case", ["gather_replicas", "gather_tag_replicas", "cta_sort",
-                                  "warp_sort", "gather_tag_dense", "cta_sort_dense"])
+                                  "warp_sort", "gather_tag_dense", "cta_sort_dense",
+                                  "fused_replicas", "staged_replicas", "staged_tag_replicas"])
 def test_binning_paths(cuda, case):
     # Each K2-K3b variant against the oracle's bins (bit-exact) and sense outputs:
     # K3g (per-cell gather, several replicas), K3b' (one CTA per cell: few cells, N above
@@ -219,9 +220,14 @@ def test_binning_paths(cuda, case):
     elif case == "gather_tag_dense":         # cells above 1,024 members: K3g's fallback
         p, kps = vi.tag_params(4000), 3
         rows = np.arange(0, 4000, 7)
-    else:                                    # N > 16,384 with dense cells: K3b''s fallback
+    elif case == "cta_sort_dense":           # N > 16,384 with dense cells: K3b''s fallback
         p, kps = vi.flock_params(17000), 5
         rows = np.arange(0, 17000, 53)
+    elif case == "fused_replicas":           # K1-K3b fused, one CTA per replica (< n_sm replicas)
+        p, kps = vi.flock_params(2500, n_replicas=100), 2
+    else:                                    # the persistent TMA-staged fused bin (>= n_sm replicas)
+        mk = vi.flock_params if case == "staged_replicas" else vi.tag_params
+        p, kps = mk(1500, n_replicas=300), 2
     st0 = vi.clustered_state(p, seed=5, n_clusters=3, sigma=1.5) if case.endswith("dense") \
         else vi.init_state(p, seed=17)
     w = make_world(p)
@@ -231,7 +237,34 @@ def test_binning_paths(cuda, case):
         cs = host(w.get_bins()["cell_start"]).astype(np.int64)
         assert np.diff(cs).max() > 1024                  # the fallback path really runs
     w.close()
-    run_and_check(p, st0, 2, rows=rows)
+    reps = [0, 1, p.n_replicas // 2, p.n_replicas - 1] if p.n_replicas > 4 else None
+    run_and_check(p, st0, 2, rows=rows, replicas=reps)
+
+
+def test_staged_fused_bin_equals_per_replica_kernel(cuda, monkeypatch):
+    # the persistent TMA-staged fused bin and the one-CTA-per-replica kernel: bitwise the
+    # same bins and outputs on a c4-shaped world (VG_RB_STAGED=0 forces the latter)
+    torch = _torch()
+    p = vi.workload("c4").replace(n_replicas=400)
+    st0 = vi.init_state(p, seed=8)
+    act = vi.actions(p, seed=8, step=0)
+    res = []
+    for staged in ("1", "0"):
+        monkeypatch.setenv("VG_RB_STAGED", staged)
+        w = make_world(p)
+        out = w.alloc_outputs()
+        st = dev(st0)
+        w.step(st, dev(act), out)
+        torch.cuda.synchronize()
+        assert w.sync_errors() == -1
+        bins = {k: host(v).copy() for k, v in w.get_bins().items()}
+        res.append((host(st), bins, {k: host(getattr(out, k)) for k in ("obs", "reward", "n_neigh")}))
+        w.close()
+    assert np.array_equal(res[0][0].view(np.uint32), res[1][0].view(np.uint32))
+    for k in res[0][1]:
+        assert np.array_equal(res[0][1][k].view(np.uint8), res[1][1][k].view(np.uint8)), k
+    for k in res[0][2]:
+        assert np.array_equal(res[0][2][k].view(np.uint8), res[1][2][k].view(np.uint8)), k
 
 
 @pytest.mark.parametrize("grid", [9, 0])

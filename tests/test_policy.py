@@ -3,8 +3,10 @@
 Two checks:
 1. against the fp64 oracle, within a worst-case bound propagated per row from the kernel's
    arithmetic: operands rounded to fp16 (rel 2^-11, abs 2^-25 near zero), fp32
-   accumulation (K 2^-24 of sum |w x|), tanh via exp/rcp (abs <= 1e-6 taken), Lipschitz-1
-   tanh; all three layers on the tensor cores (fp16 operands, fp32 accumulate);
+   accumulation (K 2^-24 of sum |w x|), tanh by the hardware tanh.approx.f32 (abs error
+   <= 7.84e-6 measured over 2^22 points of [-12, 12] by tools/probes/tanh_probe.cu; 1e-5
+   taken), Lipschitz-1 tanh; all three layers on the tensor cores (fp16 operands, fp32
+   accumulate);
 2. against an emulation of the kernel's quantization (fp16 operands, weights and hidden
    activations, otherwise exact) within 2e-4 absolute — tight enough that any layout or
    indexing error (O(0.1)) fails.
@@ -17,7 +19,7 @@ import vg_inputs as vi
 from oracle import policy as pol
 
 U16, A16, U32 = 2.0 ** -11, 2.0 ** -25, 2.0 ** -24
-TANH_ABS = 1e-6
+TANH_ABS = 1e-5
 EMU_TOL = 2e-4
 
 
