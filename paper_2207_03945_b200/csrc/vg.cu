@@ -122,7 +122,7 @@ struct vg_world {
   int n_cells = 0;
   bool binned = false;
   bool fused_bin = false;          // K1-K3 fused per replica (small worlds)
-  bool staged_bin = false;         // ... as the persistent TMA-staged kernel (many replicas)
+  int staged_bin = 0;              // ... as a persistent shared-memory staged kernel (MODE 1 / 2)
   bool gather_bin = false;         // K2-K3b as one per-cell gather kernel (K3g)
   bool sense_def = false;          // K4 sector pass: the default-constant instance
   size_t scratch_bytes = 0;
@@ -406,13 +406,18 @@ template <int ENV, bool INTEGRATE>
 vg_status launch_fused_bin(vg_world* w, float4* io, const float4* in, const float2* act,
                            cudaStream_t s) {
   VG_CUDA(cudaMemsetAsync(w->work_cnt, 0, sizeof(uint32_t), s));   // replica CTAs append items
-  if (w->staged_bin)            // persistent, TMA-staged: one CTA per SM
-    vg::k_replica_bin<ENV, INTEGRATE, true><<<(unsigned)std::min(w->P.R, w->n_sm), vg::kRBThreads,
-                                                vg::kRBStagedSmem, s>>>(
+  if (w->staged_bin == 1)       // persistent, shared-memory staged
+    vg::k_replica_bin<ENV, INTEGRATE, 1><<<(unsigned)std::min(w->P.R, w->n_sm), vg::kRBThreads,
+                                             vg::kRBStagedSmem, s>>>(
+        w->P, io, in, act, w->cell_id, w->cell_start, w->sorted, w->perm, w->xo_rec, w->xo_perm,
+        w->xo_xy, w->sub_tab, work_list(w), w->err_dev, w->err_flag);
+  else if (w->staged_bin == 2)
+    vg::k_replica_bin<ENV, INTEGRATE, 2><<<(unsigned)std::min(w->P.R, 2 * w->n_sm), vg::kRB2Threads,
+                                             vg::kRBStaged2Smem, s>>>(
         w->P, io, in, act, w->cell_id, w->cell_start, w->sorted, w->perm, w->xo_rec, w->xo_perm,
         w->xo_xy, w->sub_tab, work_list(w), w->err_dev, w->err_flag);
   else
-    vg::k_replica_bin<ENV, INTEGRATE, false><<<w->P.R, vg::kRBThreads, 0, s>>>(
+    vg::k_replica_bin<ENV, INTEGRATE, 0><<<w->P.R, vg::kRBThreads, 0, s>>>(
         w->P, io, in, act, w->cell_id, w->cell_start, w->sorted, w->perm, w->xo_rec, w->xo_perm,
         w->xo_xy, w->sub_tab, work_list(w), w->err_dev, w->err_flag);
   if (vg_status st = launch_check("k_replica_bin")) return st;
@@ -520,14 +525,22 @@ bool sense_defaults_match(const vg::Params& P) {
 void set_kernel_attributes() {
   cudaFuncSetAttribute(vg::k_scan_cells, cudaFuncAttributeMaxDynamicSharedMemorySize,
                        vg::kScanSmallMax * 4);
-  cudaFuncSetAttribute(vg::k_replica_bin<vg::kFlock, true, true>,
+  cudaFuncSetAttribute(vg::k_replica_bin<vg::kFlock, true, 1>,
                        cudaFuncAttributeMaxDynamicSharedMemorySize, vg::kRBStagedSmem);
-  cudaFuncSetAttribute(vg::k_replica_bin<vg::kFlock, false, true>,
+  cudaFuncSetAttribute(vg::k_replica_bin<vg::kFlock, false, 1>,
                        cudaFuncAttributeMaxDynamicSharedMemorySize, vg::kRBStagedSmem);
-  cudaFuncSetAttribute(vg::k_replica_bin<vg::kTag, true, true>,
+  cudaFuncSetAttribute(vg::k_replica_bin<vg::kTag, true, 1>,
                        cudaFuncAttributeMaxDynamicSharedMemorySize, vg::kRBStagedSmem);
-  cudaFuncSetAttribute(vg::k_replica_bin<vg::kTag, false, true>,
+  cudaFuncSetAttribute(vg::k_replica_bin<vg::kTag, false, 1>,
                        cudaFuncAttributeMaxDynamicSharedMemorySize, vg::kRBStagedSmem);
+  cudaFuncSetAttribute(vg::k_replica_bin<vg::kFlock, true, 2>,
+                       cudaFuncAttributeMaxDynamicSharedMemorySize, vg::kRBStaged2Smem);
+  cudaFuncSetAttribute(vg::k_replica_bin<vg::kFlock, false, 2>,
+                       cudaFuncAttributeMaxDynamicSharedMemorySize, vg::kRBStaged2Smem);
+  cudaFuncSetAttribute(vg::k_replica_bin<vg::kTag, true, 2>,
+                       cudaFuncAttributeMaxDynamicSharedMemorySize, vg::kRBStaged2Smem);
+  cudaFuncSetAttribute(vg::k_replica_bin<vg::kTag, false, 2>,
+                       cudaFuncAttributeMaxDynamicSharedMemorySize, vg::kRBStaged2Smem);
   sense_carveouts<vg::kFlock, true, false>();
   sense_carveouts<vg::kFlock, true, true>();
   sense_carveouts<vg::kTag, true, false>();
@@ -657,6 +670,9 @@ int32_t vg_abi_version(void) { return VG_ABI_VERSION; }
 
 const char* vg_last_error(void) { return g_err; }
 
+#ifndef VG_RB_STAGED_DEFAULT
+#define VG_RB_STAGED_DEFAULT 1       // many replicas: the staged fused bin, MODE 1
+#endif
 #ifndef VG_FUSED_SINGLE_MAX
 #define VG_FUSED_SINGLE_MAX 1024     // few replicas: the fused bin only for tiny worlds
 #endif
@@ -694,8 +710,8 @@ vg_status vg_world_create(const vg_config* cfg, vg_world** out) {
                   (cfg->n_agents <= VG_FUSED_SINGLE_MAX && !gather_ok));
   {                                // VG_RB_STAGED=0: the one-CTA-per-replica fused bin (tests)
     const char* sg = std::getenv("VG_RB_STAGED");
-    w->staged_bin = w->fused_bin && cfg->n_agents <= vg::kRBStagedMax &&
-                    cfg->n_replicas >= w->n_sm && !(sg && sg[0] == '0');
+    const bool ok = w->fused_bin && cfg->n_agents <= vg::kRBStagedMax && cfg->n_replicas >= w->n_sm;
+    w->staged_bin = ok ? ((sg && sg[0] >= '0' && sg[0] <= '2') ? sg[0] - '0' : VG_RB_STAGED_DEFAULT) : 0;
   }
   {                                // VG_SENSE_GENERIC=1: always the generic instance (tests)
     const char* gen = std::getenv("VG_SENSE_GENERIC");

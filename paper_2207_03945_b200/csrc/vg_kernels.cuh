@@ -401,9 +401,10 @@ __device__ __forceinline__ unsigned bin_lanes(const unsigned (&bits)[kSubBits], 
 // sort by sub-bin, one warp.  Writes xo_* and the cell's kSub table entries.
 // The cell's records are read from sorted[rb ..] / perm[rb ..] (rb = b, or a shared-memory
 // staging copy) and written to xo_*[b ..].
+template <typename PermT>
 __device__ __forceinline__ void sense_order_cell(const Params& P, int ca, bool axis_y,
                                                  uint32_t b, int m,
-                                                 const float4* sorted, const uint32_t* perm,
+                                                 const float4* sorted, const PermT* perm,
                                                  float4* __restrict__ xo_rec,
                                                  uint32_t* __restrict__ xo_perm,
                                                  float2* __restrict__ xo_xy, uint32_t* tab,
@@ -831,27 +832,44 @@ constexpr int kRBMaxAgents = 32768;
 #endif
 constexpr int kRBThreads = VG_RB_THREADS;   // warps per replica CTA x 32; 2048 / it CTAs per SM
 
-// STAGED (many replicas of N <= kRBStagedMax agents, e.g. c4): a persistent kernel, one
-// CTA of 1024 threads per SM looping over replicas, with the replica staged in shared memory
-// (DESIGN.md §6): pass 1 keeps the integrated state and the cell ids there; pass 2 scatters
+// MODE 0: one CTA of kRBThreads per replica (above).  MODE 1 / 2 (many replicas of N <=
+// kRBStagedMax agents, e.g. c4): a persistent kernel looping over replicas with the replica
+// staged in shared memory: pass 1 keeps the cell ids there; pass 2 scatters
 // into a shared-memory copy of the cell-ordered records (no scattered global writes: they
 // were L2-transaction bound), written out to sorted / perm as one coalesced block; pass 3
-// reads the cells from that copy.  The next replica's input is prefetched into L2 while the
-// current one is processed.
+// reads the cells from that copy.
+//   MODE 1: one CTA of 1024 threads per SM; the input state arrives by a 1-D TMA bulk
+//           copy (issued during the previous replica's write-out and pass 3) and pass 1
+//           keeps the integrated state in shared memory for pass 2.
+//   MODE 2: two CTAs of 512 threads per SM (two replicas in flight, so one CTA's barriers
+//           and load latencies overlap the other's work); 16-bit staging of perm and the
+//           per-warp counts; the state is read through L2 (prefetched).
 constexpr int kRBStagedMax = 5120;
-constexpr int kRBStagedSmem = kRBStagedMax * (16 + 16 + 4 + 1);   // state, sorted, perm, cell id
+constexpr int kRBStagedSmem = kRBStagedMax * (16 + 16 + 4 + 1);   // MODE 1: state, sorted, perm, cell id
+constexpr int kRBStaged2Smem = kRBStagedMax * (16 + 2 + 1);       // MODE 2: sorted, perm (u16), cell id
+constexpr int kRB2Threads = 512;
+template <int MODE> struct RBCfg {
+  static constexpr int NT = MODE == 2 ? kRB2Threads : kRBThreads;
+  static constexpr int MINB = MODE == 1 ? 1 : MODE == 2 ? 2 : 2048 / kRBThreads;
+  using WC = typename std::conditional<MODE == 2, uint16_t, uint32_t>::type;
+  using PermT = typename std::conditional<MODE == 2, uint16_t, uint32_t>::type;
+};
 
-template <int ENV, bool INTEGRATE, bool STAGED>
-__global__ void __launch_bounds__(kRBThreads, STAGED ? 1 : 2048 / kRBThreads) k_replica_bin(
+template <int ENV, bool INTEGRATE, int MODE>
+__global__ void __launch_bounds__(RBCfg<MODE>::NT, RBCfg<MODE>::MINB) k_replica_bin(
     Params P, float4* __restrict__ state_io, const float4* __restrict__ state_in,
     const float2* __restrict__ actions, uint32_t* __restrict__ cell_id,
     uint32_t* __restrict__ cell_start, float4* __restrict__ sorted,
     uint32_t* __restrict__ perm, float4* __restrict__ xo_rec, uint32_t* __restrict__ xo_perm,
     float2* __restrict__ xo_xy, uint32_t* __restrict__ sub_tab, WorkList WL,
     unsigned long long* __restrict__ err, volatile uint32_t* flag) {
-  constexpr int NW = kRBThreads / 32;
-  __shared__ uint32_t s_wc[NW][kRBMaxCells + 1];     // per-warp counts, then offsets (+1: banks)
+  constexpr bool STAGED = MODE != 0, TMA = MODE == 1;
+  constexpr int NT = RBCfg<MODE>::NT;
+  constexpr int NW = NT / 32;
+  using PermT = typename RBCfg<MODE>::PermT;
+  __shared__ typename RBCfg<MODE>::WC s_wc[NW][kRBMaxCells + 1];   // per-warp counts, then offsets (+1: banks)
   __shared__ uint32_t s_tot[kRBMaxCells];
+  __shared__ __align__(8) uint64_t s_bar;                    // STAGED: input-state TMA barrier
   extern __shared__ __align__(128) unsigned char rb_dyn[];   // STAGED: see kRBStagedSmem
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int N = P.N, C = P.G2;
@@ -860,9 +878,9 @@ __global__ void __launch_bounds__(kRBThreads, STAGED ? 1 : 2048 / kRBThreads) k_
   const int i0 = min(N, warp * span), i1 = min(N, i0 + span);
   unsigned lt;
   asm("mov.u32 %0, %%lanemask_lt;" : "=r"(lt));
-  float4* st = reinterpret_cast<float4*>(rb_dyn);                 // integrated, id order
-  float4* s_sorted = st + kRBStagedMax;                            // cell order
-  uint32_t* s_perm = reinterpret_cast<uint32_t*>(s_sorted + kRBStagedMax);
+  float4* st = reinterpret_cast<float4*>(rb_dyn);                 // MODE 1: integrated, id order
+  float4* s_sorted = st + (TMA ? kRBStagedMax : 0);                // cell order
+  PermT* s_perm = reinterpret_cast<PermT*>(s_sorted + kRBStagedMax);
   uint8_t* s_cid = reinterpret_cast<uint8_t*>(s_perm + kRBStagedMax);
   // Ask L2 for a replica's input (state, actions) up front: the warp walks its range one
   // 32-agent round at a time, so later rounds wait on L2, not HBM.  STAGED: the whole CTA
@@ -873,10 +891,34 @@ __global__ void __launch_bounds__(kRBThreads, STAGED ? 1 : 2048 / kRBThreads) k_
       asm volatile("prefetch.global.L2 [%0];" ::"l"(a));
   };
   const int r_step = STAGED ? (int)gridDim.x : P.R;
-  if (STAGED && VG_RB_PREFETCH && (int)blockIdx.x < P.R) {
-    pf(src + (size_t)blockIdx.x * N, (size_t)N * sizeof(float4), tid, kRBThreads);
-    if (INTEGRATE) pf(actions + (size_t)blockIdx.x * N, (size_t)N * sizeof(float2), tid, kRBThreads);
+  // STAGED: the input state of each replica arrives in `st` by one 1-D TMA bulk copy
+  // (cp.async.bulk + mbarrier complete_tx), issued as soon as the previous replica's pass 2
+  // has read `st` (it overlaps that replica's write-out and pass 3).
+  const uint32_t bar = (uint32_t)__cvta_generic_to_shared(&s_bar);
+  auto tma_state = [&](int rr) {
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");   // generic writes of st first
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar),
+                 "r"((uint32_t)N * 16u) : "memory");
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+            (uint32_t)__cvta_generic_to_shared(st)),
+        "l"(src + (size_t)rr * N), "r"((uint32_t)N * 16u), "r"(bar) : "memory");
+  };
+  if (STAGED && !TMA && VG_RB_PREFETCH && (int)blockIdx.x < P.R) {
+    pf(src + (size_t)blockIdx.x * N, (size_t)N * sizeof(float4), tid, NT);
+    if (INTEGRATE) pf(actions + (size_t)blockIdx.x * N, (size_t)N * sizeof(float2), tid, NT);
   }
+  if (TMA) {
+    if (tid == 0) {
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(bar));
+      asm volatile("fence.mbarrier_init.release.cluster;");
+      if ((int)blockIdx.x < P.R) tma_state(blockIdx.x);
+    }
+    if (INTEGRATE && VG_RB_PREFETCH && (int)blockIdx.x < P.R)
+      pf(actions + (size_t)blockIdx.x * N, (size_t)N * sizeof(float2), tid, NT);
+    __syncthreads();
+  }
+  uint32_t phase = 0u;
   for (int r = blockIdx.x; r < P.R; r += r_step) {
   const size_t base = (size_t)r * N;
   for (int c = lane; c < C; c += 32) s_wc[warp][c] = 0u;
@@ -887,9 +929,18 @@ __global__ void __launch_bounds__(kRBThreads, STAGED ? 1 : 2048 / kRBThreads) k_
     }
     if (STAGED && r + r_step < P.R) {
       const size_t nb = (size_t)(r + r_step) * N;
-      pf(src + nb, (size_t)N * sizeof(float4), tid, kRBThreads);
-      if (INTEGRATE) pf(actions + nb, (size_t)N * sizeof(float2), tid, kRBThreads);
+      if (!TMA) pf(src + nb, (size_t)N * sizeof(float4), tid, NT);
+      if (INTEGRATE) pf(actions + nb, (size_t)N * sizeof(float2), tid, NT);
     }
+  }
+  if (TMA) {                                       // this replica's input state has landed
+    asm volatile(
+        "{\n\t.reg .pred done;\n"
+        "RBW_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 done, [%0], %1;\n\t"
+        "@!done bra RBW_%=;\n\t}\n" ::"r"(bar), "r"(phase)
+        : "memory");
+    phase ^= 1u;
   }
   __syncwarp();
   // ---- pass 1: integrate + cell id + warp-private histogram
@@ -899,7 +950,7 @@ __global__ void __launch_bounds__(kRBThreads, STAGED ? 1 : 2048 / kRBThreads) k_
     uint32_t c = 0xFFFFFFFFu;
     if (valid) {
       const size_t gi = base + i;
-      float4 s = src[gi];
+      float4 s = TMA ? st[i] : src[gi];
       bool bad = !(s.x >= 0.f && s.x < P.L && s.y >= 0.f && s.y < P.L && s.z >= 0.f &&
                    s.z < P.two_pi);
       if (ENV == kFlock) bad |= !isfinite(s.w);
@@ -925,7 +976,7 @@ __global__ void __launch_bounds__(kRBThreads, STAGED ? 1 : 2048 / kRBThreads) k_
         s.y = wrap_pos(s.y, __fmul_rn(dist, sn), P.L);
         state_io[gi] = s;
       }
-      if (STAGED) st[i] = s;                           // pass 2 reads it back from here
+      if (TMA) st[i] = s;                              // pass 2 reads it back from here
       if (bad) report_bad(err, flag, (unsigned long long)gi);
       int cx = __float2int_rz(__fmul_rn(s.x, P.gs));
       int cy = __float2int_rz(__fmul_rn(s.y, P.gs));
@@ -941,7 +992,7 @@ __global__ void __launch_bounds__(kRBThreads, STAGED ? 1 : 2048 / kRBThreads) k_
   }
   __syncthreads();
   // ---- per cell: exclusive scan over the NW warps; totals per cell
-  for (int cc = tid; cc < C; cc += kRBThreads) {
+  for (int cc = tid; cc < C; cc += NT) {
     uint32_t run = 0;
 #pragma unroll
     for (int w = 0; w < NW; ++w) {
@@ -1014,11 +1065,11 @@ __global__ void __launch_bounds__(kRBThreads, STAGED ? 1 : 2048 / kRBThreads) k_
     const unsigned grp = __match_any_sync(kFull, c);
     if (valid) {
       const uint32_t pos = s_tot[c] + s_wc[warp][c] + __popc(grp & lt);
-      float4 s = STAGED ? st[i] : src[base + i];
+      float4 s = TMA ? st[i] : src[base + i];
       if (ENV == kTag) s.w = (i >= P.first_chaser) ? 1.f : 0.f;
       if (STAGED) {
         s_sorted[pos] = s;
-        s_perm[pos] = (uint32_t)i;
+        s_perm[pos] = (PermT)i;
       } else {
         sorted[base + pos] = s;
         perm[base + pos] = (uint32_t)i;
@@ -1029,18 +1080,25 @@ __global__ void __launch_bounds__(kRBThreads, STAGED ? 1 : 2048 / kRBThreads) k_
     __syncwarp();
   }
   __syncthreads();                   // the block's sorted / perm writes are now visible
+  if (TMA && tid == 0 && r + r_step < P.R) tma_state(r + r_step);      // st is free again
   if (STAGED)                        // the cell-ordered replica out as one coalesced block
-    for (int e = tid; e < N; e += kRBThreads) {
+    for (int e = tid; e < N; e += NT) {
       sorted[base + e] = s_sorted[e];
-      perm[base + e] = s_perm[e];
+      perm[base + e] = (uint32_t)s_perm[e];
     }
   // ---- pass 3: K4 sense order of each cell (see K3b)
   for (int c = warp; c < C; c += NW) {
     const int m = ((c + 1 < C) ? (int)s_tot[c + 1] : N) - (int)s_tot[c];
-    sense_order_cell(P, c % P.G, false, (uint32_t)base + s_tot[c], m,
-                     STAGED ? s_sorted : sorted, STAGED ? s_perm : perm, xo_rec, xo_perm, xo_xy,
-                     sub_tab + ((size_t)r * C + c) * kSub, lane, lt,
-                     STAGED ? s_tot[c] : (uint32_t)base + s_tot[c]);
+    if (STAGED) {
+      const uint32_t c0 = s_tot[c];
+      sense_order_cell(P, c % P.G, false, (uint32_t)base + c0, m, s_sorted, s_perm,
+                       xo_rec, xo_perm, xo_xy, sub_tab + ((size_t)r * C + c) * kSub, lane, lt,
+                       c0);
+    } else {
+      sense_order_cell(P, c % P.G, false, (uint32_t)base + s_tot[c], m, sorted, perm, xo_rec,
+                       xo_perm, xo_xy, sub_tab + ((size_t)r * C + c) * kSub, lane, lt,
+                       (uint32_t)base + s_tot[c]);
+    }
   }
   if (r == P.R - 1 && tid == 0) sub_tab[(size_t)P.R * C * kSub] = (uint32_t)P.total;
   __syncthreads();                   // s_wc, s_tot, s_cid and this buffer are reused next
@@ -1428,6 +1486,7 @@ __global__ void __launch_bounds__(kSenseWarps * 32, (DEF && ENV == kTag) ? VG_SE
     __syncwarp();
 
     const uint32_t srow = sh_addr(&s_min[warp][0][0]);         // this warp's sector rows
+    const uint32_t seg_base = sh_addr(&s_seg[0]);
     // Pair pass over one queue entry (dx, dy, d^2, index | type << 31) of query t.
     auto process = [&](const int t, const float4 e) {
       const uint32_t tagbits = __float_as_uint(e.w);
@@ -1606,7 +1665,7 @@ __global__ void __launch_bounds__(kSenseWarps * 32, (DEF && ENV == kTag) ? VG_SE
       if (wb >= we) continue;                                        // warp-uniform
       Seg sg;
       {                                     // the run's image shifts: one broadcast load
-        const float4 sh = *reinterpret_cast<const float4*>(&s_seg[sgi]);
+        const float4 sh = lds128(seg_base + (uint32_t)(sgi * sizeof(Seg)));
         sg.csx = sh.x;
         sg.csy = sh.y;
         sg.qsx = sh.z;

@@ -242,14 +242,15 @@ def test_binning_paths(cuda, case):
 
 
 def test_staged_fused_bin_equals_per_replica_kernel(cuda, monkeypatch):
-    # the persistent TMA-staged fused bin and the one-CTA-per-replica kernel: bitwise the
-    # same bins and outputs on a c4-shaped world (VG_RB_STAGED=0 forces the latter)
+    # the persistent staged fused bins (MODE 1: one 1024-thread CTA per SM with TMA input;
+    # MODE 2: two 512-thread CTAs per SM) and the one-CTA-per-replica kernel (VG_RB_STAGED=0):
+    # bitwise the same bins and outputs on a c4-shaped world
     torch = _torch()
     p = vi.workload("c4").replace(n_replicas=400)
     st0 = vi.init_state(p, seed=8)
     act = vi.actions(p, seed=8, step=0)
     res = []
-    for staged in ("1", "0"):
+    for staged in ("1", "2", "0"):
         monkeypatch.setenv("VG_RB_STAGED", staged)
         w = make_world(p)
         out = w.alloc_outputs()
@@ -260,11 +261,12 @@ def test_staged_fused_bin_equals_per_replica_kernel(cuda, monkeypatch):
         bins = {k: host(v).copy() for k, v in w.get_bins().items()}
         res.append((host(st), bins, {k: host(getattr(out, k)) for k in ("obs", "reward", "n_neigh")}))
         w.close()
-    assert np.array_equal(res[0][0].view(np.uint32), res[1][0].view(np.uint32))
-    for k in res[0][1]:
-        assert np.array_equal(res[0][1][k].view(np.uint8), res[1][1][k].view(np.uint8)), k
-    for k in res[0][2]:
-        assert np.array_equal(res[0][2][k].view(np.uint8), res[1][2][k].view(np.uint8)), k
+    for other in res[1:]:
+        assert np.array_equal(res[0][0].view(np.uint32), other[0].view(np.uint32))
+        for k in res[0][1]:
+            assert np.array_equal(res[0][1][k].view(np.uint8), other[1][k].view(np.uint8)), k
+        for k in res[0][2]:
+            assert np.array_equal(res[0][2][k].view(np.uint8), other[2][k].view(np.uint8)), k
 
 
 @pytest.mark.parametrize("grid", [9, 0])
