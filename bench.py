@@ -57,6 +57,9 @@ def parse():
                     help="bounded oracle sample for cpu_baseline (seconds of CPU work)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--slab-scheme", default="halo", choices=["halo", "allgather"],
+                    help="c5 at N > 1: x-slabs + halo exchange (default) or the replicated-"
+                         "state ablation (all-gather of the actions, DESIGN.md §7b)")
     ap.add_argument("--no-c4-binning", action="store_true",
                     help="skip the c4 binning sub-measurement of the default c5 line")
     ap.add_argument("--no-policy", action="store_true",
@@ -344,6 +347,82 @@ class SlabRunner:
         return float(self.out.n_neigh[0, :n].sum(dtype=self.torch.float64).item())
 
 
+class AllGatherRunner:
+    """c5 at N > 1 with --slab-scheme allgather: SURVEY §8e's replicated-state ablation
+    (DESIGN.md §7b).  Every rank holds the whole world; each step the ranks all-gather the
+    step's actions (rank g contributes agents [g N/P, (g+1) N/P): 8 B x N per step over
+    NCCL), every rank integrates and bins the whole world, and senses only its own x-slab of
+    cell columns (vg_sense_columns).  Compare its all-gather volume with the halo scheme's
+    two ~0.6 MB messages."""
+
+    def __init__(self, p, device, rank, world, torch, vg):
+        import torch.distributed as dist
+        self.p, self.torch, self.dist = p, torch, dist
+        if p.n_agents % world:
+            raise SystemExit(f"allgather: {p.n_agents} agents not divisible by {world}")
+        self.w = vg.World(p, device=device)
+        self.out = self.w.alloc_outputs()
+        self.out.n_neigh.zero_()                 # rows of other ranks' columns stay 0
+        init = vi.clustered_state if STATE == "clustered" else vi.init_state
+        self.state = torch.from_numpy(init(p, seed=0)).to(device)   # same world everywhere
+        G = self.w.grid
+        if G % world:
+            raise SystemExit(f"allgather: G = {G} not divisible by {world}")
+        self.lo, self.hi = rank * (G // world), (rank + 1) * (G // world)
+        self.n_loc = p.n_agents // world
+        self.a0 = rank * self.n_loc
+        self.acts_all = torch.empty((1, p.n_agents, 2), dtype=torch.float32, device=device)
+        self.act_dev = torch.zeros((1, p.n_agents, 2), dtype=torch.float32, device=device)
+        self.launches = 1 + 6 + 1                # (all-gather) + K1 + K1-K3b binning + K4
+        self.exchange = (f"NCCL all_gather_into_tensor of the step's actions "
+                         f"({8 * p.n_agents / 1e6:.1f} MB per step)")
+        self.phase_names = {"integrate_bin": "all-gather + integrate (replicated)",
+                            "scan_cells": "bin whole world (replicated)",
+                            "scatter": "-", "cell_sort": "-",
+                            "sense": "sense own columns"}
+        self._prof = None
+
+    def step(self, acts):
+        torch = self.torch
+        ev = None
+        if self._prof is not None and self._prof["n"] < self._prof["max"]:
+            ev = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
+            ev[0].record()
+        local = acts[0, self.a0:self.a0 + self.n_loc].contiguous()
+        self.dist.all_gather_into_tensor(self.acts_all.view(-1), local.view(-1))
+        self.w.integrate(self.state, self.acts_all)
+        if ev: ev[1].record()
+        self.w.bin(self.state)
+        if ev: ev[2].record()
+        self.w.sense_columns(self.out, self.lo, self.hi)
+        if ev:
+            ev[3].record()
+            self._prof["ev"].append(ev)
+            self._prof["n"] += 1
+
+    def step_host(self, acts_h, rew_h):
+        self.act_dev.copy_(acts_h, non_blocking=True)
+        self.step(self.act_dev)
+        rew_h.copy_(self.out.reward, non_blocking=True)
+
+    def profile_begin(self, k):
+        self._prof = {"max": k, "n": 0, "ev": []}
+
+    def profile_end(self):
+        self.torch.cuda.synchronize()
+        ph = {"integrate_bin": 0.0, "scan_cells": 0.0, "scatter": 0.0, "cell_sort": 0.0, "sense": 0.0}
+        for e in self._prof["ev"]:
+            ph["integrate_bin"] += e[0].elapsed_time(e[1])
+            ph["scan_cells"] += e[1].elapsed_time(e[2])
+            ph["sense"] += e[2].elapsed_time(e[3])
+        n = self._prof["n"]
+        self._prof = None
+        return ph, n
+
+    def pairs_local(self):
+        return float(self.out.n_neigh.sum(dtype=self.torch.float64).item())
+
+
 def run_ours(args):
     import importlib.util
     import torch
@@ -366,7 +445,8 @@ def run_ours(args):
     slab_mode = args.config == "c5" and world > 1
     if slab_mode:
         p, scaling = vi.workload("c5").replace(vision=args.vision), "strong"
-        run = SlabRunner(p, device, rank, world, torch, vg)
+        run = (AllGatherRunner if args.slab_scheme == "allgather" else SlabRunner)(
+            p, device, rank, world, torch, vg)
     else:
         p, scaling = local_params(args.config, world, rank)
         p = p.replace(vision=args.vision)
@@ -402,12 +482,12 @@ def run_ours(args):
             dist.barrier()
         # pass 2: the same K steps with per-kernel CUDA events recorded by libvg on the
         # launching stream (eager launches) -> stages and the k_sense roofline
-        w.profile_begin(K)
+        (run.profile_begin if hasattr(run, "profile_begin") else w.profile_begin)(K)
         for k in range(K):
             flush.fill_(k & 0xFF)
             run.step(acts[k % len(acts)])
         torch.cuda.synchronize()
-        phases, nrec = w.profile_end()
+        phases, nrec = (run.profile_end if hasattr(run, "profile_end") else w.profile_end)()
     if world > 1:
         dist.barrier()
     step_ms = [a.elapsed_time(b) for a, b in zip(ev0, ev1)]
@@ -421,7 +501,9 @@ def run_ours(args):
     value = agents_all * K / (max_ms / 1e3)
     pairs_local = run.pairs_local()            # in-radius pairs of the last step (this rank)
     san = None
-    if args.vision == "sector" and args.config in ("c2", "c3", "c4", "c5") and STATE == "uniform":
+    ag = slab_mode and args.slab_scheme == "allgather"
+    if args.vision == "sector" and args.config in ("c2", "c3", "c4", "c5") and STATE == "uniform" \
+            and not ag:
         rows = run.w.slab_own_count() if slab_mode else p.total_agents
         san = sanity(p, run.out, rows, torch)
 
@@ -453,7 +535,7 @@ def run_ours(args):
     # ---- K7: shared-policy forward + sampling over this rank's obs,
     # timed separately (not part of the env-step metric)
     policy = None
-    if not args.no_policy and run.out.obs is not None:
+    if not args.no_policy and run.out.obs is not None and not ag:
         from paper_2207_03945_b200.policy import Policy, action_box
         lo, hi = action_box(p)
         pl = Policy(w.obs_dim, lo, hi, device=device)
@@ -628,7 +710,7 @@ def run_ours(args):
         alu_peak = 148 * 128 * sm_mhz * 1e6 / 1e12      # fp32 lane-ops/s, TFLOP/s-equivalent
         # K4 time: slab mode senses in two launches (the interior phase, which also bins
         # the interior columns, and the boundary phase)
-        sense_ms = phases["sense"] + (phases["scan_cells"] if slab_mode else 0.0)
+        sense_ms = phases["sense"] + (phases["scan_cells"] if slab_mode and not ag else 0.0)
         sense_s = sense_ms / 1e3 / nrec
         achieved = ALG_OPS_PER_PAIR * pairs_local / sense_s / 1e12
         n = p.total_agents if not slab_mode else p.n_agents // world
@@ -639,7 +721,10 @@ def run_ours(args):
         scan_b = 8 * w.n_cells
         stage_bytes = {"integrate_bin": (92 if fused else 48) * n, "scan_cells": scan_b,
                        "scatter": 44 * n, "cell_sort": 68 * n, "sense": obs_b * n}
-        if slab_mode:     # begin | interior bin + sense | halo wait + unpack | boundary bin | sense
+        if ag:            # all-gather + integrate (whole world) | bin (whole world) | sense own
+            stage_bytes = {"integrate_bin": (8 + 48) * p.n_agents, "scan_cells": (44 + 68) * p.n_agents,
+                           "sense": obs_b * n}
+        elif slab_mode:   # begin | interior bin + sense | halo wait + unpack | boundary bin | sense
             msg = 2 * int(w.slab_io.message_bytes)
             stage_bytes = {"integrate_bin": 48 * n, "scan_cells": (44 + 68) * n + obs_b * n,
                            "scatter": msg, "cell_sort": (44 + 68) * 4 * n // (w.grid // world),
@@ -725,7 +810,9 @@ def run_ours(args):
             rate, sample, cores = oracle_rate(p, args.cpu_seconds)
             cpu = {"value": rate, "unit": UNIT, "cores": cores, "kind": "oracle",
                    "sample": sample}
-        if slab_mode:
+        if slab_mode and args.slab_scheme == "allgather":
+            par = f"replicated state over {world} ranks ({w.grid // world} sensed columns each): {run.exchange}"
+        elif slab_mode:
             par = f"slab{world}: x-slabs of {w.grid // world} cell columns + halo: {run.exchange}"
         elif world > 1:
             par = f"replicas over {world} ranks (no collective)"

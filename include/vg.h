@@ -147,6 +147,14 @@ vg_status vg_bin(vg_world* w, const float* state, void* stream);
  * snapshot.  Requires a prior vg_bin (or vg_step) on the same stream. */
 vg_status vg_sense(vg_world* w, const vg_outputs* outs, void* stream);
 
+/* vg_sense restricted to the cells of grid columns [col_lo, col_hi) of a one-replica world
+ * (n_replicas = 1): writes the output rows of exactly the agents binned in those columns
+ * (other rows untouched); the same values vg_sense writes for them.  For the replicated-
+ * state multi-GPU scheme (every rank holds and bins the whole world and
+ * senses its own columns).  Errors: VG_EINVAL (slab world, R > 1, bad range, no binning). */
+vg_status vg_sense_columns(vg_world* w, const vg_outputs* outs, int32_t col_lo, int32_t col_hi,
+                           void* stream);
+
 /* Reward and neighbour/contact counts only (no bearings, no observation), for the state
  * last binned: flock r_i = sum over j != i with d_ij < d_v of f(d_ij) (Eq. 1, P:174-175;
  * f = the Fig. 4 shape, reading A5: -c_collide for d <= 2 d_r, else rising

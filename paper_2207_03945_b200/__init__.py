@@ -259,6 +259,12 @@ class World:
         self._check_tensor(actions, "actions", (1, self.N, 2))
         check(_lib.lib.vg_slab_begin(self._h, actions.data_ptr(), self._stream()))
 
+    def sense_columns(self, out: Outputs, col_lo: int, col_hi: int) -> None:
+        """vg_sense_columns: sense only the cells of grid columns [col_lo, col_hi) (R = 1)."""
+        o = self._outs(out)
+        check(_lib.lib.vg_sense_columns(self._h, byref(o), int(col_lo), int(col_hi),
+                                        self._stream()))
+
     def slab_interior(self, out: Outputs) -> None:
         """vg_slab_interior: bin + sense the interior columns (no halo needed)."""
         o = self._outs(out)

@@ -99,6 +99,7 @@ SIGNATURES = {
     "vg_slab_begin": (c_int32, [c_void_p, c_void_p, c_void_p]),
     "vg_slab_get_io": (c_int32, [c_void_p, POINTER(VgSlabIo)]),
     "vg_slab_exchange_loopback": (c_int32, [POINTER(c_void_p), c_int32, c_void_p]),
+    "vg_sense_columns": (c_int32, [c_void_p, POINTER(VgOutputs), c_int32, c_int32, c_void_p]),
     "vg_slab_interior": (c_int32, [c_void_p, POINTER(VgOutputs), c_void_p]),
     "vg_slab_finish": (c_int32, [c_void_p, POINTER(VgOutputs), c_void_p]),
     "vg_slab_step": (c_int32, [c_void_p, c_void_p, POINTER(VgOutputs), c_void_p]),

@@ -629,14 +629,16 @@ vg_status slab_bin(vg_world* w, cudaStream_t s, int phase = kSlabAll) {
     return VG_OK;
   }
   const unsigned nb = stride_blocks(w->SB.cap_loc);
-  vg::k_slab_keys<<<nb, 256, 0, s>>>(w->P, w->SL, w->SB, w->cell_id, w->slot, w->count, phase);
-  if (vg_status st = launch_check("k_slab_keys")) return st;
+  if (phase == kSlabAll) {     // (the step phases' keys were computed by begin / unpack)
+    vg::k_slab_keys<<<nb, 256, 0, s>>>(w->P, w->SL, w->SB, w->cell_id, w->slot, w->count, phase);
+    if (vg_status st = launch_check("k_slab_keys")) return st;
+  }
   const int c0 = (phase == kSlabBoundary) ? nA : 0;
   const int c1 = (phase == kSlabInterior) ? nA : w->n_cells;
   if (vg_status st = scan_cells(w, s, c0, c1, phase == kSlabBoundary)) return st;
   vg::k_slab_scatter<ENV><<<nb, 256, 0, s>>>(w->P, w->SB, w->cell_id, w->slot, w->cell_start,
                                               w->tmp_rec, w->tmp_id, w->work_cnt,
-                                              phase != kSlabBoundary);
+                                              phase != kSlabBoundary, (uint32_t)c0, (uint32_t)c1);
   if (vg_status st = launch_check("k_slab_scatter")) return st;
   if (vg_status st = launch_cell_sort(w, s, c0, c1)) return st;
   if (phase != kSlabInterior) w->binned = true;
@@ -778,6 +780,11 @@ vg_status vg_world_create(const vg_config* cfg, vg_world** out) {
   if (!st) st = dalloc(w, &w->cell_start, w->n_cells + 1);
   if (!st) st = dalloc(w, &w->cell_id, n);
   if (!st) st = dalloc(w, &w->slot, n);
+  if (!st && w->slab) {                // k_slab_begin / k_slab_unpack write the binning keys
+    w->SB.cell_id = w->cell_id;
+    w->SB.slot = w->slot;
+    w->SB.count = w->count;
+  }
   if (!st) st = dalloc(w, &w->tmp_id, n);
   if (!st) st = dalloc(w, &w->perm, n);
   if (!st) st = dalloc(w, &w->tmp_rec, n);
@@ -903,6 +910,29 @@ vg_status vg_sense(vg_world* w, const vg_outputs* outs, void* stream) {
   DeviceGuard dg_(w->device);
   if (vg_status st = check_pending(w)) return st;
   return launch_sense<true>(w, outs, as_stream(stream));
+}
+
+vg_status vg_sense_columns(vg_world* w, const vg_outputs* outs, int32_t col_lo, int32_t col_hi,
+                           void* stream) {
+  NvtxRange nvtx_("vg_sense_columns");
+  if (!w || !outs) return fail(VG_EINVAL, "world/outs: NULL");
+  if (vg_status st = need_slab(w, false, "vg_sense_columns")) return st;
+  if (w->P.R != 1) return fail(VG_EINVAL, "vg_sense_columns: needs n_replicas = 1");
+  if (col_lo < 0 || col_hi > w->P.G || col_lo >= col_hi)
+    return fail(VG_EINVAL, "vg_sense_columns: need 0 <= col_lo < col_hi <= G (G = %d)", w->P.G);
+  if (!w->binned) return fail(VG_EINVAL, "vg_sense_columns: no binned state (call vg_bin or vg_step first)");
+  DeviceGuard dg_(w->device);
+  if (vg_status st = check_pending(w)) return st;
+  const vg::Slab saved = w->SL;
+  w->SL.sc0 = col_lo;
+  w->SL.snc = col_hi - col_lo;
+  w->SL.snl = 0;
+  const vg::Outs O = to_outs(w, outs);
+  const int cells = (col_hi - col_lo) * w->P.G;
+  if (w->P.env == vg::kFlock) sense_kernel<vg::kFlock, true, false>(w, cells, O, as_stream(stream));
+  else sense_kernel<vg::kTag, true, false>(w, cells, O, as_stream(stream));
+  w->SL = saved;
+  return launch_check("k_sense(columns)");
 }
 
 vg_status vg_reward(vg_world* w, const vg_outputs* outs, void* stream) {
@@ -1187,7 +1217,7 @@ vg_status slab_interior_launch(vg_world* w, const vg_outputs* outs, cudaStream_t
 // The boundary phase, once the halo arrived: append the received records, bin the boundary
 // and ghost columns, sense the owned cells whose stencil reaches them.
 vg_status slab_finish_launch(vg_world* w, const vg_outputs* outs, cudaStream_t s) {
-  vg::k_slab_unpack<<<stride_blocks(2ull * w->SB.cap_msg), 256, 0, s>>>(w->SB);
+  vg::k_slab_unpack<<<stride_blocks(2ull * w->SB.cap_msg), 256, 0, s>>>(w->P, w->SL, w->SB);
   if (vg_status st = launch_check("k_slab_unpack")) return st;
   prof_mark(w, 3, s);
   vg_status st = (w->P.env == vg::kFlock) ? slab_bin<vg::kFlock>(w, s, kSlabBoundary)

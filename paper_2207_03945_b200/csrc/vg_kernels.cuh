@@ -1387,9 +1387,15 @@ __global__ void __launch_bounds__(kSenseWarps * 32, (DEF && ENV == kTag) ? VG_SE
       if (k >= *work_n) return;
       item = work[k];
       if (SLAB && !slab_senses(SL, (int)item.x / P.G)) return;       // another launch's cell
+      if (!SLAB && SL.snc > 0) {                                      // column-restricted launch
+        const int cxi = ((int)item.x % P.G2) % P.G;
+        if (cxi < SL.sc0 || cxi >= SL.sc0 + SL.snc) return;
+      }
     } else if (SLAB) {                                                // this launch's k-th cell
       const int kc = (int)blockIdx.x / P.G;
       item.x = (uint32_t)(((SL.snl ? SL.scol[kc] : SL.sc0 + kc)) * P.G + (int)blockIdx.x % P.G);
+    } else if (SL.snc > 0) {          // replica world, one replica: cell columns [sc0, sc0 + snc)
+      item.x = (uint32_t)(((int)blockIdx.x / SL.snc) * P.G + SL.sc0 + (int)blockIdx.x % SL.snc);
     }
     const int c = (int)item.x;
   // Replica layout: cell = r G^2 + cy G + cx.  Slab layout: memory cell c = m G + cy of
@@ -1873,6 +1879,11 @@ struct SlabBufs {
   const unsigned char* recv_r;
   uint32_t cap_msg;        // records per message
   uint32_t* overflow;      // device flag (VG_EOVERFLOW)
+  // binning keys, computed as records enter the local set (k_slab_begin, k_slab_unpack):
+  // cell_id[k] (memory-order local cell) and slot[k] (arrival slot within it, count[cell])
+  uint32_t* cell_id;
+  uint32_t* slot;
+  uint32_t* count;
 };
 
 __device__ __forceinline__ uint32_t* msg_count(unsigned char* m) { return reinterpret_cast<uint32_t*>(m); }
@@ -1893,10 +1904,11 @@ __device__ __forceinline__ uint32_t warp_reserve(uint32_t* counter) {
   return base + (uint32_t)__popc(m & ((1u << lane) - 1u));
 }
 
-__device__ __forceinline__ void loc_append(const SlabBufs& B, float4 s, uint32_t id) {
+__device__ __forceinline__ uint32_t loc_append(const SlabBufs& B, float4 s, uint32_t id) {
   const uint32_t k = warp_reserve(B.n_loc);
   if (k < B.cap_loc) { B.loc_rec[k] = s; B.loc_id[k] = id; }
   else atomicExch(B.overflow, 1u);
+  return k;
 }
 
 __device__ __forceinline__ void msg_append(unsigned char* m, uint32_t cap, uint32_t* ovf,
@@ -1910,6 +1922,24 @@ __device__ __forceinline__ int global_col(const Params& P, float x) {
   return min(max(__float2int_rz(__fmul_rn(x, P.gs)), 0), P.G - 1);   // A16
 }
 
+// Binning key of local record k (memory-order local cell, A16 global formula) and its
+// arrival slot in the cell's histogram; warp-aggregated (records arrive cell-major).
+__device__ __forceinline__ void slab_key(const Params& P, const Slab& SL, const SlabBufs& B,
+                                         uint32_t k, float4 s) {
+  const int gx = global_col(P, s.x), gy = global_col(P, s.y);
+  const int lcx = min((gx - SL.lo + 1 + P.G) % P.G, SL.W + 1);
+  const uint32_t c = (uint32_t)(slab_mcol(lcx, SL.W) * P.G + gy);
+  const unsigned grp = __match_any_sync(__activemask(), c);
+  const int lane = threadIdx.x & 31, leader = __ffs(grp) - 1;
+  uint32_t base = 0u;
+  if (lane == leader) base = atomicAdd(&B.count[c], (uint32_t)__popc(grp));
+  base = __shfl_sync(grp, base, leader);
+  if (k < B.cap_loc) {
+    B.cell_id[k] = c;
+    B.slot[k] = base + (uint32_t)__popc(grp & ((1u << lane) - 1u));
+  }
+}
+
 // Route one post-integrate agent of this rank: owned columns stay local; columns lo-1 / hi
 // (migrants, <= 1 column per step since s_max < cell size) stay local as ghosts and go to
 // the neighbour that now owns them; boundary columns lo / hi-1 go to the neighbour as ghosts.
@@ -1921,7 +1951,7 @@ __device__ __forceinline__ void slab_route(const Params& P, const Slab& SL, cons
     report_bad(err, flag, id);
     return;
   }
-  loc_append(B, s, id);
+  slab_key(P, SL, B, loc_append(B, s, id), s);
   if (d == 0 || d == P.G - 1) msg_append(B.send_l, B.cap_msg, B.overflow, s, id);
   if (d == SL.W - 1 || d == SL.W) msg_append(B.send_r, B.cap_msg, B.overflow, s, id);
 }
@@ -1983,7 +2013,7 @@ __global__ void __launch_bounds__(256) k_slab_load(Params P, Slab SL, SlabBufs B
 }
 
 // Append the records received from both neighbours to the local set.
-__global__ void __launch_bounds__(256) k_slab_unpack(SlabBufs B) {
+__global__ void __launch_bounds__(256) k_slab_unpack(Params P, Slab SL, SlabBufs B) {
   const uint32_t nl = min(*reinterpret_cast<const uint32_t*>(B.recv_l), B.cap_msg);
   const uint32_t nr = min(*reinterpret_cast<const uint32_t*>(B.recv_r), B.cap_msg);
   if (*reinterpret_cast<const uint32_t*>(B.recv_l) > B.cap_msg ||
@@ -1994,8 +2024,8 @@ __global__ void __launch_bounds__(256) k_slab_unpack(SlabBufs B) {
        i += gridDim.x * blockDim.x) {
     const unsigned char* m = (i < nl) ? B.recv_l : B.recv_r;
     const uint32_t k = (i < nl) ? i : i - nl;
-    loc_append(B, reinterpret_cast<const float4*>(m + 16)[k],
-               reinterpret_cast<const uint32_t*>(m + 16 + 16 * (size_t)B.cap_msg)[k]);
+    const float4 s = reinterpret_cast<const float4*>(m + 16)[k];
+    slab_key(P, SL, B, loc_append(B, s, reinterpret_cast<const uint32_t*>(m + 16 + 16 * (size_t)B.cap_msg)[k]), s);
   }
 }
 
@@ -2039,14 +2069,15 @@ __global__ void __launch_bounds__(256) k_slab_scatter(Params P, SlabBufs B,
                                                       float4* __restrict__ tmp_rec,
                                                       uint32_t* __restrict__ tmp_id,
                                                       uint32_t* __restrict__ work_n,
-                                                      int reset_work) {
+                                                      int reset_work, uint32_t c_lo,
+                                                      uint32_t c_hi) {
   // K3b appends the K4 items next (the boundary phase keeps the interior phase's items)
   if (reset_work && blockIdx.x == 0 && threadIdx.x == 0) *work_n = 0u;
   const uint32_t n = min(*B.n_loc, B.cap_loc);
   for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n;
        i += gridDim.x * blockDim.x) {
     const uint32_t c = cell_id[i];
-    if (c == kNoCell) continue;                              // the other binning phase's
+    if (c < c_lo || c >= c_hi) continue;                     // the other binning phase's
     const uint32_t pos = cell_start[c] + slot[i];
     float4 s = B.loc_rec[i];
     const uint32_t id = B.loc_id[i];

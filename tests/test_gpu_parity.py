@@ -605,3 +605,38 @@ def test_out_of_box_actions_are_clamped(cuda):
     torch.cuda.synchronize()
     parity.check_integrate(p, host(st), oracle.integrate(p, prev, act))
     w.close()
+
+
+@pytest.mark.parametrize("env", ["flock", "tag"])
+def test_sense_columns_partition_equals_sense(cuda, env):
+    # vg_sense_columns over a partition of the grid columns (the replicated-state scheme,
+    # DESIGN.md §7b) writes every row exactly as vg_sense does; a range writes only the rows
+    # of agents binned in its columns.
+    torch = _torch()
+    p = (vi.flock_params(20000, width=200.0, d_v=10.0) if env == "flock"
+         else vi.tag_params(20000, width=200.0, d_v=10.0))
+    w = make_world(p)
+    st = dev(vi.init_state(p, seed=12))
+    w.bin(st)
+    full = w.alloc_outputs()
+    w.sense(full)
+    part = w.alloc_outputs()
+    for k in ("obs", "reward", "n_neigh", "n_collide", "sector_occ", "n_touch"):
+        t = getattr(part, k)
+        if t is not None:
+            t.view(torch.int32).fill_(-7)
+    G = w.grid
+    cuts = [0, 5, 11, G]
+    w.sense_columns(part, cuts[0], cuts[1])
+    torch.cuda.synchronize()
+    cx = np.floor(host(st)[0, :, 0].astype(np.float32) * np.float32(np.float32(G) / np.float32(p.width)))
+    first = np.minimum(cx, G - 1) < cuts[1]
+    got = host(part.n_neigh)[0].view(np.int32)
+    assert np.all(got[~first] == -7) and np.all(got[first] != -7)
+    for a, b in zip(cuts[1:-1], cuts[2:]):
+        w.sense_columns(part, a, b)
+    torch.cuda.synchronize()
+    for k in ("obs", "reward", "n_neigh", "n_collide", "sector_occ", "n_touch"):
+        if getattr(full, k) is not None:
+            assert torch.equal(getattr(part, k).view(torch.int32), getattr(full, k).view(torch.int32)), k
+    w.close()

@@ -30,8 +30,11 @@ def launches(path):
     rows = [r for r in csv.reader(open(path)) if len(r) > 5]
     hdr = rows[0]
     ki, vi = hdr.index("Kernel Name"), hdr.index("Metric Value")
+    mi = hdr.index("Metric Name") if "Metric Name" in hdr else None
     d = collections.defaultdict(list)
     for r in rows[1:]:
+        if mi is not None and r[mi] != "gpu__time_duration.sum":
+            continue                           # (launch lists may carry DRAM bytes too)
         d[r[ki].split("(")[0][:70]].append(float(r[vi].replace(",", "")))
     tot = sum(sum(v) for v in d.values())
     out = ["| kernel | launches | mean us | share of all GPU time |", "|---|---|---|---|"]
