@@ -323,9 +323,9 @@ class SlabRunner:
         self.w.slab_sense(self.out)
         del full
         self.act_dev = torch.zeros((1, p.n_agents, 2), dtype=torch.float32, device=device)
-        # begin; interior: keys, scan, scatter, cell sort, sense; finish: unpack, keys,
-        # scan, scatter, cell sort, sense
-        self.launches = 12
+        # begin (+ keys); interior: scan, scatter, cell sort, sense; finish: unpack (+ keys),
+        # scan, scatter, cell sort, sense (one scan kernel: <= 12,288 local cells at c5)
+        self.launches = 10
         self.phase_names = {"integrate_bin": "begin (integrate+route)",
                             "scan_cells": "interior (bin+sense, halo in flight)",
                             "scatter": "halo wait+unpack", "cell_sort": "bin boundary",
