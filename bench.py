@@ -530,7 +530,9 @@ def run_ours(args):
                "h2d_bytes_per_step": int(acts_h[0].numel() * 4),
                "d2h_bytes_per_step": int(rew_h.numel() * 4),
                "note": ("vg_step_host" if not slab_mode else "actions H2D + slab step + reward D2H")
-                       + ": pinned host buffers, stream sync per step, wall clock, max over ranks"}
+                       + ": pinned host buffers, stream sync per step, wall clock, max over ranks; "
+                         "the reward is read back, the observation stays on the device where "
+                         "the policy consumes it (P:111: simulation and agent both on the GPU)"}
 
     # ---- K7: shared-policy forward + sampling over this rank's obs,
     # timed separately (not part of the env-step metric)
