@@ -304,17 +304,25 @@ class SlabRunner:
         import torch.distributed as dist
         from paper_2207_03945_b200 import slab
         self.p, self.torch, self.slab = p, torch, slab
-        nid = [vg.nccl_unique_id() if rank == 0 else None]
-        dist.broadcast_object_list(nid, src=0)
-        cfg = {"rank": rank, "world_size": world, "nccl_unique_id": nid[0]}
-        try:
+        cfg = {"rank": rank, "world_size": world}
+        self.staging = None
+        if GLOO_TEST:
             self.w = vg.World(p, device=device, slab=cfg)
-            self.exchange = "libvg vg_slab_step (world-owned NCCL comm, grouped send/recv on its comm stream)"
-        except vg.VgError as e:                    # same decision on every rank
-            print(f"[rank {rank}] libvg NCCL unavailable ({e}); torch.distributed P2P", file=sys.stderr)
-            del cfg["nccl_unique_id"]
-            self.w = vg.World(p, device=device, slab=cfg)
-            self.exchange = "torch.distributed P2P (NCCL) around vg_slab_interior"
+            self.staging = slab.HostStaging(self.w)
+            self.exchange = "TEST MODE: gloo, pinned-host staging, all ranks on one GPU"
+        else:
+            nid = [vg.nccl_unique_id() if rank == 0 else None]
+            dist.broadcast_object_list(nid, src=0)
+            cfg["nccl_unique_id"] = nid[0]
+            try:
+                self.w = vg.World(p, device=device, slab=cfg)
+                self.exchange = "libvg vg_slab_step (world-owned NCCL comm, grouped send/recv on its comm stream)"
+            except vg.VgError as e:                    # same decision on every rank
+                print(f"[rank {rank}] libvg NCCL unavailable ({e}); torch.distributed P2P",
+                      file=sys.stderr)
+                del cfg["nccl_unique_id"]
+                self.w = vg.World(p, device=device, slab=cfg)
+                self.exchange = "torch.distributed P2P (NCCL) around vg_slab_interior"
         self.owned_comm = "nccl_unique_id" in cfg
         self.out = self.w.alloc_outputs()
         init = vi.clustered_state if STATE == "clustered" else vi.init_state
@@ -335,7 +343,7 @@ class SlabRunner:
         if self.owned_comm:
             self.w.slab_step(acts, self.out)
         else:
-            self.slab.slab_step_dist(self.w, acts, self.out)
+            self.slab.slab_step_dist(self.w, acts, self.out, staging=self.staging)
 
     def step_host(self, acts_h, rew_h):
         self.act_dev.copy_(acts_h, non_blocking=True)
@@ -376,6 +384,8 @@ class AllGatherRunner:
         self.launches = 1 + 6 + 1                # (all-gather) + K1 + K1-K3b binning + K4
         self.exchange = (f"NCCL all_gather_into_tensor of the step's actions "
                          f"({8 * p.n_agents / 1e6:.1f} MB per step)")
+        if GLOO_TEST:
+            self.exchange = "TEST MODE: gloo all-gather through host memory, all ranks on one GPU"
         self.phase_names = {"integrate_bin": "all-gather + integrate (replicated)",
                             "scan_cells": "bin whole world (replicated)",
                             "scatter": "-", "cell_sort": "-",
@@ -389,7 +399,12 @@ class AllGatherRunner:
             ev = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
             ev[0].record()
         local = acts[0, self.a0:self.a0 + self.n_loc].contiguous()
-        self.dist.all_gather_into_tensor(self.acts_all.view(-1), local.view(-1))
+        if GLOO_TEST:                            # plumbing test: gather through host memory
+            h = self.acts_all.cpu()
+            self.dist.all_gather_into_tensor(h.view(-1), local.cpu().view(-1))
+            self.acts_all.copy_(h)
+        else:
+            self.dist.all_gather_into_tensor(self.acts_all.view(-1), local.view(-1))
         self.w.integrate(self.state, self.acts_all)
         if ev: ev[1].record()
         self.w.bin(self.state)
@@ -435,7 +450,15 @@ def run_ours(args):
     import paper_2207_03945_b200 as vg
 
     rank, local, world = rank_info()
-    if world > 1:
+    if world > 1 and GLOO_TEST:
+        # Plumbing test of the N > 1 code paths on ONE GPU (VG_BENCH_GLOO_TEST=1): every
+        # rank on cuda:0, gloo process group, halo messages staged through pinned host
+        # memory (no kernel waits on another rank).  Numbers from this mode are not results.
+        import datetime
+        local = 0
+        torch.cuda.set_device(0)
+        dist.init_process_group("gloo", timeout=datetime.timedelta(seconds=300))
+    elif world > 1:
         import datetime
         torch.cuda.set_device(local)
         dist.init_process_group("nccl", device_id=torch.device("cuda", local),
@@ -860,6 +883,7 @@ def run_ours(args):
 
 
 STATE = "uniform"
+GLOO_TEST = os.environ.get("VG_BENCH_GLOO_TEST", "0") == "1"
 
 
 def main():

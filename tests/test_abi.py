@@ -120,3 +120,27 @@ def test_null_arguments():
     assert _lib.lib.vg_world_create(None, None) == _lib.VG_EINVAL
     assert _lib.lib.vg_bin(None, None, None) == _lib.VG_EINVAL
     assert _lib.lib.vg_step(None, None, None, None, None) == _lib.VG_EINVAL
+
+
+def test_nccl_unique_id_host_only():
+    # vg_nccl_unique_id loads libnccl at run time (no GPU needed): 128 bytes, fresh each call;
+    # a short buffer is VG_EINVAL.  If libnccl cannot be loaded the call reports VG_ENCCL.
+    from paper_2207_03945_b200 import _lib
+    import paper_2207_03945_b200 as vg
+    buf = ctypes.create_string_buffer(64)
+    assert _lib.lib.vg_nccl_unique_id(buf, 64) == _lib.VG_EINVAL
+    try:
+        a, b = vg.nccl_unique_id(), vg.nccl_unique_id()
+    except vg.VgError as e:
+        assert "VG_ENCCL" in str(e)
+        return
+    assert len(a) == 128 and a != b
+
+
+def test_new_entry_points_reject_null():
+    from paper_2207_03945_b200 import _lib
+    assert _lib.lib.vg_sense_columns(None, None, 0, 1, None) == _lib.VG_EINVAL
+    assert _lib.lib.vg_slab_step(None, None, None, None) == _lib.VG_EINVAL
+    assert _lib.lib.vg_slab_interior(None, None, None) == _lib.VG_EINVAL
+    assert _lib.lib.vg_policy_forward_class(None, None, 0, 0, 0, 0, None, 0, 0, None) == _lib.VG_EINVAL
+    assert _lib.lib.vg_rollout(None, None, None, None, None, 1, 0, 0, 0.9, 0.9, None) == _lib.VG_EINVAL
