@@ -350,6 +350,9 @@ vg_status launch_check(const char* what) {
 // K4 work items (WorkList, appended by K3b / the fused bin): queries per item, chosen so a world has ~4 items per
 // resident CTA when it is small (c1-c3) and whole cells (~54 queries at c5) when it is
 // large; dense cells (clusters) are split into many items.
+#ifndef VG_SLAB_BCHUNK
+#define VG_SLAB_BCHUNK 0   // slab boundary-phase K4 chunk (8 measured 2.1x slower: per-CTA setup)
+#endif
 int sense_chunk_q(const vg_world* w) {
   const long long queries = w->slab ? (long long)w->P.N / w->cfg.world_size : w->P.total;
 #ifndef VG_SENSE_ITEMS_PER_SLOT
@@ -370,6 +373,10 @@ vg::WorkList work_list(vg_world* w) {
   WL.chunk_q = sense_chunk_q(w);
   WL.lo = 0;                                              // slab: owned memory columns 0..W-1
   WL.hi = w->slab ? w->SL.W * w->P.G : w->n_cells;
+  WL.G = w->P.G;
+  WL.nb = w->slab ? w->SL.nb : 0;
+  WL.chunk_qb = w->slab ? w->SL.chunk_qb : WL.chunk_q;
+  for (int k = 0; k < 4; ++k) WL.bcol[k] = w->SL.bcol[k];
   return WL;
 }
 
@@ -432,7 +439,7 @@ vg_status launch_fused_bin(vg_world* w, float4* io, const float4* in, const floa
 // Cells [c0, c1) (default: all), + the sentinel row at c1.
 vg_status launch_cell_sort(vg_world* w, cudaStream_t s, int c0 = 0, int c1 = -1) {
   if (c1 < 0) c1 = w->n_cells;
-  if (w->n_cells <= (long long)VG_CTA_SORT_CELLS_PER_SM * w->n_sm) {
+  if (c1 - c0 <= (long long)VG_CTA_SORT_CELLS_PER_SM * w->n_sm) {
     vg::k_cell_sort_cta<<<(unsigned)(c1 - c0 + 1), vg::kCtaSortThreads, 0, s>>>(
         w->P, c1, w->slab ? 1 : 0, w->cell_start, w->tmp_rec, w->tmp_id, w->sorted,
         w->perm, w->xo_rec, w->xo_perm, w->xo_xy, w->sub_tab, work_list(w), w->slot, c0);
@@ -556,7 +563,8 @@ void sense_kernel(vg_world* w, int cells, const vg::Outs& O, cudaStream_t s) {
   const int cq = sense_chunk_q(w);
   // one CTA per sensed cell + an upper bound on the overflow items (surplus CTAs exit)
   const long long queries = w->slab ? (long long)w->P.N : w->P.total;
-  const unsigned grid = (unsigned)(cells + std::min<long long>(queries / cq + 1, w->work_cap));
+  const int cq_min = w->slab ? std::min(cq, w->SL.chunk_qb) : cq;
+  const unsigned grid = (unsigned)(cells + std::min<long long>(queries / cq_min + 1, w->work_cap));
   if (w->cfg.vision == VG_VISION_RAY && VISION && w->sense_def)
     vg::k_sense<ENV, VISION, SLAB, true, VISION><<<grid, vg::kSenseWarps * 32, 0, s>>>(
         w->P, w->cell_start, w->xo_rec, w->xo_xy, w->xo_perm, O, w->SL, w->ray_dir, w->sub_tab,
@@ -728,6 +736,13 @@ vg_status vg_world_create(const vg_config* cfg, vg_world** out) {
     const int P = cfg->world_size, W = g / P;
     w->slab = true;
     w->SL = vg::Slab{cfg->rank * W, (cfg->rank + 1) * W, W, (W + 2) * g};
+    // the boundary phase's columns: memory 0, W-3, W-2, W-1 (W >= 5), with
+    // their own K4 chunk size VG_SLAB_BCHUNK (0: the same as every other cell)
+    if (W >= 5 && VG_SLAB_BCHUNK > 0) {
+      w->SL.nb = 4;
+      w->SL.bcol[0] = 0; w->SL.bcol[1] = W - 3; w->SL.bcol[2] = W - 2; w->SL.bcol[3] = W - 1;
+    }
+    w->SL.chunk_qb = VG_SLAB_BCHUNK > 0 ? VG_SLAB_BCHUNK : sense_chunk_q(w);
     w->n_cells = w->SL.n_lcells;
     w->left = (cfg->rank + P - 1) % P;
     w->right = (cfg->rank + 1) % P;

@@ -78,6 +78,9 @@ struct Slab {
   // cells sensed by this K4 launch: memory columns [sc0, sc0 + snc), or, if snl > 0, the
   // memory columns scol[0..snl)
   int sc0, snc, snl, scol[4];
+  // the boundary phase's memory columns bcol[0..nb) are cut into K4 work items of chunk_qb
+  // queries (WorkList has the same fields for the items' creation)
+  int chunk_qb, nb, bcol[4];
 };
 __host__ __device__ __forceinline__ int slab_mcol(int l, int W) {
   return (l >= 2 && l <= W - 1) ? l - 2 : (l == 1) ? W - 2 : (l == W) ? W - 1 : (l == 0) ? W : W + 1;
@@ -356,12 +359,20 @@ struct WorkList {
   uint32_t* n;          // item count (zeroed by the kernel before the appending one)
   int chunk_q;
   int lo, hi;           // local cells [lo, hi) are sensed, as item cell index (cell - lo)
+  // slab mode: the cells of memory columns bcol[0..nb) (sensed by the boundary-phase K4,
+  // a small launch) are cut into chunks of chunk_qb queries (more, shorter work items)
+  int chunk_qb, nb, G, bcol[4];
 };
 
+__device__ __forceinline__ uint32_t work_chunk_q(const WorkList& WL, int cell) {
+  bool b = false;
+  for (int k = 0; k < 4; ++k) b |= (k < WL.nb && WL.bcol[k] == cell / WL.G);
+  return (uint32_t)(b ? WL.chunk_qb : WL.chunk_q);
+}
 // Overflow chunks of a cell (its chunks after the first; K4 CTA c senses the first one).
 __device__ __forceinline__ uint32_t work_chunks(const WorkList& WL, int cell, uint32_t m) {
-  return (cell >= WL.lo && cell < WL.hi && m > (uint32_t)WL.chunk_q)
-             ? (m - 1u) / (uint32_t)WL.chunk_q : 0u;
+  const uint32_t cq = work_chunk_q(WL, cell);
+  return (cell >= WL.lo && cell < WL.hi && m > cq) ? (m - 1u) / cq : 0u;
 }
 
 // --------------------------------------------------------------------------------- K3b
@@ -533,7 +544,7 @@ __global__ void __launch_bounds__(256) k_cell_sort(
   if (cell < n_cells) {
     const uint32_t nch = work_chunks(WL, cell, m0), at = s_base + s_nch[wib];
     for (uint32_t k = lane; k < nch; k += 32)
-      WL.item[at + k] = make_uint2((uint32_t)(cell - WL.lo), b0 + (k + 1u) * (uint32_t)WL.chunk_q);
+      WL.item[at + k] = make_uint2((uint32_t)(cell - WL.lo), b0 + (k + 1u) * work_chunk_q(WL, cell));
   }
   if (cell > n_cells) return;
   const uint32_t b = cell_start[cell];
@@ -616,7 +627,7 @@ __global__ void __launch_bounds__(kCtaSortThreads) k_cell_sort_cta(
     const uint32_t nch = work_chunks(WL, cell, (uint32_t)m);
     const uint32_t at = nch ? atomicAdd(WL.n, nch) : 0u;
     for (uint32_t k = 0; k < nch; ++k)
-      WL.item[at + k] = make_uint2((uint32_t)(cell - WL.lo), b + (k + 1u) * (uint32_t)WL.chunk_q);
+      WL.item[at + k] = make_uint2((uint32_t)(cell - WL.lo), b + (k + 1u) * work_chunk_q(WL, cell));
   }
   const int ca = cell % P.G;
   if (m > kCtaRankMax) {                                 // rare: the warp path
@@ -1459,8 +1470,12 @@ __global__ void __launch_bounds__(kSenseWarps * 32, (DEF && ENV == kTag) ? VG_SE
   }
     __syncthreads();
     const int nseg = s_nseg;
+    uint32_t cq = (uint32_t)chunk_q;
+    if (SLAB)
+      for (int k2 = 0; k2 < 4; ++k2)
+        if (k2 < SL.nb && SL.bcol[k2] == c / P.G) cq = (uint32_t)SL.chunk_qb;
     const uint32_t qb = (item.y == 0xffffffffu) ? cs[cl] : item.y;
-    const uint32_t qe = min(cs[cl + 1], qb + (uint32_t)chunk_q);
+    const uint32_t qe = min(cs[cl + 1], qb + cq);
     const uint32_t qstride = NQ * kSenseWarps;
     for (uint32_t q0 = qb + NQ * warp; q0 < qe; q0 += qstride) {
     float4 me[NQ];
