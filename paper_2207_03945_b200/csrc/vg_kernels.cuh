@@ -1209,15 +1209,13 @@ __device__ __forceinline__ f32x2 pk2(float lo, float hi) {
   return r;
 }
 __device__ __forceinline__ float lo2(f32x2 r) {
-  float a, b;
-  asm("mov.b64 {%0, %1}, %2;" : "=f"(a), "=f"(b) : "l"(r));
-  (void)b;
+  float a;
+  asm("{\n\t.reg .f32 t;\n\tmov.b64 {%0, t}, %1;\n\t}" : "=f"(a) : "l"(r));
   return a;
 }
 __device__ __forceinline__ float hi2(f32x2 r) {
-  float a, b;
-  asm("mov.b64 {%0, %1}, %2;" : "=f"(a), "=f"(b) : "l"(r));
-  (void)a;
+  float b;
+  asm("{\n\t.reg .f32 t;\n\tmov.b64 {t, %0}, %1;\n\t}" : "=f"(b) : "l"(r));
   return b;
 }
 __device__ __forceinline__ f32x2 sub2(f32x2 a, f32x2 b) {
