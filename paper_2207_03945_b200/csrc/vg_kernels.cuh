@@ -856,7 +856,7 @@ constexpr int kRBThreads = VG_RB_THREADS;   // warps per replica CTA x 32; 2048 
 //           and load latencies overlap the other's work); 16-bit staging of perm and the
 //           per-warp counts; the state is read through L2 (prefetched).
 constexpr int kRBStagedMax = 5120;
-constexpr int kRBStagedSmem = kRBStagedMax * (16 + 16 + 4 + 1);   // MODE 1: state, sorted, perm, cell id
+constexpr int kRBStagedSmem = kRBStagedMax * (16 + 16 + 4 + 1 + 1);   // MODE 1: state, sorted, perm, cell id, rank
 constexpr int kRBStaged2Smem = kRBStagedMax * (16 + 2 + 1);       // MODE 2: sorted, perm (u16), cell id
 constexpr int kRB2Threads = 512;
 template <int MODE> struct RBCfg {
@@ -893,6 +893,7 @@ __global__ void __launch_bounds__(RBCfg<MODE>::NT, RBCfg<MODE>::MINB) k_replica_
   float4* s_sorted = st + (TMA ? kRBStagedMax : 0);                // cell order
   PermT* s_perm = reinterpret_cast<PermT*>(s_sorted + kRBStagedMax);
   uint8_t* s_cid = reinterpret_cast<uint8_t*>(s_perm + kRBStagedMax);
+  uint8_t* s_rank = s_cid + kRBStagedMax;                          // MODE 1 (span <= 160 < 256)
   // Ask L2 for a replica's input (state, actions) up front: the warp walks its range one
   // 32-agent round at a time, so later rounds wait on L2, not HBM.  STAGED: the whole CTA
   // prefetches the next replica while processing the current one.
@@ -998,7 +999,20 @@ __global__ void __launch_bounds__(RBCfg<MODE>::NT, RBCfg<MODE>::MINB) k_replica_
       if (STAGED) s_cid[i] = (uint8_t)c;               // re-read in pass 2 (same warp)
     }
     const unsigned grp = __match_any_sync(kFull, c);
-    if (valid && (grp & lt) == 0u) s_wc[warp][c] += __popc(grp);
+    if (TMA) {
+      // MODE 1: each record's rank among its warp's earlier records of its cell, kept for
+      // pass 2 (which then has no round-to-round dependency)
+      const int leader = __ffs(grp) - 1;
+      uint32_t old = 0u;
+      if (valid && lane == leader) {
+        old = s_wc[warp][c];
+        s_wc[warp][c] = old + (uint32_t)__popc(grp);
+      }
+      old = __shfl_sync(kFull, old, leader);
+      if (valid) s_rank[i] = (uint8_t)(old + (uint32_t)__popc(grp & lt));
+    } else if (valid && (grp & lt) == 0u) {
+      s_wc[warp][c] += __popc(grp);
+    }
     __syncwarp();
   }
   __syncthreads();
@@ -1069,6 +1083,16 @@ __global__ void __launch_bounds__(RBCfg<MODE>::NT, RBCfg<MODE>::MINB) k_replica_
   }
   __syncthreads();
   // ---- pass 2: in-order walk of this warp's range, stable positions, scatter
+  if (TMA) {                         // position = cell start + earlier warps + own rank
+    for (int i = i0 + lane; i < i1; i += 32) {
+      const uint32_t c = s_cid[i];
+      const uint32_t pos = s_tot[c] + s_wc[warp][c] + (uint32_t)s_rank[i];
+      float4 s = st[i];
+      if (ENV == kTag) s.w = (i >= P.first_chaser) ? 1.f : 0.f;
+      s_sorted[pos] = s;
+      s_perm[pos] = (PermT)i;
+    }
+  } else
   for (int b = i0; b < i1; b += 32) {
     const int i = b + lane;
     const bool valid = i < i1;
