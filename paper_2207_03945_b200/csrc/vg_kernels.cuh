@@ -411,28 +411,17 @@ __device__ __forceinline__ unsigned bin_lanes(const unsigned (&bits)[kSubBits], 
 // Sense order of one cell from its stable (id-ordered) records [b, b + m): a stable counting
 // sort by sub-bin, one warp.  Writes xo_* and the cell's kSub table entries.
 // The cell's records are read from sorted[rb ..] / perm[rb ..] (rb = b, or a shared-memory
-// staging copy) and written to xo_*[b ..].
+// staging copy) and written to xo_*[b ..].  sense_order_place takes the sub-bin counts
+// (lane s < kSub: records of the cell in sub-bin s); sense_order_cell counts them first.
 template <typename PermT>
-__device__ __forceinline__ void sense_order_cell(const Params& P, int ca, bool axis_y,
-                                                 uint32_t b, int m,
-                                                 const float4* sorted, const PermT* perm,
-                                                 float4* __restrict__ xo_rec,
-                                                 uint32_t* __restrict__ xo_perm,
-                                                 float2* __restrict__ xo_xy, uint32_t* tab,
-                                                 int lane, unsigned lt, uint32_t rb) {
-  uint32_t cnt = 0;                                       // lane s < kSub: records in sub-bin s
-  for (int ib = 0; ib < m; ib += 32) {
-    const bool valid = ib + lane < m;
-    int sb = 0;
-    if (valid) {
-      const float4 rec = sorted[rb + ib + lane];
-      sb = sub_bin(P, ca, axis_y ? rec.y : rec.x);
-    }
-    unsigned bits[kSubBits];
-#pragma unroll
-    for (int k = 0; k < kSubBits; ++k) bits[k] = __ballot_sync(kFull, (sb >> k) & 1);
-    cnt += __popc(bin_lanes(bits, __ballot_sync(kFull, valid), lane));   // (lane < kSub used)
-  }
+__device__ __forceinline__ void sense_order_place(const Params& P, int ca, bool axis_y,
+                                                  uint32_t b, int m,
+                                                  const float4* sorted, const PermT* perm,
+                                                  float4* __restrict__ xo_rec,
+                                                  uint32_t* __restrict__ xo_perm,
+                                                  float2* __restrict__ xo_xy, uint32_t* tab,
+                                                  int lane, unsigned lt, uint32_t rb,
+                                                  uint32_t cnt) {
   uint32_t inc = cnt;                                     // exclusive scan over lanes < kSub
 #pragma unroll
   for (int o = 1; o < kSub; o <<= 1) {
@@ -465,6 +454,31 @@ __device__ __forceinline__ void sense_order_cell(const Params& P, int ca, bool a
     }
     run += __popc(bin_lanes(bits, vmask, lane));          // (lane < kSub used)
   }
+}
+
+template <typename PermT>
+__device__ __forceinline__ void sense_order_cell(const Params& P, int ca, bool axis_y,
+                                                 uint32_t b, int m,
+                                                 const float4* sorted, const PermT* perm,
+                                                 float4* __restrict__ xo_rec,
+                                                 uint32_t* __restrict__ xo_perm,
+                                                 float2* __restrict__ xo_xy, uint32_t* tab,
+                                                 int lane, unsigned lt, uint32_t rb) {
+  uint32_t cnt = 0;                                       // lane s < kSub: records in sub-bin s
+  for (int ib = 0; ib < m; ib += 32) {
+    const bool valid = ib + lane < m;
+    int sb = 0;
+    if (valid) {
+      const float4 rec = sorted[rb + ib + lane];
+      sb = sub_bin(P, ca, axis_y ? rec.y : rec.x);
+    }
+    unsigned bits[kSubBits];
+#pragma unroll
+    for (int k = 0; k < kSubBits; ++k) bits[k] = __ballot_sync(kFull, (sb >> k) & 1);
+    cnt += __popc(bin_lanes(bits, __ballot_sync(kFull, valid), lane));   // (lane < kSub used)
+  }
+  sense_order_place(P, ca, axis_y, b, m, sorted, perm, xo_rec, xo_perm, xo_xy, tab, lane, lt,
+                    rb, cnt);
 }
 
 // Dense cells (m > kRankMax): sort the cell's (id, arrival index) pairs by id with
@@ -856,13 +870,14 @@ constexpr int kRBThreads = VG_RB_THREADS;   // warps per replica CTA x 32; 2048 
 //           and load latencies overlap the other's work); 16-bit staging of perm and the
 //           per-warp counts; the state is read through L2 (prefetched).
 constexpr int kRBStagedMax = 5120;
-constexpr int kRBStagedSmem = kRBStagedMax * (16 + 16 + 4 + 1 + 1);   // MODE 1: state, sorted, perm, cell id, rank
+// MODE 1: state, sorted, perm, cell id, rank + the (cell, sub-bin) histogram (two u16 a word)
+constexpr int kRBStagedSmem = kRBStagedMax * (16 + 16 + 4 + 1 + 1) + kRBMaxCells * (kSub / 2) * 4;
 constexpr int kRBStaged2Smem = kRBStagedMax * (16 + 2 + 1);       // MODE 2: sorted, perm (u16), cell id
 constexpr int kRB2Threads = 512;
 template <int MODE> struct RBCfg {
   static constexpr int NT = MODE == 2 ? kRB2Threads : kRBThreads;
   static constexpr int MINB = MODE == 1 ? 1 : MODE == 2 ? 2 : 2048 / kRBThreads;
-  using WC = typename std::conditional<MODE == 2, uint16_t, uint32_t>::type;
+  using WC = typename std::conditional<MODE != 0, uint16_t, uint32_t>::type;
   using PermT = typename std::conditional<MODE == 2, uint16_t, uint32_t>::type;
 };
 
@@ -894,6 +909,7 @@ __global__ void __launch_bounds__(RBCfg<MODE>::NT, RBCfg<MODE>::MINB) k_replica_
   PermT* s_perm = reinterpret_cast<PermT*>(s_sorted + kRBStagedMax);
   uint8_t* s_cid = reinterpret_cast<uint8_t*>(s_perm + kRBStagedMax);
   uint8_t* s_rank = s_cid + kRBStagedMax;                          // MODE 1 (span <= 160 < 256)
+  uint32_t* s_sbh = reinterpret_cast<uint32_t*>(s_rank + kRBStagedMax);   // MODE 1
   // Ask L2 for a replica's input (state, actions) up front: the warp walks its range one
   // 32-agent round at a time, so later rounds wait on L2, not HBM.  STAGED: the whole CTA
   // prefetches the next replica while processing the current one.
@@ -934,6 +950,8 @@ __global__ void __launch_bounds__(RBCfg<MODE>::NT, RBCfg<MODE>::MINB) k_replica_
   for (int r = blockIdx.x; r < P.R; r += r_step) {
   const size_t base = (size_t)r * N;
   for (int c = lane; c < C; c += 32) s_wc[warp][c] = 0u;
+  if (TMA)
+    for (int e = tid; e < C * (kSub / 2); e += NT) s_sbh[e] = 0u;
   if (VG_RB_PREFETCH) {
     if (!STAGED && i1 > i0) {
       pf(src + base + i0, (size_t)(i1 - i0) * sizeof(float4), lane, 32);
@@ -1091,6 +1109,9 @@ __global__ void __launch_bounds__(RBCfg<MODE>::NT, RBCfg<MODE>::MINB) k_replica_
       if (ENV == kTag) s.w = (i >= P.first_chaser) ? 1.f : 0.f;
       s_sorted[pos] = s;
       s_perm[pos] = (PermT)i;
+      // the (cell, sub-bin) histogram for pass 3's sense order (no count pass there)
+      const int sb = sub_bin(P, (int)(c % (uint32_t)P.G), s.x);
+      atomicAdd(&s_sbh[c * (kSub / 2) + (sb >> 1)], (sb & 1) ? 65536u : 1u);
     }
   } else
   for (int b = i0; b < i1; b += 32) {
@@ -1124,7 +1145,13 @@ __global__ void __launch_bounds__(RBCfg<MODE>::NT, RBCfg<MODE>::MINB) k_replica_
   // ---- pass 3: K4 sense order of each cell (see K3b)
   for (int c = warp; c < C; c += NW) {
     const int m = ((c + 1 < C) ? (int)s_tot[c + 1] : N) - (int)s_tot[c];
-    if (STAGED) {
+    if (TMA) {
+      const uint32_t c0 = s_tot[c];
+      const uint32_t w2 = (lane < kSub) ? s_sbh[c * (kSub / 2) + (lane >> 1)] : 0u;
+      sense_order_place(P, c % P.G, false, (uint32_t)base + c0, m, s_sorted, s_perm, xo_rec,
+                        xo_perm, xo_xy, sub_tab + ((size_t)r * C + c) * kSub, lane, lt, c0,
+                        (lane & 1) ? (w2 >> 16) : (w2 & 0xffffu));
+    } else if (STAGED) {
       const uint32_t c0 = s_tot[c];
       sense_order_cell(P, c % P.G, false, (uint32_t)base + c0, m, s_sorted, s_perm,
                        xo_rec, xo_perm, xo_xy, sub_tab + ((size_t)r * C + c) * kSub, lane, lt,
