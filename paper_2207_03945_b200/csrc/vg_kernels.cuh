@@ -1051,29 +1051,15 @@ __global__ void __launch_bounds__(RBCfg<MODE>::NT, RBCfg<MODE>::MINB) k_replica_
   }
   __syncthreads();
   // ---- per cell: exclusive scan over the NW warps; totals per cell
-  if (NW == 32) {                    // one warp per cell, lane w = warp w's count: 5 shuffles
-    for (int cc = warp; cc < C; cc += NW) {
-      const uint32_t t = s_wc[lane][cc];
-      uint32_t inc = t;
+  for (int cc = tid; cc < C; cc += NT) {
+    uint32_t run = 0;
 #pragma unroll
-      for (int o = 1; o < 32; o <<= 1) {
-        const uint32_t y = __shfl_up_sync(kFull, inc, o);
-        if (lane >= o) inc += y;
-      }
-      s_wc[lane][cc] = inc - t;
-      if (lane == 31) s_tot[cc] = inc;
+    for (int w = 0; w < NW; ++w) {
+      const uint32_t t = s_wc[w][cc];
+      s_wc[w][cc] = run;
+      run += t;
     }
-  } else {
-    for (int cc = tid; cc < C; cc += NT) {
-      uint32_t run = 0;
-#pragma unroll
-      for (int w = 0; w < NW; ++w) {
-        const uint32_t t = s_wc[w][cc];
-        s_wc[w][cc] = run;
-        run += t;
-      }
-      s_tot[cc] = run;
-    }
+    s_tot[cc] = run;
   }
   __syncthreads();
   // ---- exclusive scan over the (<= 256) cells by warp 0: 8 consecutive cells per lane
