@@ -962,12 +962,14 @@ __global__ void __launch_bounds__(RBCfg<MODE>::NT, RBCfg<MODE>::MINB) k_replica_
       pf(actions + (size_t)blockIdx.x * N, (size_t)N * sizeof(float2), tid, NT);
     __syncthreads();
   }
+  if (TMA) {                         // pass 3 re-zeroes each cell's counts after use
+    for (int e = tid; e < kRBMaxCells * (kSub / 2); e += NT) s_sbh[e] = 0u;
+    __syncthreads();
+  }
   uint32_t phase = 0u;
   for (int r = blockIdx.x; r < P.R; r += r_step) {
   const size_t base = (size_t)r * N;
   for (int c = lane; c < C; c += 32) s_wc[warp][c] = 0u;
-  if (TMA)
-    for (int e = tid; e < C * (kSub / 2); e += NT) s_sbh[e] = 0u;
   if (VG_RB_PREFETCH) {
     if (!STAGED && i1 > i0) {
       pf(src + base + i0, (size_t)(i1 - i0) * sizeof(float4), lane, 32);
@@ -1164,6 +1166,8 @@ __global__ void __launch_bounds__(RBCfg<MODE>::NT, RBCfg<MODE>::MINB) k_replica_
     if (TMA) {
       const uint32_t c0 = s_tot[c];
       const uint32_t w2 = (lane < kSub) ? s_sbh[c * (kSub / 2) + (lane >> 1)] : 0u;
+      __syncwarp();
+      if (lane < kSub / 2) s_sbh[c * (kSub / 2) + lane] = 0u;      // ready for the next replica
       sense_order_place(P, c % P.G, false, (uint32_t)base + c0, m, s_sorted, s_perm, xo_rec,
                         xo_perm, xo_xy, sub_tab + ((size_t)r * C + c) * kSub, lane, lt, c0,
                         (lane & 1) ? (w2 >> 16) : (w2 & 0xffffu));
@@ -1179,7 +1183,11 @@ __global__ void __launch_bounds__(RBCfg<MODE>::NT, RBCfg<MODE>::MINB) k_replica_
     }
   }
   if (r == P.R - 1 && tid == 0) sub_tab[(size_t)P.R * C * kSub] = (uint32_t)P.total;
-  __syncthreads();                   // s_wc, s_tot, s_cid and this buffer are reused next
+  // MODE 1 needs no barrier here: a warp done with pass 3 goes on to the next replica's
+  // pass 1, which touches only its own s_wc row, s_cid / s_rank / st (pass 3 reads none of
+  // them) and the new TMA'd state; s_tot and s_sorted are rewritten only after the barrier
+  // that ends that pass 1, when every warp has finished this pass 3.
+  if (!TMA) __syncthreads();         // s_wc, s_tot, s_cid and this buffer are reused next
   }
 }
 
