@@ -46,8 +46,16 @@ constexpr int kABytes = kPolTile * kPolK1 * 2;             // 36864
 constexpr int kOffC = kOffA + 2 * kABytes;                 // fp32 constants
 // consts: b1[128] b2[128] | b3_0 b3_1 c3 pad | log_std[2] | lo[2] hi[2]
 constexpr int kConstFloats = 128 + 128 + 4 + 2 + 4;
-constexpr int kOffBar = kOffC + ((kConstFloats * 4 + 15) / 16) * 16;   // 4 mbarriers + tmem slot
-constexpr int kOffStage = ((kOffBar + 48 + 127) / 128) * 128;            // raw fp32 obs tile (TMA)
+// VG_POL_QUARTERS: each tile's obs arrive as four 32-row TMA copies with a barrier each, and
+// a quarter of the stage is re-filled with the next tile's rows as soon as it is converted
+// (the next tile's transfer overlaps this tile's conversion instead of following it).
+#ifndef VG_POL_QUARTERS
+#define VG_POL_QUARTERS 0
+#endif
+constexpr int kPolQ = VG_POL_QUARTERS ? 4 : 1;           // TMA pieces per tile
+constexpr int kOffBar = kOffC + ((kConstFloats * 4 + 15) / 16) * 16;   // mbarriers + tmem slot
+constexpr int kBarBytes = 8 * (2 + 2 * kPolQ) + 16;
+constexpr int kOffStage = ((kOffBar + kBarBytes + 127) / 128) * 128;     // raw fp32 obs tile (TMA)
 constexpr int kStageBytes = kPolTile * kPolK1 * 4;                       // >= 128 rows x obs_dim
 constexpr int kPolSmem = kOffStage + kStageBytes;
 
@@ -254,10 +262,10 @@ __global__ void __launch_bounds__(kPolThreads, 1) k_policy(
   __half* sB3 = reinterpret_cast<__half*>(smem + kOffB3);
   float* sC = reinterpret_cast<float*>(smem + kOffC);
   const float* sStage = reinterpret_cast<const float*>(smem + kOffStage);
-  // mbarriers: [g] MMA completion of group g; [2 + g] TMA arrival of group g's tiles (a
-  // barrier per group keeps each one's phases in its own tile order).
+  // mbarriers: [g] MMA completion of group g; [2 + g kPolQ + q] TMA arrival of piece q of
+  // group g's tiles (a barrier per group keeps each one's phases in its own tile order).
   uint64_t* bar = reinterpret_cast<uint64_t*>(smem + kOffBar);
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + kOffBar + 32);
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + kOffBar + 8 * (2 + 2 * kPolQ));
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int g = warp >> 3, gw = warp & 7, gtid = tid & (kPolGroup - 1);
   __half* sA = reinterpret_cast<__half*>(smem + kOffA + g * kABytes);
@@ -281,7 +289,7 @@ __global__ void __launch_bounds__(kPolThreads, 1) k_policy(
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
   }
   if (tid == 0) {
-    for (int i = 0; i < 4; ++i)
+    for (int i = 0; i < 2 + 2 * kPolQ; ++i)
       asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&bar[i])));
     asm volatile("fence.mbarrier_init.release.cluster;");
   }
@@ -290,8 +298,8 @@ __global__ void __launch_bounds__(kPolThreads, 1) k_policy(
   __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;");
   const uint32_t tmem = *tmem_slot + (uint32_t)(g * 256);   // D: +0..127, D3: +128..143
-  const uint32_t bar_mma = smem_u32(&bar[g]), bar_tma = smem_u32(&bar[2 + g]);
-  const uint32_t bar_tma_next = smem_u32(&bar[3 - g]);      // the other group's
+  const uint32_t bar_mma = smem_u32(&bar[g]), bar_tma = smem_u32(&bar[2 + g * kPolQ]);
+  const uint32_t bar_tma_next = smem_u32(&bar[2 + (1 - g) * kPolQ]);   // the other group's
   const uint32_t stage = smem_u32(sStage);
   const uint32_t a = smem_u32(sA);
   const uint32_t b1 = smem_u32(sB1), b2 = smem_u32(sB2), b3 = smem_u32(sB3);
@@ -311,8 +319,12 @@ __global__ void __launch_bounds__(kPolThreads, 1) k_policy(
   const bool bulk_ok = (tile_bytes % 16u) == 0u &&
                        (reinterpret_cast<uintptr_t>(obs) % 16u) == 0u;
   auto is_full = [&](int64_t t) { return bulk_ok && (t + 1) * kPolTile <= M; };
+  const uint32_t piece_bytes = tile_bytes / kPolQ;         // 32 rows x obs_dim x 4 (16 | it)
   if (tid == 0 && blockIdx.x < n_tiles && is_full(blockIdx.x))     // group 0's first tile
-    tma_load_1d(stage, obs + (int64_t)blockIdx.x * kPolTile * obs_dim, tile_bytes, bar_tma);
+    for (int q = 0; q < kPolQ; ++q)
+      tma_load_1d(stage + q * piece_bytes,
+                  obs + ((int64_t)blockIdx.x * kPolTile + q * (kPolTile / kPolQ)) * obs_dim,
+                  piece_bytes, bar_tma + 8u * q);
 
   // MMA issue (one thread per group): ksteps K-steps of 16 from A (128 rows), B (rb rows).
   auto issue = [&](uint32_t d, uint32_t aa, uint32_t b, int ksteps, int rb, uint32_t idesc) {
@@ -377,14 +389,15 @@ __global__ void __launch_bounds__(kPolThreads, 1) k_policy(
        tile += 2 * (int64_t)gridDim.x) {
     const int64_t m0 = tile * kPolTile;
     const bool full = is_full(tile);
-    // ---- A1: obs rows -> fp16 core-matrix layout (zero pad rows >= M, cols >= obs_dim).
-    if (full) {                                          // this tile's TMA has landed
-      mbar_wait(bar_tma, ph_tma);
-      ph_tma ^= 1u;
-    }
+    // ---- A1: obs rows -> fp16 core-matrix layout (zero pad rows >= M, cols >= obs_dim),
+    // one TMA piece (kPolTile / kPolQ rows) at a time.
+    const int64_t nt = tile + gridDim.x;                 // the CTA's next tile (other group's)
+    constexpr int kPR = kPolTile / kPolQ;                // rows per piece
+    for (int q = 0; q < kPolQ; ++q) {
+    if (full) mbar_wait(bar_tma + 8u * q, ph_tma);       // this piece's TMA has landed
     // Thread -> (row r, 8-column chunk kc); a warp shares kc, so the chunk bounds are uniform.
-    for (int it = gtid; it < kPolTile * (kPolK1 / 8); it += kPolGroup) {
-      const int r = it % kPolTile, kc = it / kPolTile;
+    for (int it = gtid; it < kPR * (kPolK1 / 8); it += kPolGroup) {
+      const int r = q * kPR + it % kPR, kc = it / kPR;
       const int nv = obs_dim - kc * 8;                    // valid columns in this chunk
       const int64_t gr = m0 + r;
       float x[8];
@@ -410,15 +423,16 @@ __global__ void __launch_bounds__(kPolThreads, 1) k_policy(
       *reinterpret_cast<uint4*>(sA + cm_offset(r, kc * 8, kPolTile)) = pkd;
     }
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-    asm volatile("tcgen05.fence::before_thread_sync;");
+    if (q == kPolQ - 1) asm volatile("tcgen05.fence::before_thread_sync;");
     group_sync(g);
-    // ---- the stage is free: load the CTA's next tile (the other group's); layer 1
-    if (gtid == 0) {
-      const int64_t nt = tile + gridDim.x;
-      if (nt < n_tiles && is_full(nt))
-        tma_load_1d(stage, obs + nt * kPolTile * obs_dim, tile_bytes, bar_tma_next);
-      issue(tmem, a, b1, kPolK1 / 16, kPolN, kPolIdesc);
+    // ---- this piece of the stage is free: load the next tile's rows into it
+    if (gtid == 0 && nt < n_tiles && is_full(nt))
+      tma_load_1d(stage + q * piece_bytes, obs + (nt * kPolTile + q * kPR) * obs_dim,
+                  piece_bytes, bar_tma_next + 8u * q);
     }
+    if (full) ph_tma ^= 1u;
+    // ---- layer 1
+    if (gtid == 0) issue(tmem, a, b1, kPolK1 / 16, kPolN, kPolIdesc);
     wait_mma();
     hidden_epilogue(sC);                                 // h1 -> A (A1 consumed)
     // ---- layer 2
