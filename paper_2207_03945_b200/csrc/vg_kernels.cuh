@@ -868,6 +868,9 @@ constexpr int kRBMaxAgents = 32768;
 #ifndef VG_RB_PREFETCH
 #define VG_RB_PREFETCH 1
 #endif
+#ifndef VG_RB_APRE
+#define VG_RB_APRE 1
+#endif
 #ifndef VG_RB_THREADS
 #define VG_RB_THREADS 1024
 #endif
@@ -991,8 +994,22 @@ __global__ void __launch_bounds__(RBCfg<MODE>::NT, RBCfg<MODE>::MINB) k_replica_
     phase ^= 1u;
   }
   __syncwarp();
+  // MODE 1: every round's actions are requested before the first round is integrated (one
+  // L2 latency per replica instead of one per round)
+  constexpr int kRounds = TMA ? (kRBStagedMax / NW + 31) / 32 : 1;
+  float2 apre[kRounds];
+  if (TMA && INTEGRATE && VG_RB_APRE) {
+#pragma unroll
+    for (int k = 0; k < kRounds; ++k) {
+      const int i = i0 + 32 * k + lane;
+      apre[k] = (i < i1) ? actions[base + i] : make_float2(0.f, 0.f);
+    }
+  }
   // ---- pass 1: integrate + cell id + warp-private histogram
-  for (int b = i0; b < i1; b += 32) {
+#pragma unroll
+  for (int kr = 0; !TMA || kr < kRounds; ++kr) {    // MODE 1: a fixed trip count (unrolled)
+    const int b = i0 + 32 * kr;
+    if (b >= i1) break;
     const int i = b + lane;
     const bool valid = i < i1;
     uint32_t c = 0xFFFFFFFFu;
@@ -1003,7 +1020,7 @@ __global__ void __launch_bounds__(RBCfg<MODE>::NT, RBCfg<MODE>::MINB) k_replica_
                    s.z < P.two_pi);
       if (ENV == kFlock) bad |= !isfinite(s.w);
       if (INTEGRATE) {
-        const float2 a = actions[gi];
+        const float2 a = (TMA && VG_RB_APRE) ? apre[kr] : actions[gi];
         bad |= isnan(a.x) || isnan(a.y);
         float turn, dist;
         if (ENV == kFlock) {
