@@ -203,7 +203,9 @@ def sense_rows(p, state_r: np.ndarray, rows, overrides: dict | None = None) -> d
     hx, hy = np.cos(th), np.sin(th)
     fwd = hx * dx + hy * dy
     left = hx * dy - hy * dx
-    phi = np.arctan2(left, fwd)                 # atan2(0, 0) = 0 (A13)
+    # atan2(0, 0) = 0 (A13): a coincident agent is dead ahead.  Set explicitly: at d = 0,
+    # h . d and h x d are signed zeros, which IEEE atan2 maps to +-pi when cos(theta) < 0.
+    phi = np.where(d == 0.0, 0.0, np.arctan2(left, fwd))
     u = (phi + fov / 2.0) / fov
 
     in_r = d < p.d_v

@@ -131,6 +131,18 @@ def test_dead_ahead_is_banded():
     assert o2["obs"][0, 63] == pytest.approx(0.3, rel=1e-12) and o2["obs"][0, 64] == 1.0
 
 
+@pytest.mark.parametrize("heading", [0.0, 1.0, 2.5, 3.2, 4.2572885, 5.9])
+def test_coincident_agent_dead_ahead_any_heading(heading):
+    # A13: a coincident other agent (d = 0) is dead ahead, phi = 0, whatever the heading —
+    # including headings with cos < 0, where h . d and h x d are signed zeros that IEEE
+    # atan2 would map to +-pi (behind, outside the field of view).
+    p, st = world(vi.flock_params(2), [[50, 50, heading, 0.275], [50, 50, 1.0, 0.275]])
+    o = oracle.sense_rows(p, st[0], [0])
+    assert o["obs"][0, 64] == 0.0 and o["n_collide"][0] == 1 and o["n_neigh"][0] == 1
+    (j, alts), = o["bands"][0]
+    assert j == 1 and sorted(a[2] for a in alts) == [63, 64]
+
+
 def test_neighbours_match_kdtree():
     # Library routine: scipy cKDTree with periodic boxsize (uses <=; compare off-band).
     from scipy.spatial import cKDTree
