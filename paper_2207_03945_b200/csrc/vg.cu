@@ -806,7 +806,7 @@ vg_status vg_world_create(const vg_config* cfg, vg_world** out) {
   if (!st) st = dalloc(w, &w->sorted, n);
   if (!st) st = dalloc(w, &w->xo_rec, n);
   if (!st) st = dalloc(w, &w->xo_perm, n);
-  if (!st) st = dalloc(w, &w->xo_xy, n + 32 * vg::kSenseHalves);   // padded: unpredicated K4 loads
+  if (!st) st = dalloc(w, &w->xo_xy, n + vg::kSensePad);   // padded: unpredicated K4 loads
   if (!st) st = dalloc(w, &w->sub_tab, ((size_t)w->n_cells + 1) * vg::kSub);
   if (!st) {
     w->work_cap = (long long)w->n_cells + (long long)n / 8 + 1;       // chunk_q >= 8

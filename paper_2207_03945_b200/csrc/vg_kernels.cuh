@@ -1251,6 +1251,19 @@ constexpr int kSenseHalves = VG_SENSE_HALVES;
 #define VG_SENSE_QUEUE (VG_SENSE_HALVES > 2 ? 256 : 128)
 #endif
 constexpr int kQueue = VG_SENSE_QUEUE;
+// Flock sector vision (E8): 8-byte ring entries (dx, dy) — d^2 is recomputed bitwise in the
+// pair pass and the self pair is the entry with dx = dy = +0 (a coincident other agent is
+// restored at the emit) — so the same ring bytes hold 2 kQueue entries: VG_SENSE_E8_HALVES
+// 32-slot halves per chunk and one warp sync per chunk.
+#ifndef VG_SENSE_E8
+#define VG_SENSE_E8 1
+#endif
+#ifndef VG_SENSE_E8_HALVES
+#define VG_SENSE_E8_HALVES 4
+#endif
+static_assert(31 + 32 * VG_SENSE_E8_HALVES <= 2 * kQueue, "E8 ring: carried + one chunk of pushes");
+// candidate slots read past a window's end (xo_xy padding): the longest chunk of any instance
+constexpr int kSensePad = 32 * (VG_SENSE_E8_HALVES > kSenseHalves ? VG_SENSE_E8_HALVES : kSenseHalves);
 static_assert(kQueue >= 31 + 32 * kSenseHalves, "ring: carried + one chunk of pushes");
 
 // atan2(y, x) in (-pi, pi] with |error| <~ 3.3e-7 rad (the sector band is
@@ -1381,6 +1394,14 @@ __device__ __forceinline__ void sts128(uint32_t a, float4 v) {
                "f"(v.w)
                : "memory");
 }
+__device__ __forceinline__ void sts64(uint32_t a, float x, float y) {
+  asm volatile("st.shared.v2.f32 [%0], {%1, %2};" ::"r"(a), "f"(x), "f"(y) : "memory");
+}
+__device__ __forceinline__ float2 lds64(uint32_t a) {
+  float2 v;
+  asm volatile("ld.shared.v2.f32 {%0, %1}, [%2];" : "=f"(v.x), "=f"(v.y) : "r"(a) : "memory");
+  return v;
+}
 __device__ __forceinline__ float4 lds128(uint32_t a) {
   float4 v;
   asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
@@ -1463,6 +1484,11 @@ __global__ void __launch_bounds__(kSenseWarps * 32, (DEF && ENV == kTag) ? VG_SE
   // paired pair pass (process2).  Ray vision keeps the per-query pass.
   constexpr bool PAIRED = VG_SENSE_PAIRED && !RAY && NQ == 2;
   constexpr bool PACKED_SCAN = VG_SENSE_PACKED_SCAN && NQ == 2;
+  // Ring entry layout: E8 (flock sector vision) 8 bytes (dx, dy), else 16 (dx, dy, d^2, word).
+  constexpr bool E8 = VG_SENSE_E8 && ENV == kFlock && !RAY && !PAIRED && !PACKED_SCAN;
+  constexpr uint32_t ES = E8 ? 8u : 16u, ES_SH = E8 ? 3u : 4u;
+  constexpr uint32_t kRingMask = kQueue * 16u - ES;      // byte offsets within a ring
+  constexpr int HV = E8 ? VG_SENSE_E8_HALVES : kSenseHalves;   // 32-slot halves per chunk
   // Pair-pass constants.  (ptxas sees through this empty asm and re-loads them from the
   // parameter bank per pair batch; forcing them into registers with an opaque add costs 8
   // registers and measured 4 % slower.)
@@ -1598,13 +1624,27 @@ __global__ void __launch_bounds__(kSenseWarps * 32, (DEF && ENV == kTag) ? VG_SE
 
     const uint32_t srow = sh_addr(&s_min[warp][0][0]);         // this warp's sector rows
     const uint32_t seg_base = sh_addr(&s_seg[0]);
+    // Ring entry at byte offset `off` of query t's ring (E8: d^2 recomputed with the scan's
+    // own operation, bitwise the value it tested).
+    auto ring_entry = [&](const int t, const uint32_t off) {
+      if (E8) {
+        const float2 v = lds64(qbase[t] | (off & kRingMask));
+        return make_float4(v.x, v.y, fmaf(v.x, v.x, v.y * v.y), 0.f);
+      }
+      return lds128(qbase[t] | (off & kRingMask));
+    };
     // Pair pass over one queue entry (dx, dy, d^2, index | type << 31) of query t.
     auto process = [&](const int t, const float4 e) {
       const uint32_t tagbits = __float_as_uint(e.w);
       // j != i.  The sector pass takes no branch for it: the self pair (always in
       // the queue exactly once, at d = 0: a contact with f = -c_collide) is counted and
       // removed exactly at the emit; it only has to be kept out of the sector minima.
-      const bool self = ENV == kFlock ? tagbits == q0 + t : (tagbits & 0x7fffffffu) == q0 + t;
+      // E8 has no index: "self" is every entry at dx = dy = +0 (the self pair, and any other
+      // agent at exactly the same position, whose sector slot the emit restores; nnb counts
+      // them).
+      const bool self = E8 ? (__float_as_uint(e.x) | __float_as_uint(e.y)) == 0u
+                           : ENV == kFlock ? tagbits == q0 + t : (tagbits & 0x7fffffffu) == q0 + t;
+      if (E8) nnb[t] += self ? 1u : 0u;
       if ((RAY || PAIRED) && self) return;
       const uint32_t tj = (ENV == kTag) ? tagbits >> 31 : 0u;
       const float d2 = e.z;
@@ -1788,7 +1828,7 @@ __global__ void __launch_bounds__(kSenseWarps * 32, (DEF && ENV == kTag) ? VG_SE
         qx[t] = me[t].x + sg.qsx;                                     // exact (Sterbenz)
         qy[t] = me[t].y + sg.qsy;
       }
-      for (uint32_t p0 = wb; p0 < we; p0 += 32 * kSenseHalves) {
+      for (uint32_t p0 = wb; p0 < we; p0 += 32 * HV) {
         // Ballot the in-radius candidates of one 32-slot half and append them to each
         // query's ring (dx, dy, d^2, index | type << 31).
         auto scan = [&](const float cx_, const float cy_, const uint32_t word) {
@@ -1814,19 +1854,22 @@ __global__ void __launch_bounds__(kSenseWarps * 32, (DEF && ENV == kTag) ? VG_SE
             }
             const bool in = d2 < (RAY ? VG_SC(cand2) : VG_SC(dv2));                // Eq. 1: d < d_v
             const unsigned bal = __ballot_sync(kFull, in);
-            if (in)
-              sts128(qbase[t] | ((tail[t] + (__popc(bal & lt_mask) << 4)) & (kQueue * 16 - 16)),
+            if (E8) {
+              if (in) sts64(qbase[t] | ((tail[t] + (__popc(bal & lt_mask) << 3)) & kRingMask), dx, dy);
+            } else if (in) {
+              sts128(qbase[t] | ((tail[t] + (__popc(bal & lt_mask) << 4)) & kRingMask),
                      make_float4(dx, dy, d2, __uint_as_float(word)));
-            tail[t] += __popc(bal) << 4;
+            }
+            tail[t] += __popc(bal) << ES_SH;
           }
         };
-        // kSenseHalves 32-slot halves per chunk, 1 candidate per lane each (sorted_xy is
-        // padded by 32 kSenseHalves: no load predicate); slots past the run end get a NaN
+        // HV 32-slot halves per chunk, 1 candidate per lane each (sorted_xy is padded by
+        // kSensePad >= 32 HV: no load predicate); slots past the run end get a NaN
         // position, never within d_v of anyone; halves wholly past it are skipped.
-        float cxh[kSenseHalves], cyh[kSenseHalves];
-        uint32_t wh[kSenseHalves];
+        float cxh[HV], cyh[HV];
+        uint32_t wh[HV];
 #pragma unroll
-        for (int h = 0; h < kSenseHalves; ++h) {
+        for (int h = 0; h < HV; ++h) {
           const uint32_t pj = p0 + 32u * h + lane;
           const float2 o = __ldg(&sorted_xy[pj]);
           float x = o.x;
@@ -1837,10 +1880,10 @@ __global__ void __launch_bounds__(kSenseWarps * 32, (DEF && ENV == kTag) ? VG_SE
           }
           cxh[h] = (pj < we) ? x + sg.csx : __int_as_float(0x7fc00000);   // exact (Sterbenz)
           cyh[h] = o.y + sg.csy;
-          wh[h] = pj | tj;
+          wh[h] = E8 ? 0u : pj | tj;
         }
 #pragma unroll
-        for (int h = 0; h < kSenseHalves; ++h)
+        for (int h = 0; h < HV; ++h)
           if (h == 0 || p0 + 32u * h < we) scan(cxh[h], cyh[h], wh[h]);   // warp-uniform
         __syncwarp();                       // ring pushes above are visible to the warp
         if (PAIRED) {
@@ -1863,15 +1906,15 @@ __global__ void __launch_bounds__(kSenseWarps * 32, (DEF && ENV == kTag) ? VG_SE
         } else {
 #pragma unroll
           for (int t = 0; t < NQ; ++t) {
-            while (tail[t] - head[t] >= 32u * 16u) {
-              process(t, lds128(qbase[t] | ((head[t] + lane * 16u) & (kQueue * 16 - 16))));
-              head[t] += 32u * 16u;
+            while (tail[t] - head[t] >= 32u * ES) {
+              process(t, ring_entry(t, head[t] + lane * ES));
+              head[t] += 32u * ES;
             }
           }
         }
         // Drained slots may be rewritten by the next chunk's pushes unless the ring holds
         // the carried entries + a chunk + 2 x 32 entries.
-        if ((PAIRED ? 63 : 31) + 32 * kSenseHalves + 64 > kQueue) __syncwarp();
+        if ((PAIRED ? 63 : 31) + 32 * HV + 64 > (int)(kQueue * 16u / ES)) __syncwarp();
       }
     }
     __syncwarp();
@@ -1891,8 +1934,7 @@ __global__ void __launch_bounds__(kSenseWarps * 32, (DEF && ENV == kTag) ? VG_SE
     } else {
 #pragma unroll
       for (int t = 0; t < NQ; ++t)
-        if (lane * 16u < tail[t] - head[t])
-          process(t, lds128(qbase[t] | ((head[t] + lane * 16u) & (kQueue * 16 - 16))));
+        if (lane * ES < tail[t] - head[t]) process(t, ring_entry(t, head[t] + lane * ES));
     }
     __syncwarp();
 
@@ -1901,7 +1943,20 @@ __global__ void __launch_bounds__(kSenseWarps * 32, (DEF && ENV == kTag) ? VG_SE
       if (!live[t]) continue;                                        // warp-uniform
       const uint32_t q = q0 + t;
       const uint32_t nn = RAY ? __reduce_add_sync(kFull, nnb[t])
-                              : (tail[t] >> 4) - 1u;            // minus the self pair
+                              : (tail[t] >> ES_SH) - 1u;        // minus the self pair
+      if (E8 && VISION && __reduce_add_sync(kFull, nnb[t]) > 1u) {
+        // another agent at exactly this position: its (dx, dy) = (+0, +0) entry was kept out
+        // of the sector minima with the self pair's; apply it here as `process` would have
+        if (lane == 0) {
+          const float z = 0.f;
+          const float fwd = fmaf(csn[t], z, sn[t] * z);
+          const float left = fmaf(csn[t], z, -sn[t] * z);
+          const int k = __float2int_rd(fmaf(vg_atan2(left, fwd), c_inv_w, c_half_v));
+          if ((unsigned)k < (unsigned)VG_SC(v))
+            red_min(srow + (uint32_t)(t * kMaxViewSlots * 4) + (uint32_t)k * 4u, 0u);
+        }
+        __syncwarp();
+      }
       // Warp reductions (REDUX): the int64 reward sum as four exact 16-bit-limb partial sums
       // (no 32-bit wrap for any reward validate() admits).
       // the self pair's contact and -c_collide term (sector pass, see `process`), removed

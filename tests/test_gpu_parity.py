@@ -353,6 +353,33 @@ def test_edge_cases(cuda, case):
     run_and_check(p, st0, 3, replicas=reps)
 
 
+@pytest.mark.parametrize("env", ["flock", "tag"])
+def test_coincident_agents(cuda, env):
+    # Agents at exactly the same position (A13: d = 0, phi = atan2(0, 0) = 0, a contact):
+    # exact duplicates, a triple, and a pair one ulp apart.  The flock sector pass keeps
+    # every (dx, dy) = (+0, +0) entry out of the sector minima with the self pair and
+    # restores a coincident other agent at the emit (K4 8-byte ring entries).
+    torch = _torch()
+    p = vi.flock_params(600, width=60.0) if env == "flock" else vi.tag_params(600, width=60.0)
+    st = vi.init_state(p, seed=8)
+    st[0, 10:20, :2] = st[0, 0:10, :2]
+    st[0, 20:23, :2] = st[0, 30, :2]
+    st[0, 40, :2] = st[0, 41, :2]
+    st[0, 40, 0] = np.nextafter(st[0, 41, 0], np.float32(np.inf))
+    w = make_world(p)
+    out = w.alloc_outputs()
+    w.bin(dev(st))
+    w.sense(out)
+    torch.cuda.synchronize()
+    assert w.sync_errors() == -1
+    parity.check_sense(p, st[0], outs_np(out, 0))
+    contacts = host(out.n_collide)[0].astype(np.int64)
+    if env == "tag":
+        contacts += host(out.n_touch)[0]
+    assert (contacts[list(range(23)) + [30]] >= 1).all()
+    w.close()
+
+
 def test_dyadic_world_bit_exact_thresholds(cuda):
     # On a 2^-8 lattice with L = 128 every difference and d^2 is exact in fp32 and fp64:
     # radius and contact decisions must agree exactly, even for pairs exactly on them.
