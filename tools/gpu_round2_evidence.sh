@@ -14,3 +14,4 @@ ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum 
 ncu --set full --clock-control none --import-source on -k regex:k_sense -s 3 -c 1 -o gpurun_out/prof_k4_r2b -f $B > gpurun_out/ncu_k4.log 2>&1; echo "k4 $?"
 ncu --set full --clock-control none --import-source on -k regex:k_replica_bin -s 2 -c 1 -o gpurun_out/prof_rb_r2b -f $B --config c4 > gpurun_out/ncu_rb.log 2>&1; echo "rb $?"
 ncu --set full --clock-control none --import-source on -k regex:k_policy -s 3 -c 1 -o gpurun_out/prof_k7_r2b -f python bench.py --steps 2 --warmup 1 --no-cpu-baseline --no-e2e --no-c4-binning > gpurun_out/ncu_k7.log 2>&1; echo "k7 $?"
+ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_slab8_r2.csv python tools/slab8_launches.py 8 > gpurun_out/slab8_r2.log 2>&1; echo "slab8 launches rc $?"

@@ -98,6 +98,24 @@ w("Keys computed as records enter the local set (10 kernels per rank-step):\n")
 w("| P | group GPU ms | per-rank ms | host enqueue ms |\n|---|---|---|---|")
 for p, d in sl.items():
     w(f"| {p} | {d['group_gpu_ms']:.3f} | {d['per_rank_gpu_ms']:.3f} | {d['host_enqueue_ms']:.3f} |")
+rows = [r for r in csv.reader(open(os.path.join(P, "r2_launches_slab8.csv"))) if len(r) > 5]
+h = rows[0]
+ki, mi, vi, ui = (h.index(x) for x in ("Kernel Name", "Metric Name", "Metric Value", "Metric Unit"))
+seq = [(r[ki].split("(")[0].replace("void ", "").replace("vg::", ""),
+        float(r[vi].replace(",", "")) / (1e3 if r[ui] == "ns" else 1.0))
+       for r in rows[1:] if r[mi] == "gpu__time_duration.sum"]
+last = seq[-80:]                                  # the last step: 8 ranks x 10 kernels
+per = collections.defaultdict(float)
+sense = [v for k, v in last if k.startswith("k_sense")]
+for k, v in last:
+    per[k] += v / 8
+w("\nOne step of P = 8 under ncu (`r2_launches_slab8.csv`, cold caches, serialised), us per rank:\n")
+w("| kernel | us per rank |\n|---|---|")
+for k, v in sorted(per.items(), key=lambda x: -x[1]):
+    w(f"| `{k}` | {v:.1f} |")
+w(f"| total | {sum(per.values()):.1f} |")
+w(f"\nk_sense per rank: interior phase {sum(sense[:8]) / 8:.1f} us (13 of 17 columns), boundary phase "
+  f"{sum(sense[8:]) / 8:.1f} us (4 columns; about one wave of CTAs, so its tail is not hidden).")
 w("\nRound 1 (one binning phase, no overlap possible): 0.51 / 0.27 / 0.164 ms per rank at\n"
   "P = 2 / 4 / 8.  The loopback serialises all P ranks' launches on one GPU, so it charges\n"
   "the phase split's extra launches in full and cannot show the overlap it buys.")

@@ -15,7 +15,8 @@ G, P = os.path.join(ROOT, "gpurun_out"), os.path.join(ROOT, "profiles")
 os.chdir(ROOT)
 for a, b in (("bench_c5_r2.json", "r2_bench_c5.json"), ("bench_c4_r2.json", "r2_bench_c4.json"),
              ("launches_c5_r2.csv", "r2_launches_c5.csv"), ("launches_c4_r2.csv", "r2_launches_c4.csv"),
-             ("parity_stats_r2.json", "parity_stats.json"), ("slab_timing.json", "r2_slab_timing_1gpu.json")):
+             ("parity_stats_r2.json", "parity_stats.json"), ("slab_timing.json", "r2_slab_timing_1gpu.json"),
+             ("launches_slab8_r2.csv", "r2_launches_slab8.csv")):
     shutil.copy(os.path.join(G, a), os.path.join(P, b))
 
 KEYS = ['gpu__time_duration.sum', 'dram__bytes_read.sum', 'dram__bytes_write.sum',
