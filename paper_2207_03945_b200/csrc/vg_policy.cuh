@@ -52,7 +52,7 @@ constexpr int kConstFloats = 128 + 128 + 4 + 2 + 4;
 #ifndef VG_POL_QUARTERS
 #define VG_POL_QUARTERS 0
 #endif
-constexpr int kPolQ = VG_POL_QUARTERS ? 4 : 1;           // TMA pieces per tile
+constexpr int kPolQ = VG_POL_QUARTERS > 1 ? VG_POL_QUARTERS : VG_POL_QUARTERS ? 4 : 1;   // TMA pieces per tile (1, 2, 4)
 constexpr int kOffBar = kOffC + ((kConstFloats * 4 + 15) / 16) * 16;   // mbarriers + tmem slot
 constexpr int kBarBytes = 8 * (2 + 2 * kPolQ) + 16;
 constexpr int kOffStage = ((kOffBar + kBarBytes + 127) / 128) * 128;     // raw fp32 obs tile (TMA)
