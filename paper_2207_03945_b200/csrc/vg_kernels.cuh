@@ -1228,9 +1228,9 @@ __global__ void __launch_bounds__(RBCfg<MODE>::NT, RBCfg<MODE>::MINB) k_replica_
 constexpr int kSenseWarps = VG_SENSE_WARPS;
 constexpr int kSenseNQ = VG_SENSE_NQ;         // queries sensed together by one warp
 constexpr int kSenseMinBlocks = VG_SENSE_MINB;  // launch-bounds minimum; 64 registers give 8 CTAs/SM
-// Ring (power of 2): >= 31 carried + 64 pushed, and large enough that one chunk's pushes
-// never reach the slots the previous drain read (carried + 64 + 2 x 32 <= kQueue), so one
-// warp sync per chunk (before the drain) orders all ring traffic.
+// Ring (power of 2): >= 31 carried + one chunk of pushes (32 per half); a second warp sync
+// per chunk (after the drain) unless the ring also keeps the next chunk's pushes off the
+// slots the drain read (carried + 2 x 32 halves <= ring entries, see the chunk loop).
 #ifndef VG_SENSE_PAIRED
 #define VG_SENSE_PAIRED 0           // sector pass: both queries' pair batches in packed pairs
 #endif
@@ -1253,10 +1253,13 @@ constexpr int kSenseHalves = VG_SENSE_HALVES;
 constexpr int kQueue = VG_SENSE_QUEUE;
 // Flock sector vision (E8): 8-byte ring entries (dx, dy) — d^2 is recomputed bitwise in the
 // pair pass and the self pair is the entry with dx = dy = +0 (a coincident other agent is
-// restored at the emit) — so the same ring bytes hold 2 kQueue entries: VG_SENSE_E8_HALVES
-// 32-slot halves per chunk and one warp sync per chunk.
+// restored at the emit) — so the same ring bytes hold 2 kQueue entries and a chunk can be
+// VG_SENSE_E8_HALVES 32-slot halves.
 #ifndef VG_SENSE_E8
 #define VG_SENSE_E8 1
+#endif
+#ifndef VG_SENSE_LDPRED
+#define VG_SENSE_LDPRED 1
 #endif
 #ifndef VG_SENSE_E8_HALVES
 #define VG_SENSE_E8_HALVES 4
@@ -1453,7 +1456,7 @@ __host__ __device__ constexpr SenseConst sense_defaults() {
                     v, ch * v, ch * v + ((ENV == kFlock) ? 1 : 0), (ch * v + 31) / 32};
 }
 
-template <int ENV, bool VISION, bool SLAB, bool RAY, bool DEF>
+template <int ENV, bool VISION, bool SLAB, bool RAY, bool DEF, bool E8T = true>
 __global__ void __launch_bounds__(kSenseWarps * 32, (DEF && ENV == kTag) ? VG_SENSE_TAG_DEF_MINB : DEF ? VG_SENSE_DEF_MINB : kSenseMinBlocks) k_sense(
     Params P, const uint32_t* __restrict__ cell_start, const float4* __restrict__ sorted,
     const float2* __restrict__ sorted_xy, const uint32_t* __restrict__ perm, Outs O, Slab SL,
@@ -1485,7 +1488,8 @@ __global__ void __launch_bounds__(kSenseWarps * 32, (DEF && ENV == kTag) ? VG_SE
   constexpr bool PAIRED = VG_SENSE_PAIRED && !RAY && NQ == 2;
   constexpr bool PACKED_SCAN = VG_SENSE_PACKED_SCAN && NQ == 2;
   // Ring entry layout: E8 (flock sector vision) 8 bytes (dx, dy), else 16 (dx, dy, d^2, word).
-  constexpr bool E8 = VG_SENSE_E8 && ENV == kFlock && !RAY && !PAIRED && !PACKED_SCAN;
+  // (E8T = false: the replica-world instances, where 16-byte entries measured faster)
+  constexpr bool E8 = E8T && VG_SENSE_E8 && ENV == kFlock && !RAY && !PAIRED && !PACKED_SCAN;
   constexpr uint32_t ES = E8 ? 8u : 16u, ES_SH = E8 ? 3u : 4u;
   constexpr uint32_t kRingMask = kQueue * 16u - ES;      // byte offsets within a ring
   constexpr int HV = E8 ? VG_SENSE_E8_HALVES : kSenseHalves;   // 32-slot halves per chunk
@@ -1871,7 +1875,9 @@ __global__ void __launch_bounds__(kSenseWarps * 32, (DEF && ENV == kTag) ? VG_SE
 #pragma unroll
         for (int h = 0; h < HV; ++h) {
           const uint32_t pj = p0 + 32u * h + lane;
-          const float2 o = __ldg(&sorted_xy[pj]);
+          // VG_SENSE_LDPRED: halves wholly past the window end load nothing (predicated)
+          const float2 o = (!VG_SENSE_LDPRED || h == 0 || p0 + 32u * h < we)
+                               ? __ldg(&sorted_xy[pj]) : make_float2(0.f, 0.f);
           float x = o.x;
           uint32_t tj = 0u;
           if (ENV == kTag) {                 // type in the sign bit of x (K3b)
@@ -1912,9 +1918,12 @@ __global__ void __launch_bounds__(kSenseWarps * 32, (DEF && ENV == kTag) ? VG_SE
             }
           }
         }
-        // Drained slots may be rewritten by the next chunk's pushes unless the ring holds
-        // the carried entries + a chunk + 2 x 32 entries.
-        if ((PAIRED ? 63 : 31) + 32 * HV + 64 > (int)(kQueue * 16u / ES)) __syncwarp();
+        // The drain above read ring entries [h, t + P) with h >= t - carried (P: this chunk's
+        // pushes, <= 32 HV); the next chunk writes [t + P, t + P + 32 HV).  Without a warp
+        // sync between them a write may land on an entry another lane has not read yet
+        // unless carried + 2 x 32 HV <= ring entries (E8 with four halves: 31 + 256 > 256, so
+        // it syncs; a warp-uniform test of this chunk's P instead measured slower).
+        if ((PAIRED ? 63 : 31) + 64 * HV > (int)(kQueue * 16u / ES)) __syncwarp();
       }
     }
     __syncwarp();
