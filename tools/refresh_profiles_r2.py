@@ -62,7 +62,7 @@ def mb(f, k):
 
 
 k4 = "prof_k4_r2b"
-json.dump({"config": "c5", "kernel": "void k_sense<0, 1, 0, 0, 1> (round 2)",
+json.dump({"config": "c5", "kernel": m[k4]["kernel"].split("(")[0] + " (round 2)",
            "bytes_per_launch": mb(k4, "dram__bytes_read.sum") + mb(k4, "dram__bytes_write.sum"),
            "dram_read_bytes": mb(k4, "dram__bytes_read.sum"), "dram_write_bytes": mb(k4, "dram__bytes_write.sum"),
            "warp_instructions": v(k4, "smsp__inst_executed.sum"), "candidate_tests": None,
@@ -86,8 +86,12 @@ for r in rows[1:]:
         val /= 1e3
     agg[r[ki].split("(")[0]][r[mi]].append(val)
 mean = lambda k, mm: sum(agg[k][mm]) / len(agg[k][mm])  # noqa: E731
-mp = {"integrate_bin": ["void vg::k_integrate_bin<0, 1, 1>"], "scan_cells": ["vg::k_scan_tiles", "vg::k_scan_apply"],
-      "scatter": ["void vg::k_scatter<0>"], "cell_sort": ["vg::k_cell_sort"], "sense": ["void vg::k_sense<0, 1, 0, 0, 1>"]}
+names = sorted(agg)
+pick = lambda pre: next(n for n in names if n.startswith(pre))  # noqa: E731
+mp = {"integrate_bin": [pick("void vg::k_integrate_bin<0, 1, 1>")],
+      "scan_cells": [pick("vg::k_scan_tiles"), pick("vg::k_scan_apply")],
+      "scatter": [pick("void vg::k_scatter<0>")], "cell_sort": [pick("vg::k_cell_sort")],
+      "sense": [pick("void vg::k_sense<0, 1, 0, 0, 1")]}
 json.dump({"config": "c5", "source": "ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum "
                                      "(cold caches, serialised launches; round-2 kernels; profiles/r2_launches_c5.csv)",
            "stages": {st: {"dram_read_B": int(sum(mean(k, "dram__bytes_read.sum") for k in ks)),
