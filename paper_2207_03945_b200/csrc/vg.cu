@@ -567,8 +567,11 @@ void set_kernel_attributes() {
 template <int ENV, bool VISION, bool SLAB>
 bool sense_replica_e16(vg_world* w, unsigned grid, const vg::Outs& O, cudaStream_t s, int cq,
                        int cells) {
+#ifndef VG_SENSE_REPLICA_E16
+#define VG_SENSE_REPLICA_E16 1
+#endif
   if constexpr (ENV == vg::kFlock && VISION && !SLAB) {
-    if (w->P.R <= 1) return false;
+    if (w->P.R <= 1 || !VG_SENSE_REPLICA_E16) return false;
     if (w->sense_def)
       vg::k_sense<ENV, VISION, SLAB, false, true, false><<<grid, vg::kSenseWarps * 32, 0, s>>>(
           w->P, w->cell_start, w->xo_rec, w->xo_xy, w->xo_perm, O, w->SL, w->ray_dir, w->sub_tab,

@@ -1258,6 +1258,9 @@ constexpr int kQueue = VG_SENSE_QUEUE;
 #ifndef VG_SENSE_E8
 #define VG_SENSE_E8 1
 #endif
+#ifndef VG_SENSE_SCANSELF
+#define VG_SENSE_SCANSELF 1
+#endif
 #ifndef VG_SENSE_LDPRED
 #define VG_SENSE_LDPRED 1
 #endif
@@ -1493,6 +1496,10 @@ __global__ void __launch_bounds__(kSenseWarps * 32, (DEF && ENV == kTag) ? VG_SE
   constexpr uint32_t ES = E8 ? 8u : 16u, ES_SH = E8 ? 3u : 4u;
   constexpr uint32_t kRingMask = kQueue * 16u - ES;      // byte offsets within a ring
   constexpr int HV = E8 ? VG_SENSE_E8_HALVES : kSenseHalves;   // 32-slot halves per chunk
+  // SS: the self pair never enters the ring — the candidate test also requires slot pj !=
+  // the query's own sense-order index (an extra predicate input of the radius test), so
+  // the pair pass, the counts and the emit need no self handling at all.
+  constexpr bool SS = VG_SENSE_SCANSELF && !PAIRED;
   // Pair-pass constants.  (ptxas sees through this empty asm and re-loads them from the
   // parameter bank per pair batch; forcing them into registers with an opaque add costs 8
   // registers and measured 4 % slower.)
@@ -1646,9 +1653,10 @@ __global__ void __launch_bounds__(kSenseWarps * 32, (DEF && ENV == kTag) ? VG_SE
       // E8 has no index: "self" is every entry at dx = dy = +0 (the self pair, and any other
       // agent at exactly the same position, whose sector slot the emit restores; nnb counts
       // them).
-      const bool self = E8 ? (__float_as_uint(e.x) | __float_as_uint(e.y)) == 0u
+      const bool self = SS ? false
+                      : E8 ? (__float_as_uint(e.x) | __float_as_uint(e.y)) == 0u
                            : ENV == kFlock ? tagbits == q0 + t : (tagbits & 0x7fffffffu) == q0 + t;
-      if (E8) nnb[t] += self ? 1u : 0u;
+      if (E8 && !SS) nnb[t] += self ? 1u : 0u;
       if ((RAY || PAIRED) && self) return;
       const uint32_t tj = (ENV == kTag) ? tagbits >> 31 : 0u;
       const float d2 = e.z;
@@ -1835,7 +1843,7 @@ __global__ void __launch_bounds__(kSenseWarps * 32, (DEF && ENV == kTag) ? VG_SE
       for (uint32_t p0 = wb; p0 < we; p0 += 32 * HV) {
         // Ballot the in-radius candidates of one 32-slot half and append them to each
         // query's ring (dx, dy, d^2, index | type << 31).
-        auto scan = [&](const float cx_, const float cy_, const uint32_t word) {
+        auto scan = [&](const float cx_, const float cy_, const uint32_t word, const uint32_t pj_) {
           // PAIRED: dx, dy, d^2 of both queries as packed pairs (FADD2 with the candidate
           // broadcast, FMUL2, FFMA2), bitwise the scalar fmaf(dx, dx, dy * dy).
           f32x2 dx2 = 0ull, dy2 = 0ull, dd2 = 0ull;
@@ -1856,7 +1864,8 @@ __global__ void __launch_bounds__(kSenseWarps * 32, (DEF && ENV == kTag) ? VG_SE
               dy = cy_ - qy[t];
               d2 = fmaf(dx, dx, dy * dy);
             }
-            const bool in = d2 < (RAY ? VG_SC(cand2) : VG_SC(dv2));                // Eq. 1: d < d_v
+            const bool in = d2 < (RAY ? VG_SC(cand2) : VG_SC(dv2)) &&             // Eq. 1: d < d_v
+                            (!SS || pj_ != q0 + (uint32_t)t);                        // j != i
             const unsigned bal = __ballot_sync(kFull, in);
             if (E8) {
               if (in) sts64(qbase[t] | ((tail[t] + (__popc(bal & lt_mask) << 3)) & kRingMask), dx, dy);
@@ -1890,7 +1899,7 @@ __global__ void __launch_bounds__(kSenseWarps * 32, (DEF && ENV == kTag) ? VG_SE
         }
 #pragma unroll
         for (int h = 0; h < HV; ++h)
-          if (h == 0 || p0 + 32u * h < we) scan(cxh[h], cyh[h], wh[h]);   // warp-uniform
+          if (h == 0 || p0 + 32u * h < we) scan(cxh[h], cyh[h], wh[h], p0 + 32u * h + lane);
         __syncwarp();                       // ring pushes above are visible to the warp
         if (PAIRED) {
           // Full batches of both queries together (process2); a query's ring is drained
@@ -1952,8 +1961,8 @@ __global__ void __launch_bounds__(kSenseWarps * 32, (DEF && ENV == kTag) ? VG_SE
       if (!live[t]) continue;                                        // warp-uniform
       const uint32_t q = q0 + t;
       const uint32_t nn = RAY ? __reduce_add_sync(kFull, nnb[t])
-                              : (tail[t] >> ES_SH) - 1u;        // minus the self pair
-      if (E8 && VISION && __reduce_add_sync(kFull, nnb[t]) > 1u) {
+                              : (tail[t] >> ES_SH) - (SS ? 0u : 1u);   // minus the self pair
+      if (E8 && !SS && VISION && __reduce_add_sync(kFull, nnb[t]) > 1u) {
         // another agent at exactly this position: its (dx, dy) = (+0, +0) entry was kept out
         // of the sector minima with the self pair's; apply it here as `process` would have
         if (lane == 0) {
@@ -1969,7 +1978,7 @@ __global__ void __launch_bounds__(kSenseWarps * 32, (DEF && ENV == kTag) ? VG_SE
       // Warp reductions (REDUX): the int64 reward sum as four exact 16-bit-limb partial sums
       // (no 32-bit wrap for any reward validate() admits).
       // the self pair's contact and -c_collide term (sector pass, see `process`), removed
-      const uint32_t nc = __reduce_add_sync(kFull, ncol[t]) - ((RAY || PAIRED) ? 0u : 1u);
+      const uint32_t nc = __reduce_add_sync(kFull, ncol[t]) - ((RAY || PAIRED || SS) ? 0u : 1u);
       const uint32_t nt = (ENV == kTag) ? __reduce_add_sync(kFull, ntouch[t]) : 0u;
       const unsigned long long ur = (unsigned long long)rs[t];
       const uint32_t s_lo = __reduce_add_sync(kFull, (uint32_t)(ur & 0xffffu));
@@ -1979,7 +1988,7 @@ __global__ void __launch_bounds__(kSenseWarps * 32, (DEF && ENV == kTag) ? VG_SE
       long long rsum = (long long)(((unsigned long long)(long long)s_top << 48) +
                                    ((unsigned long long)s_hi << 32) +
                                    ((unsigned long long)s_mid << 16) + (unsigned long long)s_lo);
-      if (!RAY && !PAIRED) {
+      if (!RAY && !PAIRED && !SS) {
         if (ENV == kFlock) rsum -= __float2ll_rn(c_mcollide);
         else if (tq[t] == 0u) rsum -= __float2ll_rn(VG_SC(w_prox) * c_mcollide);
       }
