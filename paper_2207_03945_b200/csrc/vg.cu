@@ -514,10 +514,6 @@ void sense_carveouts() {
   if (VISION) {
     sense_carveout(vg::k_sense<ENV, VISION, SLAB, false, VISION>, VG_SENSE_CARVEOUT);
     sense_carveout(vg::k_sense<ENV, VISION, SLAB, true, VISION>, VG_SENSE_CARVEOUT_RAY);
-    if constexpr (ENV == vg::kFlock && !SLAB && VISION) {  // replica-world (16-byte entry) instances
-      sense_carveout(vg::k_sense<ENV, VISION, SLAB, false, true, false>, VG_SENSE_CARVEOUT);
-      sense_carveout(vg::k_sense<ENV, VISION, SLAB, false, false, false>, VG_SENSE_CARVEOUT);
-    }
   }
 }
 
@@ -562,30 +558,6 @@ void set_kernel_attributes() {
   sense_carveouts<vg::kTag, false, true>();
 }
 
-// Flock sector vision over replica worlds (c4): K4 with 16-byte ring entries, measured
-// faster there than the 8-byte entries single worlds use (v20).
-template <int ENV, bool VISION, bool SLAB>
-bool sense_replica_e16(vg_world* w, unsigned grid, const vg::Outs& O, cudaStream_t s, int cq,
-                       int cells) {
-#ifndef VG_SENSE_REPLICA_E16
-#define VG_SENSE_REPLICA_E16 1
-#endif
-  if constexpr (ENV == vg::kFlock && VISION && !SLAB) {
-    if (w->P.R <= 1 || !VG_SENSE_REPLICA_E16) return false;
-    if (w->sense_def)
-      vg::k_sense<ENV, VISION, SLAB, false, true, false><<<grid, vg::kSenseWarps * 32, 0, s>>>(
-          w->P, w->cell_start, w->xo_rec, w->xo_xy, w->xo_perm, O, w->SL, w->ray_dir, w->sub_tab,
-          w->work, w->work_cnt, cq, cells);
-    else
-      vg::k_sense<ENV, VISION, SLAB, false, false, false><<<grid, vg::kSenseWarps * 32, 0, s>>>(
-          w->P, w->cell_start, w->xo_rec, w->xo_xy, w->xo_perm, O, w->SL, w->ray_dir, w->sub_tab,
-          w->work, w->work_cnt, cq, cells);
-    return true;
-  } else {
-    return false;
-  }
-}
-
 template <int ENV, bool VISION, bool SLAB>
 void sense_kernel(vg_world* w, int cells, const vg::Outs& O, cudaStream_t s) {
   const int cq = sense_chunk_q(w);
@@ -601,8 +573,6 @@ void sense_kernel(vg_world* w, int cells, const vg::Outs& O, cudaStream_t s) {
     vg::k_sense<ENV, VISION, SLAB, true, false><<<grid, vg::kSenseWarps * 32, 0, s>>>(
         w->P, w->cell_start, w->xo_rec, w->xo_xy, w->xo_perm, O, w->SL, w->ray_dir, w->sub_tab,
         w->work, w->work_cnt, cq, cells);
-  else if (sense_replica_e16<ENV, VISION, SLAB>(w, grid, O, s, cq, cells))
-    return;                            // replica worlds: the 16-byte-entry instances
   else if (VISION && w->sense_def)
     vg::k_sense<ENV, VISION, SLAB, false, VISION><<<grid, vg::kSenseWarps * 32, 0, s>>>(
         w->P, w->cell_start, w->xo_rec, w->xo_xy, w->xo_perm, O, w->SL, w->ray_dir, w->sub_tab,

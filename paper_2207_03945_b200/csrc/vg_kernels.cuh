@@ -1459,7 +1459,7 @@ __host__ __device__ constexpr SenseConst sense_defaults() {
                     v, ch * v, ch * v + ((ENV == kFlock) ? 1 : 0), (ch * v + 31) / 32};
 }
 
-template <int ENV, bool VISION, bool SLAB, bool RAY, bool DEF, bool E8T = true>
+template <int ENV, bool VISION, bool SLAB, bool RAY, bool DEF>
 __global__ void __launch_bounds__(kSenseWarps * 32, (DEF && ENV == kTag) ? VG_SENSE_TAG_DEF_MINB : DEF ? VG_SENSE_DEF_MINB : kSenseMinBlocks) k_sense(
     Params P, const uint32_t* __restrict__ cell_start, const float4* __restrict__ sorted,
     const float2* __restrict__ sorted_xy, const uint32_t* __restrict__ perm, Outs O, Slab SL,
@@ -1491,8 +1491,7 @@ __global__ void __launch_bounds__(kSenseWarps * 32, (DEF && ENV == kTag) ? VG_SE
   constexpr bool PAIRED = VG_SENSE_PAIRED && !RAY && NQ == 2;
   constexpr bool PACKED_SCAN = VG_SENSE_PACKED_SCAN && NQ == 2;
   // Ring entry layout: E8 (flock sector vision) 8 bytes (dx, dy), else 16 (dx, dy, d^2, word).
-  // (E8T = false: the replica-world instances, where 16-byte entries measured faster)
-  constexpr bool E8 = E8T && VG_SENSE_E8 && ENV == kFlock && !RAY && !PAIRED && !PACKED_SCAN;
+  constexpr bool E8 = VG_SENSE_E8 && ENV == kFlock && !RAY && !PAIRED && !PACKED_SCAN;
   constexpr uint32_t ES = E8 ? 8u : 16u, ES_SH = E8 ? 3u : 4u;
   constexpr uint32_t kRingMask = kQueue * 16u - ES;      // byte offsets within a ring
   constexpr int HV = E8 ? VG_SENSE_E8_HALVES : kSenseHalves;   // 32-slot halves per chunk
