@@ -1468,7 +1468,10 @@ __global__ void __launch_bounds__(kSenseWarps * 32, (DEF && ENV == kTag) ? VG_SE
     int n_first) {
   // sorted / sorted_xy / perm are the sense-order arrays (xo_* of K3b): within a cell the
   // records ascend in x (replica grid, runs along rows) or y (slab grid, runs along columns).
-  __shared__ uint32_t s_min[kSenseWarps][kSenseNQ][kMaxViewSlots];
+  // per (warp, query) sector row + one spare slot (index v <= kMaxViewSlots) that absorbs
+  // the minima of invisible flock pairs without a select
+  constexpr int kRowW = kMaxViewSlots + 1;
+  __shared__ uint32_t s_min[kSenseWarps][kSenseNQ][kRowW];
   __shared__ float2 s_ray[RAY ? kMaxViewSlots : 1];
   // Ring queues, kQueue float4 each, at shared addresses aligned to the ring size (the
   // shared window has a reserved prefix, so the alignment is done on the address).
@@ -1732,11 +1735,17 @@ __global__ void __launch_bounds__(kSenseWarps * 32, (DEF && ENV == kTag) ? VG_SE
         const float left = fmaf(csn[t], e.y, -sn[t] * e.x);
         // Sector coordinate (phi + fov/2) v / fov; visible iff 0 <= k < v (A3).
         const int k = __float2int_rd(fmaf(vg_atan2(left, fwd), c_inv_w, c_half_v));
-        const bool vis = (unsigned)k < (unsigned)VG_SC(v) && !self;
-        // Branch-free update: an invisible pair applies the no-op min(x, ~0) to slot 0.
-        const uint32_t val = vis ? __float_as_uint(fminf(d * c_inv_dv, kBelowOne)) : 0xffffffffu;
-        red_min(srow + (uint32_t)(t * kMaxViewSlots * 4) +
-                             (uint32_t)(tj * VG_SC(v) + (vis ? k : 0)) * 4u, val);
+        if (ENV == kFlock && SS) {
+          // an invisible pair (k outside [0, v)) updates the spare slot v, never read
+          const uint32_t idx = min((uint32_t)k, (uint32_t)VG_SC(v));
+          red_min(srow + (uint32_t)(t * kRowW * 4) + idx * 4u,
+                  __float_as_uint(fminf(d * c_inv_dv, kBelowOne)));
+        } else {
+          const bool vis = (unsigned)k < (unsigned)VG_SC(v) && !self;
+          // Branch-free update: an invisible pair applies the no-op min(x, ~0) to slot 0.
+          const uint32_t val = vis ? __float_as_uint(fminf(d * c_inv_dv, kBelowOne)) : 0xffffffffu;
+          red_min(srow + (uint32_t)(t * kRowW * 4) + (uint32_t)(tj * VG_SC(v) + (vis ? k : 0)) * 4u, val);
+        }
       }
     };
 
@@ -1783,7 +1792,7 @@ __global__ void __launch_bounds__(kSenseWarps * 32, (DEF && ENV == kTag) ? VG_SE
         red_min_if(ok0 && (unsigned)k0 < (unsigned)VG_SC(v), srow + (uint32_t)(tj0 * VG_SC(v) + k0) * 4u,
                    __float_as_uint(fminf(lo2(val), kBelowOne)));
         red_min_if(ok1 && (unsigned)k1 < (unsigned)VG_SC(v),
-                   srow + (uint32_t)(kMaxViewSlots * 4) + (uint32_t)(tj1 * VG_SC(v) + k1) * 4u,
+                   srow + (uint32_t)(kRowW * 4) + (uint32_t)(tj1 * VG_SC(v) + k1) * 4u,
                    __float_as_uint(fminf(hi2(val), kBelowOne)));
       }
     };
@@ -1970,7 +1979,7 @@ __global__ void __launch_bounds__(kSenseWarps * 32, (DEF && ENV == kTag) ? VG_SE
           const float left = fmaf(csn[t], z, -sn[t] * z);
           const int k = __float2int_rd(fmaf(vg_atan2(left, fwd), c_inv_w, c_half_v));
           if ((unsigned)k < (unsigned)VG_SC(v))
-            red_min(srow + (uint32_t)(t * kMaxViewSlots * 4) + (uint32_t)k * 4u, 0u);
+            red_min(srow + (uint32_t)(t * kRowW * 4) + (uint32_t)k * 4u, 0u);
         }
         __syncwarp();
       }
