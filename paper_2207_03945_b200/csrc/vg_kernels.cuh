@@ -1258,6 +1258,9 @@ constexpr int kQueue = VG_SENSE_QUEUE;
 #ifndef VG_SENSE_E8
 #define VG_SENSE_E8 1
 #endif
+#ifndef VG_SENSE_PREDCNT
+#define VG_SENSE_PREDCNT 1
+#endif
 #ifndef VG_SENSE_SCANSELF
 #define VG_SENSE_SCANSELF 1
 #endif
@@ -1674,9 +1677,16 @@ __global__ void __launch_bounds__(kSenseWarps * 32, (DEF && ENV == kTag) ? VG_SE
       }
       // Eq. 1 / Fig. 4 (A5): contact -> -c_collide, else the tent min(rise, fall); in
       // fixed-point units (x 2^32, A16b).
-      const float f = contact ? c_mcollide
-                              : fminf(fmaf(c_k_rise, d, c_b_rise), fmaf(c_nk_fall, d, c_b_fall));
-      if (!RAY || d2 < VG_SC(dv2)) {                                       // Eq. 1: d < d_v
+      const float tent = fminf(fmaf(c_k_rise, d, c_b_rise), fmaf(c_nk_fall, d, c_b_fall));
+      float f = contact ? c_mcollide : tent;
+      if (ENV == kFlock && !RAY && VG_SENSE_PREDCNT) {
+        // the contact test, the term's select and the contact count under one predicate
+        // (ptxas otherwise counts with an add, a predicated move and a copy)
+        asm("{\n\t.reg .pred p;\n\tsetp.le.f32 p, %2, %3;\n\tselp.f32 %0, %4, %5, p;\n\t"
+            "@p add.u32 %1, %1, 1;\n\t}"
+            : "=f"(f), "+r"(ncol[t]) : "f"(d2), "f"(c_contact2), "f"(c_mcollide), "f"(tent));
+        rs[t] += __float2ll_rn(f);
+      } else if (!RAY || d2 < VG_SC(dv2)) {                                // Eq. 1: d < d_v
         if (RAY) ++nnb[t];
         if (ENV == kFlock) {
           rs[t] += __float2ll_rn(f);
