@@ -1258,6 +1258,9 @@ constexpr int kQueue = VG_SENSE_QUEUE;
 #ifndef VG_SENSE_E8
 #define VG_SENSE_E8 1
 #endif
+#ifndef VG_SENSE_MIXTAIL
+#define VG_SENSE_MIXTAIL 1
+#endif
 #ifndef VG_SENSE_PREDCNT
 #define VG_SENSE_PREDCNT 1
 #endif
@@ -1649,8 +1652,36 @@ __global__ void __launch_bounds__(kSenseWarps * 32, (DEF && ENV == kTag) ? VG_SE
       }
       return lds128(qbase[t] | (off & kRingMask));
     };
+    // FLOCK1: flock sector vision with 8-byte entries, no self pairs in the rings — the pair
+    // pass on (dx, dy, d^2) for a query given by its heading (cs_, sn_), sector row offset
+    // and accumulators (so the last, partial batches of both queries can share one pass).
+    constexpr bool FLOCK1 = ENV == kFlock && E8 && SS && !RAY && VISION && VG_SENSE_PREDCNT;
+    auto flock_pair = [&](const float4 e, const float cs_, const float sn_, const uint32_t rowoff,
+                          long long& racc, uint32_t& cacc) {
+      const float d2 = e.z;
+      float d;
+      asm("sqrt.approx.ftz.f32 %0, %1;" : "=f"(d) : "f"(d2));
+      // Eq. 1 / Fig. 4 (A5) in fixed point (A16b); contact (A6, inclusive) test, the term's
+      // select and the contact count under one predicate
+      const float tent = fminf(fmaf(c_k_rise, d, c_b_rise), fmaf(c_nk_fall, d, c_b_fall));
+      float f;
+      asm("{\n\t.reg .pred p;\n\tsetp.le.f32 p, %2, %3;\n\tselp.f32 %0, %4, %5, p;\n\t"
+          "@p add.u32 %1, %1, 1;\n\t}"
+          : "=f"(f), "+r"(cacc) : "f"(d2), "f"(c_contact2), "f"(c_mcollide), "f"(tent));
+      racc += __float2ll_rn(f);
+      // bearing (A3) and sector; an invisible pair updates the row's spare slot v
+      const float fwd = fmaf(cs_, e.x, sn_ * e.y);
+      const float left = fmaf(cs_, e.y, -sn_ * e.x);
+      const int k = __float2int_rd(fmaf(vg_atan2(left, fwd), c_inv_w, c_half_v));
+      const uint32_t idx = min((uint32_t)k, (uint32_t)VG_SC(v));
+      red_min(srow + rowoff + idx * 4u, __float_as_uint(fminf(d * c_inv_dv, kBelowOne)));
+    };
     // Pair pass over one queue entry (dx, dy, d^2, index | type << 31) of query t.
     auto process = [&](const int t, const float4 e) {
+      if (FLOCK1) {
+        flock_pair(e, csn[t], sn[t], (uint32_t)(t * kRowW * 4), rs[t], ncol[t]);
+        return;
+      }
       const uint32_t tagbits = __float_as_uint(e.w);
       // j != i.  The sector pass takes no branch for it: the self pair (always in
       // the queue exactly once, at d = 0: a contact with f = -c_collide) is counted and
@@ -1968,9 +1999,30 @@ __global__ void __launch_bounds__(kSenseWarps * 32, (DEF && ENV == kTag) ? VG_SE
         n1 -= 32;
       }
     } else {
+      const uint32_t n0 = (tail[0] - head[0]) >> ES_SH, n1 = (tail[NQ - 1] - head[NQ - 1]) >> ES_SH;
+      if (FLOCK1 && NQ == 2 && VG_SENSE_MIXTAIL && n0 + n1 <= 32u) {
+        // both queries' last entries in one batch: lanes < n0 query 0, the next n1 query 1
+        if (lane < n0 + n1) {
+          const bool t1 = lane >= n0;
+          const uint32_t off = t1 ? head[NQ - 1] + (lane - n0) * ES : head[0] + lane * ES;
+          const float2 v = lds64((t1 ? qbase[NQ - 1] : qbase[0]) | (off & kRingMask));
+          long long racc = 0;
+          uint32_t cacc = 0u;
+          flock_pair(make_float4(v.x, v.y, fmaf(v.x, v.x, v.y * v.y), 0.f), t1 ? csn[NQ - 1] : csn[0],
+                     t1 ? sn[NQ - 1] : sn[0], t1 ? (uint32_t)(kRowW * 4) : 0u, racc, cacc);
+          if (t1) {
+            rs[NQ - 1] += racc;
+            ncol[NQ - 1] += cacc;
+          } else {
+            rs[0] += racc;
+            ncol[0] += cacc;
+          }
+        }
+      } else {
 #pragma unroll
-      for (int t = 0; t < NQ; ++t)
-        if (lane * ES < tail[t] - head[t]) process(t, ring_entry(t, head[t] + lane * ES));
+        for (int t = 0; t < NQ; ++t)
+          if (lane * ES < tail[t] - head[t]) process(t, ring_entry(t, head[t] + lane * ES));
+      }
     }
     __syncwarp();
 
@@ -1993,19 +2045,18 @@ __global__ void __launch_bounds__(kSenseWarps * 32, (DEF && ENV == kTag) ? VG_SE
         }
         __syncwarp();
       }
-      // Warp reductions (REDUX): the int64 reward sum as four exact 16-bit-limb partial sums
-      // (no 32-bit wrap for any reward validate() admits).
+      // Warp reductions (REDUX): the int64 reward sum as three exact limb partial sums —
+      // bits 0-21 and 22-43 unsigned, 44-63 signed: 32 lanes of 22 (20) bits cannot wrap 32
+      // bits, so every reward validate() admits (|sum| < 2^63) is reassembled exactly.
       // the self pair's contact and -c_collide term (sector pass, see `process`), removed
       const uint32_t nc = __reduce_add_sync(kFull, ncol[t]) - ((RAY || PAIRED || SS) ? 0u : 1u);
       const uint32_t nt = (ENV == kTag) ? __reduce_add_sync(kFull, ntouch[t]) : 0u;
       const unsigned long long ur = (unsigned long long)rs[t];
-      const uint32_t s_lo = __reduce_add_sync(kFull, (uint32_t)(ur & 0xffffu));
-      const uint32_t s_mid = __reduce_add_sync(kFull, (uint32_t)((ur >> 16) & 0xffffu));
-      const uint32_t s_hi = __reduce_add_sync(kFull, (uint32_t)((ur >> 32) & 0xffffu));
-      const int s_top = __reduce_add_sync(kFull, (int)((long long)ur >> 48));
-      long long rsum = (long long)(((unsigned long long)(long long)s_top << 48) +
-                                   ((unsigned long long)s_hi << 32) +
-                                   ((unsigned long long)s_mid << 16) + (unsigned long long)s_lo);
+      const uint32_t s_lo = __reduce_add_sync(kFull, (uint32_t)(ur & 0x3fffffu));
+      const uint32_t s_mid = __reduce_add_sync(kFull, (uint32_t)((ur >> 22) & 0x3fffffu));
+      const int s_top = __reduce_add_sync(kFull, (int)((long long)ur >> 44));
+      long long rsum = (long long)(((unsigned long long)(long long)s_top << 44) +
+                                   ((unsigned long long)s_mid << 22) + (unsigned long long)s_lo);
       if (!RAY && !PAIRED && !SS) {
         if (ENV == kFlock) rsum -= __float2ll_rn(c_mcollide);
         else if (tq[t] == 0u) rsum -= __float2ll_rn(VG_SC(w_prox) * c_mcollide);
