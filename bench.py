@@ -542,16 +542,21 @@ def run_ours(args):
         if world > 1:
             dist.barrier()
         t0 = time.perf_counter()
+        t_step = []
         for k in range(K):
             run.step_host(acts_h[k % 2], rew_h)
             stream.synchronize()               # the step's reward is readable on the host
+            t_step.append(time.perf_counter())
         e2e_s = time.perf_counter() - t0
+        t_step = [b - a for a, b in zip([t0] + t_step[:-1], t_step)]
         te = torch.tensor([e2e_s], dtype=torch.float64, device=device)
         if world > 1:
             dist.all_reduce(te, op=dist.ReduceOp.MAX)
         e2e = {"value": agents_all * K / float(te.item()), "unit": UNIT,
                "h2d_bytes_per_step": int(acts_h[0].numel() * 4),
                "d2h_bytes_per_step": int(rew_h.numel() * 4),
+               "step_ms": {"median": 1e3 * statistics.median(t_step), "max": 1e3 * max(t_step),
+                           "min": 1e3 * min(t_step)},
                "note": ("vg_step_host" if not slab_mode else "actions H2D + slab step + reward D2H")
                        + ": pinned host buffers, stream sync per step, wall clock, max over ranks; "
                          "the reward is read back, the observation stays on the device where "
