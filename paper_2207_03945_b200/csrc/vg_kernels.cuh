@@ -1258,6 +1258,9 @@ constexpr int kQueue = VG_SENSE_QUEUE;
 #ifndef VG_SENSE_E8
 #define VG_SENSE_E8 1
 #endif
+#ifndef VG_SENSE_UNSH
+#define VG_SENSE_UNSH 1
+#endif
 #ifndef VG_SENSE_MIXTAIL
 #define VG_SENSE_MIXTAIL 1
 #endif
@@ -1889,6 +1892,10 @@ __global__ void __launch_bounds__(kSenseWarps * 32, (DEF && ENV == kTag) ? VG_SE
         qx[t] = me[t].x + sg.qsx;                                     // exact (Sterbenz)
         qy[t] = me[t].y + sg.qsy;
       }
+      // UNSH: a run without image shifts (every run of an interior cell) reads the candidate
+      // positions as they are (x + 0 = x: positions are >= +0); its own instance of the loop.
+      auto chunk_loop = [&](auto unsh_c) {
+      constexpr bool UNSH = decltype(unsh_c)::value;
       for (uint32_t p0 = wb; p0 < we; p0 += 32 * HV) {
         // Ballot the in-radius candidates of one 32-slot half and append them to each
         // query's ring (dx, dy, d^2, index | type << 31).
@@ -1942,8 +1949,8 @@ __global__ void __launch_bounds__(kSenseWarps * 32, (DEF && ENV == kTag) ? VG_SE
             tj = __float_as_uint(x) & 0x80000000u;
             x = fabsf(x);
           }
-          cxh[h] = (pj < we) ? x + sg.csx : __int_as_float(0x7fc00000);   // exact (Sterbenz)
-          cyh[h] = o.y + sg.csy;
+          cxh[h] = (pj < we) ? (UNSH ? x : x + sg.csx) : __int_as_float(0x7fc00000);   // exact (Sterbenz)
+          cyh[h] = UNSH ? o.y : o.y + sg.csy;
           wh[h] = E8 ? 0u : pj | tj;
         }
 #pragma unroll
@@ -1983,6 +1990,9 @@ __global__ void __launch_bounds__(kSenseWarps * 32, (DEF && ENV == kTag) ? VG_SE
         // it syncs; a warp-uniform test of this chunk's P instead measured slower).
         if ((PAIRED ? 63 : 31) + 64 * HV > (int)(kQueue * 16u / ES)) __syncwarp();
       }
+      };
+      if (VG_SENSE_UNSH && sg.csx == 0.f && sg.csy == 0.f) chunk_loop(std::true_type{});   // warp-uniform
+      else chunk_loop(std::false_type{});
     }
     __syncwarp();
     if (PAIRED) {
