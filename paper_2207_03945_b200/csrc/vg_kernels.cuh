@@ -1258,6 +1258,9 @@ constexpr int kQueue = VG_SENSE_QUEUE;
 #ifndef VG_SENSE_E8
 #define VG_SENSE_E8 1
 #endif
+#ifndef VG_SENSE_NONAN
+#define VG_SENSE_NONAN 1
+#endif
 #ifndef VG_SENSE_UNSH
 #define VG_SENSE_UNSH 1
 #endif
@@ -1511,6 +1514,7 @@ __global__ void __launch_bounds__(kSenseWarps * 32, (DEF && ENV == kTag) ? VG_SE
   // the query's own sense-order index (an extra predicate input of the radius test), so
   // the pair pass, the counts and the emit need no self handling at all.
   constexpr bool SS = VG_SENSE_SCANSELF && !PAIRED;
+  constexpr bool NONAN = VG_SENSE_NONAN && SS && !PACKED_SCAN;
   // Pair-pass constants.  (ptxas sees through this empty asm and re-loads them from the
   // parameter bank per pair batch; forcing them into registers with an opaque add costs 8
   // registers and measured 4 % slower.)
@@ -1921,7 +1925,8 @@ __global__ void __launch_bounds__(kSenseWarps * 32, (DEF && ENV == kTag) ? VG_SE
               d2 = fmaf(dx, dx, dy * dy);
             }
             const bool in = d2 < (RAY ? VG_SC(cand2) : VG_SC(dv2)) &&             // Eq. 1: d < d_v
-                            (!SS || pj_ != q0 + (uint32_t)t);                        // j != i
+                            (!SS || pj_ != q0 + (uint32_t)t) &&                      // j != i
+                            (!NONAN || pj_ < we);
             const unsigned bal = __ballot_sync(kFull, in);
             if (E8) {
               if (in) sts64(qbase[t] | ((tail[t] + (__popc(bal & lt_mask) << 3)) & kRingMask), dx, dy);
@@ -1949,7 +1954,9 @@ __global__ void __launch_bounds__(kSenseWarps * 32, (DEF && ENV == kTag) ? VG_SE
             tj = __float_as_uint(x) & 0x80000000u;
             x = fabsf(x);
           }
-          cxh[h] = (pj < we) ? (UNSH ? x : x + sg.csx) : __int_as_float(0x7fc00000);   // exact (Sterbenz)
+          // slots past the run end: a NaN position (never within d_v), or with NONAN the
+          // window test folded into the candidate test's predicate
+          cxh[h] = (NONAN || pj < we) ? (UNSH ? x : x + sg.csx) : __int_as_float(0x7fc00000);   // exact (Sterbenz)
           cyh[h] = UNSH ? o.y : o.y + sg.csy;
           wh[h] = E8 ? 0u : pj | tj;
         }
