@@ -1258,6 +1258,9 @@ constexpr int kQueue = VG_SENSE_QUEUE;
 #ifndef VG_SENSE_E8
 #define VG_SENSE_E8 1
 #endif
+#ifndef VG_SENSE_W2
+#define VG_SENSE_W2 1
+#endif
 #ifndef VG_SENSE_NONAN
 #define VG_SENSE_NONAN 1
 #endif
@@ -1619,6 +1622,11 @@ __global__ void __launch_bounds__(kSenseWarps * 32, (DEF && ENV == kTag) ? VG_SE
     const uint32_t qb = (item.y == 0xffffffffu) ? cs[cl] : item.y;
     const uint32_t qe = min(cs[cl + 1], qb + cq);
     const uint32_t qstride = NQ * kSenseWarps;
+    // W2: the run windows of two warp-iterations in one pass (lanes [nseg, 2 nseg) take the
+    // next iteration's queries); the odd iterations reuse them.
+    constexpr bool W2 = VG_SENSE_W2 != 0;
+    uint32_t w2_wb = 0u, w2_we = 0u;
+    bool w2_have = false;
     for (uint32_t q0 = qb + NQ * warp; q0 < qe; q0 += qstride) {
     float4 me[NQ];
     bool live[NQ];
@@ -1850,12 +1858,27 @@ __global__ void __launch_bounds__(kSenseWarps * 32, (DEF && ENV == kTag) ? VG_SE
     // run axis bounds the reach along it to sqrt(r^2 - dperp^2); keys in the candidates' raw
     // frame.  A dead query (NaN) drops out of fminf / fmaxf (dperp -> 0: only ever wider).
     uint32_t my_wb = 0u, my_we = 0u;
-    if (lane < nseg) {
-      const Seg sg = s_seg[lane];
+    int woff = 0;                          // lane holding run 0's window of this iteration
+    if (W2 && w2_have) {
+      my_wb = w2_wb;
+      my_we = w2_we;
+      woff = nseg;
+      w2_have = false;
+    } else {
+      const bool nxt = W2 && lane >= nseg;
+      if (lane < (W2 ? 2 * nseg : nseg)) {
+      const Seg sg = s_seg[nxt ? lane - nseg : lane];
       float amin = 3.0e38f, amax = -3.0e38f, dperp = 3.0e38f;
 #pragma unroll
       for (int t = 0; t < NQ; ++t) {
-        const float qxs = me[t].x + sg.qsx, qys = me[t].y + sg.qsy;   // exact (Sterbenz)
+        float px = me[t].x, py = me[t].y;
+        if (nxt) {                         // the next iteration's query t (NaN if none)
+          const uint32_t qn = q0 + qstride + (uint32_t)t;
+          const float4 rn = (qn < qe) ? sorted[qn] : make_float4(__int_as_float(0x7fc00000), 0.f, 0.f, 0.f);
+          px = rn.x;
+          py = rn.y;
+        }
+        const float qxs = px + sg.qsx, qys = py + sg.qsy;             // exact (Sterbenz)
         const float aq = SLAB ? qys : qxs, pq = SLAB ? qxs : qys;
         amin = fminf(amin, aq);
         amax = fmaxf(amax, aq);
@@ -1878,9 +1901,15 @@ __global__ void __launch_bounds__(kSenseWarps * 32, (DEF && ENV == kTag) ? VG_SE
         my_wb = __ldg(&tb[g_lo]);
         my_we = __ldg(&tb[g_hi + 1]);
       }
+      }
+      if (W2) {
+        w2_wb = my_wb;
+        w2_we = my_we;
+        w2_have = q0 + qstride < qe;
+      }
     }
     for (int sgi = 0; sgi < nseg; ++sgi) {
-      const uint32_t wb = __shfl_sync(kFull, my_wb, sgi), we = __shfl_sync(kFull, my_we, sgi);
+      const uint32_t wb = __shfl_sync(kFull, my_wb, woff + sgi), we = __shfl_sync(kFull, my_we, woff + sgi);
       if (wb >= we) continue;                                        // warp-uniform
       Seg sg;
       {                                     // the run's image shifts: one broadcast load
