@@ -1259,7 +1259,10 @@ constexpr int kQueue = VG_SENSE_QUEUE;
 #define VG_SENSE_E8 1
 #endif
 #ifndef VG_SENSE_W2
-#define VG_SENSE_W2 1
+#define VG_SENSE_W2 32
+#endif
+#ifndef VG_SENSE_KITF
+#define VG_SENSE_KITF 1
 #endif
 #ifndef VG_SENSE_NONAN
 #define VG_SENSE_NONAN 1
@@ -1622,11 +1625,14 @@ __global__ void __launch_bounds__(kSenseWarps * 32, (DEF && ENV == kTag) ? VG_SE
     const uint32_t qb = (item.y == 0xffffffffu) ? cs[cl] : item.y;
     const uint32_t qe = min(cs[cl + 1], qb + cq);
     const uint32_t qstride = NQ * kSenseWarps;
-    // W2: the run windows of two warp-iterations in one pass (lanes [nseg, 2 nseg) take the
-    // next iteration's queries); the odd iterations reuse them.
-    constexpr bool W2 = VG_SENSE_W2 != 0;
+    // W2: the run windows of wn = min(32 / nseg, VG_SENSE_W2) warp-iterations in one pass —
+    // lane L computes run L mod nseg of iteration +L / nseg; the next wn - 1 iterations reuse
+    // them (an interior cell, 3 runs: 10 iterations, i.e. every window of the warp's queries).
+    constexpr bool W2 = VG_SENSE_W2 > 1;
+    const int wn = W2 ? min(32 / nseg, VG_SENSE_W2) : 1;
+    const float inv_nseg = 1.f / (float)nseg;
     uint32_t w2_wb = 0u, w2_we = 0u;
-    bool w2_have = false;
+    int w2_left = 0;                       // iterations that still have windows in w2_*
     for (uint32_t q0 = qb + NQ * warp; q0 < qe; q0 += qstride) {
     float4 me[NQ];
     bool live[NQ];
@@ -1859,21 +1865,28 @@ __global__ void __launch_bounds__(kSenseWarps * 32, (DEF && ENV == kTag) ? VG_SE
     // frame.  A dead query (NaN) drops out of fminf / fmaxf (dperp -> 0: only ever wider).
     uint32_t my_wb = 0u, my_we = 0u;
     int woff = 0;                          // lane holding run 0's window of this iteration
-    if (W2 && w2_have) {
+    if (W2 && w2_left > 0) {
       my_wb = w2_wb;
       my_we = w2_we;
-      woff = nseg;
-      w2_have = false;
+      woff = (wn - w2_left) * nseg;
+      --w2_left;
     } else {
-      const bool nxt = W2 && lane >= nseg;
-      if (lane < (W2 ? 2 * nseg : nseg)) {
-      const Seg sg = s_seg[nxt ? lane - nseg : lane];
+      int kit = 0;                           // this lane's iteration offset lane / nseg
+      if (VG_SENSE_KITF) {                   // (lane + 1/2) / nseg is >= 1/12 from an integer
+        kit = W2 ? __float2int_rz(((float)lane + 0.5f) * inv_nseg) : 0;
+      } else {
+#pragma unroll
+        for (int k = 1; k < 11; ++k) kit += (lane >= k * nseg) ? 1 : 0;   // nseg >= 3: kit <= 10
+      }
+      const bool nxt = kit > 0;
+      if (lane < wn * nseg) {
+      const Seg sg = s_seg[lane - kit * nseg];
       float amin = 3.0e38f, amax = -3.0e38f, dperp = 3.0e38f;
 #pragma unroll
       for (int t = 0; t < NQ; ++t) {
         float px = me[t].x, py = me[t].y;
         if (nxt) {                         // the next iteration's query t (NaN if none)
-          const uint32_t qn = q0 + qstride + (uint32_t)t;
+          const uint32_t qn = q0 + (uint32_t)kit * qstride + (uint32_t)t;
           const float4 rn = (qn < qe) ? sorted[qn] : make_float4(__int_as_float(0x7fc00000), 0.f, 0.f, 0.f);
           px = rn.x;
           py = rn.y;
@@ -1905,7 +1918,7 @@ __global__ void __launch_bounds__(kSenseWarps * 32, (DEF && ENV == kTag) ? VG_SE
       if (W2) {
         w2_wb = my_wb;
         w2_we = my_we;
-        w2_have = q0 + qstride < qe;
+        w2_left = wn - 1;                  // (iterations past qe never run)
       }
     }
     for (int sgi = 0; sgi < nseg; ++sgi) {
