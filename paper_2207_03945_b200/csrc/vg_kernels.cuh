@@ -1628,7 +1628,9 @@ __global__ void __launch_bounds__(kSenseWarps * 32, (DEF && ENV == kTag) ? VG_SE
     // W2: the run windows of wn = min(32 / nseg, VG_SENSE_W2) warp-iterations in one pass —
     // lane L computes run L mod nseg of iteration +L / nseg; the next wn - 1 iterations reuse
     // them (an interior cell, 3 runs: 10 iterations, i.e. every window of the warp's queries).
-    constexpr bool W2 = VG_SENSE_W2 > 1;
+    // (not for slab ranks: their items are short (chunk 24: ~3 iterations per warp), and the
+    // batched pass measured 0.186 -> 0.230 ms per rank at P = 8)
+    constexpr bool W2 = VG_SENSE_W2 > 1 && !SLAB;
     const int wn = W2 ? min(32 / nseg, VG_SENSE_W2) : 1;
     const float inv_nseg = 1.f / (float)nseg;
     uint32_t w2_wb = 0u, w2_we = 0u;
