@@ -1261,6 +1261,9 @@ constexpr int kQueue = VG_SENSE_QUEUE;
 #ifndef VG_SENSE_W2
 #define VG_SENSE_W2 32
 #endif
+#ifndef VG_SENSE_W2_SLAB
+#define VG_SENSE_W2_SLAB 0
+#endif
 #ifndef VG_SENSE_KITF
 #define VG_SENSE_KITF 1
 #endif
@@ -1630,7 +1633,7 @@ __global__ void __launch_bounds__(kSenseWarps * 32, (DEF && ENV == kTag) ? VG_SE
     // them (an interior cell, 3 runs: 10 iterations, i.e. every window of the warp's queries).
     // (not for slab ranks: their items are short (chunk 24: ~3 iterations per warp), and the
     // batched pass measured 0.186 -> 0.230 ms per rank at P = 8)
-    constexpr bool W2 = VG_SENSE_W2 > 1 && !SLAB;
+    constexpr bool W2 = VG_SENSE_W2 > 1 && (!SLAB || VG_SENSE_W2_SLAB);
     const int wn = W2 ? min(32 / nseg, VG_SENSE_W2) : 1;
     const float inv_nseg = 1.f / (float)nseg;
     uint32_t w2_wb = 0u, w2_we = 0u;
