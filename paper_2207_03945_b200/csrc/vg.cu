@@ -363,7 +363,11 @@ int sense_chunk_q(const vg_world* w) {
 #ifndef VG_SENSE_CHUNK_MAX
 #define VG_SENSE_CHUNK_MAX 128
 #endif
-  return (int)std::max(8LL, std::min(q, (long long)VG_SENSE_CHUNK_MAX));
+#ifndef VG_SENSE_CHUNK_MAX_SINGLE
+#define VG_SENSE_CHUNK_MAX_SINGLE 64   // one large world (c5): 64 measured 0.6 % faster; c4 keeps 128
+#endif
+  const long long cap = (w->P.R == 1 && !w->slab) ? VG_SENSE_CHUNK_MAX_SINGLE : VG_SENSE_CHUNK_MAX;
+  return (int)std::max(8LL, std::min(q, cap));
 }
 
 vg::WorkList work_list(vg_world* w) {

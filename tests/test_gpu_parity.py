@@ -304,7 +304,7 @@ def test_long_run_stability(cuda):
 
 def test_c5_clustered_sampled_rows(cuda):
     # The stress state at full size: cells with ~2000 agents are split into many K4 work
-    # items (chunk_q = 128); rows sampled from the densest cells and at random.
+    # items (chunk_q = 64); rows sampled from the densest cells and at random.
     torch = _torch()
     p = vi.workload("c5")
     w = make_world(p)
