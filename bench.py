@@ -494,7 +494,7 @@ def run_ours(args):
         # A spin kernel first holds the stream while the host enqueues every step, so no
         # host-side launch latency lands between a step's events (small worlds take only
         # tens of us per step; host cost is what e2e measures).
-        torch.cuda._sleep(200_000 * K + 2_000_000)     # ~0.1 ms per step at ~2 GHz
+        torch.cuda._sleep(400_000 * K + 4_000_000)     # ~0.2 ms per step at ~2 GHz
         for k in range(K):
             flush.fill_(k & 0xFF)                 # evict L2 between steps (not timed)
             ev0[k].record()

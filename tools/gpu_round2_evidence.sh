@@ -3,10 +3,10 @@
 python paper_2207_03945_b200/_build.py --force > gpurun_out/build_r2.log 2>&1
 timeout 1500 python -m pytest tests -m gpu -q -p no:cacheprovider > gpurun_out/gpu_tests_r2.log 2>&1; echo "tests rc $?"
 grep -E "passed|failed" gpurun_out/gpu_tests_r2.log | tail -3
-timeout 1200 python tools/parity_stats.py > gpurun_out/parity_stats_r2.log 2>&1; echo "parity rc $?"
-cp profiles/parity_stats.json gpurun_out/parity_stats_r2.json
 timeout 900 python bench.py > gpurun_out/bench_c5_r2.json 2> gpurun_out/bench_c5_r2.err; echo "bench c5 rc $?"
 timeout 600 python bench.py --config c4 --steps 20 --warmup 5 --no-cpu-baseline > gpurun_out/bench_c4_r2.json 2> gpurun_out/bench_c4_r2.err; echo "bench c4 rc $?"
+timeout 1200 python tools/parity_stats.py > gpurun_out/parity_stats_r2.log 2>&1; echo "parity rc $?"
+cp profiles/parity_stats.json gpurun_out/parity_stats_r2.json
 timeout 300 python tools/slab_timing.py > gpurun_out/slab_timing_r2.txt 2>&1; echo "slab rc $?"
 B="python bench.py --steps 2 --warmup 1 --no-cpu-baseline --no-e2e --no-policy --no-c4-binning"
 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none --csv --log-file gpurun_out/launches_c5_r2.csv $B > gpurun_out/ncu_launch.log 2>&1; echo "launches rc $?"
