@@ -1210,12 +1210,15 @@ __global__ void __launch_bounds__(RBCfg<MODE>::NT, RBCfg<MODE>::MINB) k_replica_
 
 
 // ---------------------------------------------------------------------------------- K4
-// One CTA per (replica, cell); warp w handles the cell's query agents w, w+W, ...  Each
-// query scans the 3x3 cell stencil — up to 6 contiguous runs of the sorted arrays, each
-// with a uniform torus image shift — for neighbours within d_v, compacts
-// them with ballot/popc into a per-warp queue, and processes full warps of 32 pairs:
-// contact test, reward term (fixed point, A16b), bearing, sector, and the per-sector
-// nearest distance by shared-memory atomicMin on the float bits (A2, A3).
+// One CTA per work item (a cell, or a chunk of a dense cell's queries); each warp takes two
+// queries at a time.  The queries scan the 3x3 cell stencil — up to 6 contiguous runs of
+// the sense-order arrays, each with a uniform torus image shift, each cut to the window the
+// two queries can reach — for neighbours within d_v other than themselves
+// (P:68); the hits are compacted with ballot/popc into one ring per query (8-byte
+// (dx, dy) entries for flock sector vision, 16-byte (dx, dy, d^2, index | type) otherwise),
+// and every full batch of 32 pairs takes the contact test, the reward term (fixed point,
+// A16b), the bearing, the sector and the per-sector nearest distance by a shared-memory
+// min on the float bits (A2, A3).  DESIGN.md §6 (v19-v21) lists each step and its measure.
 #ifndef VG_SENSE_NQ
 #define VG_SENSE_NQ 2
 #endif
@@ -1702,7 +1705,7 @@ __global__ void __launch_bounds__(kSenseWarps * 32, (DEF && ENV == kTag) ? VG_SE
       const uint32_t idx = min((uint32_t)k, (uint32_t)VG_SC(v));
       red_min(srow + rowoff + idx * 4u, __float_as_uint(fminf(d * c_inv_dv, kBelowOne)));
     };
-    // Pair pass over one queue entry (dx, dy, d^2, index | type << 31) of query t.
+    // Pair pass over one ring entry (dx, dy, d^2 [, index | type << 31]) of query t.
     auto process = [&](const int t, const float4 e) {
       if (FLOCK1) {
         flock_pair(e, csn[t], sn[t], (uint32_t)(t * kRowW * 4), rs[t], ncol[t]);
@@ -1949,7 +1952,7 @@ __global__ void __launch_bounds__(kSenseWarps * 32, (DEF && ENV == kTag) ? VG_SE
       constexpr bool UNSH = decltype(unsh_c)::value;
       for (uint32_t p0 = wb; p0 < we; p0 += 32 * HV) {
         // Ballot the in-radius candidates of one 32-slot half and append them to each
-        // query's ring (dx, dy, d^2, index | type << 31).
+        // query's ring ((dx, dy), or (dx, dy, d^2, index | type << 31)).
         auto scan = [&](const float cx_, const float cy_, const uint32_t word, const uint32_t pj_) {
           // PAIRED: dx, dy, d^2 of both queries as packed pairs (FADD2 with the candidate
           // broadcast, FMUL2, FFMA2), bitwise the scalar fmaf(dx, dx, dy * dy).
