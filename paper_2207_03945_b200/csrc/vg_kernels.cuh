@@ -1264,6 +1264,9 @@ constexpr int kQueue = VG_SENSE_QUEUE;
 #ifndef VG_SENSE_W2
 #define VG_SENSE_W2 32
 #endif
+#ifndef VG_SENSE_SCANASM
+#define VG_SENSE_SCANASM 1
+#endif
 #ifndef VG_SENSE_W2_SLAB
 #define VG_SENSE_W2_SLAB 0
 #endif
@@ -1527,6 +1530,7 @@ __global__ void __launch_bounds__(kSenseWarps * 32, (DEF && ENV == kTag) ? VG_SE
   // the pair pass, the counts and the emit need no self handling at all.
   constexpr bool SS = VG_SENSE_SCANSELF && !PAIRED;
   constexpr bool NONAN = VG_SENSE_NONAN && SS && !PACKED_SCAN;
+  constexpr bool SCANASM = VG_SENSE_SCANASM && E8 && SS && NONAN && NQ == 2;
   // Pair-pass constants.  (ptxas sees through this empty asm and re-loads them from the
   // parameter bank per pair batch; forcing them into registers with an opaque add costs 8
   // registers and measured 4 % slower.)
@@ -1957,6 +1961,36 @@ __global__ void __launch_bounds__(kSenseWarps * 32, (DEF && ENV == kTag) ? VG_SE
           // PAIRED: dx, dy, d^2 of both queries as packed pairs (FADD2 with the candidate
           // broadcast, FMUL2, FFMA2), bitwise the scalar fmaf(dx, dx, dy * dy).
           f32x2 dx2 = 0ull, dy2 = 0ull, dd2 = 0ull;
+          if (SCANASM) {
+            // E8 + SS + NONAN, two queries: the window test once as a predicate that both
+            // queries' tests take as an input; each query's test, ballot, rank and push.
+            const float dxa = cx_ - qx[0], dya = cy_ - qy[0], dxb = cx_ - qx[NQ - 1], dyb = cy_ - qy[NQ - 1];
+            const float d2a = fmaf(dxa, dxa, dya * dya), d2b = fmaf(dxb, dxb, dyb * dyb);
+            asm volatile(
+                "{\n\t.reg .pred pw, pa, pb;\n\t.reg .b32 ba, bb, ra, rb;\n\t"
+                "setp.lt.u32 pw, %2, %3;\n\t"
+                "setp.ne.and.u32 pa, %2, %4, pw;\n\t"
+                "setp.ne.and.u32 pb, %2, %5, pw;\n\t"
+                "setp.lt.and.f32 pa, %6, %8, pa;\n\t"
+                "setp.lt.and.f32 pb, %7, %8, pb;\n\t"
+                "vote.sync.ballot.b32 ba, pa, 0xffffffff;\n\t"
+                "vote.sync.ballot.b32 bb, pb, 0xffffffff;\n\t"
+                "and.b32 ra, ba, %9;\n\tpopc.b32 ra, ra;\n\t"
+                "and.b32 rb, bb, %9;\n\tpopc.b32 rb, rb;\n\t"
+                "shl.b32 ra, ra, 3;\n\tadd.u32 ra, ra, %0;\n\tand.b32 ra, ra, %12;\n\tor.b32 ra, ra, %10;\n\t"
+                "shl.b32 rb, rb, 3;\n\tadd.u32 rb, rb, %1;\n\tand.b32 rb, rb, %12;\n\tor.b32 rb, rb, %11;\n\t"
+                "@pa st.shared.v2.f32 [ra], {%13, %14};\n\t"
+                "@pb st.shared.v2.f32 [rb], {%15, %16};\n\t"
+                "popc.b32 ba, ba;\n\tpopc.b32 bb, bb;\n\t"
+                "shl.b32 ba, ba, 3;\n\tshl.b32 bb, bb, 3;\n\t"
+                "add.u32 %0, %0, ba;\n\tadd.u32 %1, %1, bb;\n\t}"
+                : "+r"(tail[0]), "+r"(tail[NQ - 1])
+                : "r"(pj_), "r"(we), "r"(q0), "r"(q0 + 1u), "f"(d2a), "f"(d2b),
+                  "f"(VG_SC(dv2)), "r"(lt_mask), "r"(qbase[0]), "r"(qbase[NQ - 1]),
+                  "r"(kRingMask), "f"(dxa), "f"(dya), "f"(dxb), "f"(dyb)
+                : "memory");
+            return;
+          }
           if (PACKED_SCAN) {
             dx2 = sub2(bc2(cx_), pk2(qx[0], qx[NQ - 1]));
             dy2 = sub2(bc2(cy_), pk2(qy[0], qy[NQ - 1]));
