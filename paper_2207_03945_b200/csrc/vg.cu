@@ -495,6 +495,7 @@ vg::Outs to_outs(const vg_world* w, const vg_outputs* o) {
                    (w->P.env != vg::kTag || r.n_touch) && (!w->slab || r.agent_id);
   const long long rows = w->slab ? (long long)w->P.N : w->P.total;
   r.fast = (all && rows * (w->P.obs_dim + 1) < (1LL << 31)) ? 1 : 0;
+  if (r.fast && w->P.occ_words == 4 && (reinterpret_cast<uintptr_t>(r.occ) & 15u) == 0) r.fast = 2;
   return r;
 }
 

@@ -61,7 +61,8 @@ struct Outs {
   uint32_t* occ;
   uint32_t* agent_id;   // slab mode: global id of each output row
   int fast;             // every output K4 writes is present and rows x obs_dim < 2^31:
-                        // K4 skips the NULL checks and indexes in 32 bits
+                        // K4 skips the NULL checks and indexes in 32 bits; 2: also the
+                        // occupancy rows (4 words) are 16-byte aligned (one vector store)
 };
 
 // Slab mode: this rank owns global cell columns [lo, hi), W = hi - lo >= 2.
@@ -1264,6 +1265,9 @@ constexpr int kQueue = VG_SENSE_QUEUE;
 #ifndef VG_SENSE_W2
 #define VG_SENSE_W2 32
 #endif
+#ifndef VG_OCC_V4
+#define VG_OCC_V4 1
+#endif
 #ifndef VG_SENSE_SCANASM
 #define VG_SENSE_SCANASM 1
 #endif
@@ -2192,13 +2196,20 @@ __global__ void __launch_bounds__(kSenseWarps * 32, (DEF && ENV == kTag) ? VG_SE
             if (ENV == kFlock && lane == 0) vg_st_out(&orow[VG_SC(view_slots)], me[t].w * VG_SC(inv_smax));  // A24
           }
           if (FAST || O.occ) {
-            uint32_t mine = 0u;
+            uint32_t mine = 0u, bw[kMaxViewSlots / 32];
 #pragma unroll
             for (int w = 0; w < kMaxViewSlots / 32; ++w) {
-              const unsigned bits = __ballot_sync(kFull, vals[w] < kOneBits);
-              if (lane == w) mine = bits;
+              bw[w] = __ballot_sync(kFull, vals[w] < kOneBits);
+              if (lane == w) mine = bw[w];
             }
-            if (lane < VG_SC(occ_words)) vg_st_out(&O.occ[row * (idx_t)VG_SC(occ_words) + lane], mine);
+            if (FAST && VG_OCC_V4 && kMaxViewSlots == 128 && VG_SC(occ_words) == 4 && O.fast == 2) {
+              // four occupancy words, 16-byte aligned rows: one vector store by lane 0
+              if (lane == 0)
+                asm volatile("st.global.cs.v4.u32 [%0], {%1, %2, %3, %4};" ::"l"(O.occ + row * (idx_t)4),
+                             "r"(bw[0]), "r"(bw[1]), "r"(bw[2]), "r"(bw[3]) : "memory");
+            } else if (lane < VG_SC(occ_words)) {
+              vg_st_out(&O.occ[row * (idx_t)VG_SC(occ_words) + lane], mine);
+            }
           }
         }
       };

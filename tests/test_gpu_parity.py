@@ -504,6 +504,28 @@ def test_partial_outputs_equal_full(cuda, which):
         w.close()
 
 
+def test_unaligned_occupancy_rows_equal_aligned(cuda):
+    # K4 writes the four occupancy words of a row as one 16-byte store when the caller's
+    # tensor is 16-byte aligned, and word by word otherwise: both give the same words.
+    torch = _torch()
+    for p in (vi.workload("c2"), vi.tag_params(3000, width=60.0)):
+        w = make_world(p)
+        st = dev(vi.init_state(p, seed=6))
+        full = w.alloc_outputs()
+        odd = w.alloc_outputs()
+        n = p.n_replicas * p.n_agents * w.occ_words
+        raw = torch.empty(n + 1, dtype=torch.int32, device="cuda")
+        odd.sector_occ = raw[1:].view(p.n_replicas, p.n_agents, w.occ_words)   # 4-byte offset
+        assert odd.sector_occ.data_ptr() % 16 != 0
+        w.bin(st)
+        w.sense(full)
+        w.sense(odd)
+        torch.cuda.synchronize()
+        for k in ("obs", "reward", "n_neigh", "n_collide", "sector_occ"):
+            assert torch.equal(getattr(odd, k).view(torch.int32), getattr(full, k).view(torch.int32)), k
+        w.close()
+
+
 def test_integrate_then_bin_sense_equals_step(cuda):
     torch = _torch()
     p = vi.workload("c2")
