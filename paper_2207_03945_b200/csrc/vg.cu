@@ -305,6 +305,8 @@ vg::Params derive(const vg_config& c, int g) {
   P.fx_nk_fall = P.nk_fall * 4294967296.0f;
   P.fx_b_fall = P.b_fall * 4294967296.0f;
   P.fx_mcollide = -P.c_collide * 4294967296.0f;
+  P.fx_cnear = c.c_near * 4294967296.0f;
+  P.tent_sym = (VG_TENT_SYM && P.k_rise == P.k_fall) ? 1 : 0;
   P.half_v = 0.5f * (float)c.v;
   P.touch_fix = (long long)std::llrint((double)c.r_touch * 4294967296.0);
   P.cell = L / (float)g;

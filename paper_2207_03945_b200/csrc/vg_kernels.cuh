@@ -44,6 +44,10 @@ struct Params {
   // The same line pair and -c_collide times 2^32 (exact scalings): K4 evaluates f directly
   // in fixed-point units, f * 2^32 (A16b), bit-identical to scaling afterwards.
   float fx_k_rise, fx_b_rise, fx_nk_fall, fx_b_fall, fx_mcollide;
+  // symmetric tent (k_rise == k_fall, d_peak the midpoint of [2 d_r, d_v]: the defaults):
+  // f = c_near - k |d - d_peak|, one add and one FMA (fx_cnear = c_near 2^32)
+  int tent_sym;
+  float fx_cnear;
   float half_v;                    // v / 2: sector coordinate phi v / fov + v / 2 (A3)
   float d_r, cand2, inv_w;         // ray vision: body radius, RN32((d_v + d_r)^2), v / fov
   float cell;                      // RN32(L / G) (K4 windows only)
@@ -1265,6 +1269,9 @@ constexpr int kQueue = VG_SENSE_QUEUE;
 #ifndef VG_SENSE_W2
 #define VG_SENSE_W2 32
 #endif
+#ifndef VG_TENT_SYM
+#define VG_TENT_SYM 1
+#endif
 #ifndef VG_OCC_V4
 #define VG_OCC_V4 1
 #endif
@@ -1468,12 +1475,15 @@ struct SenseConst {
   float inv_w, half_v, inv_dv, dv2, w_prox, inv_smax;
   float d_r, cand2, half_fov, two_pi, d_v;         // ray vision
   int v, view_slots, obs_dim, occ_words;
+  int tent_sym;
+  float d_peak, fx_cnear;
 };
 __host__ __device__ __forceinline__ SenseConst sense_const(const Params& P) {
   return SenseConst{P.contact2, P.fx_mcollide, P.fx_k_rise, P.fx_b_rise, P.fx_nk_fall,
                     P.fx_b_fall, P.inv_w, P.half_v, P.inv_dv, P.dv2, P.w_prox, P.inv_smax,
                     P.d_r, P.cand2, P.half_fov, P.two_pi, P.d_v,
-                    P.v, P.view_slots, P.obs_dim, P.occ_words};
+                    P.v, P.view_slots, P.obs_dim, P.occ_words,
+                    P.tent_sym, P.d_peak, P.fx_cnear};
 }
 template <int ENV>
 __host__ __device__ constexpr SenseConst sense_defaults() {
@@ -1487,7 +1497,8 @@ __host__ __device__ constexpr SenseConst sense_defaults() {
                     1.0f / d_v, d_v * d_v, 0.1f, 1.0f / 0.5f,
                     0.25f, (d_v + 0.25f) * (d_v + 0.25f), 0.5f * fov,
                     (float)(2.0 * 3.14159265358979323846), d_v,
-                    v, ch * v, ch * v + ((ENV == kFlock) ? 1 : 0), (ch * v + 31) / 32};
+                    v, ch * v, ch * v + ((ENV == kFlock) ? 1 : 0), (ch * v + 31) / 32,
+                    VG_TENT_SYM ? ((k_rise == k_fall) ? 1 : 0) : 0, d_peak, c_near * fx};
 }
 
 template <int ENV, bool VISION, bool SLAB, bool RAY, bool DEF>
@@ -1700,7 +1711,8 @@ __global__ void __launch_bounds__(kSenseWarps * 32, (DEF && ENV == kTag) ? VG_SE
       asm("sqrt.approx.ftz.f32 %0, %1;" : "=f"(d) : "f"(d2));
       // Eq. 1 / Fig. 4 (A5) in fixed point (A16b); contact (A6, inclusive) test, the term's
       // select and the contact count under one predicate
-      const float tent = fminf(fmaf(c_k_rise, d, c_b_rise), fmaf(c_nk_fall, d, c_b_fall));
+      const float tent = VG_SC(tent_sym) ? fmaf(c_nk_fall, fabsf(d - VG_SC(d_peak)), VG_SC(fx_cnear))
+                                         : fminf(fmaf(c_k_rise, d, c_b_rise), fmaf(c_nk_fall, d, c_b_fall));
       float f;
       asm("{\n\t.reg .pred p;\n\tsetp.le.f32 p, %2, %3;\n\tselp.f32 %0, %4, %5, p;\n\t"
           "@p add.u32 %1, %1, 1;\n\t}"
@@ -1745,7 +1757,8 @@ __global__ void __launch_bounds__(kSenseWarps * 32, (DEF && ENV == kTag) ? VG_SE
       }
       // Eq. 1 / Fig. 4 (A5): contact -> -c_collide, else the tent min(rise, fall); in
       // fixed-point units (x 2^32, A16b).
-      const float tent = fminf(fmaf(c_k_rise, d, c_b_rise), fmaf(c_nk_fall, d, c_b_fall));
+      const float tent = VG_SC(tent_sym) ? fmaf(c_nk_fall, fabsf(d - VG_SC(d_peak)), VG_SC(fx_cnear))
+                                         : fminf(fmaf(c_k_rise, d, c_b_rise), fmaf(c_nk_fall, d, c_b_fall));
       float f = contact ? c_mcollide : tent;
       if (ENV == kFlock && !RAY && VG_SENSE_PREDCNT) {
         // the contact test, the term's select and the contact count under one predicate
