@@ -1269,6 +1269,9 @@ constexpr int kQueue = VG_SENSE_QUEUE;
 #ifndef VG_SENSE_W2
 #define VG_SENSE_W2 32
 #endif
+#ifndef VG_SENSE_HFORCE
+#define VG_SENSE_HFORCE 2
+#endif
 #ifndef VG_TENT_SYM
 #define VG_TENT_SYM 1
 #endif
@@ -2063,7 +2066,9 @@ __global__ void __launch_bounds__(kSenseWarps * 32, (DEF && ENV == kTag) ? VG_SE
         }
 #pragma unroll
         for (int h = 0; h < HV; ++h)
-          if (h == 0 || p0 + 32u * h < we) scan(cxh[h], cyh[h], wh[h], p0 + 32u * h + lane);
+          // the first VG_SENSE_HFORCE halves without the skip test (a window is almost never
+          // shorter; past its end the candidate predicate is false anyway)
+          if (h < (NONAN ? VG_SENSE_HFORCE : 1) || p0 + 32u * h < we) scan(cxh[h], cyh[h], wh[h], p0 + 32u * h + lane);
         __syncwarp();                       // ring pushes above are visible to the warp
         if (PAIRED) {
           // Full batches of both queries together (process2); a query's ring is drained
