@@ -2050,7 +2050,7 @@ __global__ void __launch_bounds__(kSenseWarps * 32, (DEF && ENV == kTag) ? VG_SE
         for (int h = 0; h < HV; ++h) {
           const uint32_t pj = p0 + 32u * h + lane;
           // VG_SENSE_LDPRED: halves wholly past the window end load nothing (predicated)
-          const float2 o = (!VG_SENSE_LDPRED || h == 0 || p0 + 32u * h < we)
+          const float2 o = (!VG_SENSE_LDPRED || h < (NONAN ? VG_SENSE_HFORCE : 1) || p0 + 32u * h < we)
                                ? __ldg(&sorted_xy[pj]) : make_float2(0.f, 0.f);
           float x = o.x;
           uint32_t tj = 0u;
