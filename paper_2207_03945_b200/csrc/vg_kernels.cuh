@@ -1284,6 +1284,11 @@ constexpr int kQueue = VG_SENSE_QUEUE;
 #ifndef VG_SENSE_W2_SLAB
 #define VG_SENSE_W2_SLAB 0
 #endif
+// UNI: the item bounds, the stencil-run count and each run's window pass through a REDUX
+// (uniform registers), so ptxas can prove the sense loops warp-uniform.
+#ifndef VG_SENSE_UNI
+#define VG_SENSE_UNI 1
+#endif
 #ifndef VG_SENSE_KITF
 #define VG_SENSE_KITF 1
 #endif
@@ -1524,7 +1529,8 @@ __global__ void __launch_bounds__(kSenseWarps * 32, (DEF && ENV == kTag) ? VG_SE
   __shared__ Seg s_seg[6];
   __shared__ int s_nseg;
 
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int lane = threadIdx.x & 31;
+  const int warp = VG_SENSE_UNI ? (int)__reduce_max_sync(kFull, threadIdx.x >> 5) : (int)(threadIdx.x >> 5);
   if (RAY) {
     for (int k = threadIdx.x; k < P.v; k += blockDim.x) s_ray[k] = ray_dir[k];
   }
@@ -1645,13 +1651,17 @@ __global__ void __launch_bounds__(kSenseWarps * 32, (DEF && ENV == kTag) ? VG_SE
     s_nseg = ns;
   }
     __syncthreads();
-    const int nseg = s_nseg;
+    const int nseg = VG_SENSE_UNI ? (int)__reduce_max_sync(kFull, (uint32_t)s_nseg) : s_nseg;
     uint32_t cq = (uint32_t)chunk_q;
     if (SLAB)
       for (int k2 = 0; k2 < 4; ++k2)
         if (k2 < SL.nb && SL.bcol[k2] == c / P.G) cq = (uint32_t)SL.chunk_qb;
-    const uint32_t qb = (item.y == 0xffffffffu) ? cs[cl] : item.y;
-    const uint32_t qe = min(cs[cl + 1], qb + cq);
+    uint32_t qb = (item.y == 0xffffffffu) ? cs[cl] : item.y;
+    uint32_t qe = min(cs[cl + 1], qb + cq);
+    if (VG_SENSE_UNI) {
+      qb = __reduce_max_sync(kFull, qb);
+      qe = __reduce_max_sync(kFull, qe);
+    }
     const uint32_t qstride = NQ * kSenseWarps;
     // W2: the run windows of wn = min(32 / nseg, VG_SENSE_W2) warp-iterations in one pass —
     // lane L computes run L mod nseg of iteration +L / nseg; the next wn - 1 iterations reuse
@@ -1954,7 +1964,15 @@ __global__ void __launch_bounds__(kSenseWarps * 32, (DEF && ENV == kTag) ? VG_SE
       }
     }
     for (int sgi = 0; sgi < nseg; ++sgi) {
-      const uint32_t wb = __shfl_sync(kFull, my_wb, woff + sgi), we = __shfl_sync(kFull, my_we, woff + sgi);
+      uint32_t wb, we;
+      if (VG_SENSE_UNI) {
+        const bool src = lane == woff + sgi;
+        wb = __reduce_max_sync(kFull, src ? my_wb : 0u);
+        we = __reduce_max_sync(kFull, src ? my_we : 0u);
+      } else {
+        wb = __shfl_sync(kFull, my_wb, woff + sgi);
+        we = __shfl_sync(kFull, my_we, woff + sgi);
+      }
       if (wb >= we) continue;                                        // warp-uniform
       Seg sg;
       {                                     // the run's image shifts: one broadcast load
@@ -2104,7 +2122,10 @@ __global__ void __launch_bounds__(kSenseWarps * 32, (DEF && ENV == kTag) ? VG_SE
         if ((PAIRED ? 63 : 31) + 64 * HV > (int)(kQueue * 16u / ES)) __syncwarp();
       }
       };
-      if (VG_SENSE_UNSH && sg.csx == 0.f && sg.csy == 0.f) chunk_loop(std::true_type{});   // warp-uniform
+      const bool unsh = VG_SENSE_UNI
+          ? __reduce_or_sync(kFull, (sg.csx == 0.f && sg.csy == 0.f) ? 0u : 1u) == 0u
+          : (sg.csx == 0.f && sg.csy == 0.f);
+      if (VG_SENSE_UNSH && unsh) chunk_loop(std::true_type{});   // warp-uniform
       else chunk_loop(std::false_type{});
     }
     __syncwarp();
