@@ -412,6 +412,15 @@ __device__ __forceinline__ uint32_t work_chunks(const WorkList& WL, int cell, ui
 #define VG_SUB_BINS 32
 #endif
 constexpr int kSub = VG_SUB_BINS;           // power of 2, 2..32
+// VG_BIN_UNI: warp-uniform values (warp index, cell index, member count) of the binning
+// kernels pass through a REDUX into uniform registers, so ptxas can prove their warp loops
+// convergent (no BRA.DIV / BSSY around every ballot, shuffle and match).
+#ifndef VG_BIN_UNI
+#define VG_BIN_UNI 1
+#endif
+__device__ __forceinline__ uint32_t bin_uni(uint32_t v) {
+  return VG_BIN_UNI ? __reduce_max_sync(0xffffffffu, v) : v;
+}
 __device__ __forceinline__ int sub_bin(const Params& P, int ca, float a) {
   const int sb = __float2int_rd(__fmul_rn(a, P.gs) * (float)kSub) - kSub * ca;
   return min(max(sb, 0), kSub - 1);
@@ -443,6 +452,7 @@ __device__ __forceinline__ void sense_order_place(const Params& P, int ca, bool 
                                                   float2* __restrict__ xo_xy, uint32_t* tab,
                                                   int lane, unsigned lt, uint32_t rb,
                                                   uint32_t cnt) {
+  m = (int)bin_uni((uint32_t)m);
   uint32_t inc = cnt;                                     // exclusive scan over lanes < kSub
 #pragma unroll
   for (int o = 1; o < kSub; o <<= 1) {
@@ -485,6 +495,7 @@ __device__ __forceinline__ void sense_order_cell(const Params& P, int ca, bool a
                                                  uint32_t* __restrict__ xo_perm,
                                                  float2* __restrict__ xo_xy, uint32_t* tab,
                                                  int lane, unsigned lt, uint32_t rb) {
+  m = (int)bin_uni((uint32_t)m);
   uint32_t cnt = 0;                                       // lane s < kSub: records in sub-bin s
   for (int ib = 0; ib < m; ib += 32) {
     const bool valid = ib + lane < m;
@@ -562,8 +573,8 @@ __global__ void __launch_bounds__(256) k_cell_sort(
     uint32_t* __restrict__ xo_perm, float2* __restrict__ xo_xy, uint32_t* __restrict__ sub_tab,
     WorkList WL, uint32_t* __restrict__ scratch, int cell0) {
   // cells [cell0, n_cells) (slab binning phases: a range of memory columns)
-  const int cell = cell0 + (int)(((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5);
-  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  const int cell = (int)bin_uni((uint32_t)(cell0 + (int)(((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5)));
+  const int lane = threadIdx.x & 31, wib = (int)bin_uni(threadIdx.x >> 5);
   // K4 work items of this block's 8 cells: one atomic per block.
   __shared__ uint32_t s_nch[8], s_base;
   const uint32_t b0 = (cell < n_cells) ? cell_start[cell] : 0u;
@@ -582,12 +593,12 @@ __global__ void __launch_bounds__(256) k_cell_sort(
       WL.item[at + k] = make_uint2((uint32_t)(cell - WL.lo), b0 + (k + 1u) * work_chunk_q(WL, cell));
   }
   if (cell > n_cells) return;
-  const uint32_t b = cell_start[cell];
+  const uint32_t b = bin_uni(cell_start[cell]);
   if (cell == n_cells) {
     if (lane == 0) sub_tab[(size_t)n_cells * kSub] = b;
     return;
   }
-  const int m = (int)(cell_start[cell + 1] - b);
+  const int m = (int)bin_uni(cell_start[cell + 1] - b);
   if (m > kRankMax) {                                   // dense cell: merge sort
     uint32_t *ks, *vs;
     cell_merge_sort(b, m, const_cast<uint32_t*>(tmp_id), scratch, perm, xo_perm, lane, ks, vs);
@@ -921,7 +932,7 @@ __global__ void __launch_bounds__(RBCfg<MODE>::NT, RBCfg<MODE>::MINB) k_replica_
   __shared__ uint32_t s_tot[kRBMaxCells];
   __shared__ __align__(8) uint64_t s_bar;                    // STAGED: input-state TMA barrier
   extern __shared__ __align__(128) unsigned char rb_dyn[];   // STAGED: see kRBStagedSmem
-  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int tid = threadIdx.x, warp = (int)bin_uni(tid >> 5), lane = tid & 31;
   const int N = P.N, C = P.G2;
   const float4* src = INTEGRATE ? state_io : state_in;
   const int span = (N + NW - 1) / NW;
