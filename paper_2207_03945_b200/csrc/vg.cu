@@ -520,6 +520,7 @@ void sense_carveouts() {
   sense_carveout(vg::k_sense<ENV, VISION, SLAB, false, false>, VG_SENSE_CARVEOUT);
   if (VISION) {
     sense_carveout(vg::k_sense<ENV, VISION, SLAB, false, VISION>, VG_SENSE_CARVEOUT);
+    if constexpr (VISION && !SLAB) sense_carveout(vg::k_sense<ENV, VISION, SLAB, false, 2>, VG_SENSE_CARVEOUT);
     sense_carveout(vg::k_sense<ENV, VISION, SLAB, true, VISION>, VG_SENSE_CARVEOUT_RAY);
   }
 }
@@ -578,6 +579,10 @@ void sense_kernel(vg_world* w, int cells, const vg::Outs& O, cudaStream_t s) {
         w->work, w->work_cnt, cq, cells);
   else if (w->cfg.vision == VG_VISION_RAY)
     vg::k_sense<ENV, VISION, SLAB, true, false><<<grid, vg::kSenseWarps * 32, 0, s>>>(
+        w->P, w->cell_start, w->xo_rec, w->xo_xy, w->xo_perm, O, w->SL, w->ray_dir, w->sub_tab,
+        w->work, w->work_cnt, cq, cells);
+  else if (VISION && w->sense_def && !SLAB && w->P.R == 1)      // one large world
+    vg::k_sense<ENV, VISION, SLAB, false, (VISION && !SLAB) ? 2 : 0><<<grid, vg::kSenseWarps * 32, 0, s>>>(
         w->P, w->cell_start, w->xo_rec, w->xo_xy, w->xo_perm, O, w->SL, w->ray_dir, w->sub_tab,
         w->work, w->work_cnt, cq, cells);
   else if (VISION && w->sense_def)

@@ -1520,7 +1520,14 @@ __host__ __device__ constexpr SenseConst sense_defaults() {
                     VG_TENT_SYM ? ((k_rise == k_fall) ? 1 : 0) : 0, d_peak, c_near * fx};
 }
 
-template <int ENV, bool VISION, bool SLAB, bool RAY, bool DEF>
+// DEF: 0 generic constants; 1 the paper's defaults as immediates (vg::sense_defaults);
+// 2 the same for one large world (c5), whose chunks take VG_SENSE_HFORCE_SINGLE halves
+// without the window-end skip (measured 681 vs 688 us; replica worlds (c4) 3,605 vs 3,629 us
+// with VG_SENSE_HFORCE, and a kernel argument in their place measured slower for both).
+#ifndef VG_SENSE_HFORCE_SINGLE
+#define VG_SENSE_HFORCE_SINGLE 3
+#endif
+template <int ENV, bool VISION, bool SLAB, bool RAY, int DEF>
 __global__ void __launch_bounds__(kSenseWarps * 32, (DEF && ENV == kTag) ? VG_SENSE_TAG_DEF_MINB : DEF ? VG_SENSE_DEF_MINB : kSenseMinBlocks) k_sense(
     Params P, const uint32_t* __restrict__ cell_start, const float4* __restrict__ sorted,
     const float2* __restrict__ sorted_xy, const uint32_t* __restrict__ perm, Outs O, Slab SL,
@@ -1560,6 +1567,7 @@ __global__ void __launch_bounds__(kSenseWarps * 32, (DEF && ENV == kTag) ? VG_SE
   constexpr uint32_t ES = E8 ? 8u : 16u, ES_SH = E8 ? 3u : 4u;
   constexpr uint32_t kRingMask = kQueue * 16u - ES;      // byte offsets within a ring
   constexpr int HV = E8 ? VG_SENSE_E8_HALVES : kSenseHalves;   // 32-slot halves per chunk
+  constexpr int HF = (DEF == 2) ? VG_SENSE_HFORCE_SINGLE : VG_SENSE_HFORCE;   // halves without the skip test
   // SS: the self pair never enters the ring — the candidate test also requires slot pj !=
   // the query's own sense-order index (an extra predicate input of the radius test), so
   // the pair pass, the counts and the emit need no self handling at all.
@@ -2079,7 +2087,7 @@ __global__ void __launch_bounds__(kSenseWarps * 32, (DEF && ENV == kTag) ? VG_SE
         for (int h = 0; h < HV; ++h) {
           const uint32_t pj = p0 + 32u * h + lane;
           // VG_SENSE_LDPRED: halves wholly past the window end load nothing (predicated)
-          const float2 o = (!VG_SENSE_LDPRED || h < (NONAN ? VG_SENSE_HFORCE : 1) || p0 + 32u * h < we)
+          const float2 o = (!VG_SENSE_LDPRED || h < (NONAN ? HF : 1) || p0 + 32u * h < we)
                                ? __ldg(&sorted_xy[pj]) : make_float2(0.f, 0.f);
           float x = o.x;
           uint32_t tj = 0u;
@@ -2097,7 +2105,7 @@ __global__ void __launch_bounds__(kSenseWarps * 32, (DEF && ENV == kTag) ? VG_SE
         for (int h = 0; h < HV; ++h)
           // the first VG_SENSE_HFORCE halves without the skip test (a window is almost never
           // shorter; past its end the candidate predicate is false anyway)
-          if (h < (NONAN ? VG_SENSE_HFORCE : 1) || p0 + 32u * h < we) scan(cxh[h], cyh[h], wh[h], p0 + 32u * h + lane);
+          if (h < (NONAN ? HF : 1) || p0 + 32u * h < we) scan(cxh[h], cyh[h], wh[h], p0 + 32u * h + lane);
         __syncwarp();                       // ring pushes above are visible to the warp
         if (PAIRED) {
           // Full batches of both queries together (process2); a query's ring is drained

@@ -91,7 +91,7 @@ pick = lambda pre: next(n for n in names if n.startswith(pre))  # noqa: E731
 mp = {"integrate_bin": [pick("void vg::k_integrate_bin<0, 1, 1>")],
       "scan_cells": [pick("vg::k_scan_tiles"), pick("vg::k_scan_apply")],
       "scatter": [pick("void vg::k_scatter<0>")], "cell_sort": [pick("vg::k_cell_sort")],
-      "sense": [pick("void vg::k_sense<0, 1, 0, 0, 1")]}
+      "sense": [pick("void vg::k_sense<0, 1, 0, 0, 2")]}
 json.dump({"config": "c5", "source": "ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum "
                                      "(cold caches, serialised launches; round-2 kernels; profiles/r2_launches_c5.csv)",
            "stages": {st: {"dram_read_B": int(sum(mean(k, "dram__bytes_read.sum") for k in ks)),
