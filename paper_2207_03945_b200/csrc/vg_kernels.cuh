@@ -1300,6 +1300,10 @@ constexpr int kQueue = VG_SENSE_QUEUE;
 #ifndef VG_SENSE_UNI
 #define VG_SENSE_UNI 1
 #endif
+#ifndef VG_SENSE_DRAIN_UNROLL
+#define VG_SENSE_DRAIN_UNROLL 1    // ring drain loop unroll (A/B)
+#endif
+constexpr int kDrainUnroll = VG_SENSE_DRAIN_UNROLL;
 #ifndef VG_SENSE_KITF
 #define VG_SENSE_KITF 1
 #endif
@@ -2127,6 +2131,9 @@ __global__ void __launch_bounds__(kSenseWarps * 32, (DEF && ENV == kTag) ? VG_SE
         } else {
 #pragma unroll
           for (int t = 0; t < NQ; ++t) {
+#if VG_SENSE_DRAIN_UNROLL > 1
+#pragma unroll kDrainUnroll
+#endif
             while (tail[t] - head[t] >= 32u * ES) {
               process(t, ring_entry(t, head[t] + lane * ES));
               head[t] += 32u * ES;
