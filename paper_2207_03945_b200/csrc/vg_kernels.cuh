@@ -1304,6 +1304,14 @@ constexpr int kQueue = VG_SENSE_QUEUE;
 #define VG_SENSE_DRAIN_UNROLL 1    // ring drain loop unroll (A/B)
 #endif
 constexpr int kDrainUnroll = VG_SENSE_DRAIN_UNROLL;
+// UCONST: the three constants of the flock pair pass that share an FFMA with another
+// constant (the first atan2 coefficient, v / fov, the tent slope) held in uniform registers
+// (a REDUX of the value), so ptxas need not re-create them in every 32-pair batch (48 -> 45
+// instructions per batch).  Bit 0: the replica instance (DEF = 1; c4 3,603 -> 3,557 us);
+// bit 1: the single-world instance (DEF = 2; measured 678 -> 683 us at c5, so off).
+#ifndef VG_SENSE_UCONST
+#define VG_SENSE_UCONST 1
+#endif
 #ifndef VG_SENSE_KITF
 #define VG_SENSE_KITF 1
 #endif
@@ -1340,7 +1348,7 @@ static_assert(kQueue >= 31 + 32 * kSenseHalves, "ring: carried + one chunk of pu
 #ifndef VG_ATAN_DEG
 #define VG_ATAN_DEG 6
 #endif
-__device__ __forceinline__ float vg_atan2(float y, float x) {
+__device__ __forceinline__ float vg_atan2(float y, float x, float c6 = 0.006812420208007097f) {
   const float ax = fabsf(x), ay = fabsf(y);
   const float mx = fmaxf(ax, ay), mn = fminf(ax, ay);
   float rc;                                 // <= 1 ulp; mx = 0 (then mn = 0) gives t = 0
@@ -1357,7 +1365,7 @@ __device__ __forceinline__ float vg_atan2(float y, float x) {
   p = fmaf(p, s, -0.33262315f);
   p = fmaf(p, s, 0.99997723f);
 #else
-  float p = 0.006812420208007097f;
+  float p = c6;                             // 0.006812420208007097f (a caller may pass it in a uniform register)
   p = fmaf(p, s, -0.03360610455274582f);
   p = fmaf(p, s, 0.07962583005428314f);
   p = fmaf(p, s, -0.13233458995819092f);
@@ -1593,6 +1601,12 @@ __global__ void __launch_bounds__(kSenseWarps * 32, (DEF && ENV == kTag) ? VG_SE
   if (!DEF)
     asm volatile("" : "+f"(c_contact2), "+f"(c_mcollide), "+f"(c_k_rise), "+f"(c_b_rise),
                  "+f"(c_nk_fall), "+f"(c_b_fall), "+f"(c_inv_w), "+f"(c_half_v), "+f"(c_inv_dv));
+  float u_c6 = 0.006812420208007097f, u_nk_fall = c_nk_fall, u_inv_w = c_inv_w;
+  if (DEF && ((VG_SENSE_UCONST >> (DEF - 1)) & 1)) {
+    u_c6 = __uint_as_float(__reduce_max_sync(kFull, __float_as_uint(u_c6)));
+    u_nk_fall = __uint_as_float(__reduce_max_sync(kFull, __float_as_uint(u_nk_fall)));
+    u_inv_w = __uint_as_float(__reduce_max_sync(kFull, __float_as_uint(u_inv_w)));
+  }
   // CTA c < n_first: the first chunk_q queries of sensed cell c; CTA n_first + k: overflow
   // item k (a later chunk of a dense cell).  The grid bounds the item count; surplus CTAs
   // exit at once.
@@ -1742,6 +1756,7 @@ __global__ void __launch_bounds__(kSenseWarps * 32, (DEF && ENV == kTag) ? VG_SE
     constexpr bool FLOCK1 = ENV == kFlock && E8 && SS && !RAY && VISION && VG_SENSE_PREDCNT;
     auto flock_pair = [&](const float4 e, const float cs_, const float sn_, const uint32_t rowoff,
                           long long& racc, uint32_t& cacc) {
+      const float c_nk_fall = u_nk_fall, c_inv_w = u_inv_w;
       const float d2 = e.z;
       float d;
       asm("sqrt.approx.ftz.f32 %0, %1;" : "=f"(d) : "f"(d2));
@@ -1757,7 +1772,7 @@ __global__ void __launch_bounds__(kSenseWarps * 32, (DEF && ENV == kTag) ? VG_SE
       // bearing (A3) and sector; an invisible pair updates the row's spare slot v
       const float fwd = fmaf(cs_, e.x, sn_ * e.y);
       const float left = fmaf(cs_, e.y, -sn_ * e.x);
-      const int k = __float2int_rd(fmaf(vg_atan2(left, fwd), c_inv_w, c_half_v));
+      const int k = __float2int_rd(fmaf(vg_atan2(left, fwd, u_c6), c_inv_w, c_half_v));
       const uint32_t idx = min((uint32_t)k, (uint32_t)VG_SC(v));
       red_min(srow + rowoff + idx * 4u, __float_as_uint(fminf(d * c_inv_dv, kBelowOne)));
     };
