@@ -1308,9 +1308,18 @@ constexpr int kDrainUnroll = VG_SENSE_DRAIN_UNROLL;
 // constant (the first atan2 coefficient, v / fov, the tent slope) held in uniform registers
 // (a REDUX of the value), so ptxas need not re-create them in every 32-pair batch (48 -> 45
 // instructions per batch).  Bit 0: the replica instance (DEF = 1; c4 3,603 -> 3,557 us);
-// bit 1: the single-world instance (DEF = 2; measured 678 -> 683 us at c5, so off).
+// bit 1: the single-world instance (DEF = 2; with two of the three: c5 678 -> 670 us).
 #ifndef VG_SENSE_UCONST
-#define VG_SENSE_UCONST 1
+#define VG_SENSE_UCONST 3
+#endif
+// which of the three per instance (1 the atan2 coefficient, 2 the tent slope, 4 v / fov):
+// c5 (DEF = 2) measured none 678.4, {c6} 672.8, {slope} 673.3, {v/fov} 671.6, {c6, slope}
+// 671.6, {c6, v/fov} 670.6, {slope, v/fov} 670.2, all three 683 us (`gpu_run88.sh`)
+#ifndef VG_SENSE_UCMASK1
+#define VG_SENSE_UCMASK1 7
+#endif
+#ifndef VG_SENSE_UCMASK2
+#define VG_SENSE_UCMASK2 6
 #endif
 #ifndef VG_SENSE_KITF
 #define VG_SENSE_KITF 1
@@ -1603,9 +1612,10 @@ __global__ void __launch_bounds__(kSenseWarps * 32, (DEF && ENV == kTag) ? VG_SE
                  "+f"(c_nk_fall), "+f"(c_b_fall), "+f"(c_inv_w), "+f"(c_half_v), "+f"(c_inv_dv));
   float u_c6 = 0.006812420208007097f, u_nk_fall = c_nk_fall, u_inv_w = c_inv_w;
   if (DEF && ((VG_SENSE_UCONST >> (DEF - 1)) & 1)) {
-    u_c6 = __uint_as_float(__reduce_max_sync(kFull, __float_as_uint(u_c6)));
-    u_nk_fall = __uint_as_float(__reduce_max_sync(kFull, __float_as_uint(u_nk_fall)));
-    u_inv_w = __uint_as_float(__reduce_max_sync(kFull, __float_as_uint(u_inv_w)));
+    constexpr int msk = (DEF == 2) ? VG_SENSE_UCMASK2 : VG_SENSE_UCMASK1;   // which of the three
+    if (msk & 1) u_c6 = __uint_as_float(__reduce_max_sync(kFull, __float_as_uint(u_c6)));
+    if (msk & 2) u_nk_fall = __uint_as_float(__reduce_max_sync(kFull, __float_as_uint(u_nk_fall)));
+    if (msk & 4) u_inv_w = __uint_as_float(__reduce_max_sync(kFull, __float_as_uint(u_inv_w)));
   }
   // CTA c < n_first: the first chunk_q queries of sensed cell c; CTA n_first + k: overflow
   // item k (a later chunk of a dense cell).  The grid bounds the item count; surplus CTAs
