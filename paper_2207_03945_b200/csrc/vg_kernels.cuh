@@ -1321,6 +1321,12 @@ constexpr int kDrainUnroll = VG_SENSE_DRAIN_UNROLL;
 #ifndef VG_SENSE_UCMASK2
 #define VG_SENSE_UCMASK2 6
 #endif
+// XYPTR: the candidate halves of a chunk load from one 64-bit pointer at immediate offsets
+// (+0x100 per half) instead of an IMAD.WIDE per half: c5 k_sense 670 -> 663 us, c4 3.556 ->
+// 3.445 ms (`tools/runs/gpu_run90.sh`)
+#ifndef VG_SENSE_XYPTR
+#define VG_SENSE_XYPTR 1
+#endif
 #ifndef VG_SENSE_KITF
 #define VG_SENSE_KITF 1
 #endif
@@ -2112,12 +2118,14 @@ __global__ void __launch_bounds__(kSenseWarps * 32, (DEF && ENV == kTag) ? VG_SE
         // position, never within d_v of anyone; halves wholly past it are skipped.
         float cxh[HV], cyh[HV];
         uint32_t wh[HV];
+        // XYPTR: one 64-bit address per chunk; the halves load at immediate offsets
+        const float2* xyp = sorted_xy + (size_t)(p0 + lane);
 #pragma unroll
         for (int h = 0; h < HV; ++h) {
           const uint32_t pj = p0 + 32u * h + lane;
           // VG_SENSE_LDPRED: halves wholly past the window end load nothing (predicated)
           const float2 o = (!VG_SENSE_LDPRED || h < (NONAN ? HF : 1) || p0 + 32u * h < we)
-                               ? __ldg(&sorted_xy[pj]) : make_float2(0.f, 0.f);
+                               ? __ldg(VG_SENSE_XYPTR ? xyp + 32 * h : &sorted_xy[pj]) : make_float2(0.f, 0.f);
           float x = o.x;
           uint32_t tj = 0u;
           if (ENV == kTag) {                 // type in the sign bit of x (K3b)
