@@ -1324,6 +1324,12 @@ constexpr int kDrainUnroll = VG_SENSE_DRAIN_UNROLL;
 // XYPTR: the candidate halves of a chunk load from one 64-bit pointer at immediate offsets
 // (+0x100 per half) instead of an IMAD.WIDE per half: c5 k_sense 670 -> 663 us, c4 3.556 ->
 // 3.445 ms (`tools/runs/gpu_run90.sh`)
+// RINGB: a full drain batch addressed as (ring base + lane offset) + (head mod ring size)
+// with the head in a uniform register: c5 k_sense 662 -> 652 us, c4 3.445 -> 3.424 ms
+// (`tools/runs/gpu_run93.sh`)
+#ifndef VG_SENSE_RINGB
+#define VG_SENSE_RINGB 1
+#endif
 #ifndef VG_SENSE_XYPTR
 #define VG_SENSE_XYPTR 1
 #endif
@@ -2168,6 +2174,17 @@ __global__ void __launch_bounds__(kSenseWarps * 32, (DEF && ENV == kTag) ? VG_SE
 #pragma unroll kDrainUnroll
 #endif
             while (tail[t] - head[t] >= 32u * ES) {
+              // RINGB: head only ever advances by whole batches from 0, so a batch never
+              // wraps: lane offset + (head mod ring), a uniform add instead of an add + mask
+              if (VG_SENSE_RINGB) {
+                const uint32_t a = (qbase[t] + lane * ES) + (head[t] & (kQueue * 16u - 1u));
+                if (E8) {
+                  const float2 v = lds64(a);
+                  process(t, make_float4(v.x, v.y, fmaf(v.x, v.x, v.y * v.y), 0.f));
+                } else {
+                  process(t, lds128(a));
+                }
+              } else
               process(t, ring_entry(t, head[t] + lane * ES));
               head[t] += 32u * ES;
             }
