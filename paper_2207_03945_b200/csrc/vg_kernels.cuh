@@ -1623,7 +1623,7 @@ __global__ void __launch_bounds__(kSenseWarps * 32, (DEF && ENV == kTag) ? VG_SE
     asm volatile("" : "+f"(c_contact2), "+f"(c_mcollide), "+f"(c_k_rise), "+f"(c_b_rise),
                  "+f"(c_nk_fall), "+f"(c_b_fall), "+f"(c_inv_w), "+f"(c_half_v), "+f"(c_inv_dv));
   float u_c6 = 0.006812420208007097f, u_nk_fall = c_nk_fall, u_inv_w = c_inv_w;
-  if (DEF && ((VG_SENSE_UCONST >> (DEF - 1)) & 1)) {
+  if (DEF && ((VG_SENSE_UCONST >> (DEF > 0 ? DEF - 1 : 0)) & 1)) {
     constexpr int msk = (DEF == 2) ? VG_SENSE_UCMASK2 : VG_SENSE_UCMASK1;   // which of the three
     if (msk & 1) u_c6 = __uint_as_float(__reduce_max_sync(kFull, __float_as_uint(u_c6)));
     if (msk & 2) u_nk_fall = __uint_as_float(__reduce_max_sync(kFull, __float_as_uint(u_nk_fall)));
